@@ -1,0 +1,388 @@
+/*
+ * arc_oracle.c -- plain, slow, obviously-correct CPU oracle for the ARCQuant
+ * (arxiv 2601.07475) online hot path.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and the
+ * cpu_baseline / --impl reference legs of bench.py may load this library.  The
+ * product path (libarc.so, paper_2601_07475_b200/) never links, imports or calls
+ * it, and shares no code, header, table or constant generator with it.
+ *
+ * Citations "P:<line>" are /root/reference/PAPER.md line numbers (section,
+ * equation or table named beside them); "Q<n>" are the readings of the paper
+ * listed in DESIGN.md ("Readings") where the paper is silent or ambiguous.
+ *
+ * Floating point: every float operation below is one IEEE binary32 operation
+ * with round-to-nearest-even (compiled with -O2 -ffp-contract=off, SSE, no
+ * fast-math), in exactly the order written.  That order is the pinned op order
+ * of reading Q7; the CUDA path reproduces it with __fmul_rn/__fdiv_rn.
+ *
+ * What pins each function (tests/test_oracle_*.py):
+ *   e2m1_*        Table 7 values; brute-force argmin over the 16 codes;
+ *                 SPEC example 5.0 -> 4.0; worst error 1.0 on [-6, 6].
+ *   e4m3_*        Table 7 bias 7 / max 448; torch.float8_e4m3fn decode of
+ *                 all codes; brute-force scan for ceil; alpha in [1, 1.125).
+ *   stage         brute force over every block of small tensors; the worked
+ *                 example in DESIGN.md; 16 x 6.0 -> SF 0x38.
+ *   arc_*         S = 0 reduces to plain NVFP4; representable input -> zero
+ *                 residual; Eq.4 bound and alpha1*alpha2 <= 1.125^2;
+ *                 duplicate blocks bitwise equal.
+ *   pack/layout   the layout map is a bijection; GEMM identical across layouts.
+ *   calibration   S:188 example; perm prefix = {j : max_j > tau}.
+ *   gemm_exact    Eq.2 identity as an integer equality; brute
+ *                 float64 dequantized product on small shapes.
+ * Parity unpinned (decisions, not values the paper prints): Q2 ceil-rounded
+ * E4M3 block scales, Q4 static activation tensor scale, Q6/Q7 residual domain
+ * and op order, Q12 default layout.  See DESIGN.md.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define OR_OK 0
+#define OR_ERR_SHAPE 2
+#define OR_ERR_NONFINITE 7
+
+/* ------------------------------------------------------------------------- */
+/* C1: E2M1 (Table 7: FP4 E2M1, bias 1, max +-6).                      */
+/* The 8 magnitudes follow from 1 sign, 2 exponent (bias 1), 1 mantissa bit:  */
+/* subnormal 0, 0.5; normal 1, 1.5, 2, 3, 4, 6.                               */
+/* ------------------------------------------------------------------------- */
+static const float E2M1_MAG[8] = {0.0f, 0.5f, 1.0f, 1.5f, 2.0f, 3.0f, 4.0f, 6.0f};
+
+float or_e2m1_value(uint8_t q) {
+    float m = E2M1_MAG[q & 7];
+    return (q & 8) ? -m : m;
+}
+
+/* Eq.1 round() read as round-to-nearest, ties to the even code,
+ * saturating at +-6, sign kept (reading Q1).  The thresholds are the midpoints
+ * of adjacent magnitudes; '>' vs '>=' encodes the tie going to the even code:
+ * 0.25->0, 0.75->1.0, 1.25->1.0, 1.75->2, 2.5->2, 3.5->4, 5->4. */
+uint8_t or_e2m1_encode(float t) {
+    float a = fabsf(t);
+    uint8_t mag = (uint8_t)((a > 0.25f) + (a >= 0.75f) + (a > 1.25f) + (a >= 1.75f) +
+                            (a > 2.5f) + (a >= 3.5f) + (a > 5.0f));
+    return (uint8_t)(mag | (signbit(t) ? 8 : 0));
+}
+
+/* ------------------------------------------------------------------------- */
+/* C2: E4M3 (Table 7: bias 7, max +-448; OCP E4M3FN, 0x7F = NaN).      */
+/* ------------------------------------------------------------------------- */
+float or_e4m3_value(uint8_t c) {
+    int e = (c >> 3) & 15, m = c & 7;
+    float v;
+    if (e == 0) v = ldexpf((float)m, -9);                  /* subnormal: m * 2^-9 */
+    else        v = ldexpf(1.0f + (float)m / 8.0f, e - 7);
+    return (c & 0x80) ? -v : v;
+}
+
+/* Block-scale encoder, reading Q2: smallest non-negative E4M3 code whose value
+ * is >= v (alpha = s/M >= 1; "2^-3 step size"), saturating at
+ * 448 (0x7E).  Plain linear scan of the 127 finite codes. */
+uint8_t or_e4m3_ceil(float v) {
+    if (!(v > 0.0f)) return 0;
+    for (int c = 0; c <= 0x7E; ++c)
+        if (or_e4m3_value((uint8_t)c) >= v) return (uint8_t)c;
+    return 0x7E;
+}
+
+/* Round-to-nearest-even E4M3 with saturation: used only by the MXFP8
+ * comparator of Eq.3.  Linear scan; ties -> even code. */
+uint8_t or_e4m3_rn(float x) {
+    float a = fabsf(x);
+    int best = 0;
+    double bd = 1e300;
+    for (int c = 0; c <= 0x7E; ++c) {
+        double d = fabs((double)or_e4m3_value((uint8_t)c) - (double)a);
+        if (d < bd || (d == bd && (c & 1) == 0)) { bd = d; best = c; }
+    }
+    return (uint8_t)(best | (signbit(x) ? 0x80 : 0));
+}
+
+/* E8M0 round-up (MX scale, "shared exponent"): smallest power of two >= v. */
+float or_e8m0_up(float v) {
+    int e;
+    float f = frexpf(v, &e);               /* v = f * 2^e, f in [0.5, 1) */
+    if (f == 0.5f) return ldexpf(1.0f, e - 1);
+    return ldexpf(1.0f, e);
+}
+
+/* ------------------------------------------------------------------------- */
+/* C4: STAGE -- one NVFP4 block quantization, Eq.1 with the two-  */
+/* level NVFP4 scaling of P:118 / P:453: value = v(q) * d / gs.               */
+/* base = gs for the primary stage; base = d1 for the residual stage (Q6).    */
+/* ------------------------------------------------------------------------- */
+void or_stage(const float z[16], float base, uint8_t* sf, float* d_out, float t[16], uint8_t q[16]) {
+    float a = 0.0f;
+    for (int i = 0; i < 16; ++i) {                /* a = max |z|  (exact) */
+        float m = fabsf(z[i]);
+        if (m > a) a = m;
+    }
+    float c6 = base / 6.0f;                        /* q_max = 6 (Table 7) */
+    uint8_t s = or_e4m3_ceil(a * c6);             /* s_X = max|X| / q_max, rounded up */
+    float d = or_e4m3_value(s);
+    float k = (d == 0.0f) ? 0.0f : base / d;
+    for (int i = 0; i < 16; ++i) {
+        t[i] = z[i] * k;                           /* X / s_X in E2M1 units */
+        q[i] = or_e2m1_encode(t[i]);               /* Q_X = round(X / s_X) */
+    }
+    *sf = s;
+    *d_out = d;
+}
+
+/* bf16 -> fp32 widening is exact: the bf16 bits are the top 16 fp32 bits. */
+static float bf16_to_f32(uint16_t h) {
+    uint32_t u = (uint32_t)h << 16;
+    float f;
+    memcpy(&f, &u, 4);
+    return f;
+}
+
+/* ------------------------------------------------------------------------- */
+/* C5: ARC activation row, logical (unpacked) order -- P:138 §3.2 "Online     */
+/* Activation Quantization": (1) reorder + primary quantization of all K      */
+/* channels, (2) residual R_o = X_o - s*Q_Xo of the first S reordered         */
+/* (outlier) channels, quantized again, (3) concatenation along K.            */
+/* Output: codes[K+S] (one 4-bit code per byte), sf[(K+S)/16].                */
+/* Logical block b < K/16 = primary block b; logical block K/16+j = residual  */
+/* of primary block j (j < S/16).                                             */
+/* ------------------------------------------------------------------------- */
+int or_arc_row_logical(const uint16_t* x_row, const int32_t* perm, int K, int S, float gs,
+                       uint8_t* codes, uint8_t* sf) {
+    if (K <= 0 || K % 16 || S < 0 || S % 16 || S > K) return OR_ERR_SHAPE;
+    int nb = K / 16;
+    for (int b = 0; b < nb; ++b) {
+        float z[16], t[16], e[16], t2[16], d1, d2;
+        uint8_t q1[16], q2[16], s1, s2;
+        for (int i = 0; i < 16; ++i) {
+            z[i] = bf16_to_f32(x_row[perm[16 * b + i]]);       /* (1) reorder */
+            if (!isfinite(z[i])) return OR_ERR_NONFINITE;
+        }
+        or_stage(z, gs, &s1, &d1, t, q1);                      /* (1) primary */
+        memcpy(codes + 16 * b, q1, 16);
+        sf[b] = s1;
+        if (b < S / 16) {                                      /* (2) outlier block */
+            for (int i = 0; i < 16; ++i)
+                e[i] = t[i] - or_e2m1_value(q1[i]);             /* residual, units d1/gs */
+            or_stage(e, d1, &s2, &d2, t2, q2);                 /* fresh block scale, same gs */
+            memcpy(codes + K + 16 * b, q2, 16);                /* (3) appended along K */
+            sf[nb + b] = s2;
+        }
+    }
+    return OR_OK;
+}
+
+/* C6: weight row, logical order -- P:140 "Offline Weight Quantization":
+ * reorder, quantize, then duplicate the *quantized* outlier blocks (codes and
+ * block scale bitwise, reading Q13) instead of computing residuals. */
+int or_weight_row_logical(const uint16_t* w_row, const int32_t* perm, int K, int S, float gs,
+                          uint8_t* codes, uint8_t* sf) {
+    if (K <= 0 || K % 16 || S < 0 || S % 16 || S > K) return OR_ERR_SHAPE;
+    int nb = K / 16;
+    for (int b = 0; b < nb; ++b) {
+        float z[16], t[16], d;
+        uint8_t q[16], s;
+        for (int i = 0; i < 16; ++i) {
+            z[i] = bf16_to_f32(w_row[perm[16 * b + i]]);
+            if (!isfinite(z[i])) return OR_ERR_NONFINITE;
+        }
+        or_stage(z, gs, &s, &d, t, q);
+        memcpy(codes + 16 * b, q, 16);
+        sf[b] = s;
+    }
+    for (int j = 0; j < S / 16; ++j) {                          /* Q_Waug = [Q_W | Q_Wo] */
+        memcpy(codes + K + 16 * j, codes + 16 * j, 16);
+        sf[nb + j] = sf[j];
+    }
+    return OR_OK;
+}
+
+/* ------------------------------------------------------------------------- */
+/* C8: block map.  P:591-597 App.D "Interleaved Channel Layout": each 16-     */
+/* channel primary outlier block is immediately followed by its residual      */
+/* block.  layout 0 = INTERLEAVED, 1 = CONTIGUOUS (the logical concat). */
+/* ------------------------------------------------------------------------- */
+int or_physical_block(int l, int K, int S, int layout) {
+    int nb = K / 16, ns = S / 16;
+    if (layout == 1) return l;
+    if (l < ns) return 2 * l;                  /* primary outlier block j -> 2j   */
+    if (l < nb) return l + ns;                 /* remaining primary blocks        */
+    return 2 * (l - nb) + 1;                   /* residual block j -> 2j+1        */
+}
+
+/* Kp: K+S padded to the 64-element MMA K step (reading Q14). */
+int64_t or_kp(int K, int S) { return ((int64_t)(K + S) + 63) / 64 * 64; }
+
+/* C9: the 128x4 scale-factor tile layout (reading Q15): byte offset of the
+ * scale for row m, physical scale column c, in a buffer of Kp/16 columns. */
+int64_t or_sf_offset(int64_t m, int64_t c, int64_t Kp) {
+    return ((m >> 7) * (Kp / 64) + (c >> 2)) * 512 + (m & 31) * 16 + ((m >> 5) & 3) * 4 + (c & 3);
+}
+
+/* Pack one logical row: codes (one per byte, logical order) -> nibble-packed
+ * physical row (element 2j in the low nibble of byte j) plus SF bytes into
+ * the swizzled buffer.  Padding blocks Ka..Kp hold code 0 and SF 0x00. */
+void or_pack_row(const uint8_t* lcodes, const uint8_t* lsf, int K, int S, int layout, int64_t m,
+                 uint8_t* codes_row, uint8_t* sf_buf) {
+    int64_t Kp = or_kp(K, S);
+    int nlog = (K + S) / 16;
+    uint8_t* phys = (uint8_t*)calloc((size_t)Kp, 1);
+    uint8_t* psf = (uint8_t*)calloc((size_t)(Kp / 16), 1);
+    for (int l = 0; l < nlog; ++l) {
+        int p = or_physical_block(l, K, S, layout);
+        memcpy(phys + 16 * p, lcodes + 16 * l, 16);
+        psf[p] = lsf[l];
+    }
+    for (int64_t j = 0; j < Kp / 2; ++j)
+        codes_row[j] = (uint8_t)((phys[2 * j] & 15) | ((phys[2 * j + 1] & 15) << 4));
+    for (int64_t c = 0; c < Kp / 16; ++c) sf_buf[or_sf_offset(m, c, Kp)] = psf[c];
+    free(phys);
+    free(psf);
+}
+
+/* Whole-tensor ARC activation quantization (C5 + C8 + C9) on host buffers.
+ * x: bf16 bits [M][ldx]; codes: [M][Kp/2]; sf: roundup(M,128)*Kp/16 bytes. */
+int or_quantize_activation(const uint16_t* x, int64_t M, int K, int64_t ldx, const int32_t* perm,
+                           int S, float gs, int layout, uint8_t* codes, uint8_t* sf) {
+    int64_t Kp = or_kp(K, S);
+    uint8_t* lc = (uint8_t*)malloc((size_t)(K + S));
+    uint8_t* ls = (uint8_t*)malloc((size_t)((K + S) / 16 + 1));
+    int rc = OR_OK;
+    for (int64_t m = 0; m < M && rc == OR_OK; ++m) {
+        rc = or_arc_row_logical(x + m * ldx, perm, K, S, gs, lc, ls);
+        if (rc == OR_OK) or_pack_row(lc, ls, K, S, layout, m, codes + m * (Kp / 2), sf);
+    }
+    free(lc);
+    free(ls);
+    return rc;
+}
+
+/* Whole-tensor weight preparation (C6 + C8 + C9). */
+int or_quantize_weight(const uint16_t* w, int64_t N, int K, int64_t ldw, const int32_t* perm, int S,
+                       float gs, int layout, uint8_t* codes, uint8_t* sf) {
+    int64_t Kp = or_kp(K, S);
+    uint8_t* lc = (uint8_t*)malloc((size_t)(K + S));
+    uint8_t* ls = (uint8_t*)malloc((size_t)((K + S) / 16 + 1));
+    int rc = OR_OK;
+    for (int64_t n = 0; n < N && rc == OR_OK; ++n) {
+        rc = or_weight_row_logical(w + n * ldw, perm, K, S, gs, lc, ls);
+        if (rc == OR_OK) or_pack_row(lc, ls, K, S, layout, n, codes + n * (Kp / 2), sf);
+    }
+    free(lc);
+    free(ls);
+    return rc;
+}
+
+/* ------------------------------------------------------------------------- */
+/* C7: calibration -- P:136 "Adaptive Outlier Identification".         */
+/* ------------------------------------------------------------------------- */
+/* Per-channel abs-max over all calibration rows (exact), max-aggregated into
+ * chan_max (caller initialises it, e.g. to zeros). */
+int or_calib_absmax(const uint16_t* x, int64_t rows, int K, int64_t ldx, float* chan_max) {
+    for (int64_t r = 0; r < rows; ++r)
+        for (int j = 0; j < K; ++j) {
+            float v = bf16_to_f32(x[r * ldx + j]);
+            if (!isfinite(v)) return OR_ERR_NONFINITE;
+            if (fabsf(v) > chan_max[j]) chan_max[j] = fabsf(v);
+        }
+    return OR_OK;
+}
+
+/* perm = channels sorted by abs-max descending, ties to the lower index (Q9);
+ * M = layer-wise max; tau = 2^-3 M; S_raw = #{chan_max > tau} (strict, Q8);
+ * S = min(K, 16*ceil(S_raw/16)) (Q10) unless s_override >= 0.
+ * Plain insertion sort: obviously stable. */
+int or_select_outliers(const float* chan_max, int K, int s_override, int32_t* perm, int* S,
+                       int* S_raw, float* M, float* tau) {
+    if (K <= 0 || K % 16) return OR_ERR_SHAPE;
+    if (s_override > K || (s_override >= 0 && s_override % 16)) return OR_ERR_SHAPE;
+    float mx = 0.0f;
+    for (int j = 0; j < K; ++j) {
+        if (!isfinite(chan_max[j]) || chan_max[j] < 0.0f) return OR_ERR_NONFINITE;
+        if (chan_max[j] > mx) mx = chan_max[j];
+    }
+    for (int j = 0; j < K; ++j) perm[j] = j;
+    for (int i = 1; i < K; ++i) {
+        int32_t v = perm[i];
+        int p = i - 1;
+        while (p >= 0 && chan_max[perm[p]] < chan_max[v]) { perm[p + 1] = perm[p]; --p; }
+        perm[p + 1] = v;
+    }
+    float t = mx * 0.125f;                        /* tau = 2^-3 M, exact */
+    int sr = 0;
+    for (int j = 0; j < K; ++j) sr += chan_max[j] > t;
+    int s = (sr + 15) / 16 * 16;
+    if (s > K) s = K;
+    *S_raw = sr;
+    *S = (s_override >= 0) ? s_override : s;
+    *M = mx;
+    *tau = t;
+    return OR_OK;
+}
+
+/* ------------------------------------------------------------------------- */
+/* C10: the augmented GEMM, exact -- Eq.2: Y = s_Xaug Q_Xaug       */
+/* (s_Waug Q_Waug)^T over the extended reduction dimension K+S. */
+/* Work in integer units: V(q) = 2 v(q) in [-12, 12], D(sf) = 512 E4M3(sf);    */
+/* one term = V_a D_a V_b D_b = 2^20 * (product of the four real factors).     */
+/* The int64 sum is exact and order-independent (|sum| < 2.5e17 < 2^63).      */
+/* rows: list of A row indices to compute (nrows of them); T, Tabs: [nrows][N]. */
+/* ------------------------------------------------------------------------- */
+/* Integer value V(q)*D(sf) of physical element p of row r of a packed operand. */
+static int64_t elem_units(const uint8_t* codes, const uint8_t* sf, int64_t r, int64_t p, int64_t Kp) {
+    uint8_t byte = codes[r * (Kp / 2) + p / 2];
+    uint8_t q = (p & 1) ? (byte >> 4) : (byte & 15);
+    int64_t V = (int64_t)(2.0f * or_e2m1_value(q));
+    int64_t D = (int64_t)(512.0f * or_e4m3_value(sf[or_sf_offset(r, p / 16, Kp)]));
+    return V * D;
+}
+
+void or_gemm_exact(const uint8_t* a_codes, const uint8_t* a_sf, const uint8_t* b_codes,
+                   const uint8_t* b_sf, int64_t N, int64_t Kp, const int64_t* rows, int64_t nrows,
+                   int64_t* T, int64_t* Tabs) {
+    int64_t* Va = (int64_t*)malloc(sizeof(int64_t) * (size_t)(Kp * nrows));
+    int64_t* Vb = (int64_t*)malloc(sizeof(int64_t) * (size_t)Kp);
+    for (int64_t ri = 0; ri < nrows; ++ri)
+        for (int64_t p = 0; p < Kp; ++p) Va[ri * Kp + p] = elem_units(a_codes, a_sf, rows[ri], p, Kp);
+    for (int64_t n = 0; n < N; ++n) {
+        for (int64_t p = 0; p < Kp; ++p) Vb[p] = elem_units(b_codes, b_sf, n, p, Kp);
+        for (int64_t ri = 0; ri < nrows; ++ri) {
+            int64_t acc = 0, aabs = 0;
+            for (int64_t p = 0; p < Kp; ++p) {
+                int64_t term = Va[ri * Kp + p] * Vb[p];
+                acc += term;
+                aabs += term < 0 ? -term : term;
+            }
+            T[ri * N + n] = acc;
+            Tabs[ri * N + n] = aabs;
+        }
+    }
+    free(Va);
+    free(Vb);
+}
+
+/* ------------------------------------------------------------------------- */
+/* Eq.3 comparator: single-stage MXFP8 -- g = 32, E4M3 elements,  */
+/* E8M0 block scale = smallest power of two >= amax/448 (alpha_mx in [1,2)).  */
+/* Returns the dequantized block in xhat[32] and the scale.                    */
+/* ------------------------------------------------------------------------- */
+void or_mxfp8_block(const float x[32], float* scale, float xhat[32]) {
+    float a = 0.0f;
+    for (int i = 0; i < 32; ++i) if (fabsf(x[i]) > a) a = fabsf(x[i]);
+    float s = (a > 0.0f) ? or_e8m0_up(a / 448.0f) : 1.0f;
+    for (int i = 0; i < 32; ++i) xhat[i] = or_e4m3_value(or_e4m3_rn(x[i] / s)) * s;
+    *scale = s;
+}
+
+/* Batch helpers so the Python tests can sweep the codecs without a per-call
+ * ctypes round trip.  They only loop over the scalar functions above. */
+void or_e2m1_encode_n(const float* t, int64_t n, uint8_t* q) {
+    for (int64_t i = 0; i < n; ++i) q[i] = or_e2m1_encode(t[i]);
+}
+void or_e4m3_ceil_n(const float* v, int64_t n, uint8_t* c) {
+    for (int64_t i = 0; i < n; ++i) c[i] = or_e4m3_ceil(v[i]);
+}
+void or_e4m3_rn_n(const float* v, int64_t n, uint8_t* c) {
+    for (int64_t i = 0; i < n; ++i) c[i] = or_e4m3_rn(v[i]);
+}
