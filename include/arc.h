@@ -1,0 +1,181 @@
+/*
+ * arc.h -- C ABI of libarc.so, the B200-native (sm_100a) ARCQuant hot path.
+ *
+ * ARCQuant (arxiv 2601.07475) keeps a linear layer Y = X W^T ("Problem
+ * Definition") in a strictly unified NVFP4 W4A4 data path by appending, along the
+ * reduction dimension, the NVFP4-quantized residuals of the S calibrated outlier
+ * channels of X and a duplicate of the matching quantized weight columns, so one
+ * block-scaled GEMM over K+S computes the primary product plus the correction
+ * (§3.2, Eq.2).  This header exposes the calls of the paper's problem
+ * statement: calibration (arc_calib_absmax + arc_select_outliers),
+ * offline weight preparation (arc_quantize_weight), online activation
+ * quantization (arc_quantize_activation, P:138 + the fused kernel of P:164), and
+ * the augmented GEMM (arc_gemm / arc_linear).
+ *
+ * Notation: M = tokens, K = input features, N = output features,
+ * S = augmented (outlier) channels, a multiple of 16 with 0 <= S <= K.
+ * Ka = K+S; Kp = roundup(Ka, 64) is the physical reduction length.
+ *
+ * Data formats (all produced and consumed by this library):
+ *  - codes: uint8 [rows][Kp/2]; physical element 2j in the low nibble of byte
+ *    j (E2M1: 1 sign, 2 exponent, 1 mantissa bit; Table 7).
+ *  - sf: E4M3 block scales (Table 7), one per 16 physical elements, in the
+ *    tcgen05 / cuBLASLt 128x4 tile layout: byte of (row m, scale column c) at
+ *    ((m>>7)*(Kp/64) + (c>>2))*512 + (m&31)*16 + ((m>>5)&3)*4 + (c&3).
+ *    The buffer holds roundup(rows,128)*Kp/16 bytes; bytes of rows >= rows in
+ *    the last 128-row tile are left unspecified (they only feed discarded
+ *    output rows/columns).
+ *  - value of an element = e2m1(code) * e4m3(sf) / gs, gs the FP32 tensor scale
+ *    ("secondary per-tensor scaling factor"), gs = 2688/amax.
+ *  - physical block order: ARC_LAYOUT_INTERLEAVED places the residual block of
+ *    outlier block j right after it (App.D); ARC_LAYOUT_CONTIGUOUS is
+ *    the logical concatenation [Q_X | Q_Ro].  Blocks Ka/16..Kp/16-1 are
+ *    zero codes with scale 0x00.
+ *
+ * Conventions for every call:
+ *  - Pointers are DEVICE pointers unless the parameter name ends in _host.
+ *  - Buffers are owned by the caller; the library keeps no pointer after a call
+ *    returns, allocates no device memory and never synchronizes the device.
+ *    Device work is enqueued on `stream` (a cudaStream_t passed as void*;
+ *    NULL = legacy default stream) and is asynchronous.
+ *  - Argument checks are synchronous and happen before anything is enqueued:
+ *    ARC_ERR_NULL (null pointer), ARC_ERR_SHAPE (K <= 0, K%16, S%16, S < 0,
+ *    S > K, M < 0, N <= 0, leading dimension < K or not a multiple of 8
+ *    elements, profile / qweight mismatch), ARC_ERR_ALIGN (a base pointer not
+ *    16-byte aligned), ARC_ERR_WORKSPACE (workspace too small),
+ *    ARC_ERR_UNSUPPORTED (the current device is not sm_100; there is no
+ *    fallback of any kind), ARC_ERR_CUDA (a CUDA call or launch failed; text in
+ *    arc_last_error()).  M == 0 (no rows) is a successful no-op; the row
+ *    buffers may then be NULL.
+ *  - Non-finite device inputs are not detected; their outputs are unspecified.
+ *  - Calls are reentrant; concurrent calls on different streams are allowed.
+ */
+#ifndef ARC_H_
+#define ARC_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define ARC_API __attribute__((visibility("default")))
+#else
+#define ARC_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  ARC_OK = 0,
+  ARC_ERR_NULL = 1,
+  ARC_ERR_SHAPE = 2,
+  ARC_ERR_ALIGN = 3,
+  ARC_ERR_UNSUPPORTED = 4,
+  ARC_ERR_WORKSPACE = 5,
+  ARC_ERR_CUDA = 6,
+  ARC_ERR_NONFINITE = 7
+} arc_status_t;
+
+typedef enum { ARC_BF16 = 0, ARC_FP32 = 2 } arc_dtype_t;
+
+typedef enum { ARC_LAYOUT_INTERLEAVED = 0, ARC_LAYOUT_CONTIGUOUS = 1 } arc_layout_t;
+
+/* Calibration profile of one activation site (the q/k/v projections share one,
+ * gate/up share one): "pre-determine both the channel reordering indices
+ * and the number of outlier channels S". */
+typedef struct {
+  int64_t K;              /* input features                                       */
+  int32_t S;              /* augmented channels, multiple of 16, 0 <= S <= K      */
+  const int32_t* perm;    /* device int32[K]: reordered position i reads channel
+                             perm[i]; perm[0:S] are the outlier channels  */
+  const float* gs;        /* device scalar: activation encode tensor scale
+                             2688/M_calib (static, reading Q4)                    */
+  arc_layout_t layout;
+} arc_profile_t;
+
+/* A prepared (quantized, reordered, outlier-duplicated) weight. */
+typedef struct {
+  int64_t N, K, Kp;
+  int32_t S;
+  arc_layout_t layout;
+  const uint8_t* codes;   /* device [N][Kp/2]                                     */
+  const uint8_t* sf;      /* device roundup(N,128)*Kp/16, 128x4 tile layout       */
+  const float* gs;        /* device scalar gs_w = 2688/amax(W)                    */
+} arc_qweight_t;
+
+/* ---------------------------------------------------------------- utilities */
+ARC_API const char* arc_status_string(arc_status_t s);
+/* Thread-local text of the last ARC_ERR_CUDA / argument error of this thread. */
+ARC_API const char* arc_last_error(void);
+/* 1 if the current CUDA device is sm_100 (B200-class), else 0. */
+ARC_API int arc_device_supported(void);
+/* Sizes of a quantized operand of `rows` rows (codes / sf bytes, Kp). */
+ARC_API arc_status_t arc_buffer_sizes(int64_t rows, int64_t K, int32_t S, int64_t* Kp, size_t* code_bytes,
+                              size_t* sf_bytes);
+/* Workspace arc_linear needs (the quantized activation): code + sf bytes for M rows,
+ * each 256-byte aligned. */
+ARC_API arc_status_t arc_workspace_size(int64_t M, int64_t K, int32_t S, size_t* bytes);
+
+/* ---------------------------------------------------------------- calibration (offline) */
+/* chan_max[j] = max(chan_max[j], max_r |x[r, j]|) over the `rows` bf16 rows of x
+ * (row stride ldx elements).  chan_max is a device float[K] the caller
+ * initialises (zeros) and may accumulate over several batches (exact). */
+ARC_API arc_status_t arc_calib_absmax(const void* x, int64_t rows, int64_t K, int64_t ldx, float* chan_max,
+                              void* stream);
+/* Host, synchronous.  perm_host = channels sorted by chan_max descending, ties to
+ * the lower index (reading Q9); M = max chan_max; tau = 2^-3 M;
+ * S_raw = #{j : chan_max[j] > tau} (strict, Q8); S = min(K, 16*ceil(S_raw/16))
+ * (Q10) unless s_override >= 0 (must be a multiple of 16 <= K); gs = 2688/M as
+ * one fp32 division (1 if M == 0): the static activation tensor scale (Q3, Q4).
+ * ARC_ERR_NONFINITE if chan_max has a NaN/Inf or negative entry. */
+ARC_API arc_status_t arc_select_outliers(const float* chan_max_host, int64_t K, int32_t s_override,
+                                         int32_t* perm_host, int32_t* S, int32_t* S_raw, float* M, float* tau,
+                                         float* gs);
+/* gs_out[0] = 2688 / max|x| over a rows x K bf16 matrix (1.0 if the max is 0):
+ * the NVFP4 encode tensor scale (reading Q3).  gs_out is a device float. */
+ARC_API arc_status_t arc_tensor_scale(const void* x, int64_t rows, int64_t K, int64_t ldx, float* gs_out,
+                              void* stream);
+
+/* ---------------------------------------------------------------- quantization */
+/* Offline weight preparation: reorder the N x K bf16 weight by perm,
+ * quantize every 16-block to NVFP4 against gs_w (block scale = smallest E4M3 >=
+ * amax*gs_w/6, reading Q2), and duplicate the quantized outlier blocks
+ * (codes and scale byte, bitwise) into the augmented blocks. */
+ARC_API arc_status_t arc_quantize_weight(const void* w, int64_t N, int64_t K, int64_t ldw, const int32_t* perm,
+                                 int32_t S, const float* gs_w, arc_layout_t layout, uint8_t* codes,
+                                 uint8_t* sf, void* stream);
+/* Online activation quantization: reorder, primary NVFP4 quantization of
+ * all K channels, residual of the S outlier channels (against the encoded
+ * primary, reading Q6) quantized again with fresh E4M3 block scales and the same
+ * tensor scale (Q5), written as augmented blocks in the profile's layout.
+ * x: bf16 [M][ldx]; codes [M][Kp/2]; sf roundup(M,128)*Kp/16 bytes. */
+ARC_API arc_status_t arc_quantize_activation(const void* x, int64_t M, int64_t ldx, const arc_profile_t* prof,
+                                     uint8_t* codes, uint8_t* sf, void* stream);
+
+/* ---------------------------------------------------------------- GEMM */
+/* y[M][N] (row stride ldy elements) = (1/(gs_x*gs_w)) * sum over the Kp physical
+ * elements of A_aug * B_aug^T (Eq.2), FP32 accumulation in tensor
+ * memory (tcgen05.mma kind::mxf4nvf4, scale vector 16), stored as y_dtype.
+ * a_codes/a_sf: the activation as written by arc_quantize_activation with the
+ * same K, S and layout as qw.  ldy * sizeof(y_dtype) must be a multiple of 16. */
+ARC_API arc_status_t arc_gemm(const uint8_t* a_codes, const uint8_t* a_sf, const float* gs_x, int64_t M,
+                      const arc_qweight_t* qw, void* y, arc_dtype_t y_dtype, int64_t ldy, void* stream);
+/* The full linear: arc_quantize_activation into the workspace, then arc_gemm.
+ * ws must hold arc_workspace_size(M, K, S) bytes (256-byte aligned). */
+ARC_API arc_status_t arc_linear(const void* x, int64_t M, int64_t ldx, const arc_profile_t* prof,
+                        const arc_qweight_t* qw, void* y, arc_dtype_t y_dtype, int64_t ldy, void* ws,
+                        size_t ws_bytes, void* stream);
+/* arc_linear on HOST buffers: copies x_host (bf16 [M][K], pinned or pageable) to
+ * the device, runs arc_linear, copies y back to y_host ([M][N] of y_dtype) and
+ * synchronizes `stream`.  ws must hold arc_linear_hostio_workspace_size bytes. */
+ARC_API arc_status_t arc_linear_hostio_workspace_size(int64_t M, int64_t K, int32_t S, int64_t N,
+                                              arc_dtype_t y_dtype, size_t* bytes);
+ARC_API arc_status_t arc_linear_hostio(const void* x_host, int64_t M, const arc_profile_t* prof,
+                               const arc_qweight_t* qw, void* y_host, arc_dtype_t y_dtype, void* ws,
+                               size_t ws_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ARC_H_ */

@@ -1,0 +1,25 @@
+/*
+ * arc_probe.h -- hardware-semantics probes exported by libarc.so for the test
+ * suite (not part of the hot path).  They run the exact device primitives the
+ * quantization kernel uses, element-wise, so tests can pin them against the
+ * oracle exhaustively (E2M1 rounding, E4M3 ceil).
+ * Pointers are device pointers; work is enqueued on `stream`; same status codes
+ * and validation conventions as arc.h.
+ */
+#ifndef ARC_PROBE_H_
+#define ARC_PROBE_H_
+#include "arc.h"
+#ifdef __cplusplus
+extern "C" {
+#endif
+/* out[i] = E2M1 code the kernel assigns to in[i] (cvt.rn.satfinite.e2m1x2 +
+ * sign fix-up; reading Q1). */
+ARC_API arc_status_t arc_probe_e2m1(const float* in, int64_t n, uint8_t* out, void* stream);
+/* Same, for the fp32 whose bit pattern is (uint32)(start_bits + i), i < n. */
+ARC_API arc_status_t arc_probe_e2m1_bits(uint32_t start_bits, int64_t n, uint8_t* out, void* stream);
+/* out[i] = the kernel's ceil-rounded E4M3 scale code of in[i] >= 0 (reading Q2). */
+ARC_API arc_status_t arc_probe_e4m3_ceil(const float* in, int64_t n, uint8_t* out, void* stream);
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,331 @@
+"""Thin ctypes binding of libarc.so (include/arc.h) -- argument marshalling only.
+
+Every computation runs in libarc.so's sm_100a kernels (or, for the host-side
+outlier selection, in libarc.so's C++).  PyTorch provides device memory and the
+current CUDA stream; nothing here computes on tensors.  If libarc.so is missing
+the import fails loudly: there is no CPU or PyTorch fallback.
+
+Names follow the paper (§3.2): calibrate -> (perm, S) profile,
+quantize_weight, quantize_activation, gemm / linear.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libarc.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is not built (python -m paper_2601_07475_b200.build); "
+                      "the ARC hot path has no fallback")
+
+_lib = ctypes.CDLL(LIB_PATH)
+
+INTERLEAVED = 0
+CONTIGUOUS = 1
+BF16 = 0
+FP32 = 2
+
+_P = ctypes.c_void_p
+_i64 = ctypes.c_int64
+_i32 = ctypes.c_int32
+_f32 = ctypes.c_float
+
+
+class ArcProfile(ctypes.Structure):
+    _fields_ = [("K", _i64), ("S", _i32), ("perm", _P), ("gs", _P), ("layout", ctypes.c_int)]
+
+
+class ArcQWeight(ctypes.Structure):
+    _fields_ = [("N", _i64), ("K", _i64), ("Kp", _i64), ("S", _i32), ("layout", ctypes.c_int),
+                ("codes", _P), ("sf", _P), ("gs", _P)]
+
+
+def _sig(name, args, res=ctypes.c_int):
+    f = getattr(_lib, name)
+    f.argtypes = args
+    f.restype = res
+    return f
+
+
+_lib.arc_status_string.restype = ctypes.c_char_p
+_lib.arc_status_string.argtypes = [ctypes.c_int]
+_lib.arc_last_error.restype = ctypes.c_char_p
+_lib.arc_last_error.argtypes = []
+_sig("arc_device_supported", [])
+_sig("arc_buffer_sizes", [_i64, _i64, _i32, ctypes.POINTER(_i64), ctypes.POINTER(ctypes.c_size_t),
+                          ctypes.POINTER(ctypes.c_size_t)])
+_sig("arc_workspace_size", [_i64, _i64, _i32, ctypes.POINTER(ctypes.c_size_t)])
+_sig("arc_calib_absmax", [_P, _i64, _i64, _i64, _P, _P])
+_sig("arc_select_outliers", [_P, _i64, _i32, _P, ctypes.POINTER(_i32), ctypes.POINTER(_i32),
+                             ctypes.POINTER(_f32), ctypes.POINTER(_f32), ctypes.POINTER(_f32)])
+_sig("arc_tensor_scale", [_P, _i64, _i64, _i64, _P, _P])
+_sig("arc_quantize_weight", [_P, _i64, _i64, _i64, _P, _i32, _P, ctypes.c_int, _P, _P, _P])
+_sig("arc_quantize_activation", [_P, _i64, _i64, ctypes.POINTER(ArcProfile), _P, _P, _P])
+_sig("arc_gemm", [_P, _P, _P, _i64, ctypes.POINTER(ArcQWeight), _P, ctypes.c_int, _i64, _P])
+_sig("arc_linear", [_P, _i64, _i64, ctypes.POINTER(ArcProfile), ctypes.POINTER(ArcQWeight), _P, ctypes.c_int,
+                    _i64, _P, ctypes.c_size_t, _P])
+_sig("arc_linear_hostio_workspace_size", [_i64, _i64, _i32, _i64, ctypes.c_int, ctypes.POINTER(ctypes.c_size_t)])
+_sig("arc_linear_hostio", [_P, _i64, ctypes.POINTER(ArcProfile), ctypes.POINTER(ArcQWeight), _P, ctypes.c_int, _P,
+                           ctypes.c_size_t, _P])
+_sig("arc_probe_e2m1", [_P, _i64, _P, _P])
+_sig("arc_probe_e2m1_bits", [ctypes.c_uint32, _i64, _P, _P])
+_sig("arc_probe_e4m3_ceil", [_P, _i64, _P, _P])
+
+# every symbol include/arc.h and include/arc_probe.h declare (checked by tests)
+EXPORTED = [
+    "arc_status_string", "arc_last_error", "arc_device_supported", "arc_buffer_sizes", "arc_workspace_size",
+    "arc_calib_absmax", "arc_select_outliers", "arc_tensor_scale", "arc_quantize_weight",
+    "arc_quantize_activation", "arc_gemm", "arc_linear", "arc_linear_hostio_workspace_size", "arc_linear_hostio",
+    "arc_probe_e2m1", "arc_probe_e2m1_bits", "arc_probe_e4m3_ceil",
+]
+
+
+class ArcError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        self.status = status
+        super().__init__(f"{where}: {_lib.arc_status_string(status).decode()} "
+                         f"({_lib.arc_last_error().decode()})")
+
+
+def _check(st: int, where: str):
+    if st != 0:
+        raise ArcError(st, where)
+
+
+def lib():
+    return _lib
+
+
+def _ptr(t) -> int:
+    return 0 if t is None else int(t.data_ptr())
+
+
+def _stream(stream=None) -> int:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return int(stream.cuda_stream)
+
+
+def device_supported() -> bool:
+    return bool(_lib.arc_device_supported())
+
+
+def buffer_sizes(rows: int, K: int, S: int):
+    kp = _i64()
+    cb = ctypes.c_size_t()
+    sb = ctypes.c_size_t()
+    _check(_lib.arc_buffer_sizes(rows, K, S, ctypes.byref(kp), ctypes.byref(cb), ctypes.byref(sb)),
+           "arc_buffer_sizes")
+    return kp.value, cb.value, sb.value
+
+
+def workspace_size(M: int, K: int, S: int) -> int:
+    b = ctypes.c_size_t()
+    _check(_lib.arc_workspace_size(M, K, S, ctypes.byref(b)), "arc_workspace_size")
+    return b.value
+
+
+# --------------------------------------------------------------------------- profile / weights
+@dataclass
+class Profile:
+    """Calibration profile of one activation site."""
+    K: int
+    S: int
+    perm: torch.Tensor          # device int32 [K]
+    gs: torch.Tensor            # device float32 [1], static encode tensor scale 2688/M
+    layout: int = INTERLEAVED
+    S_raw: int = 0
+    M: float = 0.0
+    tau: float = 0.0
+    _c: ArcProfile = field(default=None, repr=False)
+
+    def c(self) -> ArcProfile:
+        self._c = ArcProfile(self.K, self.S, _ptr(self.perm), _ptr(self.gs), self.layout)
+        return self._c
+
+
+@dataclass
+class QWeight:
+    """A prepared ARC weight: reordered, NVFP4-quantized, outlier blocks duplicated."""
+    N: int
+    K: int
+    Kp: int
+    S: int
+    layout: int
+    codes: torch.Tensor         # uint8 [N, Kp/2]
+    sf: torch.Tensor            # uint8 [roundup(N,128) * Kp/16]
+    gs: torch.Tensor            # float32 [1]
+    _c: ArcQWeight = field(default=None, repr=False)
+
+    def c(self) -> ArcQWeight:
+        self._c = ArcQWeight(self.N, self.K, self.Kp, self.S, self.layout, _ptr(self.codes), _ptr(self.sf),
+                             _ptr(self.gs))
+        return self._c
+
+
+def calib_absmax(x: torch.Tensor, chan_max: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """Running per-channel abs-max over bf16 rows (device)."""
+    assert x.dtype == torch.bfloat16 and x.is_cuda and x.dim() == 2
+    rows, K = x.shape
+    if chan_max is None:
+        chan_max = torch.zeros(K, dtype=torch.float32, device=x.device)
+    _check(_lib.arc_calib_absmax(_ptr(x), rows, K, x.stride(0), _ptr(chan_max), _stream(stream)),
+           "arc_calib_absmax")
+    return chan_max
+
+
+def select_outliers(chan_max_host: np.ndarray, s_override: int = -1) -> dict:
+    cm = np.ascontiguousarray(chan_max_host, dtype=np.float32)
+    K = cm.size
+    perm = np.zeros(K, np.int32)
+    S, S_raw = _i32(), _i32()
+    M, tau, gs = _f32(), _f32(), _f32()
+    _check(_lib.arc_select_outliers(cm.ctypes.data_as(_P), K, s_override, perm.ctypes.data_as(_P), ctypes.byref(S),
+                                    ctypes.byref(S_raw), ctypes.byref(M), ctypes.byref(tau), ctypes.byref(gs)),
+           "arc_select_outliers")
+    return dict(perm=perm, S=S.value, S_raw=S_raw.value, M=M.value, tau=tau.value, gs=gs.value)
+
+
+def calibrate(batches, s_override: int = -1, layout: int = INTERLEAVED, device=None) -> Profile:
+    """Offline calibration of one activation site over an iterable of bf16 [rows, K] batches."""
+    chan_max = None
+    for b in batches:
+        chan_max = calib_absmax(b, chan_max)
+    torch.cuda.current_stream().synchronize()
+    sel = select_outliers(chan_max.cpu().numpy(), s_override)
+    dev = chan_max.device if device is None else device
+    return Profile(K=chan_max.numel(), S=sel["S"], perm=torch.from_numpy(sel["perm"]).to(dev),
+                   gs=torch.tensor([sel["gs"]], dtype=torch.float32, device=dev), layout=layout,
+                   S_raw=sel["S_raw"], M=sel["M"], tau=sel["tau"])
+
+
+def profile_from(perm, S: int, gs: float, layout: int = INTERLEAVED, device="cuda") -> Profile:
+    perm = torch.as_tensor(np.asarray(perm, np.int32)).to(device)
+    return Profile(K=perm.numel(), S=S, perm=perm, gs=torch.tensor([gs], dtype=torch.float32, device=device),
+                   layout=layout)
+
+
+def tensor_scale(x: torch.Tensor, stream=None) -> torch.Tensor:
+    """Device gs = 2688/amax(x) (reading Q3)."""
+    gs = torch.empty(1, dtype=torch.float32, device=x.device)
+    _check(_lib.arc_tensor_scale(_ptr(x), x.shape[0], x.shape[1], x.stride(0), _ptr(gs), _stream(stream)),
+           "arc_tensor_scale")
+    return gs
+
+
+def quantize_weight(w: torch.Tensor, prof: Profile, gs: torch.Tensor | None = None, stream=None) -> QWeight:
+    assert w.dtype == torch.bfloat16 and w.is_cuda and w.dim() == 2 and w.shape[1] == prof.K
+    N, K = w.shape
+    Kp, cb, sb = buffer_sizes(N, K, prof.S)
+    if gs is None:
+        gs = tensor_scale(w, stream)
+    codes = torch.empty(N, Kp // 2, dtype=torch.uint8, device=w.device)
+    sf = torch.empty(sb, dtype=torch.uint8, device=w.device)
+    _check(_lib.arc_quantize_weight(_ptr(w), N, K, w.stride(0), _ptr(prof.perm), prof.S, _ptr(gs), prof.layout,
+                                    _ptr(codes), _ptr(sf), _stream(stream)), "arc_quantize_weight")
+    return QWeight(N=N, K=K, Kp=Kp, S=prof.S, layout=prof.layout, codes=codes, sf=sf, gs=gs)
+
+
+def quantize_activation(x: torch.Tensor, prof: Profile, codes=None, sf=None, stream=None):
+    assert x.dtype == torch.bfloat16 and x.is_cuda and x.dim() == 2 and x.shape[1] == prof.K
+    M = x.shape[0]
+    Kp, cb, sb = buffer_sizes(M, prof.K, prof.S)
+    if codes is None:
+        codes = torch.empty(M, Kp // 2, dtype=torch.uint8, device=x.device)
+    if sf is None:
+        sf = torch.empty(sb, dtype=torch.uint8, device=x.device)
+    _check(_lib.arc_quantize_activation(_ptr(x), M, x.stride(0), ctypes.byref(prof.c()), _ptr(codes), _ptr(sf),
+                                        _stream(stream)), "arc_quantize_activation")
+    return codes, sf
+
+
+def _dtype_code(dt) -> int:
+    if dt == torch.bfloat16:
+        return BF16
+    if dt == torch.float32:
+        return FP32
+    raise ValueError("out_dtype must be torch.bfloat16 or torch.float32")
+
+
+def gemm(a_codes, a_sf, gs_x: torch.Tensor, qw: QWeight, out_dtype=torch.bfloat16, out=None, stream=None):
+    M = a_codes.shape[0]
+    if out is None:
+        out = torch.empty(M, qw.N, dtype=out_dtype, device=a_codes.device)
+    _check(_lib.arc_gemm(_ptr(a_codes), _ptr(a_sf), _ptr(gs_x), M, ctypes.byref(qw.c()), _ptr(out),
+                         _dtype_code(out.dtype), out.stride(0), _stream(stream)), "arc_gemm")
+    return out
+
+
+class Workspace:
+    """Grow-only device workspace for arc_linear (256-byte aligned by the allocator)."""
+
+    def __init__(self, device="cuda"):
+        self.device = device
+        self.buf = None
+
+    def get(self, nbytes: int) -> torch.Tensor:
+        if self.buf is None or self.buf.numel() < nbytes:
+            self.buf = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=self.device)
+        return self.buf
+
+
+_default_ws = {}
+
+
+def linear(x: torch.Tensor, prof: Profile, qw: QWeight, out_dtype=torch.bfloat16, out=None, ws: Workspace = None,
+           stream=None):
+    """The ARC linear layer: fused activation quantize + augmented NVFP4 GEMM (two launches)."""
+    assert x.dtype == torch.bfloat16 and x.is_cuda
+    M = x.shape[0]
+    if out is None:
+        out = torch.empty(M, qw.N, dtype=out_dtype, device=x.device)
+    need = workspace_size(M, prof.K, prof.S)
+    if ws is None:
+        ws = _default_ws.setdefault(x.device, Workspace(x.device))
+    buf = ws.get(need)
+    _check(_lib.arc_linear(_ptr(x), M, x.stride(0), ctypes.byref(prof.c()), ctypes.byref(qw.c()), _ptr(out),
+                           _dtype_code(out.dtype), out.stride(0), _ptr(buf), buf.numel(), _stream(stream)),
+           "arc_linear")
+    return out
+
+
+def linear_hostio_workspace_size(M: int, K: int, S: int, N: int, out_dtype=torch.bfloat16) -> int:
+    b = ctypes.c_size_t()
+    _check(_lib.arc_linear_hostio_workspace_size(M, K, S, N, _dtype_code(out_dtype), ctypes.byref(b)),
+           "arc_linear_hostio_workspace_size")
+    return b.value
+
+
+def linear_hostio(x_host: torch.Tensor, prof: Profile, qw: QWeight, y_host: torch.Tensor, ws: torch.Tensor,
+                  stream=None):
+    """arc_linear on host buffers (H2D of x, D2H of y inside the call; synchronizes the stream)."""
+    assert not x_host.is_cuda and not y_host.is_cuda
+    _check(_lib.arc_linear_hostio(_ptr(x_host), x_host.shape[0], ctypes.byref(prof.c()), ctypes.byref(qw.c()),
+                                  _ptr(y_host), _dtype_code(y_host.dtype), _ptr(ws), ws.numel(), _stream(stream)),
+           "arc_linear_hostio")
+    return y_host
+
+
+# --------------------------------------------------------------------------- probes (tests only)
+def probe_e2m1(x: torch.Tensor) -> torch.Tensor:
+    out = torch.empty(x.numel(), dtype=torch.uint8, device=x.device)
+    _check(_lib.arc_probe_e2m1(_ptr(x), x.numel(), _ptr(out), _stream()), "arc_probe_e2m1")
+    return out
+
+
+def probe_e2m1_bits(start: int, n: int, device="cuda") -> torch.Tensor:
+    out = torch.empty(n, dtype=torch.uint8, device=device)
+    _check(_lib.arc_probe_e2m1_bits(start, n, _ptr(out), _stream()), "arc_probe_e2m1_bits")
+    return out
+
+
+def probe_e4m3_ceil(x: torch.Tensor) -> torch.Tensor:
+    out = torch.empty(x.numel(), dtype=torch.uint8, device=x.device)
+    _check(_lib.arc_probe_e4m3_ceil(_ptr(x), x.numel(), _ptr(out), _stream()), "arc_probe_e4m3_ceil")
+    return out

@@ -1,0 +1,309 @@
+// api.cu -- the extern "C" boundary of libarc.so (include/arc.h): synchronous
+// argument validation, then kernel launches on the caller's stream.  No device
+// memory is allocated and the device is never synchronized (except by the
+// documented host-IO variant).  There is no fallback path: a non-sm_100 device
+// is ARC_ERR_UNSUPPORTED.
+#include "arc.h"
+#include "arc_internal.h"
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+namespace arc {
+
+static thread_local char g_err[512] = "";
+
+static arc_status_t fail(arc_status_t s, const char* what) {
+  std::snprintf(g_err, sizeof(g_err), "%s", what);
+  return s;
+}
+static arc_status_t cuda_fail(cudaError_t e, const char* where, const char* detail = nullptr) {
+  std::snprintf(g_err, sizeof(g_err), "%s: %s%s%s", where, cudaGetErrorString(e), detail ? " / " : "",
+                detail ? detail : "");
+  return ARC_ERR_CUDA;
+}
+
+int num_sms() {
+  static int cache[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return 148;
+  if (cache[dev] == 0) {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    cache[dev] = n > 0 ? n : 148;
+  }
+  return cache[dev];
+}
+
+static bool device_ok() {
+  static int cache[64] = {0};  // 0 unknown, 1 ok, 2 not ok
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return false;
+  if (cache[dev] == 0) {
+    int major = 0, minor = 0;
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+    cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+    cache[dev] = (major == 10 && minor == 0) ? 1 : 2;
+  }
+  return cache[dev] == 1;
+}
+
+static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+static arc_status_t check_ks(int64_t K, int64_t S) {
+  if (K <= 0 || K % 16 || K > 65535) return fail(ARC_ERR_SHAPE, "K must be a positive multiple of 16 (<= 65535)");
+  if (S < 0 || S % 16 || S > K) return fail(ARC_ERR_SHAPE, "S must be a multiple of 16 with 0 <= S <= K");
+  return ARC_OK;
+}
+
+static arc_status_t check_device() {
+  if (!device_ok()) return fail(ARC_ERR_UNSUPPORTED, "current CUDA device is not sm_100 (B200); no fallback");
+  return ARC_OK;
+}
+
+static arc_status_t check_profile(const arc_profile_t* prof) {
+  if (!prof || !prof->perm || !prof->gs) return fail(ARC_ERR_NULL, "null profile / perm / gs");
+  arc_status_t s = check_ks(prof->K, prof->S);
+  if (s != ARC_OK) return s;
+  if (prof->layout != ARC_LAYOUT_INTERLEAVED && prof->layout != ARC_LAYOUT_CONTIGUOUS)
+    return fail(ARC_ERR_SHAPE, "bad layout");
+  return ARC_OK;
+}
+
+static arc_status_t check_qweight(const arc_qweight_t* qw) {
+  if (!qw || !qw->codes || !qw->sf || !qw->gs) return fail(ARC_ERR_NULL, "null qweight / codes / sf / gs");
+  arc_status_t s = check_ks(qw->K, qw->S);
+  if (s != ARC_OK) return s;
+  if (qw->N <= 0 || qw->N > (1 << 30)) return fail(ARC_ERR_SHAPE, "N must be positive");
+  if (qw->Kp != kp_of(qw->K, qw->S)) return fail(ARC_ERR_SHAPE, "qweight Kp != roundup(K+S, 64)");
+  if (qw->layout != ARC_LAYOUT_INTERLEAVED && qw->layout != ARC_LAYOUT_CONTIGUOUS)
+    return fail(ARC_ERR_SHAPE, "bad layout");
+  if (!aligned16(qw->codes) || !aligned16(qw->sf)) return fail(ARC_ERR_ALIGN, "qweight buffers not 16B aligned");
+  return ARC_OK;
+}
+
+}  // namespace arc
+
+using namespace arc;
+
+extern "C" {
+
+const char* arc_status_string(arc_status_t s) {
+  switch (s) {
+    case ARC_OK: return "ARC_OK";
+    case ARC_ERR_NULL: return "ARC_ERR_NULL";
+    case ARC_ERR_SHAPE: return "ARC_ERR_SHAPE";
+    case ARC_ERR_ALIGN: return "ARC_ERR_ALIGN";
+    case ARC_ERR_UNSUPPORTED: return "ARC_ERR_UNSUPPORTED";
+    case ARC_ERR_WORKSPACE: return "ARC_ERR_WORKSPACE";
+    case ARC_ERR_CUDA: return "ARC_ERR_CUDA";
+    case ARC_ERR_NONFINITE: return "ARC_ERR_NONFINITE";
+  }
+  return "ARC_ERR_?";
+}
+
+const char* arc_last_error(void) { return g_err; }
+
+int arc_device_supported(void) { return device_ok() ? 1 : 0; }
+
+arc_status_t arc_buffer_sizes(int64_t rows, int64_t K, int32_t S, int64_t* Kp, size_t* code_bytes, size_t* sf_bytes) {
+  arc_status_t s = check_ks(K, S);
+  if (s != ARC_OK) return s;
+  if (rows < 0) return fail(ARC_ERR_SHAPE, "rows < 0");
+  const int64_t kp = kp_of(K, S);
+  if (Kp) *Kp = kp;
+  if (code_bytes) *code_bytes = (size_t)(rows * (kp / 2));
+  if (sf_bytes) *sf_bytes = (size_t)(round_up(rows, 128) * (kp / 16));
+  return ARC_OK;
+}
+
+arc_status_t arc_workspace_size(int64_t M, int64_t K, int32_t S, size_t* bytes) {
+  size_t cb = 0, sb = 0;
+  arc_status_t s = arc_buffer_sizes(M, K, S, nullptr, &cb, &sb);
+  if (s != ARC_OK) return s;
+  if (!bytes) return fail(ARC_ERR_NULL, "null bytes");
+  *bytes = (size_t)round_up((int64_t)cb, 256) + (size_t)round_up((int64_t)sb, 256);
+  return ARC_OK;
+}
+
+arc_status_t arc_calib_absmax(const void* x, int64_t rows, int64_t K, int64_t ldx, float* chan_max, void* stream) {
+  if (!x || !chan_max) return fail(ARC_ERR_NULL, "null x / chan_max");
+  if (K <= 0 || K % 16 || rows < 0 || ldx < K || ldx % 8) return fail(ARC_ERR_SHAPE, "bad rows/K/ldx");
+  if (!aligned16(x)) return fail(ARC_ERR_ALIGN, "x not 16B aligned");
+  arc_status_t s = check_device();
+  if (s != ARC_OK) return s;
+  if (rows == 0) return ARC_OK;
+  cudaError_t e = launch_calib_absmax(x, rows, (int)K, ldx, chan_max, (cudaStream_t)stream);
+  return e == cudaSuccess ? ARC_OK : cuda_fail(e, "arc_calib_absmax");
+}
+
+arc_status_t arc_select_outliers(const float* chan_max_host, int64_t K, int32_t s_override, int32_t* perm_host,
+                                 int32_t* S, int32_t* S_raw, float* M, float* tau, float* gs) {
+  if (!chan_max_host || !perm_host || !S || !S_raw || !M || !tau || !gs) return fail(ARC_ERR_NULL, "null argument");
+  if (K <= 0 || K % 16) return fail(ARC_ERR_SHAPE, "K must be a positive multiple of 16");
+  if (s_override > K || (s_override >= 0 && s_override % 16)) return fail(ARC_ERR_SHAPE, "bad s_override");
+  float mx = 0.0f;
+  for (int64_t j = 0; j < K; ++j) {
+    const float v = chan_max_host[j];
+    if (!(v >= 0.0f) || v > 3.4028234663852886e38f) return fail(ARC_ERR_NONFINITE, "non-finite or negative chan_max");
+    mx = std::max(mx, v);
+  }
+  std::vector<int32_t> idx((size_t)K);
+  for (int64_t j = 0; j < K; ++j) idx[(size_t)j] = (int32_t)j;
+  // descending abs-max, ties to the lower channel index (reading Q9): a total order.
+  std::stable_sort(idx.begin(), idx.end(),
+                   [&](int32_t a, int32_t b) { return chan_max_host[a] > chan_max_host[b]; });
+  std::memcpy(perm_host, idx.data(), sizeof(int32_t) * (size_t)K);
+  const float t = mx * 0.125f;  // tau = 2^-3 M, exact
+  int64_t sr = 0;
+  for (int64_t j = 0; j < K; ++j) sr += chan_max_host[j] > t;
+  const int64_t sa = std::min<int64_t>(K, (sr + 15) / 16 * 16);
+  *S_raw = (int32_t)sr;
+  *S = s_override >= 0 ? s_override : (int32_t)sa;
+  *M = mx;
+  *tau = t;
+  volatile float num = 2688.0f;  // one IEEE fp32 division
+  *gs = mx > 0.0f ? num / mx : 1.0f;
+  return ARC_OK;
+}
+
+arc_status_t arc_tensor_scale(const void* x, int64_t rows, int64_t K, int64_t ldx, float* gs_out, void* stream) {
+  if (!x || !gs_out) return fail(ARC_ERR_NULL, "null x / gs_out");
+  if (K <= 0 || K % 16 || rows < 0 || ldx < K || ldx % 8) return fail(ARC_ERR_SHAPE, "bad rows/K/ldx");
+  if (!aligned16(x)) return fail(ARC_ERR_ALIGN, "x not 16B aligned");
+  arc_status_t s = check_device();
+  if (s != ARC_OK) return s;
+  cudaError_t e = launch_tensor_scale(x, rows, (int)K, ldx, gs_out, (cudaStream_t)stream);
+  return e == cudaSuccess ? ARC_OK : cuda_fail(e, "arc_tensor_scale");
+}
+
+arc_status_t arc_quantize_weight(const void* w, int64_t N, int64_t K, int64_t ldw, const int32_t* perm, int32_t S,
+                                 const float* gs_w, arc_layout_t layout, uint8_t* codes, uint8_t* sf, void* stream) {
+  if (!w || !perm || !gs_w || !codes || !sf) return fail(ARC_ERR_NULL, "null argument");
+  arc_status_t s = check_ks(K, S);
+  if (s != ARC_OK) return s;
+  if (N < 0 || ldw < K || ldw % 8) return fail(ARC_ERR_SHAPE, "bad N/ldw");
+  if (layout != ARC_LAYOUT_INTERLEAVED && layout != ARC_LAYOUT_CONTIGUOUS) return fail(ARC_ERR_SHAPE, "bad layout");
+  if (!aligned16(w) || !aligned16(codes) || !aligned16(sf)) return fail(ARC_ERR_ALIGN, "buffer not 16B aligned");
+  s = check_device();
+  if (s != ARC_OK) return s;
+  if (N == 0) return ARC_OK;
+  cudaError_t e = launch_quant(w, N, (int)K, ldw, perm, S, gs_w, (int)layout, 1, codes, sf, (cudaStream_t)stream);
+  return e == cudaSuccess ? ARC_OK : cuda_fail(e, "arc_quantize_weight");
+}
+
+arc_status_t arc_quantize_activation(const void* x, int64_t M, int64_t ldx, const arc_profile_t* prof,
+                                     uint8_t* codes, uint8_t* sf, void* stream) {
+  arc_status_t s = check_profile(prof);
+  if (s != ARC_OK) return s;
+  if (M < 0 || ldx < prof->K || ldx % 8) return fail(ARC_ERR_SHAPE, "bad M/ldx");
+  if (M == 0) return ARC_OK;
+  if (!x || !codes || !sf) return fail(ARC_ERR_NULL, "null x / codes / sf");
+  if (!aligned16(x) || !aligned16(codes) || !aligned16(sf)) return fail(ARC_ERR_ALIGN, "buffer not 16B aligned");
+  s = check_device();
+  if (s != ARC_OK) return s;
+  if (M == 0) return ARC_OK;
+  cudaError_t e = launch_quant(x, M, (int)prof->K, ldx, prof->perm, prof->S, prof->gs, (int)prof->layout, 0, codes,
+                               sf, (cudaStream_t)stream);
+  return e == cudaSuccess ? ARC_OK : cuda_fail(e, "arc_quantize_activation");
+}
+
+arc_status_t arc_gemm(const uint8_t* a_codes, const uint8_t* a_sf, const float* gs_x, int64_t M,
+                      const arc_qweight_t* qw, void* y, arc_dtype_t y_dtype, int64_t ldy, void* stream) {
+  arc_status_t s = check_qweight(qw);
+  if (s != ARC_OK) return s;
+  if (M < 0 || M > (1 << 30)) return fail(ARC_ERR_SHAPE, "bad M");
+  if (M == 0) return ARC_OK;
+  if (!a_codes || !a_sf || !gs_x || !y) return fail(ARC_ERR_NULL, "null a_codes / a_sf / gs_x / y");
+  if (y_dtype != ARC_BF16 && y_dtype != ARC_FP32) return fail(ARC_ERR_SHAPE, "y_dtype must be ARC_BF16 or ARC_FP32");
+  if (ldy < qw->N || ldy % (y_dtype == ARC_FP32 ? 4 : 8))
+    return fail(ARC_ERR_SHAPE, "ldy must be >= N and a multiple of 16 bytes");
+  if (!aligned16(a_codes) || !aligned16(a_sf) || !aligned16(y)) return fail(ARC_ERR_ALIGN, "buffer not 16B aligned");
+  s = check_device();
+  if (s != ARC_OK) return s;
+  if (M == 0) return ARC_OK;
+  GemmProblem p;
+  p.M = M;
+  p.N = qw->N;
+  p.Kp = qw->Kp;
+  p.a_codes = a_codes;
+  p.a_sf = a_sf;
+  p.b_codes = qw->codes;
+  p.b_sf = qw->sf;
+  p.gs_x = gs_x;
+  p.gs_w = qw->gs;
+  p.y = y;
+  p.ldy = ldy;
+  p.y_fp32 = y_dtype == ARC_FP32;
+  const char* detail = nullptr;
+  cudaError_t e = launch_gemm(p, (cudaStream_t)stream, &detail);
+  return e == cudaSuccess ? ARC_OK : cuda_fail(e, "arc_gemm", detail);
+}
+
+arc_status_t arc_linear(const void* x, int64_t M, int64_t ldx, const arc_profile_t* prof, const arc_qweight_t* qw,
+                        void* y, arc_dtype_t y_dtype, int64_t ldy, void* ws, size_t ws_bytes, void* stream) {
+  arc_status_t s = check_profile(prof);
+  if (s != ARC_OK) return s;
+  s = check_qweight(qw);
+  if (s != ARC_OK) return s;
+  if (qw->K != prof->K || qw->S != prof->S || qw->layout != prof->layout)
+    return fail(ARC_ERR_SHAPE, "profile and qweight disagree on K / S / layout");
+  if (M < 0) return fail(ARC_ERR_SHAPE, "M < 0");
+  if (M == 0) return ARC_OK;
+  if (!ws) return fail(ARC_ERR_NULL, "null workspace");
+  size_t need = 0;
+  arc_workspace_size(M, prof->K, prof->S, &need);
+  if (ws_bytes < need) return fail(ARC_ERR_WORKSPACE, "workspace too small");
+  if ((reinterpret_cast<uintptr_t>(ws) & 255u) != 0) return fail(ARC_ERR_ALIGN, "workspace not 256B aligned");
+  uint8_t* codes = static_cast<uint8_t*>(ws);
+  uint8_t* sf = codes + round_up(M * (qw->Kp / 2), 256);
+  s = arc_quantize_activation(x, M, ldx, prof, codes, sf, stream);
+  if (s != ARC_OK) return s;
+  return arc_gemm(codes, sf, prof->gs, M, qw, y, y_dtype, ldy, stream);
+}
+
+arc_status_t arc_linear_hostio_workspace_size(int64_t M, int64_t K, int32_t S, int64_t N, arc_dtype_t y_dtype,
+                                              size_t* bytes) {
+  size_t w = 0;
+  arc_status_t s = arc_workspace_size(M, K, S, &w);
+  if (s != ARC_OK) return s;
+  const int64_t yb = M * N * (y_dtype == ARC_FP32 ? 4 : 2);
+  *bytes = w + (size_t)round_up(M * K * 2, 256) + (size_t)round_up(yb, 256);
+  return ARC_OK;
+}
+
+arc_status_t arc_linear_hostio(const void* x_host, int64_t M, const arc_profile_t* prof, const arc_qweight_t* qw,
+                               void* y_host, arc_dtype_t y_dtype, void* ws, size_t ws_bytes, void* stream) {
+  if (!x_host || !y_host || !ws) return fail(ARC_ERR_NULL, "null x_host / y_host / ws");
+  arc_status_t s = check_profile(prof);
+  if (s != ARC_OK) return s;
+  s = check_qweight(qw);
+  if (s != ARC_OK) return s;
+  size_t need = 0;
+  s = arc_linear_hostio_workspace_size(M, prof->K, prof->S, qw->N, y_dtype, &need);
+  if (s != ARC_OK) return s;
+  if (ws_bytes < need) return fail(ARC_ERR_WORKSPACE, "workspace too small");
+  if (M == 0) return ARC_OK;
+  size_t lin = 0;
+  arc_workspace_size(M, prof->K, prof->S, &lin);
+  uint8_t* base = static_cast<uint8_t*>(ws);
+  void* xd = base + lin;
+  void* yd = base + lin + round_up(M * prof->K * 2, 256);
+  const size_t xb = (size_t)(M * prof->K * 2);
+  const size_t yb = (size_t)(M * qw->N * (y_dtype == ARC_FP32 ? 4 : 2));
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e = cudaMemcpyAsync(xd, x_host, xb, cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) return cuda_fail(e, "arc_linear_hostio H2D");
+  s = arc_linear(xd, M, prof->K, prof, qw, yd, y_dtype, qw->N, base, lin, stream);
+  if (s != ARC_OK) return s;
+  e = cudaMemcpyAsync(y_host, yd, yb, cudaMemcpyDeviceToHost, st);
+  if (e != cudaSuccess) return cuda_fail(e, "arc_linear_hostio D2H");
+  e = cudaStreamSynchronize(st);
+  return e == cudaSuccess ? ARC_OK : cuda_fail(e, "arc_linear_hostio sync");
+}
+
+}  // extern "C"

@@ -1,0 +1,34 @@
+// arc_internal.h -- host-side declarations shared by the libarc.so translation units.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace arc {
+
+inline int64_t kp_of(int64_t K, int64_t S) { return (K + S + 63) / 64 * 64; }
+inline int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
+
+int num_sms();  // SM count of the current device (cached per device)
+
+cudaError_t launch_quant(const void* x, int64_t rows, int K, int64_t ld, const int32_t* perm, int S, const float* gs,
+                         int layout, int weight_mode, uint8_t* codes, uint8_t* sf, cudaStream_t stream);
+cudaError_t launch_calib_absmax(const void* x, int64_t rows, int K, int64_t ld, float* chan_max, cudaStream_t s);
+cudaError_t launch_tensor_scale(const void* x, int64_t rows, int K, int64_t ld, float* gs_out, cudaStream_t s);
+
+struct GemmProblem {
+  int64_t M, N, Kp;
+  const uint8_t* a_codes;
+  const uint8_t* a_sf;
+  const uint8_t* b_codes;
+  const uint8_t* b_sf;
+  const float* gs_x;
+  const float* gs_w;
+  void* y;
+  int64_t ldy;
+  int y_fp32;
+};
+// Returns a CUresult-style error through cudaError_t (cudaErrorUnknown + text) on encode failure.
+cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t stream, const char** detail);
+
+}  // namespace arc

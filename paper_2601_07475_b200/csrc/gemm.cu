@@ -1,0 +1,292 @@
+// gemm.cu -- the augmented NVFP4 block-scaled GEMM on sm_100a tensor cores.
+//
+// Y[m,n] = alpha * sum_{p < Kp} e2m1(A[m,p]) e4m3(SFA[m,p/16]) e2m1(B[n,p]) e4m3(SFB[n,p/16]),
+// alpha = 1/(gs_x*gs_w): Eq.2, the GEMM over the extended
+// reduction dimension K+S whose FP32 accumulator sums the primary products and
+// the residual corrections.
+//
+// Kernel: persistent, warp-specialized, one CTA per SM (smem-limited), 192
+// threads.
+//   warp 0 (one lane): producer.  Per K-block of 256 elements: TMA 2D loads of
+//     the A tile (128 rows x 128 B) and the B tile (256 rows x 128 B), both
+//     128B-swizzled, plus cp.async.bulk of the matching scale-factor chunks
+//     (512 B per 128 rows x 64 K, already in the tcgen05 128x4 layout in
+//     global memory, so one contiguous 2 KB copy per 128 rows), all completing
+//     on the stage's mbarrier.  4-stage ring.
+//   warp 1 (one lane): MMA issuer.  tcgen05.cp moves the stage's scales
+//     smem -> TMEM (32x128b.warpx4), then 4 x tcgen05.mma.kind::mxf4nvf4
+//     .block_scale.scale_vec::4X (M=128, N=256, K=64) accumulate into TMEM;
+//     tcgen05.commit releases the smem stage and, after the last K-block,
+//     signals the epilogue.
+//   warps 2-5: epilogue.  tcgen05.ld 32x32b.x32 (each warp owns its TMEM lane
+//     quadrant = 32 output rows), scale by alpha, convert, store.
+// TMEM: 512 columns = accumulator 256 + SFA 16 + SFB 32 (single accumulator;
+// the epilogue frees it right after its last tcgen05.ld, before its stores).
+#include "arc_device.cuh"
+#include "arc_internal.h"
+
+#include <cuda.h>
+#include <mutex>
+
+namespace arc {
+namespace {
+
+constexpr int BM = 128;
+constexpr int BN = 256;
+constexpr int BK = 256;           // K elements per stage
+constexpr int BKB = BK / 2;       // bytes per row per stage (one 128B swizzle atom)
+constexpr int STAGES = 4;
+constexpr int A_BYTES = BM * BKB;                // 16 KB
+constexpr int B_BYTES = BN * BKB;                // 32 KB
+constexpr int SFA_BYTES = (BM / 128) * 4 * 512;  // 2 KB
+constexpr int SFB_BYTES = (BN / 128) * 4 * 512;  // 4 KB
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES + SFA_BYTES + SFB_BYTES;  // 54 KB (multiple of 1024)
+constexpr int TMEM_COLS = 512;
+constexpr int ACC_COL = 0;
+constexpr int SFA_COL = 256;
+constexpr int SFB_COL = 256 + 16;
+constexpr int NUM_THREADS = 192;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align slack*/ + 256 /*barriers*/;
+
+struct Args {
+  int M, N, Kp;
+  const uint8_t* sfa;
+  const uint8_t* sfb;
+  const float* gs_x;
+  const float* gs_w;
+  void* y;
+  int64_t ldy;
+  int y_fp32;
+};
+
+// instruction descriptor: E2M1 x E2M1 (format 1), UE4M3 scales, K-major A/B,
+// N>>3 at [17,23), M>>4 at [24,29).
+constexpr uint32_t kIdesc = (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    arc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, Args args) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 1);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int M = args.M, N = args.N, Kp = args.Kp;
+  const int num_m = (M + BM - 1) / BM;
+  const int num_n = (N + BN - 1) / BN;
+  const int num_tiles = num_m * num_n;
+  const int nkb = (Kp + BK - 1) / BK;
+  const int kc_total = Kp / 64;            // 64-element scale chunks per row block
+  const int n_rb = (N + 127) / 128;        // 128-row blocks of the B scale buffer
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tfull, 1);
+    mbar_init(tempty, 128);
+    fence_mbar_init();
+    prefetch_tmap(&tmA);
+    prefetch_tmap(&tmB);
+  }
+  if (warp == 1) tmem_alloc(tmem_holder, TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_holder;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      // ---------------------------------------------------------------- producer
+      const uint64_t pol = policy_evict_last();
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const int mb = tile % num_m, nbk = tile / num_m;
+        const int nrb = min(2, n_rb - 2 * nbk);
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          const int nk = min(4, kc_total - kb * 4);
+          uint8_t* sA = smem + stage * STAGE_BYTES;
+          uint8_t* sB = sA + A_BYTES;
+          uint8_t* sSFA = sB + B_BYTES;
+          uint8_t* sSFB = sSFA + SFA_BYTES;
+          mbar_expect_tx(&full[stage], (uint32_t)(A_BYTES + B_BYTES + nk * 512 * (1 + nrb)));
+          tma_load_2d(sA, &tmA, &full[stage], kb * BKB, mb * BM, pol);
+          tma_load_2d(sB, &tmB, &full[stage], kb * BKB, nbk * BN, pol);
+          bulk_load(sSFA, args.sfa + ((int64_t)mb * kc_total + kb * 4) * 512, nk * 512, &full[stage]);
+          for (int rb = 0; rb < nrb; ++rb)
+            bulk_load(sSFB + rb * 2048, args.sfb + ((int64_t)(2 * nbk + rb) * kc_total + kb * 4) * 512, nk * 512,
+                      &full[stage]);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (elect_one()) {
+      // ---------------------------------------------------------------- MMA issuer
+      int stage = 0;
+      uint32_t phase = 0;
+      int t = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++t) {
+        if (t > 0) mbar_wait(tempty, (t - 1) & 1);  // epilogue drained the accumulator
+        tc_fence_after();
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const int nk = min(4, kc_total - kb * 4);
+          const uint32_t sA = smem_u32(smem + stage * STAGE_BYTES);
+          const uint32_t sB = sA + A_BYTES;
+          const uint32_t sSFA = sB + B_BYTES;
+          const uint32_t sSFB = sSFA + SFA_BYTES;
+          for (int kk = 0; kk < nk; ++kk) {
+            utccp_32x128b_warpx4(tmem + SFA_COL + 4 * kk, smem_desc(sSFA + kk * 512, 0, 128, kLayoutSwizzleNone));
+            utccp_32x128b_warpx4(tmem + SFB_COL + 8 * kk, smem_desc(sSFB + kk * 512, 0, 128, kLayoutSwizzleNone));
+            utccp_32x128b_warpx4(tmem + SFB_COL + 8 * kk + 4,
+                                 smem_desc(sSFB + 2048 + kk * 512, 0, 128, kLayoutSwizzleNone));
+          }
+          for (int kk = 0; kk < nk; ++kk) {
+            const uint64_t ad = smem_desc(sA + kk * 32, 16, 1024, kLayoutSwizzle128B);
+            const uint64_t bd = smem_desc(sB + kk * 32, 16, 1024, kLayoutSwizzle128B);
+            mma_nvf4(tmem + ACC_COL, ad, bd, kIdesc, (kb | kk) != 0, tmem + SFA_COL + 4 * kk, tmem + SFB_COL + 8 * kk);
+          }
+          tc_commit(&empty[stage]);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        tc_commit(tfull);
+      }
+    }
+  } else {
+    // ---------------------------------------------------------------- epilogue (warps 2..5)
+    const int q = warp & 3;  // TMEM lane quadrant this warp may access
+    const float alpha = __fdiv_rn(1.0f, __fmul_rn(__ldg(args.gs_x), __ldg(args.gs_w)));
+    int t = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++t) {
+      const int mb = tile % num_m, nbk = tile / num_m;
+      mbar_wait(tfull, t & 1);
+      tc_fence_after();
+      const int m = mb * BM + q * 32 + lane;
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(tmem + ((uint32_t)(q * 32) << 16) + ACC_COL + c * 32, r);
+        tmem_ld_wait();
+        if (c == BN / 32 - 1) {
+          tc_fence_before();
+          mbar_arrive(tempty);
+        }
+        const int n0 = nbk * BN + c * 32;
+        if (m < M && n0 < N) {
+          if (args.y_fp32) {
+            float* yr = static_cast<float*>(args.y) + (int64_t)m * args.ldy + n0;
+            if (n0 + 32 <= N) {
+#pragma unroll
+              for (int j = 0; j < 32; j += 4)
+                *reinterpret_cast<float4*>(yr + j) =
+                    make_float4(__fmul_rn(__uint_as_float(r[j]), alpha), __fmul_rn(__uint_as_float(r[j + 1]), alpha),
+                                __fmul_rn(__uint_as_float(r[j + 2]), alpha), __fmul_rn(__uint_as_float(r[j + 3]), alpha));
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (n0 + j < N) yr[j] = __fmul_rn(__uint_as_float(r[j]), alpha);
+            }
+          } else {
+            __nv_bfloat16* yr = static_cast<__nv_bfloat16*>(args.y) + (int64_t)m * args.ldy + n0;
+            if (n0 + 32 <= N) {
+#pragma unroll
+              for (int j = 0; j < 32; j += 8) {
+                uint4 v;
+                uint32_t* pv = reinterpret_cast<uint32_t*>(&v);
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                  __nv_bfloat162 b2 = __floats2bfloat162_rn(__fmul_rn(__uint_as_float(r[j + 2 * h]), alpha),
+                                                            __fmul_rn(__uint_as_float(r[j + 2 * h + 1]), alpha));
+                  pv[h] = *reinterpret_cast<uint32_t*>(&b2);
+                }
+                *reinterpret_cast<uint4*>(yr + j) = v;
+              }
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (n0 + j < N) yr[j] = __float2bfloat16_rn(__fmul_rn(__uint_as_float(r[j]), alpha));
+            }
+          }
+        }
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, TMEM_COLS);
+  }
+}
+
+// ------------------------------------------------------------------ host side
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+bool make_map(CUtensorMap* m, const uint8_t* base, int64_t rows, int64_t row_bytes, int box_rows) {
+  EncodeTiledFn enc = get_encode_fn();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)row_bytes, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)row_bytes};
+  cuuint32_t box[2] = {(cuuint32_t)BKB, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t stream, const char** detail) {
+  CUtensorMap tmA, tmB;
+  if (!make_map(&tmA, p.a_codes, p.M, p.Kp / 2, BM) || !make_map(&tmB, p.b_codes, p.N, p.Kp / 2, BN)) {
+    if (detail) *detail = "cuTensorMapEncodeTiled failed";
+    return cudaErrorInvalidValue;
+  }
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [] {
+    attr_err = cudaFuncSetAttribute(arc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+  });
+  if (attr_err != cudaSuccess) return attr_err;
+  Args a;
+  a.M = (int)p.M;
+  a.N = (int)p.N;
+  a.Kp = (int)p.Kp;
+  a.sfa = p.a_sf;
+  a.sfb = p.b_sf;
+  a.gs_x = p.gs_x;
+  a.gs_w = p.gs_w;
+  a.y = p.y;
+  a.ldy = p.ldy;
+  a.y_fp32 = p.y_fp32;
+  const int64_t tiles = ((p.M + BM - 1) / BM) * ((p.N + BN - 1) / BN);
+  const int grid = (int)std::min<int64_t>(tiles, num_sms());
+  arc_gemm_kernel<<<grid, NUM_THREADS, SMEM_BYTES, stream>>>(tmA, tmB, a);
+  return cudaGetLastError();
+}
+
+}  // namespace arc

@@ -1,0 +1,127 @@
+"""GPU parity of the augmented NVFP4 GEMM (tcgen05.mma kind::mxf4nvf4) against the
+oracle's exact integer GEMM: |y - y_ref| <= 1e-5 * sum|a_i b_i| per element
+(BASELINE.json north_star tolerance; fp32 accumulation order), plus one bf16 ulp
+for bf16 output.  PAPER.md Eq.2."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2601_07475_b200 import synth
+from _helpers import dev_bits
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def A():
+    from paper_2601_07475_b200 import arc
+    assert arc.device_supported()
+    return arc
+
+
+def _problem(A, M, N, K, S, layout=0, seed=0, S_inj=None):
+    st = synth.Structure(K, S if S_inj is None else S_inj, seed=seed)
+    x = synth.activation(M, K, st, seed=seed + 1, device="cuda")
+    w = synth.weight(N, K, seed=seed + 2, device="cuda")
+    cal = synth.activation(max(M, 256), K, st, seed=seed + 1000, device="cuda")
+    prof = A.calibrate([cal], s_override=S, layout=layout)
+    qw = A.quantize_weight(w, prof)
+    return x, w, prof, qw
+
+
+def _check(y, yref, bound, bf16):
+    tol = bound.copy()
+    if bf16:
+        tol += np.abs(yref) * 2.0 ** -8
+    err = np.abs(y - yref)
+    bad = err > tol
+    assert not bad.any(), f"{bad.sum()} elements out of tolerance; worst err/tol {np.max(err / np.maximum(tol, 1e-300))}"
+
+
+@pytest.mark.parametrize("M,N,K,S", [(16, 256, 256, 16), (1, 256, 256, 16), (128, 256, 256, 0), (200, 300, 512, 64),
+                                     (129, 520, 1024, 128), (64, 64, 112, 48), (257, 1024, 4096, 128)])
+@pytest.mark.parametrize("layout", [0, 1])
+def test_gemm_parity_fp32(A, M, N, K, S, layout):
+    x, w, prof, qw = _problem(A, M, N, K, S, layout, seed=M + N)
+    codes, sf = A.quantize_activation(x, prof)
+    y = A.gemm(codes, sf, prof.gs, qw, out_dtype=torch.float32)
+    torch.cuda.synchronize()
+    yref, bound = oracle.gemm_reference(codes.cpu().numpy(), sf.cpu().numpy(), qw.codes.cpu().numpy(),
+                                        qw.sf.cpu().numpy(), float(prof.gs.item()), float(qw.gs.item()))
+    _check(y.cpu().numpy().astype(np.float64), yref, bound, False)
+
+
+def test_linear_bf16_cfg1(A):
+    """Config 1 (M=16, K=256, N=256, S=16) end to end through arc_linear, bf16 out;
+    the oracle recomputes quantization AND the GEMM from the raw inputs."""
+    M, N, K, S = 16, 256, 256, 16
+    x, w, prof, qw = _problem(A, M, N, K, S)
+    y = A.linear(x, prof, qw, out_dtype=torch.bfloat16)
+    torch.cuda.synchronize()
+    perm, gs, gs_w = prof.perm.cpu().numpy(), float(prof.gs.item()), float(qw.gs.item())
+    ac, asf = oracle.quantize_activation(dev_bits(x), perm, S, gs)
+    bc, bsf = oracle.quantize_weight(dev_bits(w), perm, S, gs_w)
+    yref, bound = oracle.gemm_reference(ac, asf, bc, bsf, gs, gs_w)
+    _check(y.float().cpu().numpy().astype(np.float64), yref, bound, True)
+
+
+def test_same_sign_accumulation(A):
+    """Same-sign data at K+S = 14464 stresses the fp32 accumulation (SURVEY hard part 8)."""
+    M, N, K, S = 128, 256, 14336, 128
+    x = (synth.activation(M, K, synth.Structure(K, S, 0), seed=3, device="cuda").float().abs()).to(torch.bfloat16)
+    w = (synth.weight(N, K, seed=4, device="cuda").float().abs()).to(torch.bfloat16)
+    prof = A.calibrate([x], s_override=S)
+    qw = A.quantize_weight(w, prof)
+    codes, sf = A.quantize_activation(x, prof)
+    y = A.gemm(codes, sf, prof.gs, qw, out_dtype=torch.float32)
+    torch.cuda.synchronize()
+    yref, bound = oracle.gemm_reference(codes.cpu().numpy(), sf.cpu().numpy(), qw.codes.cpu().numpy(),
+                                        qw.sf.cpu().numpy(), float(prof.gs.item()), float(qw.gs.item()))
+    _check(y.cpu().numpy().astype(np.float64), yref, bound, False)
+
+
+def test_full_size_sampled_rows(A):
+    """BASELINE config-2 prefill size (M=8192, gate-up N=28672? -> qkv N=6144, K=4096,
+    S=128) in the bench's launch configuration; the oracle's exact GEMM on sampled rows."""
+    M, N, K, S = 8192, 6144, 4096, 128
+    x, w, prof, qw = _problem(A, M, N, K, S, seed=7)
+    y = A.linear(x, prof, qw, out_dtype=torch.bfloat16)
+    codes, sf = A.quantize_activation(x, prof)
+    torch.cuda.synchronize()
+    rows = np.array([0, 1, 127, 128, 1000, 4097, 8000, 8191], np.int64)
+    yref, bound = oracle.gemm_reference(codes.cpu().numpy(), sf.cpu().numpy(), qw.codes.cpu().numpy(),
+                                        qw.sf.cpu().numpy(), float(prof.gs.item()), float(qw.gs.item()), rows=rows)
+    _check(y[torch.from_numpy(rows).cuda()].float().cpu().numpy().astype(np.float64), yref, bound, True)
+
+
+def test_hostio_matches_device_path(A):
+    M, N, K, S = 100, 512, 1024, 64
+    x, w, prof, qw = _problem(A, M, N, K, S, seed=9)
+    y_dev = A.linear(x, prof, qw, out_dtype=torch.bfloat16)
+    xh = x.cpu().pin_memory()
+    yh = torch.empty(M, N, dtype=torch.bfloat16).pin_memory()
+    ws = torch.empty(A.linear_hostio_workspace_size(M, K, S, N), dtype=torch.uint8, device="cuda")
+    A.linear_hostio(xh, prof, qw, yh, ws)
+    assert torch.equal(yh, y_dev.cpu())
+
+
+def test_cublaslt_cross_check(A):
+    """Third-party check of the operand conventions (nibble order, 128x4 scale
+    layout): cuBLASLt's NVFP4 GEMM via torch._scaled_mm on our packed operands."""
+    if not hasattr(torch, "float4_e2m1fn_x2"):
+        pytest.skip("no fp4 dtype")
+    M, N, K, S = 256, 512, 1024, 64
+    x, w, prof, qw = _problem(A, M, N, K, S, seed=5)
+    codes, sf = A.quantize_activation(x, prof)
+    y = A.gemm(codes, sf, prof.gs, qw, out_dtype=torch.float32)
+    a = codes.view(torch.float4_e2m1fn_x2)
+    b = qw.codes.view(torch.float4_e2m1fn_x2)
+    try:
+        ref = torch._scaled_mm(a, b.t(), scale_a=sf.view(torch.float8_e4m3fn), scale_b=qw.sf.view(torch.float8_e4m3fn),
+                               out_dtype=torch.float32)
+    except Exception as e:  # cuBLASLt build without NVFP4 support
+        pytest.skip(f"torch._scaled_mm NVFP4 unavailable: {e}")
+    ref = ref / (prof.gs * qw.gs)
+    torch.cuda.synchronize()
+    assert torch.allclose(y, ref, rtol=1e-4, atol=1e-3 * float(ref.abs().max()))
