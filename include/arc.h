@@ -13,7 +13,7 @@
  * the augmented GEMM (arc_gemm / arc_linear).
  *
  * Notation: M = tokens, K = input features, N = output features,
- * S = augmented (outlier) channels, a multiple of 16 with 0 <= S <= K.
+ * S = augmented (outlier) channels, a multiple of 16 with 0 <= S <= K; K + S <= 32768.
  * Ka = K+S; Kp = roundup(Ka, 64) is the physical reduction length.
  *
  * Data formats (all produced and consumed by this library):
@@ -40,7 +40,7 @@
  *    NULL = legacy default stream) and is asynchronous.
  *  - Argument checks are synchronous and happen before anything is enqueued:
  *    ARC_ERR_NULL (null pointer), ARC_ERR_SHAPE (K <= 0, K%16, S%16, S < 0,
- *    S > K, M < 0, N <= 0, leading dimension < K or not a multiple of 8
+ *    S > K, K + S > 32768, M < 0, N <= 0, leading dimension < K or not a multiple of 8
  *    elements, profile / qweight mismatch), ARC_ERR_ALIGN (a base pointer not
  *    16-byte aligned), ARC_ERR_WORKSPACE (workspace too small),
  *    ARC_ERR_UNSUPPORTED (the current device is not sm_100; there is no
@@ -132,6 +132,15 @@ ARC_API arc_status_t arc_calib_absmax(const void* x, int64_t rows, int64_t K, in
 ARC_API arc_status_t arc_select_outliers(const float* chan_max_host, int64_t K, int32_t s_override,
                                          int32_t* perm_host, int32_t* S, int32_t* S_raw, float* M, float* tau,
                                          float* gs);
+/* Host, synchronous, deterministic.  perm_out assigns every 16-channel block the
+ * same SET of channels as perm_host (so the outlier set, every block maximum and
+ * scale, the codes as a multiset and the GEMM result are unchanged; reading Q22:
+ * the channel order inside a block is free) and orders the channels inside each
+ * block so that the quantization kernel's shared-memory gathers (32 consecutive
+ * blocks per warp, one channel per lane per step) hit distinct banks as far as
+ * possible.  Use perm_out for BOTH arc_quantize_weight and the activation
+ * profile.  K must be a multiple of 16; perm_host must be a permutation. */
+ARC_API arc_status_t arc_gather_order(const int32_t* perm_host, int64_t K, int32_t* perm_out_host);
 /* gs_out[0] = 2688 / max|x| over a rows x K bf16 matrix (1.0 if the max is 0):
  * the NVFP4 encode tensor scale (reading Q3).  gs_out is a device float. */
 ARC_API arc_status_t arc_tensor_scale(const void* x, int64_t rows, int64_t K, int64_t ldx, float* gs_out,

@@ -17,6 +17,8 @@ extern "C" {
 ARC_API arc_status_t arc_probe_e2m1(const float* in, int64_t n, uint8_t* out, void* stream);
 /* Same, for the fp32 whose bit pattern is (uint32)(start_bits + i), i < n. */
 ARC_API arc_status_t arc_probe_e2m1_bits(uint32_t start_bits, int64_t n, uint8_t* out, void* stream);
+/* Raw hardware cvt.rn.satfinite.e2m1x2.f32 nibble (no sign fix-up) for bits start+i. */
+ARC_API arc_status_t arc_probe_e2m1_raw_bits(uint32_t start_bits, int64_t n, uint8_t* out, void* stream);
 /* out[i] = the kernel's ceil-rounded E4M3 scale code of in[i] >= 0 (reading Q2). */
 ARC_API arc_status_t arc_probe_e4m3_ceil(const float* in, int64_t n, uint8_t* out, void* stream);
 #ifdef __cplusplus

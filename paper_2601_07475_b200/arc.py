@@ -64,6 +64,7 @@ _sig("arc_workspace_size", [_i64, _i64, _i32, ctypes.POINTER(ctypes.c_size_t)])
 _sig("arc_calib_absmax", [_P, _i64, _i64, _i64, _P, _P])
 _sig("arc_select_outliers", [_P, _i64, _i32, _P, ctypes.POINTER(_i32), ctypes.POINTER(_i32),
                              ctypes.POINTER(_f32), ctypes.POINTER(_f32), ctypes.POINTER(_f32)])
+_sig("arc_gather_order", [_P, _i64, _P])
 _sig("arc_tensor_scale", [_P, _i64, _i64, _i64, _P, _P])
 _sig("arc_quantize_weight", [_P, _i64, _i64, _i64, _P, _i32, _P, ctypes.c_int, _P, _P, _P])
 _sig("arc_quantize_activation", [_P, _i64, _i64, ctypes.POINTER(ArcProfile), _P, _P, _P])
@@ -75,14 +76,15 @@ _sig("arc_linear_hostio", [_P, _i64, ctypes.POINTER(ArcProfile), ctypes.POINTER(
                            ctypes.c_size_t, _P])
 _sig("arc_probe_e2m1", [_P, _i64, _P, _P])
 _sig("arc_probe_e2m1_bits", [ctypes.c_uint32, _i64, _P, _P])
+_sig("arc_probe_e2m1_raw_bits", [ctypes.c_uint32, _i64, _P, _P])
 _sig("arc_probe_e4m3_ceil", [_P, _i64, _P, _P])
 
 # every symbol include/arc.h and include/arc_probe.h declare (checked by tests)
 EXPORTED = [
     "arc_status_string", "arc_last_error", "arc_device_supported", "arc_buffer_sizes", "arc_workspace_size",
-    "arc_calib_absmax", "arc_select_outliers", "arc_tensor_scale", "arc_quantize_weight",
+    "arc_calib_absmax", "arc_select_outliers", "arc_gather_order", "arc_tensor_scale", "arc_quantize_weight",
     "arc_quantize_activation", "arc_gemm", "arc_linear", "arc_linear_hostio_workspace_size", "arc_linear_hostio",
-    "arc_probe_e2m1", "arc_probe_e2m1_bits", "arc_probe_e4m3_ceil",
+    "arc_probe_e2m1", "arc_probe_e2m1_bits", "arc_probe_e2m1_raw_bits", "arc_probe_e4m3_ceil",
 ]
 
 
@@ -192,13 +194,26 @@ def select_outliers(chan_max_host: np.ndarray, s_override: int = -1) -> dict:
     return dict(perm=perm, S=S.value, S_raw=S_raw.value, M=M.value, tau=tau.value, gs=gs.value)
 
 
-def calibrate(batches, s_override: int = -1, layout: int = INTERLEAVED, device=None) -> Profile:
-    """Offline calibration of one activation site over an iterable of bf16 [rows, K] batches."""
+def gather_order(perm: np.ndarray) -> np.ndarray:
+    """Bank-conflict-aware channel order inside each 16-channel block (same block sets)."""
+    p = np.ascontiguousarray(perm, dtype=np.int32)
+    out = np.empty_like(p)
+    _check(_lib.arc_gather_order(p.ctypes.data_as(_P), p.size, out.ctypes.data_as(_P)), "arc_gather_order")
+    return out
+
+
+def calibrate(batches, s_override: int = -1, layout: int = INTERLEAVED, device=None,
+              optimize_gather: bool = True) -> Profile:
+    """Offline calibration of one activation site over an iterable of bf16 [rows, K] batches.
+    With optimize_gather the channel order inside each 16-block is re-arranged for
+    conflict-free shared-memory gathers (arc_gather_order; block sets unchanged)."""
     chan_max = None
     for b in batches:
         chan_max = calib_absmax(b, chan_max)
     torch.cuda.current_stream().synchronize()
     sel = select_outliers(chan_max.cpu().numpy(), s_override)
+    if optimize_gather:
+        sel["perm"] = gather_order(sel["perm"])
     dev = chan_max.device if device is None else device
     return Profile(K=chan_max.numel(), S=sel["S"], perm=torch.from_numpy(sel["perm"]).to(dev),
                    gs=torch.tensor([sel["gs"]], dtype=torch.float32, device=dev), layout=layout,
@@ -322,6 +337,12 @@ def probe_e2m1(x: torch.Tensor) -> torch.Tensor:
 def probe_e2m1_bits(start: int, n: int, device="cuda") -> torch.Tensor:
     out = torch.empty(n, dtype=torch.uint8, device=device)
     _check(_lib.arc_probe_e2m1_bits(start, n, _ptr(out), _stream()), "arc_probe_e2m1_bits")
+    return out
+
+
+def probe_e2m1_raw_bits(start: int, n: int, device="cuda") -> torch.Tensor:
+    out = torch.empty(n, dtype=torch.uint8, device=device)
+    _check(_lib.arc_probe_e2m1_raw_bits(start, n, _ptr(out), _stream()), "arc_probe_e2m1_raw_bits")
     return out
 
 

@@ -55,8 +55,9 @@ static bool device_ok() {
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 static arc_status_t check_ks(int64_t K, int64_t S) {
-  if (K <= 0 || K % 16 || K > 65535) return fail(ARC_ERR_SHAPE, "K must be a positive multiple of 16 (<= 65535)");
+  if (K <= 0 || K % 16) return fail(ARC_ERR_SHAPE, "K must be a positive multiple of 16");
   if (S < 0 || S % 16 || S > K) return fail(ARC_ERR_SHAPE, "S must be a multiple of 16 with 0 <= S <= K");
+  if (kp_of(K, S) > 32768) return fail(ARC_ERR_SHAPE, "K + S must be <= 32768");
   return ARC_OK;
 }
 
@@ -168,6 +169,70 @@ arc_status_t arc_select_outliers(const float* chan_max_host, int64_t K, int32_t 
   *tau = t;
   volatile float num = 2688.0f;  // one IEEE fp32 division
   *gs = mx > 0.0f ? num / mx : 1.0f;
+  return ARC_OK;
+}
+
+// Bank-conflict-aware channel order inside each 16-channel block (see arc.h).
+// Warp lanes <-> 32 consecutive blocks; at gather step q every lane reads its
+// block's q-th channel from a staged bf16 row: bank = (channel >> 1) & 31, two
+// channels in the same 32-bit word are one access.  A step costs the largest
+// number of distinct words any bank receives; a seeded local search over
+// in-block swaps minimizes the sum over the 16 steps for each 32-block chunk.
+static int gather_step_cost(const int32_t* col[32], int n) {
+  int words[32][32];
+  int cnt[32] = {0};
+  int worst = 0;
+  for (int i = 0; i < n; ++i) {
+    const int w = *col[i] >> 1, b = w & 31;
+    bool dup = false;
+    for (int k = 0; k < cnt[b]; ++k) dup |= words[b][k] == w;
+    if (!dup) {
+      words[b][cnt[b]++] = w;
+      worst = std::max(worst, cnt[b]);
+    }
+  }
+  return worst;
+}
+
+arc_status_t arc_gather_order(const int32_t* perm_host, int64_t K, int32_t* perm_out_host) {
+  if (!perm_host || !perm_out_host) return fail(ARC_ERR_NULL, "null perm");
+  if (K <= 0 || K % 16) return fail(ARC_ERR_SHAPE, "K must be a positive multiple of 16");
+  std::vector<char> seen((size_t)K, 0);
+  for (int64_t j = 0; j < K; ++j) {
+    const int32_t c = perm_host[j];
+    if (c < 0 || c >= K || seen[(size_t)c]) return fail(ARC_ERR_SHAPE, "perm_host is not a permutation");
+    seen[(size_t)c] = 1;
+  }
+  std::vector<int32_t> out(perm_host, perm_host + K);
+  const int64_t nblk = K / 16;
+  uint64_t rng = 0x9E3779B97F4A7C15ull;
+  for (int64_t c0 = 0; c0 < nblk; c0 += 32) {
+    const int n = (int)std::min<int64_t>(32, nblk - c0);
+    int32_t* B = out.data() + c0 * 16;  // B[i*16 + q]
+    const int32_t* col[32];
+    int cost[16];
+    for (int q = 0; q < 16; ++q) {
+      for (int i = 0; i < n; ++i) col[i] = &B[i * 16 + q];
+      cost[q] = gather_step_cost(col, n);
+    }
+    for (int it = 0; it < 4000; ++it) {
+      rng ^= rng << 13; rng ^= rng >> 7; rng ^= rng << 17;
+      const int i = (int)(rng % (uint64_t)n), a = (int)((rng >> 16) & 15), b = (int)((rng >> 24) & 15);
+      if (a == b) continue;
+      std::swap(B[i * 16 + a], B[i * 16 + b]);
+      for (int k = 0; k < n; ++k) col[k] = &B[k * 16 + a];
+      const int ca = gather_step_cost(col, n);
+      for (int k = 0; k < n; ++k) col[k] = &B[k * 16 + b];
+      const int cb = gather_step_cost(col, n);
+      if (ca + cb <= cost[a] + cost[b]) {
+        cost[a] = ca;
+        cost[b] = cb;
+      } else {
+        std::swap(B[i * 16 + a], B[i * 16 + b]);
+      }
+    }
+  }
+  std::memcpy(perm_out_host, out.data(), sizeof(int32_t) * (size_t)K);
   return ARC_OK;
 }
 

@@ -13,6 +13,10 @@ __global__ void probe_e2m1_kernel(const float* in, uint32_t start, int64_t n, ui
     out[i] = (uint8_t)(e2m1x2(v, 0.0f) & 15u);
   }
 }
+__global__ void probe_e2m1_raw_kernel(uint32_t start, int64_t n, uint8_t* out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (uint8_t)(e2m1x2_raw(__uint_as_float(start + (uint32_t)i), 0.0f) & 15u);
+}
 __global__ void probe_e4m3_ceil_kernel(const float* in, int64_t n, uint8_t* out) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     out[i] = (uint8_t)e4m3_ceil(in[i]);
@@ -37,6 +41,14 @@ arc_status_t arc_probe_e2m1_bits(uint32_t start_bits, int64_t n, uint8_t* out, v
   if (!arc_device_supported()) return ARC_ERR_UNSUPPORTED;
   if (n == 0) return ARC_OK;
   probe_e2m1_kernel<<<probe_grid(n), 256, 0, (cudaStream_t)stream>>>(nullptr, start_bits, n, out);
+  return probe_status(cudaGetLastError());
+}
+arc_status_t arc_probe_e2m1_raw_bits(uint32_t start_bits, int64_t n, uint8_t* out, void* stream) {
+  if (!out) return ARC_ERR_NULL;
+  if (n < 0 || n > (int64_t)1 << 32) return ARC_ERR_SHAPE;
+  if (!arc_device_supported()) return ARC_ERR_UNSUPPORTED;
+  if (n == 0) return ARC_OK;
+  probe_e2m1_raw_kernel<<<probe_grid(n), 256, 0, (cudaStream_t)stream>>>(start_bits, n, out);
   return probe_status(cudaGetLastError());
 }
 arc_status_t arc_probe_e4m3_ceil(const float* in, int64_t n, uint8_t* out, void* stream) {

@@ -22,6 +22,8 @@
 #include "arc_device.cuh"
 #include "arc_internal.h"
 
+#include <cstdlib>
+
 namespace arc {
 
 ARC_DEV int64_t dmin64(int64_t a, int64_t b) { return a < b ? a : b; }
@@ -42,139 +44,302 @@ struct QuantArgs {
   uint8_t* sf;
   int32_t Kp;
   int32_t rows_per_tile;
+  int32_t stages;
+  int32_t npw;     // primary warps
+  int32_t nrw;     // residual warps
+  int32_t debug;   // perf experiments only (env ARC_QUANT_DEBUG): 1 = skip compute, 2 = skip loads
 };
 
-// One NVFP4 stage on 16 values (oracle C4).  Writes codes (packed, element 2i in
-// the low nibble of byte i) and returns the scale code; d_out / t keep the
-// quantities the residual stage needs.
-ARC_DEV uint32_t stage16(const float (&z)[16], float base, float c6, float (&t)[16], float& d_out, uint2& packed) {
-  float a = 0.0f;
-#pragma unroll
-  for (int i = 0; i < 16; ++i) a = fmaxf(a, fabsf(z[i]));
-  const uint32_t sf = e4m3_ceil(__fmul_rn(a, c6));
-  const float d = e4m3_value(sf);
-  const float k = (d == 0.0f) ? 0.0f : __fdiv_rn(base, d);
-#pragma unroll
-  for (int i = 0; i < 16; ++i) t[i] = __fmul_rn(z[i], k);
-  uint32_t w[2] = {0u, 0u};
-#pragma unroll
-  for (int i = 0; i < 16; i += 2) w[i >> 3] |= e2m1x2(t[i], t[i + 1]) << (4 * (i & 7));
-  packed = make_uint2(w[0], w[1]);
-  d_out = d;
-  return sf;
+// Two fp32 products z*k with one FMUL2 (mul.rn.f32x2: two IEEE RN multiplies).
+ARC_DEV float2 mul2(float a, float b, float k) {
+  unsigned long long x, y, r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(x) : "f"(a), "f"(b));
+  asm("mov.b64 %0, {%1, %1};" : "=l"(y) : "f"(k));
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(x), "l"(y));
+  float2 o;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(o.x), "=f"(o.y) : "l"(r));
+  return o;
 }
 
-__global__ void __launch_bounds__(256) arc_quant_kernel(QuantArgs p) {
+// One NVFP4 stage on 16 values (oracle C4) given the block's multiplier k:
+// t = z*k, q = rne_e2m1(t), packed with element 2i in the low nibble of byte i.
+ARC_DEV uint2 encode16(const float (&z)[16], float k) {
+  uint32_t b[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const float2 t = mul2(z[2 * i], z[2 * i + 1], k);
+    b[i] = e2m1x2(t.x, t.y);  // one code byte in bits 0..7
+  }
+  // bytes -> words with byte permutes (2 pair merges + 1 word merge per 4 bytes)
+  const uint32_t p01 = __byte_perm(b[0], b[1], 0x0040), p23 = __byte_perm(b[2], b[3], 0x0040);
+  const uint32_t p45 = __byte_perm(b[4], b[5], 0x0040), p67 = __byte_perm(b[6], b[7], 0x0040);
+  return make_uint2(__byte_perm(p01, p23, 0x5410), __byte_perm(p45, p67, 0x5410));
+}
+
+// max |z| over 16 values as a shallow tree (exact; order-independent)
+ARC_DEV float absmax16(const float (&z)[16]) {
+  float m[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) m[i] = fmaxf(fabsf(z[2 * i]), fabsf(z[2 * i + 1]));
+#pragma unroll
+  for (int i = 0; i < 4; ++i) m[i] = fmaxf(m[i], m[i + 4]);
+  return fmaxf(fmaxf(m[0], m[2]), fmaxf(m[1], m[3]));
+}
+
+// Branch-free smallest E4M3 code >= v (v >= 0), saturating at 0x7E (Q2); same
+// result as arc::e4m3_ceil (probe-tested).
+ARC_DEV uint32_t e4m3_ceil_nb(float v) {
+  const uint32_t b = __float_as_uint(v);
+  const uint32_t cn = min((b >> 20) - 960u + ((b & 0xFFFFFu) != 0u), 126u);  // normal grid, saturated
+  const uint32_t cs = (uint32_t)ceilf(__fmul_rn(v, 512.0f));                 // subnormal grid (v < 2^-6)
+  return v < 0.015625f ? cs : cn;
+}
+
+ARC_DEV void cp_async16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+// arrive on `bar` once all of this thread's prior cp.async copies completed
+ARC_DEV void cp_async_arrive(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// physical block of logical block l (App.D P:591-597 interleaved, or the
+// logical concatenation of P:138): primaries l < K/16, residual j = K/16 + j
+ARC_DEV int phys_block(int l, int nb, int ns, int layout) {
+  if (layout != 0) return l;
+  if (l < ns) return 2 * l;
+  if (l < nb) return l + ns;
+  return 2 * (l - nb) + 1;
+}
+
+// gather 16 channels of one staged row (byte offsets into smem) as fp32 (exact)
+ARC_DEV void gather16(const uint8_t* base, const uint32_t (&off)[16], float (&z)[16]) {
+#pragma unroll
+  for (int q = 0; q < 16; ++q) z[q] = bf16_bits_to_f32(*reinterpret_cast<const uint16_t*>(base + off[q]));
+}
+
+// The quantization kernel.  Warp roles (no intra-warp divergence in steady state):
+//  * primary warps: lane t owns logical primary block t (or a zero pad block) for
+//    every row; its 16 gather offsets (byte offsets of the calibrated channels in
+//    a staged row, P:136's reorder) live in registers; per row: 16 LDS, block
+//    max, ceil-rounded E4M3 scale, 16 products and E2M1 codes (stage 1 of Eq.1).
+//  * residual warps: lane i owns (row i / ns, outlier block i % ns) of each tile
+//    and runs stage 1 + the residual stage 2 -- or, for weights, writes
+//    the bitwise duplicate.  Gathering the outlier blocks of all R rows
+//    of a tile into one warp keeps the heavier dual-stage work from serializing
+//    a warp of primaries.
+//  * producer warp: streams rows HBM -> smem with cp.async (16 B per
+//    lane-instruction, coalesced) into an ST-deep ring of R-row tiles, signalling
+//    full[s] with cp.async.mbarrier.arrive; compute warps release a slot by
+//    arriving on empty[s] (no CTA-wide barrier).
+// Rows sit at a fixed ROWB stride and the tile loop is unrolled over the ring so
+// the gathers are `LDS [off + const]`.
+template <int IPT, int R, int ROWB, int ST>
+__global__ void __launch_bounds__(1024) arc_quant_kernel(QuantArgs p) {
   extern __shared__ __align__(16) uint8_t smem[];
+  constexpr int SLOT = R * ROWB;
   const int K = p.K;
-  const int R = p.rows_per_tile;
-  const int kpad = (K + 7) & ~7;  // perm entries, rounded to 16 bytes
-  uint16_t* perm_s = reinterpret_cast<uint16_t*>(smem);
-  uint16_t* xs0 = perm_s + kpad;
-  uint16_t* xs1 = xs0 + (size_t)R * K;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(xs1 + (size_t)R * K);
+  const int npw = p.npw, nrw = p.nrw;
+  float* k1tab = reinterpret_cast<float*>(smem + ST * SLOT);
+  uint64_t* full = reinterpret_cast<uint64_t*>(k1tab + 128);
+  uint64_t* empty = full + ST;
 
   const int tid = threadIdx.x;
-  const int64_t ntile = (p.rows + R - 1) / R;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int ntile = (int)((p.rows + R - 1) / R);
+  const int my_tiles = ntile > (int)blockIdx.x ? (ntile - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
+  const float gs = __ldg(p.gs);
 
   if (tid == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
+#pragma unroll
+    for (int s = 0; s < ST; ++s) {
+      mbar_init(&full[s], 32);
+      mbar_init(&empty[s], npw + nrw);
+    }
     fence_mbar_init();
   }
-  for (int i = tid; i < K; i += blockDim.x) perm_s[i] = (uint16_t)__ldg(p.perm + i);
+  // k1 = RN(gs / e4m3(c)) for every scale code: the primary stage's multiplier
+  // depends only on the code, so the IEEE division is done once per CTA.
+  for (int c = tid; c < 128; c += blockDim.x) k1tab[c] = (c == 0 || c == 127) ? 0.0f : __fdiv_rn(gs, e4m3_value((uint32_t)c));
   __syncthreads();
 
-  auto issue = [&](int64_t tile, int buf) {
-    const int64_t r0 = tile * R;
-    const int nr = (int)dmin64(R, p.rows - r0);
-    uint16_t* dst = buf ? xs1 : xs0;
-    mbar_expect_tx(&bars[buf], (uint32_t)(nr * K * 2));
-    for (int r = 0; r < nr; ++r) bulk_load(dst + (size_t)r * K, p.x + (r0 + r) * p.ld, (uint32_t)K * 2, &bars[buf]);
-  };
-  if (tid == 0) {
-    if (blockIdx.x < ntile) issue(blockIdx.x, 0);
-    if (blockIdx.x + gridDim.x < ntile) issue(blockIdx.x + gridDim.x, 1);
-  }
-
-  const float gs = __ldg(p.gs);
-  const float c6g = __fdiv_rn(gs, 6.0f);
-  const int nb = K >> 4, ns = p.S >> 4;
-  const int NB = p.Kp >> 4;  // physical blocks per row (multiple of 4)
-  const int64_t sf_rb_stride = (int64_t)(p.Kp >> 6) * 512;
-  const int lane = tid & 31;
-
-  int it = 0;
-  for (int64_t tile = blockIdx.x; tile < ntile; tile += gridDim.x, ++it) {
-    const int buf = it & 1;
-    mbar_wait(&bars[buf], (it >> 1) & 1);
-    const uint16_t* xs = buf ? xs1 : xs0;
-    const int64_t r0 = tile * R;
-    const int nr = (int)dmin64(R, p.rows - r0);
-    const int items = nr * NB;
-
-    for (int base = 0; base < items; base += blockDim.x) {
-      const int i = base + tid;
-      const bool valid = i < items;
-      uint32_t sfb = 0;
-      uint2 packed = make_uint2(0u, 0u);
-      int r = 0, pb = 0;
-      if (valid) {
-        r = i / NB;
-        pb = i - r * NB;
-        // physical block -> (logical primary block l, residual?)  (App.D)
-        int l = -1;
-        bool resid = false;
-        if (p.layout == 0) {
-          if (pb < 2 * ns) { l = pb >> 1; resid = pb & 1; }
-          else if (pb < nb + ns) l = pb - ns;
-        } else {
-          if (pb < nb) l = pb;
-          else if (pb < nb + ns) { l = pb - nb; resid = true; }
-        }
-        if (l >= 0) {
-          const uint16_t* xr = xs + (size_t)r * K;
-          const uint4* pp = reinterpret_cast<const uint4*>(perm_s + 16 * l);
-          const uint4 p0 = pp[0], p1 = pp[1];
-          const uint32_t pw[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
-          float z[16];
+  if (warp == npw + nrw) {
+    // ---------------------------------------------------------------- producer warp
+    const uint32_t ring = smem_u32(smem) + (uint32_t)lane * 16u;
+    const int kc = K >> 3;  // 16-byte chunks per row
+    for (int j0 = 0; j0 < my_tiles; j0 += ST) {
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            z[2 * j] = bf16_bits_to_f32(xr[pw[j] & 0xFFFFu]);
-            z[2 * j + 1] = bf16_bits_to_f32(xr[pw[j] >> 16]);
-          }
-          float t[16], d1;
-          sfb = stage16(z, gs, c6g, t, d1, packed);
-          if (resid && !p.weight_mode) {
-            // residual in units of d1/gs, exact (P:138 R_o = X_o - s*Q_Xo; Q6)
-            float e[16];
+      for (int s = 0; s < ST; ++s) {
+        const int j = j0 + s;
+        if (j < my_tiles) {
+          if (j >= ST) mbar_wait(&empty[s], ((j / ST) - 1) & 1);
+          const int r0 = ((int)blockIdx.x + j * (int)gridDim.x) * R;
+          const int nr = min(R, (int)p.rows - r0);
+          if (p.debug != 2) {
+            const uint16_t* src0 = p.x + (int64_t)r0 * p.ld + lane * 8;
 #pragma unroll
-            for (int j = 0; j < 16; ++j) {
-              const uint32_t q = (j < 8 ? packed.x >> (4 * j) : packed.y >> (4 * (j - 8))) & 15u;
-              e[j] = __fsub_rn(t[j], e2m1_value(q));
-            }
-            float t2[16], d2;
-            sfb = stage16(e, d1, __fdiv_rn(d1, 6.0f), t2, d2, packed);
+            for (int r = 0; r < R; ++r)
+              if (r < nr)
+                for (int c = 0; c < kc - lane; c += 32)
+                  cp_async16(ring + (uint32_t)(s * SLOT + r * ROWB + c * 16), src0 + (int64_t)r * p.ld + c * 8);
           }
+          cp_async_arrive(&full[s]);
         }
-        const int64_t m = r0 + r;
-        *reinterpret_cast<uint2*>(p.codes + m * (p.Kp >> 1) + (int64_t)pb * 8) = packed;
-      }
-      // 4 consecutive lanes hold the 4 scale columns of one 128x4 tile row.
-      uint32_t w = sfb;
-      w |= __shfl_down_sync(0xffffffffu, sfb, 1) << 8;
-      w |= __shfl_down_sync(0xffffffffu, sfb, 2) << 16;
-      w |= __shfl_down_sync(0xffffffffu, sfb, 3) << 24;
-      if (valid && (lane & 3) == 0) {
-        const int64_t m = r0 + r;
-        const int64_t off = (m >> 7) * sf_rb_stride + (int64_t)(pb >> 2) * 512 + (m & 31) * 16 + ((m >> 5) & 3) * 4;
-        *reinterpret_cast<uint32_t*>(p.sf + off) = w;
       }
     }
-    __syncthreads();  // all reads of this buffer done
-    if (tid == 0 && tile + 2 * (int64_t)gridDim.x < ntile) {
-      fence_proxy_async();  // generic-proxy reads of buf ordered before the async-proxy refill
-      issue(tile + 2 * (int64_t)gridDim.x, buf);
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    return;
+  }
+
+  const int nb = K >> 4, ns = p.S >> 4;
+  const int ka16 = nb + ns, NB = p.Kp >> 4;
+  const float c6g = __fdiv_rn(gs, 6.0f);
+  const int sf_rb_stride = (p.Kp >> 6) * 512;
+  const int code_row = p.Kp >> 1;
+
+  if (warp < npw) {
+    // ---------------------------------------------------------------- primary warps
+    uint32_t off[IPT][16];
+    int pbs[IPT], kind[IPT];  // kind: 0 idle, 1 primary, 3 zero pad block
+#pragma unroll
+    for (int i = 0; i < IPT; ++i) {
+      const int t = tid + i * npw * 32;
+      int l = 0, k = 0, pb = 0;
+      if (t < nb) { l = t; k = 1; pb = phys_block(t, nb, ns, p.layout); }
+      else if (t < nb + (NB - ka16)) { k = 3; pb = ka16 + (t - nb); }
+      kind[i] = k;
+      pbs[i] = pb;
+      const int4* pp = reinterpret_cast<const int4*>(p.perm + 16 * l);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int4 v = __ldg(pp + q);
+        off[i][4 * q + 0] = (uint32_t)v.x * 2u;
+        off[i][4 * q + 1] = (uint32_t)v.y * 2u;
+        off[i][4 * q + 2] = (uint32_t)v.z * 2u;
+        off[i][4 * q + 3] = (uint32_t)v.w * 2u;
+      }
+    }
+    for (int j0 = 0; j0 < my_tiles; j0 += ST) {
+#pragma unroll
+      for (int s = 0; s < ST; ++s) {
+        const int j = j0 + s;
+        if (j < my_tiles) {
+          mbar_wait(&full[s], (j / ST) & 1);
+          if (p.debug != 1) {
+            const int r0 = ((int)blockIdx.x + j * (int)gridDim.x) * R;
+            const int nr = min(R, (int)p.rows - r0);
+#pragma unroll
+            for (int i = 0; i < IPT; ++i) {
+              if (kind[i] != 0) {
+                const int pb = pbs[i];
+                uint8_t* cptr = p.codes + (int64_t)r0 * code_row + pb * 8;
+                uint8_t* sptr = p.sf + (pb >> 2) * 512 + (pb & 3);
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                  if (r < nr) {
+                    const int m = r0 + r;
+                    uint32_t sfb = 0;
+                    uint2 packed = make_uint2(0u, 0u);
+                    if (kind[i] == 1) {
+                      float z[16];
+                      gather16(smem + s * SLOT + r * ROWB, off[i], z);
+                      // stage 1 (Eq.1 with the NVFP4 two-level scale, Q7 op order)
+                      sfb = e4m3_ceil_nb(__fmul_rn(absmax16(z), c6g));
+                      packed = encode16(z, k1tab[sfb]);
+                    }
+                    *reinterpret_cast<uint2*>(cptr + (int64_t)r * code_row) = packed;
+                    sptr[(int64_t)(m >> 7) * sf_rb_stride + (m & 31) * 16 + ((m >> 5) & 3) * 4] = (uint8_t)sfb;
+                  }
+                }
+              }
+            }
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[s]);
+        }
+      }
+    }
+    return;
+  }
+
+  // ---------------------------------------------------------------- residual warps
+  const int rl = (warp - npw) * 32 + lane;  // residual lane index
+  const int nitems = R * ns;                // (row, outlier block) pairs per tile
+  // common case (R*ns <= 32*nrw): one fixed item per lane, offsets in registers
+  int fr = 0, fjb = 0;
+  uint32_t foff[16];
+  if (rl < nitems) { fr = rl / ns; fjb = rl - fr * ns; }
+  {
+    const int4* pp = reinterpret_cast<const int4*>(p.perm + 16 * fjb);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int4 v = __ldg(pp + q);
+      foff[4 * q + 0] = (uint32_t)v.x * 2u + (uint32_t)(fr * ROWB);
+      foff[4 * q + 1] = (uint32_t)v.y * 2u + (uint32_t)(fr * ROWB);
+      foff[4 * q + 2] = (uint32_t)v.z * 2u + (uint32_t)(fr * ROWB);
+      foff[4 * q + 3] = (uint32_t)v.w * 2u + (uint32_t)(fr * ROWB);
+    }
+  }
+  const int fpb = phys_block(nb + fjb, nb, ns, p.layout);
+  for (int j0 = 0; j0 < my_tiles; j0 += ST) {
+#pragma unroll
+    for (int s = 0; s < ST; ++s) {
+      const int j = j0 + s;
+      if (j < my_tiles) {
+        mbar_wait(&full[s], (j / ST) & 1);
+        if (p.debug != 1) {
+          const int r0 = ((int)blockIdx.x + j * (int)gridDim.x) * R;
+          const int nr = min(R, (int)p.rows - r0);
+          for (int it = rl; it < nitems; it += nrw * 32) {
+            int r = fr, jb = fjb, pb = fpb;
+            uint32_t off[16];
+#pragma unroll
+            for (int q = 0; q < 16; ++q) off[q] = foff[q];
+            if (it != rl) {  // overflow items (very large S): offsets from L1
+              r = it / ns;
+              jb = it - r * ns;
+              pb = phys_block(nb + jb, nb, ns, p.layout);
+              const int4* pp = reinterpret_cast<const int4*>(p.perm + 16 * jb);
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const int4 v = __ldg(pp + q);
+                off[4 * q + 0] = (uint32_t)v.x * 2u + (uint32_t)(r * ROWB);
+                off[4 * q + 1] = (uint32_t)v.y * 2u + (uint32_t)(r * ROWB);
+                off[4 * q + 2] = (uint32_t)v.z * 2u + (uint32_t)(r * ROWB);
+                off[4 * q + 3] = (uint32_t)v.w * 2u + (uint32_t)(r * ROWB);
+              }
+            }
+            if (r < nr) {
+              const int m = r0 + r;
+              float z[16];
+              gather16(smem + s * SLOT, off, z);
+              const uint32_t sf1 = e4m3_ceil_nb(__fmul_rn(absmax16(z), c6g));
+              const float k1 = k1tab[sf1];
+              uint2 packed = encode16(z, k1);
+              uint32_t sfb = sf1;
+              if (!p.weight_mode) {
+                // residual of the encoded primary in units of d1/gs, exact (Q6); stage 2, base d1
+                float e[16];
+#pragma unroll
+                for (int q = 0; q < 16; ++q) {
+                  const uint32_t c = (q < 8 ? packed.x >> (4 * q) : packed.y >> (4 * (q - 8))) & 15u;
+                  e[q] = __fsub_rn(__fmul_rn(z[q], k1), e2m1_value(c));  // t - v(q1)
+                }
+                const float d1 = e4m3_value(sf1);
+                const uint32_t sf2 = e4m3_ceil_nb(__fmul_rn(absmax16(e), __fdiv_rn(d1, 6.0f)));
+                const float d2 = e4m3_value(sf2);
+                packed = encode16(e, d2 == 0.0f ? 0.0f : __fdiv_rn(d1, d2));
+                sfb = sf2;
+              }  // weight mode: bitwise duplicate of the primary block
+              *reinterpret_cast<uint2*>(p.codes + (int64_t)m * code_row + pb * 8) = packed;
+              p.sf[(int64_t)(m >> 7) * sf_rb_stride + (pb >> 2) * 512 + (pb & 3) + (m & 31) * 16 +
+                   ((m >> 5) & 3) * 4] = (uint8_t)sfb;
+            }
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+      }
     }
   }
 }
@@ -226,11 +391,40 @@ __global__ void arc_finalize_scale_kernel(float* gs) {
 }
 
 // ------------------------------------------------------------------ launchers
-int64_t quant_smem_bytes(int K, int R) { return (int64_t)((K + 7) & ~7) * 2 + 2LL * R * K * 2 + 16; }
 
-int quant_rows_per_tile(int K) {
-  int R = 16384 / K;  // <= 32 KB of bf16 per stage
-  return R < 1 ? 1 : (R > 8 ? 8 : R);
+// Per-(kernel, threads, smem) launch configuration, computed once per process:
+// the attribute calls and the occupancy query cost more host time than the
+// kernel itself at decode sizes.
+template <int IPT, int R, int ROWB, int ST>
+static cudaError_t launch_quant_cfg(QuantArgs a, int threads, cudaStream_t stream) {
+  a.rows_per_tile = R;
+  a.stages = ST;
+  const size_t smem = (size_t)ST * R * ROWB + 128 * 4 + 2 * ST * 8;
+  struct Cfg { int dev, threads; size_t smem; int occ; };
+  static thread_local Cfg cache[8];
+  static thread_local int ncache = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int occ = 0;
+  for (int i = 0; i < ncache && i < 8; ++i)
+    if (cache[i].dev == dev && cache[i].threads == threads && cache[i].smem == smem) occ = cache[i].occ;
+  if (occ == 0) {
+    cudaError_t e = cudaFuncSetAttribute(arc_quant_kernel<IPT, R, ROWB, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         227 * 1024);
+    if (e != cudaSuccess) return e;
+    // the full shared-memory carveout so several CTAs' rings fit per SM
+    e = cudaFuncSetAttribute(arc_quant_kernel<IPT, R, ROWB, ST>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (e != cudaSuccess) return e;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, arc_quant_kernel<IPT, R, ROWB, ST>, threads, smem);
+    if (e != cudaSuccess) return e;
+    if (occ < 1) occ = 1;
+    cache[ncache % 8] = Cfg{dev, threads, smem, occ};
+    ++ncache;
+  }
+  const int64_t ntile = (a.rows + R - 1) / R;
+  const int64_t grid = imin64(ntile, (int64_t)num_sms() * occ);
+  arc_quant_kernel<IPT, R, ROWB, ST><<<(unsigned)grid, threads, smem, stream>>>(a);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_quant(const void* x, int64_t rows, int K, int64_t ld, const int32_t* perm, int S, const float* gs,
@@ -248,19 +442,24 @@ cudaError_t launch_quant(const void* x, int64_t rows, int K, int64_t ld, const i
   a.codes = codes;
   a.sf = sf;
   a.Kp = (int)kp_of(K, S);
-  a.rows_per_tile = quant_rows_per_tile(K);
-  const int64_t smem = quant_smem_bytes(K, a.rows_per_tile);
-  if (smem > 227 * 1024) return cudaErrorInvalidValue;
-  cudaError_t e = cudaFuncSetAttribute(arc_quant_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  int occ = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, arc_quant_kernel, 256, (size_t)smem);
-  if (e != cudaSuccess) return e;
-  if (occ < 1) occ = 1;
-  const int64_t ntile = (rows + a.rows_per_tile - 1) / a.rows_per_tile;
-  const int64_t grid = imin64(ntile, (int64_t)num_sms() * occ);
-  arc_quant_kernel<<<(unsigned)grid, 256, (size_t)smem, stream>>>(a);
-  return cudaGetLastError();
+  static const int dbg = getenv("ARC_QUANT_DEBUG") ? atoi(getenv("ARC_QUANT_DEBUG")) : 0;
+  a.debug = dbg;
+  const int NB = a.Kp / 16, ns = S / 16;
+  const int nprim = NB - ns;                 // primary + pad blocks per row
+  const int ipt = (nprim + 28 * 32 - 1) / (28 * 32);  // <= 28 primary warps
+  a.npw = (nprim + ipt * 32 - 1) / (ipt * 32);
+  const int64_t rowb = (int64_t)K * 2;
+  const int R = rowb <= 16384 ? 2 : (rowb <= 32768 ? 2 : 1);
+  a.nrw = ns == 0 ? 0 : (int)imin64(2, (R * ns + 31) / 32);
+  const int threads = (a.npw + a.nrw + 1) * 32;
+  if (threads > 1024) return cudaErrorInvalidValue;
+  if (ipt == 1) {
+    if (rowb <= 8192) return launch_quant_cfg<1, 2, 8192, 4>(a, threads, stream);
+    if (rowb <= 16384) return launch_quant_cfg<1, 2, 16384, 3>(a, threads, stream);
+    return launch_quant_cfg<1, 2, 32768, 3>(a, threads, stream);
+  }
+  if (ipt == 2) return launch_quant_cfg<2, 1, 65536, 3>(a, threads, stream);
+  return cudaErrorInvalidValue;  // K + S > 32768 is rejected in api.cu
 }
 
 cudaError_t launch_calib_absmax(const void* x, int64_t rows, int K, int64_t ld, float* chan_max, cudaStream_t s) {

@@ -1,0 +1,68 @@
+"""Time arc_quantize_activation alone (CUDA events, L2-cold inputs by rotation)."""
+import argparse
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2601_07475_b200 import arc as A, synth  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--K", type=int, default=4096)
+ap.add_argument("--M", type=int, default=8192)
+ap.add_argument("--S", type=int, default=128)
+ap.add_argument("--iters", type=int, default=20)
+args = ap.parse_args()
+K, M, S = args.K, args.M, args.S
+st = synth.Structure(K, S, seed=0)
+prof = A.calibrate([synth.activation(1024, K, st, seed=1000, device="cuda")], s_override=S)
+nrot = max(2, int(4 * 126e6 // (M * K * 2)) + 1)
+xs = [synth.activation(M, K, st, seed=i, device="cuda") for i in range(nrot)]
+codes, sf = A.quantize_activation(xs[0], prof)
+for i in range(3):
+    A.quantize_activation(xs[i % nrot], prof, codes, sf)
+torch.cuda.synchronize()
+g = torch.cuda.CUDAGraph()
+s = torch.cuda.Stream()
+with torch.cuda.stream(s):
+    A.quantize_activation(xs[0], prof, codes, sf)
+    torch.cuda.synchronize()
+    with torch.cuda.graph(g, stream=s):
+        for i in range(nrot):
+            A.quantize_activation(xs[i], prof, codes, sf)
+torch.cuda.synchronize()
+ts = []
+for it in range(max(3, args.iters // nrot)):
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    ts.append(e0.elapsed_time(e1) / nrot)
+ts.sort()
+Kp = codes.shape[1] * 2
+byts = M * (2 * K + Kp // 2 + Kp // 16)
+med = ts[len(ts) // 2]
+print(f"K={K} M={M} S={S}: median {med*1e3:.1f} us  {byts/med/1e6:.0f} GB/s  (min {ts[0]*1e3:.1f} us)")
+
+# reference: plain torch streaming kernels on the same rotated buffers
+def _t(fn):
+    for i in range(3):
+        fn(i)
+    torch.cuda.synchronize()
+    e = [torch.cuda.Event(enable_timing=True) for _ in range(2 * args.iters)]
+    for i in range(args.iters):
+        e[2 * i].record()
+        fn(i)
+        e[2 * i + 1].record()
+    torch.cuda.synchronize()
+    return sorted(e[2 * i].elapsed_time(e[2 * i + 1]) for i in range(args.iters))[args.iters // 2]
+
+
+dst = torch.empty_like(xs[0])
+t = _t(lambda i: dst.copy_(xs[i % nrot]))
+print(f"torch copy_ of x ({M*K*2/1e6:.0f} MB read + write): {t*1e3:.1f} us  {2*M*K*2/t/1e6:.0f} GB/s")
+acc = torch.empty(M, dtype=torch.float32, device="cuda")
+t = _t(lambda i: torch.amax(xs[i % nrot], dim=1, out=acc.to(torch.bfloat16)) if False else xs[i % nrot].view(torch.int32).sum(dim=1))
+print(f"torch int32 row-sum of x (read only): {t*1e3:.1f} us  {M*K*2/t/1e6:.0f} GB/s")

@@ -100,3 +100,17 @@ def test_select_outliers_matches_oracle(arc):
             assert a[k] == o[k], k
     with pytest.raises(arc.ArcError):
         arc.select_outliers(np.array([np.nan] + [1.0] * 15, np.float32))
+
+
+def test_gather_order_keeps_block_sets(arc):
+    """arc_gather_order only permutes channels inside each 16-block (reading Q22)."""
+    rng = np.random.default_rng(3)
+    for K in (16, 256, 4096, 14336):
+        perm = rng.permutation(K).astype(np.int32)
+        out = arc.gather_order(perm)
+        assert sorted(out.tolist()) == list(range(K))
+        for b in range(K // 16):
+            assert set(out[16 * b:16 * b + 16]) == set(perm[16 * b:16 * b + 16])
+        assert np.array_equal(out, arc.gather_order(perm))  # deterministic
+    with pytest.raises(arc.ArcError):
+        arc.gather_order(np.zeros(32, np.int32))
