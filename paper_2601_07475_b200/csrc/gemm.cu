@@ -20,12 +20,14 @@
 //     signals the epilogue.
 //   warps 2-5: epilogue.  tcgen05.ld 32x32b.x32 (each warp owns its TMEM lane
 //     quadrant = 32 output rows), scale by alpha, convert, store.
-// TMEM: 512 columns = accumulator 256 + SFA 16 + SFB 32 (single accumulator;
-// the epilogue frees it right after its last tcgen05.ld, before its stores).
+// TMEM: 512 columns = two overlapping 256-column accumulators ([0,256) and
+// [192,448)) + SFA 16 + SFB 32; the epilogue of tile t overlaps the MMAs of t+1.
 #include "arc_device.cuh"
 #include "arc_internal.h"
 
 #include <cuda.h>
+#include <cstdlib>
+#include <cstring>
 #include <mutex>
 
 namespace arc {
@@ -42,11 +44,16 @@ constexpr int SFA_BYTES = (BM / 128) * 4 * 512;  // 2 KB
 constexpr int SFB_BYTES = (BN / 128) * 4 * 512;  // 4 KB
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES + SFA_BYTES + SFB_BYTES;  // 54 KB (multiple of 1024)
 constexpr int TMEM_COLS = 512;
-constexpr int ACC_COL = 0;
-constexpr int SFA_COL = 256;
-constexpr int SFB_COL = 256 + 16;
+// Two overlapping 256-column accumulators (CUTLASS-style "overlapping accum"):
+// buffer 0 = [0, 256), buffer 1 = [192, 448); they share [192, 256), which the
+// epilogue drains first so the next tile's MMAs can start while it drains the rest.
+constexpr int ACC1_COL = 192;  // buffer b starts at column b * ACC1_COL
+constexpr int OVL_CHUNKS = 2;  // 32-column chunks in the shared region
+constexpr int SFA_COL = 448;
+constexpr int SFB_COL = 448 + 16;
 constexpr int NUM_THREADS = 192;
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align slack*/ + 256 /*barriers*/;
+constexpr int EPI_STAGE_BYTES = 32 * 64;   // per epilogue warp: 32 rows x 32 bf16 (64B-swizzled)
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 4 * EPI_STAGE_BYTES + 1024 /*align slack*/ + 256 /*barriers*/;
 
 struct Args {
   int M, N, Kp;
@@ -57,6 +64,7 @@ struct Args {
   void* y;
   int64_t ldy;
   int y_fp32;
+  int debug;  // perf experiments only (env ARC_GEMM_DEBUG): 1 = no epilogue work, 2 = no scale copies
 };
 
 // instruction descriptor: E2M1 x E2M1 (format 1), UE4M3 scales, K-major A/B,
@@ -64,14 +72,17 @@ struct Args {
 constexpr uint32_t kIdesc = (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
 
 __global__ void __launch_bounds__(NUM_THREADS, 1)
-    arc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, Args args) {
+    arc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                    const __grid_constant__ CUtensorMap tmY, Args args) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint8_t* epi_stage = smem + STAGES * STAGE_BYTES;  // [4 warps][2 KB]
+  uint64_t* full = reinterpret_cast<uint64_t*>(epi_stage + 4 * EPI_STAGE_BYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
-  uint64_t* tempty = tfull + 1;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 1);
+  uint64_t* ovl_free = tfull + 1;
+  uint64_t* buf_free = ovl_free + 1;  // [2]
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(buf_free + 2);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -89,7 +100,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       mbar_init(&empty[s], 1);
     }
     mbar_init(tfull, 1);
-    mbar_init(tempty, 128);
+    mbar_init(ovl_free, 128);
+    mbar_init(&buf_free[0], 128);
+    mbar_init(&buf_free[1], 128);
     fence_mbar_init();
     prefetch_tmap(&tmA);
     prefetch_tmap(&tmB);
@@ -134,8 +147,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       uint32_t phase = 0;
       int t = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++t) {
-        if (t > 0) mbar_wait(tempty, (t - 1) & 1);  // epilogue drained the accumulator
+        const int b = t & 1;
+        if (t >= 1) mbar_wait(ovl_free, (t - 1) & 1);            // shared columns drained (tile t-1)
+        if (t >= 2) mbar_wait(&buf_free[b], ((t - 2) >> 1) & 1);  // own columns drained (tile t-2)
         tc_fence_after();
+        const uint32_t acc = tmem + b * ACC1_COL;
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
@@ -144,7 +160,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const uint32_t sB = sA + A_BYTES;
           const uint32_t sSFA = sB + B_BYTES;
           const uint32_t sSFB = sSFA + SFA_BYTES;
-          for (int kk = 0; kk < nk; ++kk) {
+          for (int kk = 0; kk < nk && args.debug != 2; ++kk) {
             utccp_32x128b_warpx4(tmem + SFA_COL + 4 * kk, smem_desc(sSFA + kk * 512, 0, 128, kLayoutSwizzleNone));
             utccp_32x128b_warpx4(tmem + SFB_COL + 8 * kk, smem_desc(sSFB + kk * 512, 0, 128, kLayoutSwizzleNone));
             utccp_32x128b_warpx4(tmem + SFB_COL + 8 * kk + 4,
@@ -153,7 +169,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           for (int kk = 0; kk < nk; ++kk) {
             const uint64_t ad = smem_desc(sA + kk * 32, 16, 1024, kLayoutSwizzle128B);
             const uint64_t bd = smem_desc(sB + kk * 32, 16, 1024, kLayoutSwizzle128B);
-            mma_nvf4(tmem + ACC_COL, ad, bd, kIdesc, (kb | kk) != 0, tmem + SFA_COL + 4 * kk, tmem + SFB_COL + 8 * kk);
+            mma_nvf4(acc, ad, bd, kIdesc, (kb | kk) != 0, tmem + SFA_COL + 4 * kk, tmem + SFB_COL + 8 * kk);
           }
           tc_commit(&empty[stage]);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -171,17 +187,41 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       mbar_wait(tfull, t & 1);
       tc_fence_after();
       const int m = mb * BM + q * 32 + lane;
-      for (int c = 0; c < BN / 32; ++c) {
-        uint32_t r[32];
-        tmem_ld_32x32b_x32(tmem + ((uint32_t)(q * 32) << 16) + ACC_COL + c * 32, r);
+      const int b = t & 1;
+      uint32_t pre[OVL_CHUNKS][32];  // the shared chunks, read before anything is stored
+      if (args.debug != 1) {
+#pragma unroll
+        for (int k = 0; k < OVL_CHUNKS; ++k) {
+          const int c = b == 0 ? BN / 32 - OVL_CHUNKS + k : k;
+          tmem_ld_32x32b_x32(tmem + ((uint32_t)(q * 32) << 16) + b * ACC1_COL + c * 32, pre[k]);
+        }
         tmem_ld_wait();
-        if (c == BN / 32 - 1) {
+      }
+      tc_fence_before();
+      mbar_arrive(ovl_free);  // next tile's MMAs may overwrite the shared columns now
+#pragma unroll 1
+      for (int cc = 0; cc < BN / 32; ++cc) {
+        // buffer 0 drains its shared chunks (6, 7) first, buffer 1 its (0, 1)
+        const int c = b == 0 ? (cc + BN / 32 - OVL_CHUNKS) % (BN / 32) : cc;
+        uint32_t r[32];
+        if (args.debug == 1) {
+          if (cc == BN / 32 - 1) { tc_fence_before(); mbar_arrive(&buf_free[b]); }
+          continue;
+        }
+        if (cc < OVL_CHUNKS) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) r[j] = cc == 0 ? pre[0][j] : pre[1][j];
+        } else {
+          tmem_ld_32x32b_x32(tmem + ((uint32_t)(q * 32) << 16) + b * ACC1_COL + c * 32, r);
+          tmem_ld_wait();
+        }
+        if (cc == BN / 32 - 1) {
           tc_fence_before();
-          mbar_arrive(tempty);
+          mbar_arrive(&buf_free[b]);
         }
         const int n0 = nbk * BN + c * 32;
-        if (m < M && n0 < N) {
-          if (args.y_fp32) {
+        if (args.y_fp32 && m < M && n0 < N) {
+          {
             float* yr = static_cast<float*>(args.y) + (int64_t)m * args.ldy + n0;
             if (n0 + 32 <= N) {
 #pragma unroll
@@ -194,30 +234,37 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               for (int j = 0; j < 32; ++j)
                 if (n0 + j < N) yr[j] = __fmul_rn(__uint_as_float(r[j]), alpha);
             }
-          } else {
-            __nv_bfloat16* yr = static_cast<__nv_bfloat16*>(args.y) + (int64_t)m * args.ldy + n0;
-            if (n0 + 32 <= N) {
+          }
+        }
+        if (!args.y_fp32 && mb * BM + q * 32 < M && n0 < N) {
+          // bf16: stage the 32x32 sub-tile in smem (64B swizzle: 16-byte unit u of row
+          // r lives at unit u ^ ((r >> 1) & 3), bank-conflict-free) and TMA-store it
+          // (coalesced, clipped at the M/N edges by the tensor map).
+          uint8_t* st = epi_stage + (warp - 2) * EPI_STAGE_BYTES;
+          if (lane == 0) bulk_wait_read0();  // previous store finished reading the buffer
+          __syncwarp();
 #pragma unroll
-              for (int j = 0; j < 32; j += 8) {
-                uint4 v;
-                uint32_t* pv = reinterpret_cast<uint32_t*>(&v);
+          for (int u = 0; u < 4; ++u) {
+            uint4 v;
+            uint32_t* pv = reinterpret_cast<uint32_t*>(&v);
 #pragma unroll
-                for (int h = 0; h < 4; ++h) {
-                  __nv_bfloat162 b2 = __floats2bfloat162_rn(__fmul_rn(__uint_as_float(r[j + 2 * h]), alpha),
-                                                            __fmul_rn(__uint_as_float(r[j + 2 * h + 1]), alpha));
-                  pv[h] = *reinterpret_cast<uint32_t*>(&b2);
-                }
-                *reinterpret_cast<uint4*>(yr + j) = v;
-              }
-            } else {
-#pragma unroll
-              for (int j = 0; j < 32; ++j)
-                if (n0 + j < N) yr[j] = __float2bfloat16_rn(__fmul_rn(__uint_as_float(r[j]), alpha));
+            for (int h = 0; h < 4; ++h) {
+              __nv_bfloat162 b2 = __floats2bfloat162_rn(__fmul_rn(__uint_as_float(r[8 * u + 2 * h]), alpha),
+                                                        __fmul_rn(__uint_as_float(r[8 * u + 2 * h + 1]), alpha));
+              pv[h] = *reinterpret_cast<uint32_t*>(&b2);
             }
+            *reinterpret_cast<uint4*>(st + lane * 64 + ((u ^ ((lane >> 1) & 3)) << 4)) = v;
+          }
+          fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&tmY, st, n0, mb * BM + q * 32);
+            bulk_commit();
           }
         }
       }
     }
+    if (lane == 0) bulk_wait_all();
   }
 
   tc_fence_before();
@@ -258,10 +305,26 @@ bool make_map(CUtensorMap* m, const uint8_t* base, int64_t rows, int64_t row_byt
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+bool make_y_map(CUtensorMap* m, void* y, int64_t rows, int64_t cols, int64_t ldy) {
+  EncodeTiledFn enc = get_encode_fn();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ldy * 2)};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t estr[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, y, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 }  // namespace
 
 cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t stream, const char** detail) {
-  CUtensorMap tmA, tmB;
+  CUtensorMap tmA, tmB, tmY;
+  memset(&tmY, 0, sizeof(tmY));
+  if (!p.y_fp32 && !make_y_map(&tmY, p.y, p.M, p.N, p.ldy)) {
+    if (detail) *detail = "cuTensorMapEncodeTiled (Y) failed";
+    return cudaErrorInvalidValue;
+  }
   if (!make_map(&tmA, p.a_codes, p.M, p.Kp / 2, BM) || !make_map(&tmB, p.b_codes, p.N, p.Kp / 2, BN)) {
     if (detail) *detail = "cuTensorMapEncodeTiled failed";
     return cudaErrorInvalidValue;
@@ -283,9 +346,11 @@ cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t stream, const char** 
   a.y = p.y;
   a.ldy = p.ldy;
   a.y_fp32 = p.y_fp32;
+  static const int dbg = getenv("ARC_GEMM_DEBUG") ? atoi(getenv("ARC_GEMM_DEBUG")) : 0;
+  a.debug = dbg;
   const int64_t tiles = ((p.M + BM - 1) / BM) * ((p.N + BN - 1) / BN);
   const int grid = (int)std::min<int64_t>(tiles, num_sms());
-  arc_gemm_kernel<<<grid, NUM_THREADS, SMEM_BYTES, stream>>>(tmA, tmB, a);
+  arc_gemm_kernel<<<grid, NUM_THREADS, SMEM_BYTES, stream>>>(tmA, tmB, tmY, a);
   return cudaGetLastError();
 }
 
