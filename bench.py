@@ -62,7 +62,7 @@ class Clocks:
              "clocks_event_reasons.sw_power_cap")
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "20"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -106,26 +106,32 @@ class Clocks:
 # ----------------------------------------------------------------------------- workload
 class Site:
     def __init__(self, name, K, N, M, S, rank, world, mode, device, A):
-        """mode: 'full' (1 GPU), 'col' (column-parallel shard of N), 'row' (row-parallel shard of K)."""
-        self.name, self.M = name, M
+        """mode: 'full' (1 GPU), 'col' (column-parallel shard of N), 'row' (row-parallel shard of K).
+        Sharded sites are built with paper_2601_07475_b200.tp (the tested host logic)."""
+        from paper_2601_07475_b200 import tp
+        self.name, self.M, self.mode = name, M, mode
         seed = zlib.crc32(name.encode()) % 1000
-        Kl, Nl, S_l, S_inj = K, N, S, S
-        if mode == "col":
-            Nl = N // world
-        elif mode == "row":
-            Kl = K // world
-            S_inj = S // world
-            S_l = max(16, (S // world + 15) // 16 * 16)
-        self.K, self.N, self.S, self.mode = Kl, Nl, S_l, mode
-        st = synth.Structure(Kl, S_inj, seed=seed * 31 + (rank if mode == "row" else 0))
-        cal = synth.activation(4096, Kl, st, seed=seed + 1000, device=device)
-        self.prof = A.calibrate([cal], s_override=S_l)
-        del cal
-        w = synth.weight(Nl, Kl, seed=seed * 7 + rank, device=device)
-        self.qw = A.quantize_weight(w, self.prof)
+        st = synth.Structure(K, S, seed=seed * 31)
+        cal = synth.activation(4096, K, st, seed=seed + 1000, device=device)
+        w = synth.weight(N, K, seed=seed * 7, device=device)
+        x = synth.activation(M, K, st, seed=seed + 1, device=device)
+        if mode == "full":
+            self.prof = A.calibrate([cal], s_override=S)
+            self.qw = A.quantize_weight(w, self.prof)
+            self.x = x
+        elif mode == "col":
+            prof = A.calibrate([cal], s_override=S)
+            lin = tp.ColumnParallelLinear(w, prof, rank, world, backend=A)
+            self.prof, self.qw, self.x = lin.profile, lin.qweight, x
+        else:
+            S_r = max(16, (S // world + 15) // 16 * 16)
+            lin = tp.RowParallelLinear(w, cal, rank, world, s_override=S_r, backend=A)
+            self.prof, self.qw = lin.profile, lin.qweight
+            self.x = x[:, lin.shard.lo:lin.shard.hi].contiguous()
+        del cal, w, x
+        Kl, Nl, S_l = self.prof.K, self.qw.N, self.prof.S
+        self.K, self.N, self.S = Kl, Nl, S_l
         self.gs_w = float(self.qw.gs.item())
-        del w
-        self.x = synth.activation(M, Kl, st, seed=seed + 1, device=device)
         Kp, cb, sb = A.buffer_sizes(M, Kl, S_l)
         self.Kp = Kp
         self.codes = torch.empty(M, Kp // 2, dtype=torch.uint8, device=device)
@@ -208,7 +214,7 @@ def traffic_from_profiles():
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="arc", choices=["arc", "reference"])
     ap.add_argument("--M", type=int, default=8192)
@@ -330,7 +336,9 @@ def main():
     tr = traffic_from_profiles()
     if tr:
         out["roofline"]["traffic"] = tr.get("gemm_bytes_per_launch")
-        out["quantize"]["traffic"] = tr.get("quant_bytes_per_launch")
+        out["roofline"]["traffic_note"] = "profiles/ncu_traffic.json (committed ncu capture); algorithmic " \
+            f"{tr.get('gemm_algorithmic_bytes_per_launch', 0):.3g} B per launch"
+        out["quantize"]["traffic"] = tr.get("quant_bytes_per_launch_qkv_fullset")
 
     # e2e through the public C-ABI host-buffer call (H2D of x and D2H of y inside the timed region)
     if not args.no_e2e:

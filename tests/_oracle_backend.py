@@ -1,0 +1,47 @@
+"""CPU stand-in for the libarc.so binding with the interface paper_2601_07475_b200.tp
+expects (calibrate / quantize_weight / linear), built on the oracle.  Test-only: it
+lets the tensor-parallel host logic run under torch.distributed gloo on CPU."""
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+import oracle
+
+
+@dataclass
+class Prof:
+    perm: np.ndarray
+    S: int
+    gs: float
+    layout: int
+
+
+@dataclass
+class QW:
+    codes: np.ndarray
+    sf: np.ndarray
+    gs: float
+
+
+class OracleBackend:
+    def calibrate(self, batches, s_override=-1, layout=0):
+        cm = None
+        for b in batches:
+            cm = oracle.calib_absmax(oracle.as_bf16_bits(b), cm)
+        sel = oracle.select_outliers(cm, s_override)
+        return Prof(sel["perm"], sel["S"], sel["gs"], layout)
+
+    def quantize_weight(self, w, prof):
+        gs_w = oracle.tensor_scale(float(w.float().abs().max()))
+        codes, sf = oracle.quantize_weight(oracle.as_bf16_bits(w), prof.perm, prof.S, gs_w, prof.layout)
+        return QW(codes, sf, gs_w)
+
+    def linear(self, x, prof, qw, out_dtype=torch.float32):
+        ac, asf = oracle.quantize_activation(oracle.as_bf16_bits(x), prof.perm, prof.S, prof.gs, prof.layout)
+        y, _ = oracle.gemm_reference(ac, asf, qw.codes, qw.sf, prof.gs, qw.gs)
+        return torch.from_numpy(y).to(out_dtype)
+
+    def linear_bound(self, x, prof, qw):
+        ac, asf = oracle.quantize_activation(oracle.as_bf16_bits(x), prof.perm, prof.S, prof.gs, prof.layout)
+        return oracle.gemm_reference(ac, asf, qw.codes, qw.sf, prof.gs, qw.gs)
