@@ -64,13 +64,18 @@ struct Args {
   void* y;
   int64_t ldy;
   int y_fp32;
-  int debug;  // perf experiments only (env ARC_GEMM_DEBUG): 1 = no epilogue work, 2 = no scale copies
+  int debug;  // perf experiments only (env ARC_GEMM_DEBUG): 1 = no epilogue work, 2 = no scale copies, 3 = no stores, 4 = no TMEM loads
 };
 
 // instruction descriptor: E2M1 x E2M1 (format 1), UE4M3 scales, K-major A/B,
 // N>>3 at [17,23), M>>4 at [24,29).
 constexpr uint32_t kIdesc = (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
 
+// CL = CTAs per cluster along M (1 or 2).  With CL = 2 the two CTAs compute the
+// tiles (m, n) and (m+1, n): each TMA-loads HALF of the shared B tile (and its
+// scale chunk) multicast into both CTAs' smem, halving L2->SM traffic for B --
+// at 128x256 tiles the kernel is otherwise bound by L2 bandwidth (~6 KB/clk).
+template <int CL>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     arc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const __grid_constant__ CUtensorMap tmY, Args args) {
@@ -89,7 +94,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const int M = args.M, N = args.N, Kp = args.Kp;
   const int num_m = (M + BM - 1) / BM;
   const int num_n = (N + BN - 1) / BN;
-  const int num_tiles = num_m * num_n;
+  const int num_mp = (num_m + CL - 1) / CL;   // M-tile groups (one per cluster step)
+  const int num_tiles = num_mp * num_n;       // cluster work items
+  const int rank = CL == 1 ? 0 : (int)cluster_ctarank();
+  const int cid = blockIdx.x / CL, ncl = gridDim.x / CL;
+  const uint16_t mc_mask = (uint16_t)((1u << CL) - 1u);
   const int nkb = (Kp + BK - 1) / BK;
   const int kc_total = Kp / 64;            // 64-element scale chunks per row block
   const int n_rb = (N + 127) / 128;        // 128-row blocks of the B scale buffer
@@ -97,7 +106,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], CL);  // one MMA commit from every CTA of the cluster
     }
     mbar_init(tfull, 1);
     mbar_init(ovl_free, 128);
@@ -110,6 +119,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (warp == 1) tmem_alloc(tmem_holder, TMEM_COLS);
   tc_fence_before();
   __syncthreads();
+  if (CL > 1) cluster_sync();  // peers' barriers initialised before any multicast lands
   tc_fence_after();
   const uint32_t tmem = *tmem_holder;
 
@@ -119,23 +129,33 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const uint64_t pol = policy_evict_last();
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        const int mb = tile % num_m, nbk = tile / num_m;
-        const int nrb = min(2, n_rb - 2 * nbk);
+      for (int tile = cid; tile < num_tiles; tile += ncl) {
+        const int mb = (tile % num_mp) * CL + rank, nbk = tile / num_mp;
+        const int nrb = min(2, n_rb - 2 * nbk);   // existing 128-row scale blocks of this B tile
+        const bool a_ok = mb < num_m;              // (CL = 2, odd num_m: the last rank-1 tile is empty)
         for (int kb = 0; kb < nkb; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_wait(&empty[stage], phase ^ 1);     // the slot is free in EVERY CTA of the cluster
           const int nk = min(4, kc_total - kb * 4);
           uint8_t* sA = smem + stage * STAGE_BYTES;
           uint8_t* sB = sA + A_BYTES;
           uint8_t* sSFA = sB + B_BYTES;
           uint8_t* sSFB = sSFA + SFA_BYTES;
-          mbar_expect_tx(&full[stage], (uint32_t)(A_BYTES + B_BYTES + nk * 512 * (1 + nrb)));
+          mbar_expect_tx(&full[stage], (uint32_t)(A_BYTES + B_BYTES + nk * 512 * ((a_ok ? 1 : 0) + nrb)));
           tma_load_2d(sA, &tmA, &full[stage], kb * BKB, mb * BM, pol);
-          tma_load_2d(sB, &tmB, &full[stage], kb * BKB, nbk * BN, pol);
-          bulk_load(sSFA, args.sfa + ((int64_t)mb * kc_total + kb * 4) * 512, nk * 512, &full[stage]);
-          for (int rb = 0; rb < nrb; ++rb)
-            bulk_load(sSFB + rb * 2048, args.sfb + ((int64_t)(2 * nbk + rb) * kc_total + kb * 4) * 512, nk * 512,
-                      &full[stage]);
+          if (a_ok) bulk_load(sSFA, args.sfa + ((int64_t)mb * kc_total + kb * 4) * 512, nk * 512, &full[stage]);
+          if (CL == 1) {
+            tma_load_2d(sB, &tmB, &full[stage], kb * BKB, nbk * BN, pol);
+            for (int rb = 0; rb < nrb; ++rb)
+              bulk_load(sSFB + rb * 2048, args.sfb + ((int64_t)(2 * nbk + rb) * kc_total + kb * 4) * 512, nk * 512,
+                        &full[stage]);
+          } else {
+            // this CTA's half of B (128 rows) and its scale chunk, to both CTAs
+            tma_load_2d_mc(sB + rank * (B_BYTES / 2), &tmB, &full[stage], kb * BKB, nbk * BN + rank * (BN / 2),
+                           mc_mask, pol);
+            if (rank < nrb)
+              bulk_load_mc(sSFB + rank * 2048, args.sfb + ((int64_t)(2 * nbk + rank) * kc_total + kb * 4) * 512,
+                           nk * 512, &full[stage], mc_mask);
+          }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -146,7 +166,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       int t = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++t) {
+      for (int tile = cid; tile < num_tiles; tile += ncl, ++t) {
         const int b = t & 1;
         if (t >= 1) mbar_wait(ovl_free, (t - 1) & 1);            // shared columns drained (tile t-1)
         if (t >= 2) mbar_wait(&buf_free[b], ((t - 2) >> 1) & 1);  // own columns drained (tile t-2)
@@ -171,7 +191,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             const uint64_t bd = smem_desc(sB + kk * 32, 16, 1024, kLayoutSwizzle128B);
             mma_nvf4(acc, ad, bd, kIdesc, (kb | kk) != 0, tmem + SFA_COL + 4 * kk, tmem + SFB_COL + 8 * kk);
           }
-          tc_commit(&empty[stage]);
+          if (CL == 1) tc_commit(&empty[stage]);
+          else tc_commit_mc(&empty[stage], mc_mask);  // frees the slot in both CTAs
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
         tc_commit(tfull);
@@ -182,14 +203,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int q = warp & 3;  // TMEM lane quadrant this warp may access
     const float alpha = __fdiv_rn(1.0f, __fmul_rn(__ldg(args.gs_x), __ldg(args.gs_w)));
     int t = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++t) {
-      const int mb = tile % num_m, nbk = tile / num_m;
+    for (int tile = cid; tile < num_tiles; tile += ncl, ++t) {
+      const int mb = (tile % num_mp) * CL + rank, nbk = tile / num_mp;
       mbar_wait(tfull, t & 1);
       tc_fence_after();
       const int m = mb * BM + q * 32 + lane;
       const int b = t & 1;
       uint32_t pre[OVL_CHUNKS][32];  // the shared chunks, read before anything is stored
-      if (args.debug != 1) {
+      if (args.debug != 1 && args.debug != 4) {
 #pragma unroll
         for (int k = 0; k < OVL_CHUNKS; ++k) {
           const int c = b == 0 ? BN / 32 - OVL_CHUNKS + k : k;
@@ -208,7 +229,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if (cc == BN / 32 - 1) { tc_fence_before(); mbar_arrive(&buf_free[b]); }
           continue;
         }
-        if (cc < OVL_CHUNKS) {
+        if (args.debug == 4) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) r[j] = 0u;
+        } else if (cc < OVL_CHUNKS) {
 #pragma unroll
           for (int j = 0; j < 32; ++j) r[j] = cc == 0 ? pre[0][j] : pre[1][j];
         } else {
@@ -236,12 +260,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             }
           }
         }
-        if (!args.y_fp32 && mb * BM + q * 32 < M && n0 < N) {
+        if (!args.y_fp32 && mb * BM + q * 32 < M && n0 < N && args.debug != 3) {
           // bf16: stage the 32x32 sub-tile in smem (64B swizzle: 16-byte unit u of row
           // r lives at unit u ^ ((r >> 1) & 3), bank-conflict-free) and TMA-store it
           // (coalesced, clipped at the M/N edges by the tensor map).
           uint8_t* st = epi_stage + (warp - 2) * EPI_STAGE_BYTES;
-          if (lane == 0) bulk_wait_read0();  // previous store finished reading the buffer
+          if (lane == 0 && args.debug != 5) bulk_wait_read0();  // previous store finished reading the buffer
           __syncwarp();
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
@@ -255,11 +279,26 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             }
             *reinterpret_cast<uint4*>(st + lane * 64 + ((u ^ ((lane >> 1) & 3)) << 4)) = v;
           }
-          fence_proxy_async();
-          __syncwarp();
-          if (lane == 0) {
-            tma_store_2d(&tmY, st, n0, mb * BM + q * 32);
-            bulk_commit();
+          if (args.debug == 5) {
+            // coalesced STG from the staged sub-tile: lane -> (row lane/4 + 8i, 16-byte unit lane%4)
+            __syncwarp();
+            const int rr = lane >> 2, uu = lane & 3;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const int row = rr + 8 * i;
+              const int gm = mb * BM + q * 32 + row;
+              const uint4 v = *reinterpret_cast<const uint4*>(st + row * 64 + ((uu ^ ((row >> 1) & 3)) << 4));
+              if (gm < M && n0 + uu * 8 < N)
+                *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(args.y) + (int64_t)gm * args.ldy + n0 + uu * 8) = v;
+            }
+            __syncwarp();
+          } else {
+            fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_2d(&tmY, st, n0, mb * BM + q * 32);
+              bulk_commit();
+            }
           }
         }
       }
@@ -269,6 +308,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   tc_fence_before();
   __syncthreads();
+  if (CL > 1) cluster_sync();  // no CTA leaves while its peer may still multicast into it
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem, TMEM_COLS);
@@ -319,20 +359,24 @@ bool make_y_map(CUtensorMap* m, void* y, int64_t rows, int64_t cols, int64_t ldy
 }  // namespace
 
 cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t stream, const char** detail) {
+  static const int env_cl = getenv("ARC_GEMM_CL") ? atoi(getenv("ARC_GEMM_CL")) : 2;
+  const int CL = env_cl == 1 ? 1 : 2;
   CUtensorMap tmA, tmB, tmY;
   memset(&tmY, 0, sizeof(tmY));
   if (!p.y_fp32 && !make_y_map(&tmY, p.y, p.M, p.N, p.ldy)) {
     if (detail) *detail = "cuTensorMapEncodeTiled (Y) failed";
     return cudaErrorInvalidValue;
   }
-  if (!make_map(&tmA, p.a_codes, p.M, p.Kp / 2, BM) || !make_map(&tmB, p.b_codes, p.N, p.Kp / 2, BN)) {
+  if (!make_map(&tmA, p.a_codes, p.M, p.Kp / 2, BM) || !make_map(&tmB, p.b_codes, p.N, p.Kp / 2, BN / CL)) {
     if (detail) *detail = "cuTensorMapEncodeTiled failed";
     return cudaErrorInvalidValue;
   }
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(arc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    attr_err = cudaFuncSetAttribute(arc_gemm_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    if (attr_err == cudaSuccess)
+      attr_err = cudaFuncSetAttribute(arc_gemm_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
   });
   if (attr_err != cudaSuccess) return attr_err;
   Args a;
@@ -348,9 +392,25 @@ cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t stream, const char** 
   a.y_fp32 = p.y_fp32;
   static const int dbg = getenv("ARC_GEMM_DEBUG") ? atoi(getenv("ARC_GEMM_DEBUG")) : 0;
   a.debug = dbg;
-  const int64_t tiles = ((p.M + BM - 1) / BM) * ((p.N + BN - 1) / BN);
-  const int grid = (int)std::min<int64_t>(tiles, num_sms());
-  arc_gemm_kernel<<<grid, NUM_THREADS, SMEM_BYTES, stream>>>(tmA, tmB, tmY, a);
+  const int64_t num_m = (p.M + BM - 1) / BM, num_n = (p.N + BN - 1) / BN;
+  const int64_t work = ((num_m + CL - 1) / CL) * num_n;  // cluster work items
+  const int64_t grid = std::min<int64_t>(work, num_sms() / CL) * CL;
+  cudaLaunchConfig_t cfg;
+  memset(&cfg, 0, sizeof(cfg));
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(NUM_THREADS);
+  cfg.dynamicSmemBytes = SMEM_BYTES;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = CL == 1 ? cudaLaunchKernelEx(&cfg, arc_gemm_kernel<1>, tmA, tmB, tmY, a)
+                          : cudaLaunchKernelEx(&cfg, arc_gemm_kernel<2>, tmA, tmB, tmY, a);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
