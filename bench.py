@@ -137,6 +137,7 @@ class Site:
         self.codes = torch.empty(M, Kp // 2, dtype=torch.uint8, device=device)
         self.sf = torch.empty(sb, dtype=torch.uint8, device=device)
         self.y = torch.empty(M, Nl, dtype=torch.bfloat16, device=device)
+        self.ws = A.Workspace(device)
         self.flops = 2.0 * M * Nl * (Kl + S_l)                       # SPEC S:322 cost model, algorithmic
         self.flops_eff = 2.0 * M * Nl * Kl
         self.q_bytes = M * (2 * Kl + Kp // 2 + Kp // 16) + 4 * Kl     # bf16 read + codes + scales + perm
@@ -161,7 +162,7 @@ def run_step(A, sites, ev=None, pg=None):
         A.quantize_activation(s.x, s.prof, s.codes, s.sf)
         if ev is not None:
             ev[i][1].record()
-        A.gemm(s.codes, s.sf, s.prof.gs, s.qw, out=s.y)
+        A.gemm(s.codes, s.sf, s.prof.gs, s.qw, out=s.y, ws=s.ws)
         if ev is not None:
             ev[i][2].record()
         if s.mode == "row" and pg is not None:
@@ -220,6 +221,7 @@ def main():
     ap.add_argument("--M", type=int, default=8192)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-decode", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -340,11 +342,49 @@ def main():
             f"{tr.get('gemm_algorithmic_bytes_per_launch', 0):.3g} B per launch"
         out["quantize"]["traffic"] = tr.get("quant_bytes_per_launch_qkv_fullset")
 
+    # decode-size step (BASELINE configs[1] decode M): the same 4 sites at M=16 tokens through
+    # arc_linear (quantize + split-K GEMM + fixed-order reduction), CUDA-graph replay; the
+    # weights (~126 MB for the 4 sites) stream from HBM/L2 every step.
+    if not args.no_decode and world == 1:
+        Md = 16
+        xd = [synth.activation(Md, s.K, synth.Structure(s.K, 8, seed=5), seed=9, device=device) for s in sites]
+        yd = [torch.empty(Md, s.N, dtype=torch.bfloat16, device=device) for s in sites]
+        wsd = [A.Workspace(device) for _ in sites]
+        for s, x_, y_, w_ in zip(sites, xd, yd, wsd):
+            A.linear(x_, s.prof, s.qw, out=y_, ws=w_)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        gs_ = torch.cuda.Stream()
+        with torch.cuda.stream(gs_):
+            with torch.cuda.graph(g, stream=gs_):
+                for s, x_, y_, w_ in zip(sites, xd, yd, wsd):
+                    A.linear(x_, s.prof, s.qw, out=y_, ws=w_)
+        torch.cuda.synchronize()
+        for _ in range(3):
+            g.replay()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 50
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(reps):
+            g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        dms = e0.elapsed_time(e1) / reps
+        wbytes = sum(s.N * s.Kp * 9 // 16 for s in sites)
+        dbytes = wbytes + sum(Md * s.K * 2 + Md * s.N * 2 for s in sites)
+        out["decode"] = {"M_tokens": Md, "us_per_layer_step": dms * 1e3, "tflops": sum(2.0 * Md * s.N * (s.K + s.S)
+                         for s in sites) / (dms * 1e-3) / 1e12,
+                         "bytes_per_step": dbytes, "achieved_gbs": dbytes / (dms * 1e-3) / 1e9,
+                         "hbm_frac": dbytes / (dms * 1e-3) / 1e9 / peaks["hbm"],
+                         "note": "4 sites x (quant + split-K GEMM + reduce) = 12 launches per step in one CUDA graph; "
+                                 "bound = weight bytes / HBM"}
+
     # e2e through the public C-ABI host-buffer call (H2D of x and D2H of y inside the timed region)
     if not args.no_e2e:
         xs = [s.x.cpu().pin_memory() for s in sites]
         ys = [torch.empty(s.M, s.N, dtype=torch.bfloat16).pin_memory() for s in sites]
-        wss = [torch.empty(A.linear_hostio_workspace_size(s.M, s.K, s.S, s.N), dtype=torch.uint8, device=device)
+        wss = [torch.empty(A.linear_hostio_workspace_size(s.M, s.qw), dtype=torch.uint8, device=device)
                for s in sites]
         for _ in range(2):
             for s, xh, yh, ws in zip(sites, xs, ys, wss):

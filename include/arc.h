@@ -113,9 +113,12 @@ ARC_API int arc_device_supported(void);
 /* Sizes of a quantized operand of `rows` rows (codes / sf bytes, Kp). */
 ARC_API arc_status_t arc_buffer_sizes(int64_t rows, int64_t K, int32_t S, int64_t* Kp, size_t* code_bytes,
                               size_t* sf_bytes);
-/* Workspace arc_linear needs (the quantized activation): code + sf bytes for M rows,
- * each 256-byte aligned. */
-ARC_API arc_status_t arc_workspace_size(int64_t M, int64_t K, int32_t S, size_t* bytes);
+/* Workspace arc_gemm needs for M rows against qw: the fp32 split-K partials used at
+ * decode-size M (nsplit*M*N*4 bytes; 0 when the GEMM is not split). */
+ARC_API arc_status_t arc_gemm_workspace_size(int64_t M, const arc_qweight_t* qw, size_t* bytes);
+/* Workspace arc_linear needs: the quantized activation (codes + scales for M rows,
+ * each 256-byte aligned) followed by arc_gemm's workspace. */
+ARC_API arc_status_t arc_linear_workspace_size(int64_t M, const arc_qweight_t* qw, size_t* bytes);
 
 /* ---------------------------------------------------------------- calibration (offline) */
 /* chan_max[j] = max(chan_max[j], max_r |x[r, j]|) over the `rows` bf16 rows of x
@@ -167,19 +170,23 @@ ARC_API arc_status_t arc_quantize_activation(const void* x, int64_t M, int64_t l
  * elements of A_aug * B_aug^T (Eq.2), FP32 accumulation in tensor
  * memory (tcgen05.mma kind::mxf4nvf4, scale vector 16), stored as y_dtype.
  * a_codes/a_sf: the activation as written by arc_quantize_activation with the
- * same K, S and layout as qw.  ldy * sizeof(y_dtype) must be a multiple of 16. */
+ * same K, S and layout as qw.  ldy * sizeof(y_dtype) must be a multiple of 16.
+ * ws: arc_gemm_workspace_size(M, qw) bytes (may be NULL when that is 0); at
+ * decode-size M the K range is split over the SMs and the fp32 partials are
+ * summed in a fixed order by a second kernel (deterministic). */
 ARC_API arc_status_t arc_gemm(const uint8_t* a_codes, const uint8_t* a_sf, const float* gs_x, int64_t M,
-                      const arc_qweight_t* qw, void* y, arc_dtype_t y_dtype, int64_t ldy, void* stream);
+                              const arc_qweight_t* qw, void* y, arc_dtype_t y_dtype, int64_t ldy, void* ws,
+                              size_t ws_bytes, void* stream);
 /* The full linear: arc_quantize_activation into the workspace, then arc_gemm.
- * ws must hold arc_workspace_size(M, K, S) bytes (256-byte aligned). */
+ * ws must hold arc_linear_workspace_size(M, qw) bytes (256-byte aligned). */
 ARC_API arc_status_t arc_linear(const void* x, int64_t M, int64_t ldx, const arc_profile_t* prof,
                         const arc_qweight_t* qw, void* y, arc_dtype_t y_dtype, int64_t ldy, void* ws,
                         size_t ws_bytes, void* stream);
 /* arc_linear on HOST buffers: copies x_host (bf16 [M][K], pinned or pageable) to
  * the device, runs arc_linear, copies y back to y_host ([M][N] of y_dtype) and
  * synchronizes `stream`.  ws must hold arc_linear_hostio_workspace_size bytes. */
-ARC_API arc_status_t arc_linear_hostio_workspace_size(int64_t M, int64_t K, int32_t S, int64_t N,
-                                              arc_dtype_t y_dtype, size_t* bytes);
+ARC_API arc_status_t arc_linear_hostio_workspace_size(int64_t M, const arc_qweight_t* qw, arc_dtype_t y_dtype,
+                                                      size_t* bytes);
 ARC_API arc_status_t arc_linear_hostio(const void* x_host, int64_t M, const arc_profile_t* prof,
                                const arc_qweight_t* qw, void* y_host, arc_dtype_t y_dtype, void* ws,
                                size_t ws_bytes, void* stream);

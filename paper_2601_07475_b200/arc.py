@@ -60,7 +60,8 @@ _lib.arc_last_error.argtypes = []
 _sig("arc_device_supported", [])
 _sig("arc_buffer_sizes", [_i64, _i64, _i32, ctypes.POINTER(_i64), ctypes.POINTER(ctypes.c_size_t),
                           ctypes.POINTER(ctypes.c_size_t)])
-_sig("arc_workspace_size", [_i64, _i64, _i32, ctypes.POINTER(ctypes.c_size_t)])
+_sig("arc_gemm_workspace_size", [_i64, ctypes.POINTER(ArcQWeight), ctypes.POINTER(ctypes.c_size_t)])
+_sig("arc_linear_workspace_size", [_i64, ctypes.POINTER(ArcQWeight), ctypes.POINTER(ctypes.c_size_t)])
 _sig("arc_calib_absmax", [_P, _i64, _i64, _i64, _P, _P])
 _sig("arc_select_outliers", [_P, _i64, _i32, _P, ctypes.POINTER(_i32), ctypes.POINTER(_i32),
                              ctypes.POINTER(_f32), ctypes.POINTER(_f32), ctypes.POINTER(_f32)])
@@ -68,10 +69,11 @@ _sig("arc_gather_order", [_P, _i64, _P])
 _sig("arc_tensor_scale", [_P, _i64, _i64, _i64, _P, _P])
 _sig("arc_quantize_weight", [_P, _i64, _i64, _i64, _P, _i32, _P, ctypes.c_int, _P, _P, _P])
 _sig("arc_quantize_activation", [_P, _i64, _i64, ctypes.POINTER(ArcProfile), _P, _P, _P])
-_sig("arc_gemm", [_P, _P, _P, _i64, ctypes.POINTER(ArcQWeight), _P, ctypes.c_int, _i64, _P])
+_sig("arc_gemm", [_P, _P, _P, _i64, ctypes.POINTER(ArcQWeight), _P, ctypes.c_int, _i64, _P, ctypes.c_size_t, _P])
 _sig("arc_linear", [_P, _i64, _i64, ctypes.POINTER(ArcProfile), ctypes.POINTER(ArcQWeight), _P, ctypes.c_int,
                     _i64, _P, ctypes.c_size_t, _P])
-_sig("arc_linear_hostio_workspace_size", [_i64, _i64, _i32, _i64, ctypes.c_int, ctypes.POINTER(ctypes.c_size_t)])
+_sig("arc_linear_hostio_workspace_size", [_i64, ctypes.POINTER(ArcQWeight), ctypes.c_int,
+                                         ctypes.POINTER(ctypes.c_size_t)])
 _sig("arc_linear_hostio", [_P, _i64, ctypes.POINTER(ArcProfile), ctypes.POINTER(ArcQWeight), _P, ctypes.c_int, _P,
                            ctypes.c_size_t, _P])
 _sig("arc_probe_e2m1", [_P, _i64, _P, _P])
@@ -81,7 +83,8 @@ _sig("arc_probe_e4m3_ceil", [_P, _i64, _P, _P])
 
 # every symbol include/arc.h and include/arc_probe.h declare (checked by tests)
 EXPORTED = [
-    "arc_status_string", "arc_last_error", "arc_device_supported", "arc_buffer_sizes", "arc_workspace_size",
+    "arc_status_string", "arc_last_error", "arc_device_supported", "arc_buffer_sizes", "arc_gemm_workspace_size",
+    "arc_linear_workspace_size",
     "arc_calib_absmax", "arc_select_outliers", "arc_gather_order", "arc_tensor_scale", "arc_quantize_weight",
     "arc_quantize_activation", "arc_gemm", "arc_linear", "arc_linear_hostio_workspace_size", "arc_linear_hostio",
     "arc_probe_e2m1", "arc_probe_e2m1_bits", "arc_probe_e2m1_raw_bits", "arc_probe_e4m3_ceil",
@@ -127,9 +130,15 @@ def buffer_sizes(rows: int, K: int, S: int):
     return kp.value, cb.value, sb.value
 
 
-def workspace_size(M: int, K: int, S: int) -> int:
+def gemm_workspace_size(M: int, qw) -> int:
     b = ctypes.c_size_t()
-    _check(_lib.arc_workspace_size(M, K, S, ctypes.byref(b)), "arc_workspace_size")
+    _check(_lib.arc_gemm_workspace_size(M, ctypes.byref(qw.c()), ctypes.byref(b)), "arc_gemm_workspace_size")
+    return b.value
+
+
+def linear_workspace_size(M: int, qw) -> int:
+    b = ctypes.c_size_t()
+    _check(_lib.arc_linear_workspace_size(M, ctypes.byref(qw.c()), ctypes.byref(b)), "arc_linear_workspace_size")
     return b.value
 
 
@@ -260,21 +269,19 @@ def quantize_activation(x: torch.Tensor, prof: Profile, codes=None, sf=None, str
     return codes, sf
 
 
+def _alloc_out(M: int, N: int, dtype, device) -> torch.Tensor:
+    """Output buffer whose row stride is a multiple of 16 bytes (the C ABI's ldy rule)."""
+    per16 = 16 // torch.empty(0, dtype=dtype).element_size()
+    ld = (N + per16 - 1) // per16 * per16
+    return torch.empty(M, ld, dtype=dtype, device=device)[:, :N]
+
+
 def _dtype_code(dt) -> int:
     if dt == torch.bfloat16:
         return BF16
     if dt == torch.float32:
         return FP32
     raise ValueError("out_dtype must be torch.bfloat16 or torch.float32")
-
-
-def gemm(a_codes, a_sf, gs_x: torch.Tensor, qw: QWeight, out_dtype=torch.bfloat16, out=None, stream=None):
-    M = a_codes.shape[0]
-    if out is None:
-        out = torch.empty(M, qw.N, dtype=out_dtype, device=a_codes.device)
-    _check(_lib.arc_gemm(_ptr(a_codes), _ptr(a_sf), _ptr(gs_x), M, ctypes.byref(qw.c()), _ptr(out),
-                         _dtype_code(out.dtype), out.stride(0), _stream(stream)), "arc_gemm")
-    return out
 
 
 class Workspace:
@@ -293,14 +300,32 @@ class Workspace:
 _default_ws = {}
 
 
+def gemm(a_codes, a_sf, gs_x: torch.Tensor, qw: QWeight, out_dtype=torch.bfloat16, out=None, ws: Workspace = None,
+         stream=None):
+    """The augmented NVFP4 GEMM (Eq.2): out = A_aug B_aug^T / (gs_x gs_w)."""
+    M = a_codes.shape[0]
+    if out is None:
+        out = _alloc_out(M, qw.N, out_dtype, a_codes.device)
+    need = gemm_workspace_size(M, qw)
+    buf = None
+    if need:
+        if ws is None:
+            ws = _default_ws.setdefault(("gemm", a_codes.device), Workspace(a_codes.device))
+        buf = ws.get(need)
+    _check(_lib.arc_gemm(_ptr(a_codes), _ptr(a_sf), _ptr(gs_x), M, ctypes.byref(qw.c()), _ptr(out),
+                         _dtype_code(out.dtype), out.stride(0), _ptr(buf), 0 if buf is None else buf.numel(),
+                         _stream(stream)), "arc_gemm")
+    return out
+
+
 def linear(x: torch.Tensor, prof: Profile, qw: QWeight, out_dtype=torch.bfloat16, out=None, ws: Workspace = None,
            stream=None):
     """The ARC linear layer: fused activation quantize + augmented NVFP4 GEMM (two launches)."""
     assert x.dtype == torch.bfloat16 and x.is_cuda
     M = x.shape[0]
     if out is None:
-        out = torch.empty(M, qw.N, dtype=out_dtype, device=x.device)
-    need = workspace_size(M, prof.K, prof.S)
+        out = _alloc_out(M, qw.N, out_dtype, x.device)
+    need = linear_workspace_size(M, qw)
     if ws is None:
         ws = _default_ws.setdefault(x.device, Workspace(x.device))
     buf = ws.get(need)
@@ -310,9 +335,9 @@ def linear(x: torch.Tensor, prof: Profile, qw: QWeight, out_dtype=torch.bfloat16
     return out
 
 
-def linear_hostio_workspace_size(M: int, K: int, S: int, N: int, out_dtype=torch.bfloat16) -> int:
+def linear_hostio_workspace_size(M: int, qw, out_dtype=torch.bfloat16) -> int:
     b = ctypes.c_size_t()
-    _check(_lib.arc_linear_hostio_workspace_size(M, K, S, N, _dtype_code(out_dtype), ctypes.byref(b)),
+    _check(_lib.arc_linear_hostio_workspace_size(M, ctypes.byref(qw.c()), _dtype_code(out_dtype), ctypes.byref(b)),
            "arc_linear_hostio_workspace_size")
     return b.value
 

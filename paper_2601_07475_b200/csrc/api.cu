@@ -122,12 +122,25 @@ arc_status_t arc_buffer_sizes(int64_t rows, int64_t K, int32_t S, int64_t* Kp, s
   return ARC_OK;
 }
 
-arc_status_t arc_workspace_size(int64_t M, int64_t K, int32_t S, size_t* bytes) {
-  size_t cb = 0, sb = 0;
-  arc_status_t s = arc_buffer_sizes(M, K, S, nullptr, &cb, &sb);
+static size_t act_ws_bytes(int64_t M, int64_t K, int32_t S) {
+  const int64_t kp = kp_of(K, S);
+  return (size_t)round_up(M * (kp / 2), 256) + (size_t)round_up(round_up(M, 128) * (kp / 16), 256);
+}
+
+arc_status_t arc_gemm_workspace_size(int64_t M, const arc_qweight_t* qw, size_t* bytes) {
+  arc_status_t s = check_qweight(qw);
   if (s != ARC_OK) return s;
   if (!bytes) return fail(ARC_ERR_NULL, "null bytes");
-  *bytes = (size_t)round_up((int64_t)cb, 256) + (size_t)round_up((int64_t)sb, 256);
+  if (M < 0) return fail(ARC_ERR_SHAPE, "M < 0");
+  *bytes = M == 0 ? 0 : plan_gemm(M, qw->N, qw->Kp).ws_bytes;
+  return ARC_OK;
+}
+
+arc_status_t arc_linear_workspace_size(int64_t M, const arc_qweight_t* qw, size_t* bytes) {
+  size_t g = 0;
+  arc_status_t s = arc_gemm_workspace_size(M, qw, &g);
+  if (s != ARC_OK) return s;
+  *bytes = act_ws_bytes(M, qw->K, qw->S) + (size_t)round_up((int64_t)g, 256);
   return ARC_OK;
 }
 
@@ -278,7 +291,8 @@ arc_status_t arc_quantize_activation(const void* x, int64_t M, int64_t ldx, cons
 }
 
 arc_status_t arc_gemm(const uint8_t* a_codes, const uint8_t* a_sf, const float* gs_x, int64_t M,
-                      const arc_qweight_t* qw, void* y, arc_dtype_t y_dtype, int64_t ldy, void* stream) {
+                      const arc_qweight_t* qw, void* y, arc_dtype_t y_dtype, int64_t ldy, void* ws, size_t ws_bytes,
+                      void* stream) {
   arc_status_t s = check_qweight(qw);
   if (s != ARC_OK) return s;
   if (M < 0 || M > (1 << 30)) return fail(ARC_ERR_SHAPE, "bad M");
@@ -288,6 +302,9 @@ arc_status_t arc_gemm(const uint8_t* a_codes, const uint8_t* a_sf, const float* 
   if (ldy < qw->N || ldy % (y_dtype == ARC_FP32 ? 4 : 8))
     return fail(ARC_ERR_SHAPE, "ldy must be >= N and a multiple of 16 bytes");
   if (!aligned16(a_codes) || !aligned16(a_sf) || !aligned16(y)) return fail(ARC_ERR_ALIGN, "buffer not 16B aligned");
+  const GemmPlan pl = plan_gemm(M, qw->N, qw->Kp);
+  if (pl.ws_bytes > 0 && (!ws || ws_bytes < pl.ws_bytes)) return fail(ARC_ERR_WORKSPACE, "split-K workspace too small");
+  if (ws && !aligned16(ws)) return fail(ARC_ERR_ALIGN, "ws not 16B aligned");
   s = check_device();
   if (s != ARC_OK) return s;
   if (M == 0) return ARC_OK;
@@ -304,6 +321,8 @@ arc_status_t arc_gemm(const uint8_t* a_codes, const uint8_t* a_sf, const float* 
   p.y = y;
   p.ldy = ldy;
   p.y_fp32 = y_dtype == ARC_FP32;
+  p.ws = ws;
+  p.ws_bytes = ws_bytes;
   const char* detail = nullptr;
   cudaError_t e = launch_gemm(p, (cudaStream_t)stream, &detail);
   return e == cudaSuccess ? ARC_OK : cuda_fail(e, "arc_gemm", detail);
@@ -321,23 +340,26 @@ arc_status_t arc_linear(const void* x, int64_t M, int64_t ldx, const arc_profile
   if (M == 0) return ARC_OK;
   if (!ws) return fail(ARC_ERR_NULL, "null workspace");
   size_t need = 0;
-  arc_workspace_size(M, prof->K, prof->S, &need);
+  s = arc_linear_workspace_size(M, qw, &need);
+  if (s != ARC_OK) return s;
   if (ws_bytes < need) return fail(ARC_ERR_WORKSPACE, "workspace too small");
   if ((reinterpret_cast<uintptr_t>(ws) & 255u) != 0) return fail(ARC_ERR_ALIGN, "workspace not 256B aligned");
   uint8_t* codes = static_cast<uint8_t*>(ws);
   uint8_t* sf = codes + round_up(M * (qw->Kp / 2), 256);
+  const size_t act = act_ws_bytes(M, qw->K, qw->S);
   s = arc_quantize_activation(x, M, ldx, prof, codes, sf, stream);
   if (s != ARC_OK) return s;
-  return arc_gemm(codes, sf, prof->gs, M, qw, y, y_dtype, ldy, stream);
+  return arc_gemm(codes, sf, prof->gs, M, qw, y, y_dtype, ldy, static_cast<uint8_t*>(ws) + act, ws_bytes - act,
+                  stream);
 }
 
-arc_status_t arc_linear_hostio_workspace_size(int64_t M, int64_t K, int32_t S, int64_t N, arc_dtype_t y_dtype,
+arc_status_t arc_linear_hostio_workspace_size(int64_t M, const arc_qweight_t* qw, arc_dtype_t y_dtype,
                                               size_t* bytes) {
   size_t w = 0;
-  arc_status_t s = arc_workspace_size(M, K, S, &w);
+  arc_status_t s = arc_linear_workspace_size(M, qw, &w);
   if (s != ARC_OK) return s;
-  const int64_t yb = M * N * (y_dtype == ARC_FP32 ? 4 : 2);
-  *bytes = w + (size_t)round_up(M * K * 2, 256) + (size_t)round_up(yb, 256);
+  const int64_t yb = M * qw->N * (y_dtype == ARC_FP32 ? 4 : 2);
+  *bytes = w + (size_t)round_up(M * qw->K * 2, 256) + (size_t)round_up(yb, 256);
   return ARC_OK;
 }
 
@@ -349,12 +371,12 @@ arc_status_t arc_linear_hostio(const void* x_host, int64_t M, const arc_profile_
   s = check_qweight(qw);
   if (s != ARC_OK) return s;
   size_t need = 0;
-  s = arc_linear_hostio_workspace_size(M, prof->K, prof->S, qw->N, y_dtype, &need);
+  s = arc_linear_hostio_workspace_size(M, qw, y_dtype, &need);
   if (s != ARC_OK) return s;
   if (ws_bytes < need) return fail(ARC_ERR_WORKSPACE, "workspace too small");
   if (M == 0) return ARC_OK;
   size_t lin = 0;
-  arc_workspace_size(M, prof->K, prof->S, &lin);
+  arc_linear_workspace_size(M, qw, &lin);
   uint8_t* base = static_cast<uint8_t*>(ws);
   void* xd = base + lin;
   void* yd = base + lin + round_up(M * prof->K * 2, 256);

@@ -27,7 +27,15 @@ struct GemmProblem {
   void* y;
   int64_t ldy;
   int y_fp32;
+  void* ws;          // split-K partials (decode-size M), may be null when plan.ws_bytes == 0
+  size_t ws_bytes;
 };
+struct GemmPlan {
+  int CL;            // CTAs per cluster (B-tile multicast)
+  int nsplit, kbs;   // split-K factor and K-blocks per split
+  size_t ws_bytes;   // fp32 partials nsplit*M*N
+};
+GemmPlan plan_gemm(int64_t M, int64_t N, int64_t Kp);
 // Returns a CUresult-style error through cudaError_t (cudaErrorUnknown + text) on encode failure.
 cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t stream, const char** detail);
 

@@ -64,6 +64,9 @@ struct Args {
   void* y;
   int64_t ldy;
   int y_fp32;
+  int nsplit;   // split-K factor (decode-size M): > 1 -> fp32 partials into ws[nsplit][M][N]
+  int kbs;      // K-blocks per split
+  float* ws;
   int debug;  // perf experiments only (env ARC_GEMM_DEBUG): 1 = no epilogue work, 2 = no scale copies, 3 = no stores, 4 = no TMEM loads
 };
 
@@ -95,7 +98,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const int num_m = (M + BM - 1) / BM;
   const int num_n = (N + BN - 1) / BN;
   const int num_mp = (num_m + CL - 1) / CL;   // M-tile groups (one per cluster step)
-  const int num_tiles = num_mp * num_n;       // cluster work items
+  const int nsplit = args.nsplit;
+  const int num_tiles = num_mp * num_n * nsplit;  // cluster work items (split-K innermost)
   const int rank = CL == 1 ? 0 : (int)cluster_ctarank();
   const int cid = blockIdx.x / CL, ncl = gridDim.x / CL;
   const uint16_t mc_mask = (uint16_t)((1u << CL) - 1u);
@@ -130,10 +134,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = cid; tile < num_tiles; tile += ncl) {
-        const int mb = (tile % num_mp) * CL + rank, nbk = tile / num_mp;
+        const int ks = tile % nsplit, rest = tile / nsplit;
+        const int mb = (rest % num_mp) * CL + rank, nbk = rest / num_mp;
         const int nrb = min(2, n_rb - 2 * nbk);   // existing 128-row scale blocks of this B tile
         const bool a_ok = mb < num_m;              // (CL = 2, odd num_m: the last rank-1 tile is empty)
-        for (int kb = 0; kb < nkb; ++kb) {
+        const int kb0 = ks * args.kbs, kb1 = min(nkb, kb0 + args.kbs);
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);     // the slot is free in EVERY CTA of the cluster
           const int nk = min(4, kc_total - kb * 4);
           uint8_t* sA = smem + stage * STAGE_BYTES;
@@ -168,11 +174,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       int t = 0;
       for (int tile = cid; tile < num_tiles; tile += ncl, ++t) {
         const int b = t & 1;
+        const int ks = tile % nsplit;
+        const int kb0 = ks * args.kbs, kb1 = min(nkb, kb0 + args.kbs);
         if (t >= 1) mbar_wait(ovl_free, (t - 1) & 1);            // shared columns drained (tile t-1)
         if (t >= 2) mbar_wait(&buf_free[b], ((t - 2) >> 1) & 1);  // own columns drained (tile t-2)
         tc_fence_after();
         const uint32_t acc = tmem + b * ACC1_COL;
-        for (int kb = 0; kb < nkb; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const int nk = min(4, kc_total - kb * 4);
@@ -189,7 +197,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           for (int kk = 0; kk < nk; ++kk) {
             const uint64_t ad = smem_desc(sA + kk * 32, 16, 1024, kLayoutSwizzle128B);
             const uint64_t bd = smem_desc(sB + kk * 32, 16, 1024, kLayoutSwizzle128B);
-            mma_nvf4(acc, ad, bd, kIdesc, (kb | kk) != 0, tmem + SFA_COL + 4 * kk, tmem + SFB_COL + 8 * kk);
+            mma_nvf4(acc, ad, bd, kIdesc, (kb != kb0) || (kk != 0), tmem + SFA_COL + 4 * kk, tmem + SFB_COL + 8 * kk);
           }
           if (CL == 1) tc_commit(&empty[stage]);
           else tc_commit_mc(&empty[stage], mc_mask);  // frees the slot in both CTAs
@@ -204,7 +212,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const float alpha = __fdiv_rn(1.0f, __fmul_rn(__ldg(args.gs_x), __ldg(args.gs_w)));
     int t = 0;
     for (int tile = cid; tile < num_tiles; tile += ncl, ++t) {
-      const int mb = (tile % num_mp) * CL + rank, nbk = tile / num_mp;
+      const int ks = tile % nsplit, rest = tile / nsplit;
+      const int mb = (rest % num_mp) * CL + rank, nbk = rest / num_mp;
       mbar_wait(tfull, t & 1);
       tc_fence_after();
       const int m = mb * BM + q * 32 + lane;
@@ -244,9 +253,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           mbar_arrive(&buf_free[b]);
         }
         const int n0 = nbk * BN + c * 32;
-        if (args.y_fp32 && m < M && n0 < N) {
+        if ((args.y_fp32 || nsplit > 1) && m < M && n0 < N) {
           {
-            float* yr = static_cast<float*>(args.y) + (int64_t)m * args.ldy + n0;
+            float* yr = nsplit > 1 ? args.ws + ((int64_t)ks * M + m) * N + n0
+                                   : static_cast<float*>(args.y) + (int64_t)m * args.ldy + n0;
             if (n0 + 32 <= N) {
 #pragma unroll
               for (int j = 0; j < 32; j += 4)
@@ -260,7 +270,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             }
           }
         }
-        if (!args.y_fp32 && mb * BM + q * 32 < M && n0 < N && args.debug != 3) {
+        if (!args.y_fp32 && nsplit == 1 && mb * BM + q * 32 < M && n0 < N && args.debug != 3) {
           // bf16: stage the 32x32 sub-tile in smem (64B swizzle: 16-byte unit u of row
           // r lives at unit u ^ ((r >> 1) & 3), bank-conflict-free) and TMA-store it
           // (coalesced, clipped at the M/N edges by the tensor map).
@@ -315,6 +325,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   }
 }
 
+// Deterministic split-K reduction: y[m][n] = sum_ks ws[ks][m][n] in ks order.
+__global__ void arc_splitk_reduce_kernel(const float* __restrict__ ws, int nsplit, int M, int N, void* y,
+                                         int64_t ldy, int y_fp32) {
+  const int64_t total = (int64_t)M * N;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    float acc = ws[i];
+    for (int k = 1; k < nsplit; ++k) acc = __fadd_rn(acc, ws[(int64_t)k * total + i]);
+    const int64_t m = i / N, n = i - m * N;
+    if (y_fp32) static_cast<float*>(y)[m * ldy + n] = acc;
+    else static_cast<__nv_bfloat16*>(y)[m * ldy + n] = __float2bfloat16_rn(acc);
+  }
+}
+
 // ------------------------------------------------------------------ host side
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -358,9 +381,34 @@ bool make_y_map(CUtensorMap* m, void* y, int64_t rows, int64_t cols, int64_t ldy
 
 }  // namespace
 
-cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t stream, const char** detail) {
+GemmPlan plan_gemm(int64_t M, int64_t N, int64_t Kp) {
   static const int env_cl = getenv("ARC_GEMM_CL") ? atoi(getenv("ARC_GEMM_CL")) : 2;
-  const int CL = env_cl == 1 ? 1 : 2;
+  GemmPlan pl;
+  const int64_t num_m = (M + BM - 1) / BM, num_n = (N + BN - 1) / BN, nkb = (Kp + BK - 1) / BK;
+  pl.CL = (env_cl == 1 || num_m < 2) ? 1 : 2;
+  const int64_t items = ((num_m + pl.CL - 1) / pl.CL) * num_n;  // cluster work items without split
+  const int64_t clusters = num_sms() / pl.CL;
+  pl.nsplit = 1;
+  pl.kbs = (int)nkb;
+  if (items < clusters && nkb >= 4) {
+    // decode-size M: split K so ~every SM streams weights; >= 2 K-blocks per split
+    int64_t want = std::min<int64_t>((clusters + items - 1) / items, nkb / 2);
+    if (want > 1) {
+      pl.kbs = (int)((nkb + want - 1) / want);
+      pl.nsplit = (int)((nkb + pl.kbs - 1) / pl.kbs);
+    }
+  }
+  pl.ws_bytes = pl.nsplit > 1 ? (size_t)pl.nsplit * (size_t)M * (size_t)N * sizeof(float) : 0;
+  return pl;
+}
+
+cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t stream, const char** detail) {
+  const GemmPlan pl = plan_gemm(p.M, p.N, p.Kp);
+  const int CL = pl.CL;
+  if (pl.nsplit > 1 && (p.ws == nullptr || p.ws_bytes < pl.ws_bytes)) {
+    if (detail) *detail = "split-K workspace too small";
+    return cudaErrorInvalidValue;
+  }
   CUtensorMap tmA, tmB, tmY;
   memset(&tmY, 0, sizeof(tmY));
   if (!p.y_fp32 && !make_y_map(&tmY, p.y, p.M, p.N, p.ldy)) {
@@ -392,8 +440,11 @@ cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t stream, const char** 
   a.y_fp32 = p.y_fp32;
   static const int dbg = getenv("ARC_GEMM_DEBUG") ? atoi(getenv("ARC_GEMM_DEBUG")) : 0;
   a.debug = dbg;
+  a.nsplit = pl.nsplit;
+  a.kbs = pl.kbs;
+  a.ws = static_cast<float*>(p.ws);
   const int64_t num_m = (p.M + BM - 1) / BM, num_n = (p.N + BN - 1) / BN;
-  const int64_t work = ((num_m + CL - 1) / CL) * num_n;  // cluster work items
+  const int64_t work = ((num_m + CL - 1) / CL) * num_n * pl.nsplit;  // cluster work items
   const int64_t grid = std::min<int64_t>(work, num_sms() / CL) * CL;
   cudaLaunchConfig_t cfg;
   memset(&cfg, 0, sizeof(cfg));
@@ -411,6 +462,12 @@ cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t stream, const char** 
   cudaError_t e = CL == 1 ? cudaLaunchKernelEx(&cfg, arc_gemm_kernel<1>, tmA, tmB, tmY, a)
                           : cudaLaunchKernelEx(&cfg, arc_gemm_kernel<2>, tmA, tmB, tmY, a);
   if (e != cudaSuccess) return e;
+  if (pl.nsplit > 1) {
+    const int64_t total = p.M * p.N;
+    const int64_t rg = std::min<int64_t>((total + 255) / 256, (int64_t)num_sms() * 8);
+    arc_splitk_reduce_kernel<<<(unsigned)rg, 256, 0, stream>>>(static_cast<const float*>(p.ws), pl.nsplit, (int)p.M,
+                                                              (int)p.N, p.y, p.ldy, p.y_fp32);
+  }
   return cudaGetLastError();
 }
 

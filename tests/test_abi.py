@@ -64,7 +64,7 @@ def test_validation_is_synchronous(arc):
     assert lib.arc_quantize_activation(fake, 4, 128, ctypes.byref(prof), fake, fake, None) == 2
     # qweight Kp mismatch -> ARC_ERR_SHAPE
     qw = arc.ArcQWeight(64, 256, 256, 16, 0, 0x10000, 0x10000, 0x10000)
-    assert lib.arc_gemm(fake, fake, fake, 4, ctypes.byref(qw), fake, 0, 64, None) == 2
+    assert lib.arc_gemm(fake, fake, fake, 4, ctypes.byref(qw), fake, 0, 64, None, 0, None) == 2
     # workspace too small -> ARC_ERR_WORKSPACE
     qw = arc.ArcQWeight(64, 256, 320, 16, 0, 0x10000, 0x10000, 0x10000)
     assert lib.arc_linear(fake, 4, 256, ctypes.byref(prof), ctypes.byref(qw), fake, 0, 64, fake, 16, None) == 5
@@ -83,7 +83,7 @@ def test_no_fallback_without_sm100(arc):
     assert lib.arc_device_supported() == 0
     assert lib.arc_quantize_activation(fake, 4, 256, ctypes.byref(prof), fake, fake, None) == 4
     qw = arc.ArcQWeight(64, 256, 320, 16, 0, 0x10000, 0x10000, 0x10000)
-    assert lib.arc_gemm(fake, fake, fake, 4, ctypes.byref(qw), fake, 0, 64, None) == 4
+    assert lib.arc_gemm(fake, fake, fake, 4, ctypes.byref(qw), fake, 0, 64, None, 0, None) == 4
 
 
 def test_select_outliers_matches_oracle(arc):

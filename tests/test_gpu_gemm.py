@@ -101,7 +101,7 @@ def test_hostio_matches_device_path(A):
     y_dev = A.linear(x, prof, qw, out_dtype=torch.bfloat16)
     xh = x.cpu().pin_memory()
     yh = torch.empty(M, N, dtype=torch.bfloat16).pin_memory()
-    ws = torch.empty(A.linear_hostio_workspace_size(M, K, S, N), dtype=torch.uint8, device="cuda")
+    ws = torch.empty(A.linear_hostio_workspace_size(M, qw), dtype=torch.uint8, device="cuda")
     A.linear_hostio(xh, prof, qw, yh, ws)
     assert torch.equal(yh, y_dev.cpu())
 
@@ -125,3 +125,21 @@ def test_cublaslt_cross_check(A):
     ref = ref / (prof.gs * qw.gs)
     torch.cuda.synchronize()
     assert torch.allclose(y, ref, rtol=1e-4, atol=1e-3 * float(ref.abs().max()))
+
+
+@pytest.mark.parametrize("M,N,K,S", [(1, 4096, 4096, 128), (16, 6144, 4096, 128), (64, 1024, 14336, 128),
+                                     (16, 300, 1024, 64), (33, 4096, 4096, 0)])
+def test_decode_splitk_parity(A, M, N, K, S):
+    """Decode-size M takes the split-K plan (fp32 partials + fixed-order reduction);
+    fp32 and bf16 outputs against the oracle's exact GEMM."""
+    x, w, prof, qw = _problem(A, M, N, K, S, seed=M * 7 + N)
+    codes, sf = A.quantize_activation(x, prof)
+    y32 = A.gemm(codes, sf, prof.gs, qw, out_dtype=torch.float32)
+    y16 = A.linear(x, prof, qw, out_dtype=torch.bfloat16)
+    torch.cuda.synchronize()
+    yref, bound = oracle.gemm_reference(codes.cpu().numpy(), sf.cpu().numpy(), qw.codes.cpu().numpy(),
+                                        qw.sf.cpu().numpy(), float(prof.gs.item()), float(qw.gs.item()))
+    _check(y32.cpu().numpy().astype(np.float64), yref, bound, False)
+    _check(y16.float().cpu().numpy().astype(np.float64), yref, bound, True)
+    if M <= 64 and N >= 1024:
+        assert A.gemm_workspace_size(M, qw) > 0, "decode-size M should use the split-K plan"
