@@ -22,6 +22,8 @@
 #include "arc_device.cuh"
 #include "arc_internal.h"
 
+#include <cuda_fp16.h>
+
 #include <cstdlib>
 
 namespace arc {
@@ -47,6 +49,7 @@ struct QuantArgs {
   int32_t stages;
   int32_t npw;     // primary warps
   int32_t nrw;     // residual warps
+  int32_t bulk;    // producer uses one cp.async.bulk per row (else 16-byte cp.async per lane)
   int32_t debug;   // perf experiments only (env ARC_QUANT_DEBUG): 1 = skip compute, 2 = skip loads
 };
 
@@ -62,18 +65,97 @@ ARC_DEV float2 mul2(float a, float b, float k) {
 }
 
 // One NVFP4 stage on 16 values (oracle C4) given the block's multiplier k:
-// t = z*k, q = rne_e2m1(t), packed with element 2i in the low nibble of byte i.
+// t = z*k (mul.rn.f32x2), q = rne_e2m1(t) (cvt.rn.satfinite.e2m1x2), packed with
+// element 2i in the low nibble of byte i (bytes assembled by the PTX byte-vector mov).
 ARC_DEV uint2 encode16(const float (&z)[16], float k) {
-  uint32_t b[8];
+  float t[16];
+#pragma unroll
+  for (int i = 0; i < 16; i += 2) {
+    const float2 p = mul2(z[i], z[i + 1], k);
+    t[i] = p.x;
+    t[i + 1] = p.y;
+  }
+  uint32_t w0, w1;
+  asm("{\n\t.reg .b8 b<8>;\n\t"
+      "cvt.rn.satfinite.e2m1x2.f32 b0, %3, %2;\n\t"
+      "cvt.rn.satfinite.e2m1x2.f32 b1, %5, %4;\n\t"
+      "cvt.rn.satfinite.e2m1x2.f32 b2, %7, %6;\n\t"
+      "cvt.rn.satfinite.e2m1x2.f32 b3, %9, %8;\n\t"
+      "cvt.rn.satfinite.e2m1x2.f32 b4, %11, %10;\n\t"
+      "cvt.rn.satfinite.e2m1x2.f32 b5, %13, %12;\n\t"
+      "cvt.rn.satfinite.e2m1x2.f32 b6, %15, %14;\n\t"
+      "cvt.rn.satfinite.e2m1x2.f32 b7, %17, %16;\n\t"
+      "mov.b32 %0, {b0, b1, b2, b3};\n\t"
+      "mov.b32 %1, {b4, b5, b6, b7};\n\t}"
+      : "=r"(w0), "=r"(w1)
+      : "f"(t[0]), "f"(t[1]), "f"(t[2]), "f"(t[3]), "f"(t[4]), "f"(t[5]), "f"(t[6]), "f"(t[7]), "f"(t[8]),
+        "f"(t[9]), "f"(t[10]), "f"(t[11]), "f"(t[12]), "f"(t[13]), "f"(t[14]), "f"(t[15]));
+#if ARC_E2M1_SIGN_FIXUP
+  uint32_t s0 = 0, s1 = 0;
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
-    const float2 t = mul2(z[2 * i], z[2 * i + 1], k);
-    b[i] = e2m1x2(t.x, t.y);  // one code byte in bits 0..7
+    s0 |= (__float_as_uint(t[i]) >> 31) << (4 * i + 3);
+    s1 |= (__float_as_uint(t[i + 8]) >> 31) << (4 * i + 3);
   }
-  // bytes -> words with byte permutes (2 pair merges + 1 word merge per 4 bytes)
-  const uint32_t p01 = __byte_perm(b[0], b[1], 0x0040), p23 = __byte_perm(b[2], b[3], 0x0040);
-  const uint32_t p45 = __byte_perm(b[4], b[5], 0x0040), p67 = __byte_perm(b[6], b[7], 0x0040);
-  return make_uint2(__byte_perm(p01, p23, 0x5410), __byte_perm(p45, p67, 0x5410));
+  w0 = (w0 & 0x77777777u) | s0;
+  w1 = (w1 & 0x77777777u) | s1;
+#endif
+  return make_uint2(w0, w1);
+}
+
+ARC_DEV uint2 encode16(const float (&z)[16], float k, float (&t)[16]) {
+#pragma unroll
+  for (int i = 0; i < 16; i += 2) {
+    const float2 p = mul2(z[i], z[i + 1], k);
+    t[i] = p.x;
+    t[i + 1] = p.y;
+  }
+  uint32_t w0, w1;
+  asm("{\n\t.reg .b8 b<8>;\n\t"
+      "cvt.rn.satfinite.e2m1x2.f32 b0, %3, %2;\n\t"
+      "cvt.rn.satfinite.e2m1x2.f32 b1, %5, %4;\n\t"
+      "cvt.rn.satfinite.e2m1x2.f32 b2, %7, %6;\n\t"
+      "cvt.rn.satfinite.e2m1x2.f32 b3, %9, %8;\n\t"
+      "cvt.rn.satfinite.e2m1x2.f32 b4, %11, %10;\n\t"
+      "cvt.rn.satfinite.e2m1x2.f32 b5, %13, %12;\n\t"
+      "cvt.rn.satfinite.e2m1x2.f32 b6, %15, %14;\n\t"
+      "cvt.rn.satfinite.e2m1x2.f32 b7, %17, %16;\n\t"
+      "mov.b32 %0, {b0, b1, b2, b3};\n\t"
+      "mov.b32 %1, {b4, b5, b6, b7};\n\t}"
+      : "=r"(w0), "=r"(w1)
+      : "f"(t[0]), "f"(t[1]), "f"(t[2]), "f"(t[3]), "f"(t[4]), "f"(t[5]), "f"(t[6]), "f"(t[7]), "f"(t[8]),
+        "f"(t[9]), "f"(t[10]), "f"(t[11]), "f"(t[12]), "f"(t[13]), "f"(t[14]), "f"(t[15]));
+  return make_uint2(w0, w1);
+}
+
+// e = t - v(q) for 16 codes (exact: t and v(q) are multiples of ulp(t)).  The
+// E2M1 values come from the hardware decoder cvt.rn.f16x2.e2m1x2 (exact in f16).
+ARC_DEV void residual16(const float (&t)[16], uint2 packed, float (&e)[16]) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const uint32_t w = i < 4 ? packed.x : packed.y;
+    const uint32_t byte = (w >> (8 * (i & 3))) & 0xFFu;
+    uint32_t h2;
+    asm("{\n\t.reg .b8 b;\n\t.reg .b16 lo, hi;\n\t"
+        "cvt.u8.u32 b, %1;\n\t"
+        "cvt.rn.f16x2.e2m1x2 %0, b;\n\t}"
+        : "=r"(h2)
+        : "r"(byte));
+    const float2 v = __half22float2(*reinterpret_cast<const __half2*>(&h2));
+    e[2 * i] = __fsub_rn(t[2 * i], v.x);
+    e[2 * i + 1] = __fsub_rn(t[2 * i + 1], v.y);
+  }
+}
+
+// k2 = RN(d1 / d2) for scale codes c1, c2 (oracle STAGE's k with base d1).  For two
+// normal E4M3 values the quotient is 2^(e1-e2) * (8+m1)/(8+m2), so RN commutes with
+// the power of two: k2 = RN((8+m1)/(8+m2)) scaled by 2^(e1-e2) (exact exponent add).
+// Subnormal codes take the IEEE division.
+ARC_DEV float ratio_k(uint32_t c1, uint32_t c2, const float* rat) {
+  if (c2 == 0u) return 0.0f;
+  if (c1 < 8u || c2 < 8u) return __fdiv_rn(e4m3_value(c1), e4m3_value(c2));
+  const float r = rat[((c1 & 7u) << 3) | (c2 & 7u)];
+  return __uint_as_float(__float_as_uint(r) + ((int)(c1 >> 3) - (int)(c2 >> 3)) * (1 << 23));
 }
 
 // max |z| over 16 values as a shallow tree (exact; order-independent)
@@ -141,7 +223,9 @@ __global__ void __launch_bounds__(1024) arc_quant_kernel(QuantArgs p) {
   const int K = p.K;
   const int npw = p.npw, nrw = p.nrw;
   float* k1tab = reinterpret_cast<float*>(smem + ST * SLOT);
-  uint64_t* full = reinterpret_cast<uint64_t*>(k1tab + 128);
+  float* c6tab = k1tab + 128;  // RN(e4m3(c) / 6): the residual stage's c6 for base d1 = e4m3(c)
+  float* rat = c6tab + 128;    // RN((8+m1)/(8+m2)): mantissa ratio of two normal E4M3 scales
+  uint64_t* full = reinterpret_cast<uint64_t*>(rat + 64);
   uint64_t* empty = full + ST;
 
   const int tid = threadIdx.x;
@@ -153,14 +237,18 @@ __global__ void __launch_bounds__(1024) arc_quant_kernel(QuantArgs p) {
   if (tid == 0) {
 #pragma unroll
     for (int s = 0; s < ST; ++s) {
-      mbar_init(&full[s], 32);
+      mbar_init(&full[s], p.bulk ? 1 : 32);
       mbar_init(&empty[s], npw + nrw);
     }
     fence_mbar_init();
   }
   // k1 = RN(gs / e4m3(c)) for every scale code: the primary stage's multiplier
   // depends only on the code, so the IEEE division is done once per CTA.
-  for (int c = tid; c < 128; c += blockDim.x) k1tab[c] = (c == 0 || c == 127) ? 0.0f : __fdiv_rn(gs, e4m3_value((uint32_t)c));
+  for (int c = tid; c < 128; c += blockDim.x) {
+    k1tab[c] = (c == 0 || c == 127) ? 0.0f : __fdiv_rn(gs, e4m3_value((uint32_t)c));
+    c6tab[c] = __fdiv_rn(e4m3_value((uint32_t)c), 6.0f);
+    if (c < 64) rat[c] = __fdiv_rn((float)(8 + (c >> 3)), (float)(8 + (c & 7)));
+  }
   __syncthreads();
 
   if (warp == npw + nrw) {
@@ -175,15 +263,27 @@ __global__ void __launch_bounds__(1024) arc_quant_kernel(QuantArgs p) {
           if (j >= ST) mbar_wait(&empty[s], ((j / ST) - 1) & 1);
           const int r0 = ((int)blockIdx.x + j * (int)gridDim.x) * R;
           const int nr = min(R, (int)p.rows - r0);
-          if (p.debug != 2) {
-            const uint16_t* src0 = p.x + (int64_t)r0 * p.ld + lane * 8;
+          if (p.bulk) {
+            // one cp.async.bulk per row (TMA engine, no LSU/MIO traffic); lane 0 only
+            if (lane == 0) {
+              mbar_expect_tx(&full[s], (uint32_t)(nr * K * 2));
+              if (p.debug != 2)
+                for (int r = 0; r < nr; ++r)
+                  bulk_load(smem + s * SLOT + r * ROWB, p.x + (int64_t)(r0 + r) * p.ld, (uint32_t)K * 2, &full[s]);
+              else
+                mbar_complete_tx_self(&full[s], (uint32_t)(nr * K * 2));
+            }
+          } else {
+            if (p.debug != 2) {
+              const uint16_t* src0 = p.x + (int64_t)r0 * p.ld + lane * 8;
 #pragma unroll
-            for (int r = 0; r < R; ++r)
-              if (r < nr)
-                for (int c = 0; c < kc - lane; c += 32)
-                  cp_async16(ring + (uint32_t)(s * SLOT + r * ROWB + c * 16), src0 + (int64_t)r * p.ld + c * 8);
+              for (int r = 0; r < R; ++r)
+                if (r < nr)
+                  for (int c = 0; c < kc - lane; c += 32)
+                    cp_async16(ring + (uint32_t)(s * SLOT + r * ROWB + c * 16), src0 + (int64_t)r * p.ld + c * 8);
+            }
+            cp_async_arrive(&full[s]);
           }
-          cp_async_arrive(&full[s]);
         }
       }
     }
@@ -314,21 +414,16 @@ __global__ void __launch_bounds__(1024) arc_quant_kernel(QuantArgs p) {
               float z[16];
               gather16(smem + s * SLOT, off, z);
               const uint32_t sf1 = e4m3_ceil_nb(__fmul_rn(absmax16(z), c6g));
-              const float k1 = k1tab[sf1];
-              uint2 packed = encode16(z, k1);
+              float t[16];
+              uint2 packed = encode16(z, k1tab[sf1], t);
               uint32_t sfb = sf1;
               if (!p.weight_mode) {
-                // residual of the encoded primary in units of d1/gs, exact (Q6); stage 2, base d1
+                // residual of the encoded primary in units of d1/gs, exact (Q6): e = t - v(q1);
+                // stage 2 with base d1: c6 = RN(d1/6) (table), k2 = RN(d1/d2)
                 float e[16];
-#pragma unroll
-                for (int q = 0; q < 16; ++q) {
-                  const uint32_t c = (q < 8 ? packed.x >> (4 * q) : packed.y >> (4 * (q - 8))) & 15u;
-                  e[q] = __fsub_rn(__fmul_rn(z[q], k1), e2m1_value(c));  // t - v(q1)
-                }
-                const float d1 = e4m3_value(sf1);
-                const uint32_t sf2 = e4m3_ceil_nb(__fmul_rn(absmax16(e), __fdiv_rn(d1, 6.0f)));
-                const float d2 = e4m3_value(sf2);
-                packed = encode16(e, d2 == 0.0f ? 0.0f : __fdiv_rn(d1, d2));
+                residual16(t, packed, e);
+                const uint32_t sf2 = e4m3_ceil_nb(__fmul_rn(absmax16(e), c6tab[sf1]));
+                packed = encode16(e, ratio_k(sf1, sf2, rat));
                 sfb = sf2;
               }  // weight mode: bitwise duplicate of the primary block
               *reinterpret_cast<uint2*>(p.codes + (int64_t)m * code_row + pb * 8) = packed;
@@ -399,7 +494,7 @@ template <int IPT, int R, int ROWB, int ST>
 static cudaError_t launch_quant_cfg(QuantArgs a, int threads, cudaStream_t stream) {
   a.rows_per_tile = R;
   a.stages = ST;
-  const size_t smem = (size_t)ST * R * ROWB + 128 * 4 + 2 * ST * 8;
+  const size_t smem = (size_t)ST * R * ROWB + (128 + 128 + 64) * 4 + 2 * ST * 8;
   struct Cfg { int dev, threads; size_t smem; int occ; };
   static thread_local Cfg cache[8];
   static thread_local int ncache = 0;
@@ -444,6 +539,9 @@ cudaError_t launch_quant(const void* x, int64_t rows, int K, int64_t ld, const i
   a.Kp = (int)kp_of(K, S);
   static const int dbg = getenv("ARC_QUANT_DEBUG") ? atoi(getenv("ARC_QUANT_DEBUG")) : 0;
   a.debug = dbg;
+  static const int bulk_env = getenv("ARC_QUANT_BULK") ? atoi(getenv("ARC_QUANT_BULK")) : -1;
+  // whole-row bulk copies need 16-byte aligned rows (ld % 8 == 0 is validated) -- always true here
+  a.bulk = bulk_env >= 0 ? bulk_env : 1;
   const int NB = a.Kp / 16, ns = S / 16;
   const int nprim = NB - ns;                 // primary + pad blocks per row
   const int ipt = (nprim + 28 * 32 - 1) / (28 * 32);  // <= 28 primary warps
