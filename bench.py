@@ -384,7 +384,7 @@ def main():
     if not args.no_e2e:
         xs = [s.x.cpu().pin_memory() for s in sites]
         ys = [torch.empty(s.M, s.N, dtype=torch.bfloat16).pin_memory() for s in sites]
-        wss = [torch.empty(A.linear_hostio_workspace_size(s.M, s.qw), dtype=torch.uint8, device=device)
+        wss = [torch.zeros(A.linear_hostio_workspace_size(s.M, s.qw), dtype=torch.uint8, device=device)
                for s in sites]
         for _ in range(2):
             for s, xh, yh, ws in zip(sites, xs, ys, wss):

@@ -285,7 +285,9 @@ def _dtype_code(dt) -> int:
 
 
 class Workspace:
-    """Grow-only device workspace for arc_linear (256-byte aligned by the allocator)."""
+    """Grow-only device workspace for arc_gemm / arc_linear (256-byte aligned by the
+    allocator, zero-filled on allocation: the split-K tile counters must start at 0,
+    and the kernels leave them at 0)."""
 
     def __init__(self, device="cuda"):
         self.device = device
@@ -293,7 +295,7 @@ class Workspace:
 
     def get(self, nbytes: int) -> torch.Tensor:
         if self.buf is None or self.buf.numel() < nbytes:
-            self.buf = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=self.device)
+            self.buf = torch.zeros(max(nbytes, 256), dtype=torch.uint8, device=self.device)
         return self.buf
 
 

@@ -101,7 +101,7 @@ def test_hostio_matches_device_path(A):
     y_dev = A.linear(x, prof, qw, out_dtype=torch.bfloat16)
     xh = x.cpu().pin_memory()
     yh = torch.empty(M, N, dtype=torch.bfloat16).pin_memory()
-    ws = torch.empty(A.linear_hostio_workspace_size(M, qw), dtype=torch.uint8, device="cuda")
+    ws = torch.zeros(A.linear_hostio_workspace_size(M, qw), dtype=torch.uint8, device="cuda")
     A.linear_hostio(xh, prof, qw, yh, ws)
     assert torch.equal(yh, y_dev.cpu())
 
