@@ -260,7 +260,10 @@ __global__ void __launch_bounds__(1024) arc_quant_kernel(QuantArgs p) {
       for (int s = 0; s < ST; ++s) {
         const int j = j0 + s;
         if (j < my_tiles) {
-          if (j >= ST) mbar_wait(&empty[s], ((j / ST) - 1) & 1);
+          if (j >= ST) {
+            mbar_wait(&empty[s], ((j / ST) - 1) & 1);
+            fence_proxy_async();  // order the consumers' generic-proxy reads before the async refill
+          }
           const int r0 = ((int)blockIdx.x + j * (int)gridDim.x) * R;
           const int nr = min(R, (int)p.rows - r0);
           if (p.bulk) {
