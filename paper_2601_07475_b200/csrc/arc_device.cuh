@@ -240,6 +240,11 @@ ARC_DEV uint64_t smem_desc(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_byte
 constexpr uint32_t kLayoutSwizzle128B = 2;
 constexpr uint32_t kLayoutSwizzleNone = 0;
 
+// Programmatic dependent launch: let the next kernel in the stream start its prologue,
+// and wait (before touching global memory) until the previous kernel has completed.
+ARC_DEV void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+ARC_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 ARC_DEV uint32_t elect_one() {
   uint32_t pred = 0;
   asm volatile(

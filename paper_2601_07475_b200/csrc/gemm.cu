@@ -121,10 +121,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     prefetch_tmap(&tmB);
   }
   if (warp == 1) tmem_alloc(tmem_holder, TMEM_COLS);
+  pdl_launch_dependents();
   tc_fence_before();
   __syncthreads();
   if (CL > 1) cluster_sync();  // peers' barriers initialised before any multicast lands
   tc_fence_after();
+  pdl_wait();  // everything above overlaps the previous kernel's tail (PDL)
   const uint32_t tmem = *tmem_holder;
 
   if (warp == 0) {
@@ -328,6 +330,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 // Deterministic split-K reduction: y[m][n] = sum_ks ws[ks][m][n] in ks order.
 __global__ void arc_splitk_reduce_kernel(const float* __restrict__ ws, int nsplit, int M, int N, void* y,
                                          int64_t ldy, int y_fp32) {
+  pdl_launch_dependents();
+  pdl_wait();
   const int64_t total = (int64_t)M * N;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     float acc = ws[i];
@@ -452,21 +456,34 @@ cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t stream, const char** 
   cfg.blockDim = dim3(NUM_THREADS);
   cfg.dynamicSmemBytes = SMEM_BYTES;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = CL;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   cudaError_t e = CL == 1 ? cudaLaunchKernelEx(&cfg, arc_gemm_kernel<1>, tmA, tmB, tmY, a)
                           : cudaLaunchKernelEx(&cfg, arc_gemm_kernel<2>, tmA, tmB, tmY, a);
   if (e != cudaSuccess) return e;
   if (pl.nsplit > 1) {
     const int64_t total = p.M * p.N;
     const int64_t rg = std::min<int64_t>((total + 255) / 256, (int64_t)num_sms() * 8);
-    arc_splitk_reduce_kernel<<<(unsigned)rg, 256, 0, stream>>>(static_cast<const float*>(p.ws), pl.nsplit, (int)p.M,
-                                                              (int)p.N, p.y, p.ldy, p.y_fp32);
+    cudaLaunchConfig_t rc;
+    memset(&rc, 0, sizeof(rc));
+    rc.gridDim = dim3((unsigned)rg);
+    rc.blockDim = dim3(256);
+    rc.stream = stream;
+    cudaLaunchAttribute ra[1];
+    ra[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    ra[0].val.programmaticStreamSerializationAllowed = 1;
+    rc.attrs = ra;
+    rc.numAttrs = 1;
+    e = cudaLaunchKernelEx(&rc, arc_splitk_reduce_kernel, static_cast<const float*>(p.ws), (int)pl.nsplit, (int)p.M,
+                           (int)p.N, p.y, p.ldy, p.y_fp32);
+    if (e != cudaSuccess) return e;
   }
   return cudaGetLastError();
 }

@@ -25,6 +25,7 @@
 #include <cuda_fp16.h>
 
 #include <cstdlib>
+#include <cstring>
 
 namespace arc {
 
@@ -232,6 +233,8 @@ __global__ void __launch_bounds__(1024) arc_quant_kernel(QuantArgs p) {
   const int warp = tid >> 5, lane = tid & 31;
   const int ntile = (int)((p.rows + R - 1) / R);
   const int my_tiles = ntile > (int)blockIdx.x ? (ntile - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
+  pdl_launch_dependents();
+  pdl_wait();  // (PDL) the previous kernel's writes are visible from here on
   const float gs = __ldg(p.gs);
 
   if (tid == 0) {
@@ -521,7 +524,19 @@ static cudaError_t launch_quant_cfg(QuantArgs a, int threads, cudaStream_t strea
   }
   const int64_t ntile = (a.rows + R - 1) / R;
   const int64_t grid = imin64(ntile, (int64_t)num_sms() * occ);
-  arc_quant_kernel<IPT, R, ROWB, ST><<<(unsigned)grid, threads, smem, stream>>>(a);
+  cudaLaunchConfig_t cfg;
+  memset(&cfg, 0, sizeof(cfg));
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, arc_quant_kernel<IPT, R, ROWB, ST>, a);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
