@@ -565,14 +565,20 @@ cudaError_t launch_quant(const void* x, int64_t rows, int K, int64_t ld, const i
   const int ipt = (nprim + 28 * 32 - 1) / (28 * 32);  // <= 28 primary warps
   a.npw = (nprim + ipt * 32 - 1) / (ipt * 32);
   const int64_t rowb = (int64_t)K * 2;
-  const int R = rowb <= 16384 ? 2 : (rowb <= 32768 ? 2 : 1);
-  a.nrw = ns == 0 ? 0 : (int)imin64(2, (R * ns + 31) / 32);
+  a.nrw = ns == 0 ? 0 : (int)imin64(2, (ns + 31) / 32);  // ipt == 2 configuration: R = 1
   const int threads = (a.npw + a.nrw + 1) * 32;
   if (threads > 1024) return cudaErrorInvalidValue;
+  // ring configurations (rows per tile R, row slot bytes, stages), tuned on B200:
+  // K <= 4096: R=4 (the residual warp gets a full 32 items per tile), 3 x 32 KB slots
+  // -> 2 CTAs/SM; K <= 8192: R=2, 3 x 32 KB; K <= 16384: R=2, 3 x 64 KB (1 CTA/SM).
   if (ipt == 1) {
-    if (rowb <= 8192) return launch_quant_cfg<1, 2, 8192, 4>(a, threads, stream);
-    if (rowb <= 16384) return launch_quant_cfg<1, 2, 16384, 3>(a, threads, stream);
-    return launch_quant_cfg<1, 2, 32768, 3>(a, threads, stream);
+    const int R = rowb <= 8192 ? 4 : 2;
+    a.nrw = ns == 0 ? 0 : (int)imin64(2, (R * ns + 31) / 32);
+    const int th = (a.npw + a.nrw + 1) * 32;
+    if (th > 1024) return cudaErrorInvalidValue;
+    if (rowb <= 8192) return launch_quant_cfg<1, 4, 8192, 3>(a, th, stream);
+    if (rowb <= 16384) return launch_quant_cfg<1, 2, 16384, 3>(a, th, stream);
+    return launch_quant_cfg<1, 2, 32768, 3>(a, th, stream);
   }
   if (ipt == 2) return launch_quant_cfg<2, 1, 65536, 3>(a, threads, stream);
   return cudaErrorInvalidValue;  // K + S > 32768 is rejected in api.cu
