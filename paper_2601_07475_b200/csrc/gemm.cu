@@ -395,11 +395,20 @@ GemmPlan plan_gemm(int64_t M, int64_t N, int64_t Kp) {
   pl.nsplit = 1;
   pl.kbs = (int)nkb;
   if (items < clusters && nkb >= 4) {
-    // decode-size M: split K so ~every SM streams weights; >= 2 K-blocks per split
-    int64_t want = std::min<int64_t>((clusters + items - 1) / items, nkb / 2);
-    if (want > 1) {
-      pl.kbs = (int)((nkb + want - 1) / want);
-      pl.nsplit = (int)((nkb + pl.kbs - 1) / pl.kbs);
+    // decode-size M: split K so every SM streams weights.  Cost model per split count s:
+    // waves * (K-blocks per item) * t_kb  +  fp32 partial write+read traffic / HBM,
+    // t_kb ~ one 48 KB stage at an SM's share of HBM bandwidth.
+    const double t_kb = 48e3 / 44e9, hbm = 6.0e12;
+    double best = 1e30;
+    for (int64_t s = 1; s <= std::min<int64_t>(nkb / 2, 32); ++s) {
+      const int64_t kbs = (nkb + s - 1) / s, ns = (nkb + kbs - 1) / kbs;
+      const int64_t it = items * ns, waves = (it + clusters - 1) / clusters;
+      const double cost = (double)waves * (double)kbs * t_kb + (ns > 1 ? (double)ns * M * N * 8.0 / hbm : 0.0);
+      if (cost < best - 1e-12) {
+        best = cost;
+        pl.kbs = (int)kbs;
+        pl.nsplit = (int)ns;
+      }
     }
   }
   pl.ws_bytes = pl.nsplit > 1 ? (size_t)pl.nsplit * (size_t)M * (size_t)N * sizeof(float) : 0;
