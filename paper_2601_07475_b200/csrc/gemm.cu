@@ -212,6 +212,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // ---------------------------------------------------------------- epilogue (warps 2..5)
     const int q = warp & 3;  // TMEM lane quadrant this warp may access
     const float alpha = __fdiv_rn(1.0f, __fmul_rn(__ldg(args.gs_x), __ldg(args.gs_w)));
+    const uint64_t y_policy = policy_evict_first();
     int t = 0;
     for (int tile = cid; tile < num_tiles; tile += ncl, ++t) {
       const int ks = tile % nsplit, rest = tile / nsplit;
@@ -307,8 +308,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           } else {
             fence_proxy_async();
             __syncwarp();
-            if (lane == 0) {
-              tma_store_2d(&tmY, st, n0, mb * BM + q * 32);
+            if (lane == 0 && args.debug != 6) {
+              // Y is written once: evict-first keeps the reused A/B tiles resident in L2
+              tma_store_2d_hint(&tmY, st, n0, mb * BM + q * 32, y_policy);
               bulk_commit();
             }
           }

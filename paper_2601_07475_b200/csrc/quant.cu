@@ -258,6 +258,7 @@ __global__ void __launch_bounds__(1024) arc_quant_kernel(QuantArgs p) {
     // ---------------------------------------------------------------- producer warp
     const uint32_t ring = smem_u32(smem) + (uint32_t)lane * 16u;
     const int kc = K >> 3;  // 16-byte chunks per row
+    const uint64_t x_policy = policy_evict_first();
     for (int j0 = 0; j0 < my_tiles; j0 += ST) {
 #pragma unroll
       for (int s = 0; s < ST; ++s) {
@@ -274,8 +275,9 @@ __global__ void __launch_bounds__(1024) arc_quant_kernel(QuantArgs p) {
             if (lane == 0) {
               mbar_expect_tx(&full[s], (uint32_t)(nr * K * 2));
               if (p.debug != 2)
-                for (int r = 0; r < nr; ++r)
-                  bulk_load(smem + s * SLOT + r * ROWB, p.x + (int64_t)(r0 + r) * p.ld, (uint32_t)K * 2, &full[s]);
+                for (int r = 0; r < nr; ++r)  // X is read once: evict-first
+                  bulk_load_hint(smem + s * SLOT + r * ROWB, p.x + (int64_t)(r0 + r) * p.ld, (uint32_t)K * 2, &full[s],
+                                 x_policy);
               else
                 mbar_complete_tx_self(&full[s], (uint32_t)(nr * K * 2));
             }
