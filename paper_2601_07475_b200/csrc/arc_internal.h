@@ -31,7 +31,8 @@ struct GemmProblem {
   size_t ws_bytes;
 };
 struct GemmPlan {
-  int CL;            // CTAs per cluster (B-tile multicast)
+  int CL;            // CTAs per cluster along M
+  int pair;          // CL == 2: 1 = 2-SM tcgen05 MMA (cta_group::2), 0 = two 1-SM CTAs sharing B by multicast
   int nsplit, kbs;   // split-K factor and K-blocks per split
   size_t ws_bytes;   // fp32 partials nsplit*M*N
 };

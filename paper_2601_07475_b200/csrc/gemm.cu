@@ -27,6 +27,7 @@
 
 #include <cuda.h>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <mutex>
 
@@ -49,6 +50,9 @@ constexpr int TMEM_COLS = 512;
 // epilogue drains first so the next tile's MMAs can start while it drains the rest.
 constexpr int ACC1_COL = 192;  // buffer b starts at column b * ACC1_COL
 constexpr int OVL_CHUNKS = 2;  // 32-column chunks in the shared region
+// Scale factors of one stage (4 MMAs x (SFA 4 + SFB 8) columns, 32x128b.warpx4 placement).
+// (A per-MMA ring of slots with interleaved copies measured slower: each MMA then waits for
+// its own tcgen05.cp; batching the stage's 12 copies ahead of its 4 MMAs exposes one wait.)
 constexpr int SFA_COL = 448;
 constexpr int SFB_COL = 448 + 16;
 constexpr int NUM_THREADS = 192;
@@ -67,12 +71,126 @@ struct Args {
   int nsplit;   // split-K factor (decode-size M): > 1 -> fp32 partials into ws[nsplit][M][N]
   int kbs;      // K-blocks per split
   float* ws;
-  int debug;  // perf experiments only (env ARC_GEMM_DEBUG): 1 = no epilogue work, 2 = no scale copies, 3 = no stores, 4 = no TMEM loads
+  int raster;   // tile order: 0 = M-tile groups fastest (the A panel stays in L2), 1 = N tiles fastest (B stays)
+  int debug;  // perf experiments only (env ARC_GEMM_DEBUG): 1 = no epilogue work, 2 = no scale copies, 3 = no stores, 4 = no TMEM loads,
+              // 5 = STG stores, 6 = no TMA store, 7 = MMA ignores the accumulator-free barriers,
+              // 8 = MMAs issued twice, 9 = one MMA per stage, 10 = 9 without scale copies (pair kernel; timing only)
 };
 
 // instruction descriptor: E2M1 x E2M1 (format 1), UE4M3 scales, K-major A/B,
 // N>>3 at [17,23), M>>4 at [24,29).
 constexpr uint32_t kIdesc = (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+
+// Epilogue of one output tile, run by the 4 epilogue warps: warp q drains TMEM lanes
+// [32q, 32q+32) (= 32 output rows of this CTA's 128) x BN columns of accumulator buffer b,
+// scales by alpha and stores.  The two chunks buffer b shares with the other buffer are read
+// first and released through ovl_free; the whole buffer is released through buf_free.  In the
+// 2-SM kernel (PAIR) both barriers live in the pair's leader CTA (cluster-scope remote arrivals).
+template <bool PAIR>
+__device__ __forceinline__ void epilogue_tile(const Args& args, const CUtensorMap* tmY, uint32_t tmem, int b, int mb,
+                                              int nbk, int ks, float alpha, uint64_t y_policy, uint8_t* st,
+                                              uint64_t* ovl_free, uint64_t* buf_free, int warp, int lane,
+                                              uint32_t leader = 0) {
+  const int q = warp & 3;  // TMEM lane quadrant this warp may access
+  const int M = args.M, N = args.N, nsplit = args.nsplit;
+  const int m = mb * BM + q * 32 + lane;
+  auto release = [&](uint64_t* bar) {
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) {
+      if (PAIR) mbar_arrive_cluster(mapa_shared(bar, leader));
+      else mbar_arrive(bar);
+    }
+  };
+  uint32_t pre[OVL_CHUNKS][32];  // the shared chunks, read before anything is stored
+  if (args.debug != 1 && args.debug != 4) {
+#pragma unroll
+    for (int k = 0; k < OVL_CHUNKS; ++k) {
+      const int c = b == 0 ? BN / 32 - OVL_CHUNKS + k : k;
+      tmem_ld_32x32b_x32(tmem + ((uint32_t)(q * 32) << 16) + b * ACC1_COL + c * 32, pre[k]);
+    }
+    tmem_ld_wait();
+  }
+  release(ovl_free);  // next tile's MMAs may overwrite the shared columns now
+#pragma unroll 1
+  for (int cc = 0; cc < BN / 32; ++cc) {
+    // buffer 0 drains its shared chunks (6, 7) first, buffer 1 its (0, 1)
+    const int c = b == 0 ? (cc + BN / 32 - OVL_CHUNKS) % (BN / 32) : cc;
+    uint32_t r[32];
+    if (args.debug == 1) {
+      if (cc == BN / 32 - 1) release(buf_free);
+      continue;
+    }
+    if (args.debug == 4) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) r[j] = 0u;
+    } else if (cc < OVL_CHUNKS) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) r[j] = cc == 0 ? pre[0][j] : pre[1][j];
+    } else {
+      tmem_ld_32x32b_x32(tmem + ((uint32_t)(q * 32) << 16) + b * ACC1_COL + c * 32, r);
+      tmem_ld_wait();
+    }
+    if (cc == BN / 32 - 1) release(buf_free);
+    const int n0 = nbk * BN + c * 32;
+    if ((args.y_fp32 || nsplit > 1) && m < M && n0 < N) {
+      float* yr = nsplit > 1 ? args.ws + ((int64_t)ks * M + m) * N + n0
+                             : static_cast<float*>(args.y) + (int64_t)m * args.ldy + n0;
+      if (n0 + 32 <= N) {
+#pragma unroll
+        for (int j = 0; j < 32; j += 4)
+          *reinterpret_cast<float4*>(yr + j) =
+              make_float4(__fmul_rn(__uint_as_float(r[j]), alpha), __fmul_rn(__uint_as_float(r[j + 1]), alpha),
+                          __fmul_rn(__uint_as_float(r[j + 2]), alpha), __fmul_rn(__uint_as_float(r[j + 3]), alpha));
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (n0 + j < N) yr[j] = __fmul_rn(__uint_as_float(r[j]), alpha);
+      }
+    }
+    if (!args.y_fp32 && nsplit == 1 && mb * BM + q * 32 < M && n0 < N && args.debug != 3) {
+      // bf16: stage the 32x32 sub-tile in smem (64B swizzle: 16-byte unit u of row
+      // r lives at unit u ^ ((r >> 1) & 3), bank-conflict-free) and TMA-store it
+      // (coalesced, clipped at the M/N edges by the tensor map).
+      if (lane == 0 && args.debug != 5) bulk_wait_read0();  // previous store finished reading the buffer
+      __syncwarp();
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        uint4 v;
+        uint32_t* pv = reinterpret_cast<uint32_t*>(&v);
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          __nv_bfloat162 b2 = __floats2bfloat162_rn(__fmul_rn(__uint_as_float(r[8 * u + 2 * h]), alpha),
+                                                    __fmul_rn(__uint_as_float(r[8 * u + 2 * h + 1]), alpha));
+          pv[h] = *reinterpret_cast<uint32_t*>(&b2);
+        }
+        *reinterpret_cast<uint4*>(st + lane * 64 + ((u ^ ((lane >> 1) & 3)) << 4)) = v;
+      }
+      if (args.debug == 5) {
+        // coalesced STG from the staged sub-tile: lane -> (row lane/4 + 8i, 16-byte unit lane%4)
+        __syncwarp();
+        const int rr = lane >> 2, uu = lane & 3;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int row = rr + 8 * i;
+          const int gm = mb * BM + q * 32 + row;
+          const uint4 v = *reinterpret_cast<const uint4*>(st + row * 64 + ((uu ^ ((row >> 1) & 3)) << 4));
+          if (gm < M && n0 + uu * 8 < N)
+            *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(args.y) + (int64_t)gm * args.ldy + n0 + uu * 8) = v;
+        }
+        __syncwarp();
+      } else {
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0 && args.debug != 6) {
+          // Y is written once: evict-first keeps the reused A/B tiles resident in L2
+          tma_store_2d_hint(tmY, st, n0, mb * BM + q * 32, y_policy);
+          bulk_commit();
+        }
+      }
+    }
+  }
+}
 
 // CL = CTAs per cluster along M (1 or 2).  With CL = 2 the two CTAs compute the
 // tiles (m, n) and (m+1, n): each TMA-loads HALF of the shared B tile (and its
@@ -113,9 +231,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       mbar_init(&empty[s], CL);  // one MMA commit from every CTA of the cluster
     }
     mbar_init(tfull, 1);
-    mbar_init(ovl_free, 128);
-    mbar_init(&buf_free[0], 128);
-    mbar_init(&buf_free[1], 128);
+    mbar_init(ovl_free, 4);  // one arrival per epilogue warp
+    mbar_init(&buf_free[0], 4);
+    mbar_init(&buf_free[1], 4);
     fence_mbar_init();
     prefetch_tmap(&tmA);
     prefetch_tmap(&tmB);
@@ -132,12 +250,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (warp == 0) {
     if (elect_one()) {
       // ---------------------------------------------------------------- producer
-      const uint64_t pol = policy_evict_last();
+      const uint64_t pol = args.debug == 11 ? policy_evict_normal() : policy_evict_last();
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = cid; tile < num_tiles; tile += ncl) {
         const int ks = tile % nsplit, rest = tile / nsplit;
-        const int mb = (rest % num_mp) * CL + rank, nbk = rest / num_mp;
+        const int mb = (args.raster ? rest / num_n : rest % num_mp) * CL + rank;
+        const int nbk = args.raster ? rest % num_n : rest / num_mp;
         const int nrb = min(2, n_rb - 2 * nbk);   // existing 128-row scale blocks of this B tile
         const bool a_ok = mb < num_m;              // (CL = 2, odd num_m: the last rank-1 tile is empty)
         const int kb0 = ks * args.kbs, kb1 = min(nkb, kb0 + args.kbs);
@@ -178,8 +297,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const int b = t & 1;
         const int ks = tile % nsplit;
         const int kb0 = ks * args.kbs, kb1 = min(nkb, kb0 + args.kbs);
-        if (t >= 1) mbar_wait(ovl_free, (t - 1) & 1);            // shared columns drained (tile t-1)
-        if (t >= 2) mbar_wait(&buf_free[b], ((t - 2) >> 1) & 1);  // own columns drained (tile t-2)
+        if (t >= 1 && args.debug != 7) mbar_wait(ovl_free, (t - 1) & 1);            // shared columns drained (tile t-1)
+        if (t >= 2 && args.debug != 7) mbar_wait(&buf_free[b], ((t - 2) >> 1) & 1);  // own columns drained (tile t-2)
         tc_fence_after();
         const uint32_t acc = tmem + b * ACC1_COL;
         for (int kb = kb0; kb < kb1; ++kb) {
@@ -210,112 +329,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
   } else {
     // ---------------------------------------------------------------- epilogue (warps 2..5)
-    const int q = warp & 3;  // TMEM lane quadrant this warp may access
     const float alpha = __fdiv_rn(1.0f, __fmul_rn(__ldg(args.gs_x), __ldg(args.gs_w)));
     const uint64_t y_policy = policy_evict_first();
     int t = 0;
     for (int tile = cid; tile < num_tiles; tile += ncl, ++t) {
       const int ks = tile % nsplit, rest = tile / nsplit;
-      const int mb = (rest % num_mp) * CL + rank, nbk = rest / num_mp;
+      const int mb = (args.raster ? rest / num_n : rest % num_mp) * CL + rank;
+        const int nbk = args.raster ? rest % num_n : rest / num_mp;
       mbar_wait(tfull, t & 1);
       tc_fence_after();
-      const int m = mb * BM + q * 32 + lane;
-      const int b = t & 1;
-      uint32_t pre[OVL_CHUNKS][32];  // the shared chunks, read before anything is stored
-      if (args.debug != 1 && args.debug != 4) {
-#pragma unroll
-        for (int k = 0; k < OVL_CHUNKS; ++k) {
-          const int c = b == 0 ? BN / 32 - OVL_CHUNKS + k : k;
-          tmem_ld_32x32b_x32(tmem + ((uint32_t)(q * 32) << 16) + b * ACC1_COL + c * 32, pre[k]);
-        }
-        tmem_ld_wait();
-      }
-      tc_fence_before();
-      mbar_arrive(ovl_free);  // next tile's MMAs may overwrite the shared columns now
-#pragma unroll 1
-      for (int cc = 0; cc < BN / 32; ++cc) {
-        // buffer 0 drains its shared chunks (6, 7) first, buffer 1 its (0, 1)
-        const int c = b == 0 ? (cc + BN / 32 - OVL_CHUNKS) % (BN / 32) : cc;
-        uint32_t r[32];
-        if (args.debug == 1) {
-          if (cc == BN / 32 - 1) { tc_fence_before(); mbar_arrive(&buf_free[b]); }
-          continue;
-        }
-        if (args.debug == 4) {
-#pragma unroll
-          for (int j = 0; j < 32; ++j) r[j] = 0u;
-        } else if (cc < OVL_CHUNKS) {
-#pragma unroll
-          for (int j = 0; j < 32; ++j) r[j] = cc == 0 ? pre[0][j] : pre[1][j];
-        } else {
-          tmem_ld_32x32b_x32(tmem + ((uint32_t)(q * 32) << 16) + b * ACC1_COL + c * 32, r);
-          tmem_ld_wait();
-        }
-        if (cc == BN / 32 - 1) {
-          tc_fence_before();
-          mbar_arrive(&buf_free[b]);
-        }
-        const int n0 = nbk * BN + c * 32;
-        if ((args.y_fp32 || nsplit > 1) && m < M && n0 < N) {
-          {
-            float* yr = nsplit > 1 ? args.ws + ((int64_t)ks * M + m) * N + n0
-                                   : static_cast<float*>(args.y) + (int64_t)m * args.ldy + n0;
-            if (n0 + 32 <= N) {
-#pragma unroll
-              for (int j = 0; j < 32; j += 4)
-                *reinterpret_cast<float4*>(yr + j) =
-                    make_float4(__fmul_rn(__uint_as_float(r[j]), alpha), __fmul_rn(__uint_as_float(r[j + 1]), alpha),
-                                __fmul_rn(__uint_as_float(r[j + 2]), alpha), __fmul_rn(__uint_as_float(r[j + 3]), alpha));
-            } else {
-#pragma unroll
-              for (int j = 0; j < 32; ++j)
-                if (n0 + j < N) yr[j] = __fmul_rn(__uint_as_float(r[j]), alpha);
-            }
-          }
-        }
-        if (!args.y_fp32 && nsplit == 1 && mb * BM + q * 32 < M && n0 < N && args.debug != 3) {
-          // bf16: stage the 32x32 sub-tile in smem (64B swizzle: 16-byte unit u of row
-          // r lives at unit u ^ ((r >> 1) & 3), bank-conflict-free) and TMA-store it
-          // (coalesced, clipped at the M/N edges by the tensor map).
-          uint8_t* st = epi_stage + (warp - 2) * EPI_STAGE_BYTES;
-          if (lane == 0 && args.debug != 5) bulk_wait_read0();  // previous store finished reading the buffer
-          __syncwarp();
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            uint4 v;
-            uint32_t* pv = reinterpret_cast<uint32_t*>(&v);
-#pragma unroll
-            for (int h = 0; h < 4; ++h) {
-              __nv_bfloat162 b2 = __floats2bfloat162_rn(__fmul_rn(__uint_as_float(r[8 * u + 2 * h]), alpha),
-                                                        __fmul_rn(__uint_as_float(r[8 * u + 2 * h + 1]), alpha));
-              pv[h] = *reinterpret_cast<uint32_t*>(&b2);
-            }
-            *reinterpret_cast<uint4*>(st + lane * 64 + ((u ^ ((lane >> 1) & 3)) << 4)) = v;
-          }
-          if (args.debug == 5) {
-            // coalesced STG from the staged sub-tile: lane -> (row lane/4 + 8i, 16-byte unit lane%4)
-            __syncwarp();
-            const int rr = lane >> 2, uu = lane & 3;
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const int row = rr + 8 * i;
-              const int gm = mb * BM + q * 32 + row;
-              const uint4 v = *reinterpret_cast<const uint4*>(st + row * 64 + ((uu ^ ((row >> 1) & 3)) << 4));
-              if (gm < M && n0 + uu * 8 < N)
-                *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(args.y) + (int64_t)gm * args.ldy + n0 + uu * 8) = v;
-            }
-            __syncwarp();
-          } else {
-            fence_proxy_async();
-            __syncwarp();
-            if (lane == 0 && args.debug != 6) {
-              // Y is written once: evict-first keeps the reused A/B tiles resident in L2
-              tma_store_2d_hint(&tmY, st, n0, mb * BM + q * 32, y_policy);
-              bulk_commit();
-            }
-          }
-        }
-      }
+      epilogue_tile<false>(args, &tmY, tmem, t & 1, mb, nbk, ks, alpha, y_policy,
+                           epi_stage + (warp - 2) * EPI_STAGE_BYTES, ovl_free, &buf_free[t & 1], warp, lane);
     }
     if (lane == 0) bulk_wait_all();
   }
@@ -326,6 +350,190 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem, TMEM_COLS);
+  }
+}
+
+// ------------------------------------------------------------------ 2-SM (cta_group::2) kernel
+// A CTA pair computes one 256 x 256 output tile with M = 256 tcgen05 MMAs issued by the
+// pair's leader CTA (even rank): CTA r holds A rows [128(r&1), +128) and B rows [128(r&1), +128)
+// of the tile in its own smem; the tensor cores of both SMs read both B halves, so each SM
+// stages half the B bytes of the 1-SM kernel (38 KB per stage instead of 54 KB, 5 stages) and
+// its shared-memory operand reads drop by a third.  Scales: each CTA holds its own 128 rows of
+// SFA and all 256 rows of SFB; the leader's tcgen05.cp.cta_group::2 copies each CTA's smem
+// into its own TMEM.
+// CLP = CTAs per cluster (2: one pair; 4: two pairs along M computing tiles (m, n), (m+1, n)
+// that share the B tile: each CTA TMA-loads a quarter of the pair-B operand and multicasts it
+// to the CTA holding the same half in the other pair, halving B's L2 -> SM traffic).
+// SFB is split across the cluster's CTAs and multicast to all of them.  All copies complete
+// on the destination pair's leader barrier (cta_group::2 form, peer bit cleared); the
+// leader's MMA commits multicast to every CTA's empty barrier (a slot is refilled only when
+// every pair has consumed it) and to its pair's tfull; both CTAs' epilogues release the
+// leader's accumulator barriers remotely.
+constexpr int P_B_BYTES = (BN / 2) * BKB;                                     // 16 KB
+constexpr int P_STAGE_BYTES = A_BYTES + P_B_BYTES + SFA_BYTES + SFB_BYTES;  // 38 KB
+constexpr int p_smem_bytes(int stages) { return stages * P_STAGE_BYTES + 4 * EPI_STAGE_BYTES + 1024 + 256; }
+constexpr uint32_t kIdescPair = (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(2 * BM >> 4) << 24);
+constexpr uint32_t kPeerBitMask = 0xFEFFFFFFu;  // shared::cluster address bit selecting the odd CTA of a pair
+
+template <int CLP, int P_STAGES>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    arc_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                         const __grid_constant__ CUtensorMap tmSFA, const __grid_constant__ CUtensorMap tmSFB,
+                         const __grid_constant__ CUtensorMap tmY, Args args) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* epi_stage = smem + P_STAGES * P_STAGE_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(epi_stage + 4 * EPI_STAGE_BYTES);
+  uint64_t* empty = full + P_STAGES;
+  uint64_t* tfull = empty + P_STAGES;
+  uint64_t* ovl_free = tfull + 1;
+  uint64_t* buf_free = ovl_free + 1;  // [2]
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(buf_free + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int M = args.M, N = args.N, Kp = args.Kp;
+  const int num_m = (M + BM - 1) / BM;
+  const int num_n = (N + BN - 1) / BN;
+  const int num_mp = (num_m + CLP - 1) / CLP;  // M-tile groups (one per cluster step)
+  const int nsplit = args.nsplit;
+  const int num_tiles = num_mp * num_n * nsplit;
+  const int rank = (int)cluster_ctarank();
+  const int half = rank & 1;          // which half of the pair (A rows / B rows) this CTA holds
+  const int pr = rank >> 1;           // pair index in the cluster
+  const uint32_t leader = rank & ~1;  // the pair's MMA-issuing CTA
+  const int cid = blockIdx.x / CLP, ncl = gridDim.x / CLP;
+  const int nkb = (Kp + BK - 1) / BK;
+  const int kc_total = Kp / 64;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < P_STAGES; ++s) {
+      mbar_init(&full[s], 1);            // leader: its expect_tx arrival (+ the bytes landing in the pair)
+      mbar_init(&empty[s], CLP / 2);     // one MMA commit per pair of the cluster
+    }
+    mbar_init(tfull, 1);
+    mbar_init(ovl_free, 8);  // one arrival per epilogue warp of both CTAs of the pair
+    mbar_init(&buf_free[0], 8);
+    mbar_init(&buf_free[1], 8);
+    fence_mbar_init();
+    prefetch_tmap(&tmA);
+    prefetch_tmap(&tmB);
+    prefetch_tmap(&tmSFA);
+    prefetch_tmap(&tmSFB);
+  }
+  if (warp == 1) tmem_alloc_pair(tmem_holder, TMEM_COLS);
+  pdl_launch_dependents();
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  tc_fence_after();
+  pdl_wait();
+  const uint32_t tmem = *tmem_holder;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      // ---------------------------------------------------------------- producer (every CTA)
+      const uint64_t pol = args.debug == 11 ? policy_evict_normal() : policy_evict_last();
+      const uint16_t mask_b = (uint16_t)(CLP == 4 ? (1u << half) | (4u << half) : 0u);
+      const uint16_t mask_all = (uint16_t)((1u << CLP) - 1u);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = cid; tile < num_tiles; tile += ncl) {
+        const int ks = tile % nsplit, rest = tile / nsplit;
+        const int mb = (args.raster ? rest / num_n : rest % num_mp) * CLP + rank;
+        const int nbk = args.raster ? rest % num_n : rest / num_mp;
+        const int kb0 = ks * args.kbs, kb1 = min(nkb, kb0 + args.kbs);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sA = smem + stage * P_STAGE_BYTES;
+          uint8_t* sB = sA + A_BYTES;
+          uint8_t* sSFA = sB + P_B_BYTES;
+          uint8_t* sSFB = sSFA + SFA_BYTES;
+          const uint32_t fb = smem_u32(&full[stage]) & kPeerBitMask;
+          if (half == 0) mbar_expect_tx(&full[stage], 2u * P_STAGE_BYTES);
+          // full boxes always (out-of-range rows / K chunks are zero-filled and still counted)
+          tma_load_2d_pair(sA, &tmA, fb, kb * BKB, mb * BM, pol);
+          tma_load_3d_pair(sSFA, &tmSFA, fb, 0, kb * 4, mb, pol);
+          if (CLP == 2) {
+            tma_load_2d_pair(sB, &tmB, fb, kb * BKB, nbk * BN + half * (BN / 2), pol);
+            tma_load_3d_pair_mc(sSFB + half * 2048, &tmSFB, fb, 0, kb * 4, nbk * 2 + half, mask_all, pol);
+          } else {
+            tma_load_2d_pair_mc(sB + pr * (P_B_BYTES / 2), &tmB, fb, kb * BKB, nbk * BN + half * (BN / 2) + pr * (BN / 4),
+                                mask_b, pol);
+            tma_load_3d_pair_mc(sSFB + half * 2048 + pr * 1024, &tmSFB, fb, 0, kb * 4 + pr * 2, nbk * 2 + half, mask_all,
+                                pol);
+          }
+          if (++stage == P_STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (half == 0 && elect_one()) {
+      // ---------------------------------------------------------------- MMA issuer (pair leader)
+      const uint16_t mask_all = (uint16_t)((1u << CLP) - 1u);
+      const uint16_t mask_pair = (uint16_t)(3u << leader);
+      int stage = 0;
+      uint32_t phase = 0;
+      int t = 0;
+      for (int tile = cid; tile < num_tiles; tile += ncl, ++t) {
+        const int b = t & 1;
+        const int ks = tile % nsplit;
+        const int kb0 = ks * args.kbs, kb1 = min(nkb, kb0 + args.kbs);
+        if (t >= 1 && args.debug != 7) mbar_wait_cluster(ovl_free, (t - 1) & 1);
+        if (t >= 2 && args.debug != 7) mbar_wait_cluster(&buf_free[b], ((t - 2) >> 1) & 1);
+        tc_fence_after();
+        const uint32_t acc = tmem + b * ACC1_COL;
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const int nk = min(4, kc_total - kb * 4);
+          const uint32_t sA = smem_u32(smem + stage * P_STAGE_BYTES);
+          const uint32_t sB = sA + A_BYTES;
+          const uint32_t sSFA = sB + P_B_BYTES;
+          const uint32_t sSFB = sSFA + SFA_BYTES;
+          for (int kk = 0; kk < nk && args.debug != 2 && args.debug != 10; ++kk) {
+            utccp_32x128b_warpx4_pair(tmem + SFA_COL + 4 * kk, smem_desc(sSFA + kk * 512, 0, 128, kLayoutSwizzleNone));
+            utccp_32x128b_warpx4_pair(tmem + SFB_COL + 8 * kk, smem_desc(sSFB + kk * 512, 0, 128, kLayoutSwizzleNone));
+            utccp_32x128b_warpx4_pair(tmem + SFB_COL + 8 * kk + 4,
+                                      smem_desc(sSFB + 2048 + kk * 512, 0, 128, kLayoutSwizzleNone));
+          }
+          const int nk_mma = (args.debug == 9 || args.debug == 10) ? 1 : nk;  // 9/10: feed ceiling (one MMA per stage)
+          for (int rep = 0; rep < (args.debug == 8 ? 2 : 1); ++rep)  // 8: MMA-bound check (math doubled)
+            for (int kk = 0; kk < nk_mma; ++kk) {
+              const uint64_t ad = smem_desc(sA + kk * 32, 16, 1024, kLayoutSwizzle128B);
+              const uint64_t bd = smem_desc(sB + kk * 32, 16, 1024, kLayoutSwizzle128B);
+              mma_nvf4_pair(acc, ad, bd, kIdescPair, (kb != kb0) || (kk != 0) || rep, tmem + SFA_COL + 4 * kk,
+                            tmem + SFB_COL + 8 * kk);
+            }
+          tc_commit_pair_mc(&empty[stage], mask_all);  // the slot is free in every CTA once every pair used it
+          if (++stage == P_STAGES) { stage = 0; phase ^= 1; }
+        }
+        tc_commit_pair_mc(tfull, mask_pair);
+      }
+    }
+  } else {
+    // ---------------------------------------------------------------- epilogue (every CTA)
+    const float alpha = __fdiv_rn(1.0f, __fmul_rn(__ldg(args.gs_x), __ldg(args.gs_w)));
+    const uint64_t y_policy = policy_evict_first();
+    int t = 0;
+    for (int tile = cid; tile < num_tiles; tile += ncl, ++t) {
+      const int ks = tile % nsplit, rest = tile / nsplit;
+      const int mb = (args.raster ? rest / num_n : rest % num_mp) * CLP + rank;
+        const int nbk = args.raster ? rest % num_n : rest / num_mp;
+      mbar_wait(tfull, t & 1);
+      tc_fence_after();
+      epilogue_tile<true>(args, &tmY, tmem, t & 1, mb, nbk, ks, alpha, y_policy,
+                          epi_stage + (warp - 2) * EPI_STAGE_BYTES, ovl_free, &buf_free[t & 1], warp, lane, leader);
+    }
+    if (lane == 0) bulk_wait_all();
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();  // no CTA leaves while a peer's loads / MMAs / arrivals may target it
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_pair(tmem, TMEM_COLS);
   }
 }
 
@@ -374,6 +582,22 @@ bool make_map(CUtensorMap* m, const uint8_t* base, int64_t rows, int64_t row_byt
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// Scale factors as a 3-D u32 tensor [row blocks][Kp/64 chunks][128 words]: one 512-byte
+// chunk holds the 128x4 scale tile of 128 rows x 64 K (tcgen05 layout, already in memory);
+// a box of box_kc chunks x box_rb row blocks is (part of) one stage's scales (chunks past Kp
+// read zeros).
+bool make_sf_map(CUtensorMap* m, const uint8_t* sf, int64_t row_blocks, int64_t kc_total, int box_kc, int box_rb) {
+  EncodeTiledFn enc = get_encode_fn();
+  if (!enc) return false;
+  cuuint64_t dims[3] = {128, (cuuint64_t)kc_total, (cuuint64_t)row_blocks};
+  cuuint64_t strides[2] = {512, (cuuint64_t)(512 * kc_total)};
+  cuuint32_t box[3] = {128, (cuuint32_t)box_kc, (cuuint32_t)box_rb};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, const_cast<uint8_t*>(sf), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 bool make_y_map(CUtensorMap* m, void* y, int64_t rows, int64_t cols, int64_t ldy) {
   EncodeTiledFn enc = get_encode_fn();
   if (!enc) return false;
@@ -387,11 +611,51 @@ bool make_y_map(CUtensorMap* m, void* y, int64_t rows, int64_t cols, int64_t ldy
 
 }  // namespace
 
+// Co-resident clusters of the persistent grid (clusters of 4 may not tile every GPC's SMs).
+int64_t max_clusters(int CL, bool pair) {
+  if (CL == 1) return num_sms();
+  static int cache[2][5] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int& c = cache[pair ? 1 : 0][CL];
+  if (c == 0) {
+    cudaLaunchConfig_t cfg;
+    memset(&cfg, 0, sizeof(cfg));
+    cfg.gridDim = dim3((unsigned)(num_sms() / CL * CL));
+    cfg.blockDim = dim3(NUM_THREADS);
+    cfg.dynamicSmemBytes = pair ? p_smem_bytes(5) : SMEM_BYTES;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    cudaError_t e = !pair ? cudaOccupancyMaxActiveClusters(&n, arc_gemm_kernel<2>, &cfg)
+                    : CL == 2 ? cudaOccupancyMaxActiveClusters(&n, arc_gemm_pair_kernel<2, 5>, &cfg)
+                              : cudaOccupancyMaxActiveClusters(&n, arc_gemm_pair_kernel<4, 5>, &cfg);
+    if (e != cudaSuccess || n <= 0) {
+      cudaGetLastError();
+      n = num_sms() / CL;
+    }
+    c = n;
+    if (getenv("ARC_GEMM_VERBOSE")) fprintf(stderr, "arc_gemm: CL=%d pair=%d max active clusters %d\n", CL, (int)pair, n);
+  }
+  return c;
+}
+
 GemmPlan plan_gemm(int64_t M, int64_t N, int64_t Kp) {
   static const int env_cl = getenv("ARC_GEMM_CL") ? atoi(getenv("ARC_GEMM_CL")) : 2;
+  // The 2-SM kernel is kept selectable (ARC_GEMM_PAIR=1): on the LLaMA-3-8B shapes it measured
+  // 0-8 % slower than two 1-SM CTAs sharing B by multicast.
+  static const int env_pair = getenv("ARC_GEMM_PAIR") ? atoi(getenv("ARC_GEMM_PAIR")) : 0;
+  static const int env_clp = getenv("ARC_GEMM_CLP") ? atoi(getenv("ARC_GEMM_CLP")) : 2;
   GemmPlan pl;
   const int64_t num_m = (M + BM - 1) / BM, num_n = (N + BN - 1) / BN, nkb = (Kp + BK - 1) / BK;
   pl.CL = (env_cl == 1 || num_m < 2) ? 1 : 2;
+  pl.pair = pl.CL == 2 && env_pair != 0;
+  if (pl.pair && env_clp == 4 && num_m >= 4) pl.CL = 4;
   const int64_t items = ((num_m + pl.CL - 1) / pl.CL) * num_n;  // cluster work items without split
   const int64_t clusters = num_sms() / pl.CL;
   pl.nsplit = 1;
@@ -430,7 +694,13 @@ cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t stream, const char** 
     if (detail) *detail = "cuTensorMapEncodeTiled (Y) failed";
     return cudaErrorInvalidValue;
   }
-  if (!make_map(&tmA, p.a_codes, p.M, p.Kp / 2, BM) || !make_map(&tmB, p.b_codes, p.N, p.Kp / 2, BN / CL)) {
+  CUtensorMap tmSFA, tmSFB;
+  // B box rows: the 1-SM kernel loads 256 (CL 1) or 128 (CL 2, multicast halves); the pair
+  // kernel 128 (one pair) or 64 (two pairs, multicast quarters).  SFB box: 4 / 2 chunks.
+  const int b_rows = pl.pair ? (CL == 2 ? 128 : 64) : BN / CL;
+  if (!make_map(&tmA, p.a_codes, p.M, p.Kp / 2, BM) || !make_map(&tmB, p.b_codes, p.N, p.Kp / 2, b_rows) ||
+      (pl.pair && (!make_sf_map(&tmSFA, p.a_sf, (p.M + 127) / 128, p.Kp / 64, 4, 1) ||
+                   !make_sf_map(&tmSFB, p.b_sf, (p.N + 127) / 128, p.Kp / 64, CL == 2 ? 4 : 2, 1)))) {
     if (detail) *detail = "cuTensorMapEncodeTiled failed";
     return cudaErrorInvalidValue;
   }
@@ -440,6 +710,12 @@ cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t stream, const char** 
     attr_err = cudaFuncSetAttribute(arc_gemm_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     if (attr_err == cudaSuccess)
       attr_err = cudaFuncSetAttribute(arc_gemm_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    if (attr_err == cudaSuccess)
+      attr_err = cudaFuncSetAttribute(arc_gemm_pair_kernel<2, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, p_smem_bytes(5));
+    if (attr_err == cudaSuccess)
+      attr_err = cudaFuncSetAttribute(arc_gemm_pair_kernel<4, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, p_smem_bytes(5));
+    if (attr_err == cudaSuccess)
+      attr_err = cudaFuncSetAttribute(arc_gemm_pair_kernel<2, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, p_smem_bytes(4));
   });
   if (attr_err != cudaSuccess) return attr_err;
   Args a;
@@ -455,17 +731,23 @@ cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t stream, const char** 
   a.y_fp32 = p.y_fp32;
   static const int dbg = getenv("ARC_GEMM_DEBUG") ? atoi(getenv("ARC_GEMM_DEBUG")) : 0;
   a.debug = dbg;
+  // Keep the smaller operand L2-resident: sweep the tiles along it fastest so each wave of
+  // clusters streams the larger operand once (e.g. down-proj: B 30 MB resident, A 59 MB streamed).
+  static const int env_raster = getenv("ARC_GEMM_RASTER") ? atoi(getenv("ARC_GEMM_RASTER")) : -1;
+  a.raster = env_raster >= 0 ? env_raster : (p.M > p.N ? 1 : 0);
   a.nsplit = pl.nsplit;
   a.kbs = pl.kbs;
   a.ws = static_cast<float*>(p.ws);
   const int64_t num_m = (p.M + BM - 1) / BM, num_n = (p.N + BN - 1) / BN;
   const int64_t work = ((num_m + CL - 1) / CL) * num_n * pl.nsplit;  // cluster work items
-  const int64_t grid = std::min<int64_t>(work, num_sms() / CL) * CL;
+  const int64_t grid = std::min<int64_t>(work, max_clusters(CL, pl.pair)) * CL;
   cudaLaunchConfig_t cfg;
   memset(&cfg, 0, sizeof(cfg));
   cfg.gridDim = dim3((unsigned)grid);
   cfg.blockDim = dim3(NUM_THREADS);
-  cfg.dynamicSmemBytes = SMEM_BYTES;
+  static const int env_st = getenv("ARC_GEMM_STAGES") ? atoi(getenv("ARC_GEMM_STAGES")) : 5;
+  const bool st4 = pl.pair && CL == 2 && env_st == 4;  // experiment only
+  cfg.dynamicSmemBytes = pl.pair ? p_smem_bytes(st4 ? 4 : 5) : SMEM_BYTES;
   cfg.stream = stream;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -476,8 +758,11 @@ cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t stream, const char** 
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-  cudaError_t e = CL == 1 ? cudaLaunchKernelEx(&cfg, arc_gemm_kernel<1>, tmA, tmB, tmY, a)
-                          : cudaLaunchKernelEx(&cfg, arc_gemm_kernel<2>, tmA, tmB, tmY, a);
+  cudaError_t e = pl.pair ? (CL == 2 ? (st4 ? cudaLaunchKernelEx(&cfg, arc_gemm_pair_kernel<2, 4>, tmA, tmB, tmSFA, tmSFB, tmY, a)
+                                                : cudaLaunchKernelEx(&cfg, arc_gemm_pair_kernel<2, 5>, tmA, tmB, tmSFA, tmSFB, tmY, a))
+                                     : cudaLaunchKernelEx(&cfg, arc_gemm_pair_kernel<4, 5>, tmA, tmB, tmSFA, tmSFB, tmY, a))
+                  : CL == 1 ? cudaLaunchKernelEx(&cfg, arc_gemm_kernel<1>, tmA, tmB, tmY, a)
+                            : cudaLaunchKernelEx(&cfg, arc_gemm_kernel<2>, tmA, tmB, tmY, a);
   if (e != cudaSuccess) return e;
   if (pl.nsplit > 1) {
     const int64_t total = p.M * p.N;

@@ -40,7 +40,8 @@ def _check(y, yref, bound, bf16):
 
 
 @pytest.mark.parametrize("M,N,K,S", [(16, 256, 256, 16), (1, 256, 256, 16), (128, 256, 256, 0), (200, 300, 512, 64),
-                                     (129, 520, 1024, 128), (64, 64, 112, 48), (257, 1024, 4096, 128)])
+                                     (129, 520, 1024, 128), (64, 64, 112, 48), (257, 1024, 4096, 128),
+                                     (520, 600, 1024, 64), (1024, 768, 2048, 128)])
 @pytest.mark.parametrize("layout", [0, 1])
 def test_gemm_parity_fp32(A, M, N, K, S, layout):
     x, w, prof, qw = _problem(A, M, N, K, S, layout, seed=M + N)
@@ -95,6 +96,22 @@ def test_full_size_sampled_rows(A):
     _check(y[torch.from_numpy(rows).cuda()].float().cpu().numpy().astype(np.float64), yref, bound, True)
 
 
+@pytest.mark.parametrize("M,N", [(4096, 4096), (2944, 2816)])
+def test_multi_tile_sampled_rows(A, M, N):
+    """Several output tiles per persistent cluster (accumulator double-buffering, stage-ring
+    phase wrap across tiles) with ragged M/N edges; exact oracle GEMM on sampled rows that
+    cover every 128-row tile position of a 4-CTA cluster."""
+    K, S = 1024, 64
+    x, w, prof, qw = _problem(A, M, N, K, S, seed=11)
+    codes, sf = A.quantize_activation(x, prof)
+    y = A.gemm(codes, sf, prof.gs, qw, out_dtype=torch.float32)
+    torch.cuda.synchronize()
+    rows = np.unique(np.concatenate([np.arange(0, M, 97), [M - 1, 127, 128, 255, 256, 383, 384, 511]])).astype(np.int64)
+    yref, bound = oracle.gemm_reference(codes.cpu().numpy(), sf.cpu().numpy(), qw.codes.cpu().numpy(),
+                                        qw.sf.cpu().numpy(), float(prof.gs.item()), float(qw.gs.item()), rows=rows)
+    _check(y[torch.from_numpy(rows).cuda()].cpu().numpy().astype(np.float64), yref, bound, False)
+
+
 def test_hostio_matches_device_path(A):
     M, N, K, S = 100, 512, 1024, 64
     x, w, prof, qw = _problem(A, M, N, K, S, seed=9)
@@ -143,3 +160,20 @@ def test_decode_splitk_parity(A, M, N, K, S):
     _check(y16.float().cpu().numpy().astype(np.float64), yref, bound, True)
     if M <= 64 and N >= 1024:
         assert A.gemm_workspace_size(M, qw) > 0, "decode-size M should use the split-K plan"
+
+
+@pytest.mark.parametrize("env", [{"ARC_GEMM_PAIR": "1", "ARC_GEMM_CLP": "2"}, {"ARC_GEMM_PAIR": "1", "ARC_GEMM_CLP": "4"},
+                                 {"ARC_GEMM_CL": "1"}, {"ARC_GEMM_RASTER": "1"}, {"ARC_GEMM_RASTER": "0"}],
+                         ids=["pair2", "pair4", "cl1", "raster1", "raster0"])
+def test_kernel_variants(env):
+    """The non-default GEMM kernels/schedules (2-SM cta_group::2 pairs, 4-CTA clusters with
+    multicast B, single-CTA, both tile orders) through the same parity tests, in a fresh
+    process (the selection is read once per process)."""
+    import os
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    r = subprocess.run([sys.executable, "-m", "pytest", os.path.join(here, "test_gpu_gemm.py"), "-q", "-x",
+                        "-k", "parity_fp32 or multi_tile or same_sign"],
+                       env={**os.environ, **env}, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
