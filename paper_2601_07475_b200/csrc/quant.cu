@@ -201,6 +201,23 @@ ARC_DEV void gather16(const uint8_t* base, const uint32_t (&off)[16], float (&z)
   for (int q = 0; q < 16; ++q) z[q] = bf16_bits_to_f32(*reinterpret_cast<const uint16_t*>(base + off[q]));
 }
 
+// Rows of a tile.  Tile t of the 128-row group g holds rows base + 32 i, i < R, with
+// base = 128 g + 32 R h + r (t = g * 128/R + 32 h + r): the R rows share (m & 31) and
+// have consecutive (m >> 5) & 3, so in the 128x4 scale layout the tile's scales of one
+// 4-block unit are R * 4 contiguous bytes -- staged in smem and stored as one R*4-byte
+// word per unit instead of 4R scattered bytes.
+template <int R>
+ARC_DEV int tile_base(int t) {
+  constexpr int TPG = 128 / R;
+  const int g = t / TPG, tin = t - g * TPG;
+  return g * 128 + (tin >> 5) * (R * 32) + (tin & 31);
+}
+template <int R>
+ARC_DEV int tile_rows(int base, int64_t rows) {  // valid rows base + 32 i < rows
+  const int64_t left = rows - base;
+  return left <= 0 ? 0 : (int)dmin64(R, (left + 31) / 32);
+}
+
 // The quantization kernel.  Warp roles (no intra-warp divergence in steady state):
 //  * primary warps: lane t owns logical primary block t (or a zero pad block) for
 //    every row; its 16 gather offsets (byte offsets of the calibrated channels in
@@ -211,19 +228,25 @@ ARC_DEV void gather16(const uint8_t* base, const uint32_t (&off)[16], float (&z)
 //    the bitwise duplicate.  Gathering the outlier blocks of all R rows
 //    of a tile into one warp keeps the heavier dual-stage work from serializing
 //    a warp of primaries.
-//  * producer warp: streams rows HBM -> smem with cp.async (16 B per
-//    lane-instruction, coalesced) into an ST-deep ring of R-row tiles, signalling
-//    full[s] with cp.async.mbarrier.arrive; compute warps release a slot by
-//    arriving on empty[s] (no CTA-wide barrier).
-// Rows sit at a fixed ROWB stride and the tile loop is unrolled over the ring so
-// the gathers are `LDS [off + const]`.
+//  * producer warp: streams rows HBM -> smem (one cp.async.bulk per row) into an
+//    ST-deep ring of R-row tiles (full[s] completes on the bytes); compute warps
+//    release a slot by arriving on empty[s] (no CTA-wide barrier).  Before it
+//    refills a slot the producer writes the slot's staged scale bytes out
+//    (R*4-byte words, one per 4-block unit).
+// Rows sit at a fixed ROWP stride (ROWB + 16: rows of one tile fall in different
+// banks for the residual warp's cross-row gathers) and the tile loop is unrolled
+// over the ring so the gathers are `LDS [off + const]`.
 template <int IPT, int R, int ROWB, int ST>
 __global__ void __launch_bounds__(1024) arc_quant_kernel(QuantArgs p) {
   extern __shared__ __align__(16) uint8_t smem[];
-  constexpr int SLOT = R * ROWB;
+  constexpr int ROWP = ROWB + 16;
+  constexpr int SLOT = R * ROWP;
+  constexpr int UB = R * 4;  // staged scale bytes per 4-block unit per tile
   const int K = p.K;
   const int npw = p.npw, nrw = p.nrw;
-  float* k1tab = reinterpret_cast<float*>(smem + ST * SLOT);
+  const int NU = p.Kp >> 6;  // 4-block units per row
+  uint8_t* sfst = smem + ST * SLOT;  // [ST][NU][UB]
+  float* k1tab = reinterpret_cast<float*>(sfst + ST * NU * UB);
   float* c6tab = k1tab + 128;  // RN(e4m3(c) / 6): the residual stage's c6 for base d1 = e4m3(c)
   float* rat = c6tab + 128;    // RN((8+m1)/(8+m2)): mantissa ratio of two normal E4M3 scales
   uint64_t* full = reinterpret_cast<uint64_t*>(rat + 64);
@@ -231,8 +254,10 @@ __global__ void __launch_bounds__(1024) arc_quant_kernel(QuantArgs p) {
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
-  const int ntile = (int)((p.rows + R - 1) / R);
+  const int ntile = (int)((p.rows + 127) / 128) * (128 / R);
   const int my_tiles = ntile > (int)blockIdx.x ? (ntile - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
+  const int sf_rb_stride = (p.Kp >> 6) * 512;
+  const int code_row = p.Kp >> 1;
   pdl_launch_dependents();
   pdl_wait();  // (PDL) the previous kernel's writes are visible from here on
   const float gs = __ldg(p.gs);
@@ -259,6 +284,17 @@ __global__ void __launch_bounds__(1024) arc_quant_kernel(QuantArgs p) {
     const uint32_t ring = smem_u32(smem) + (uint32_t)lane * 16u;
     const int kc = K >> 3;  // 16-byte chunks per row
     const uint64_t x_policy = policy_evict_first();
+    // scales staged for tile jt (slot s) -> global, one UB-byte word per unit
+    auto flush_sf = [&](int s, int jt) {
+      const int base = tile_base<R>((int)blockIdx.x + jt * (int)gridDim.x);
+      uint8_t* dst = p.sf + (int64_t)(base >> 7) * sf_rb_stride + (base & 31) * 16 + ((base >> 5) & 3) * 4;
+      const uint8_t* src = sfst + s * NU * UB;
+      for (int u = lane; u < NU; u += 32) {
+        if (UB == 16) *reinterpret_cast<uint4*>(dst + u * 512) = *reinterpret_cast<const uint4*>(src + u * 16);
+        else if (UB == 8) *reinterpret_cast<uint2*>(dst + u * 512) = *reinterpret_cast<const uint2*>(src + u * 8);
+        else *reinterpret_cast<uint32_t*>(dst + u * 512) = *reinterpret_cast<const uint32_t*>(src + u * 4);
+      }
+    };
     for (int j0 = 0; j0 < my_tiles; j0 += ST) {
 #pragma unroll
       for (int s = 0; s < ST; ++s) {
@@ -267,33 +303,40 @@ __global__ void __launch_bounds__(1024) arc_quant_kernel(QuantArgs p) {
           if (j >= ST) {
             mbar_wait(&empty[s], ((j / ST) - 1) & 1);
             fence_proxy_async();  // order the consumers' generic-proxy reads before the async refill
+            flush_sf(s, j - ST);
           }
-          const int r0 = ((int)blockIdx.x + j * (int)gridDim.x) * R;
-          const int nr = min(R, (int)p.rows - r0);
+          const int base = tile_base<R>((int)blockIdx.x + j * (int)gridDim.x);
+          const int nr = tile_rows<R>(base, p.rows);
           if (p.bulk) {
             // one cp.async.bulk per row (TMA engine, no LSU/MIO traffic); lane 0 only
             if (lane == 0) {
               mbar_expect_tx(&full[s], (uint32_t)(nr * K * 2));
               if (p.debug != 2)
                 for (int r = 0; r < nr; ++r)  // X is read once: evict-first
-                  bulk_load_hint(smem + s * SLOT + r * ROWB, p.x + (int64_t)(r0 + r) * p.ld, (uint32_t)K * 2, &full[s],
-                                 x_policy);
+                  bulk_load_hint(smem + s * SLOT + r * ROWP, p.x + (int64_t)(base + 32 * r) * p.ld, (uint32_t)K * 2,
+                                 &full[s], x_policy);
               else
                 mbar_complete_tx_self(&full[s], (uint32_t)(nr * K * 2));
             }
           } else {
             if (p.debug != 2) {
-              const uint16_t* src0 = p.x + (int64_t)r0 * p.ld + lane * 8;
 #pragma unroll
               for (int r = 0; r < R; ++r)
-                if (r < nr)
+                if (r < nr) {
+                  const uint16_t* src = p.x + (int64_t)(base + 32 * r) * p.ld + lane * 8;
                   for (int c = 0; c < kc - lane; c += 32)
-                    cp_async16(ring + (uint32_t)(s * SLOT + r * ROWB + c * 16), src0 + (int64_t)r * p.ld + c * 8);
+                    cp_async16(ring + (uint32_t)(s * SLOT + r * ROWP + c * 16), src + c * 8);
+                }
             }
             cp_async_arrive(&full[s]);
           }
         }
       }
+    }
+    for (int jt = my_tiles > ST ? my_tiles - ST : 0; jt < my_tiles; ++jt) {
+      const int s = jt % ST;
+      mbar_wait(&empty[s], (jt / ST) & 1);
+      flush_sf(s, jt);
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
     return;
@@ -302,8 +345,6 @@ __global__ void __launch_bounds__(1024) arc_quant_kernel(QuantArgs p) {
   const int nb = K >> 4, ns = p.S >> 4;
   const int ka16 = nb + ns, NB = p.Kp >> 4;
   const float c6g = __fdiv_rn(gs, 6.0f);
-  const int sf_rb_stride = (p.Kp >> 6) * 512;
-  const int code_row = p.Kp >> 1;
 
   if (warp < npw) {
     // ---------------------------------------------------------------- primary warps
@@ -334,30 +375,30 @@ __global__ void __launch_bounds__(1024) arc_quant_kernel(QuantArgs p) {
         if (j < my_tiles) {
           mbar_wait(&full[s], (j / ST) & 1);
           if (p.debug != 1) {
-            const int r0 = ((int)blockIdx.x + j * (int)gridDim.x) * R;
-            const int nr = min(R, (int)p.rows - r0);
+            const int base = tile_base<R>((int)blockIdx.x + j * (int)gridDim.x);
+            const int nr = tile_rows<R>(base, p.rows);
+            uint8_t* st = sfst + s * NU * UB;
 #pragma unroll
             for (int i = 0; i < IPT; ++i) {
               if (kind[i] != 0) {
                 const int pb = pbs[i];
-                uint8_t* cptr = p.codes + (int64_t)r0 * code_row + pb * 8;
-                uint8_t* sptr = p.sf + (pb >> 2) * 512 + (pb & 3);
+                uint8_t* cptr = p.codes + (int64_t)base * code_row + pb * 8;
+                uint8_t* sst = st + (pb >> 2) * UB + (pb & 3);
 #pragma unroll
                 for (int r = 0; r < R; ++r) {
+                  uint32_t sfb = 0;
                   if (r < nr) {
-                    const int m = r0 + r;
-                    uint32_t sfb = 0;
                     uint2 packed = make_uint2(0u, 0u);
                     if (kind[i] == 1) {
                       float z[16];
-                      gather16(smem + s * SLOT + r * ROWB, off[i], z);
+                      gather16(smem + s * SLOT + r * ROWP, off[i], z);
                       // stage 1 (Eq.1 with the NVFP4 two-level scale, Q7 op order)
                       sfb = e4m3_ceil_nb(__fmul_rn(absmax16(z), c6g));
                       packed = encode16(z, k1tab[sfb]);
                     }
-                    *reinterpret_cast<uint2*>(cptr + (int64_t)r * code_row) = packed;
-                    sptr[(int64_t)(m >> 7) * sf_rb_stride + (m & 31) * 16 + ((m >> 5) & 3) * 4] = (uint8_t)sfb;
+                    *reinterpret_cast<uint2*>(cptr + (int64_t)(32 * r) * code_row) = packed;
                   }
+                  sst[4 * r] = (uint8_t)sfb;  // rows past M stage a 0 scale (padding rows)
                 }
               }
             }
@@ -382,10 +423,10 @@ __global__ void __launch_bounds__(1024) arc_quant_kernel(QuantArgs p) {
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const int4 v = __ldg(pp + q);
-      foff[4 * q + 0] = (uint32_t)v.x * 2u + (uint32_t)(fr * ROWB);
-      foff[4 * q + 1] = (uint32_t)v.y * 2u + (uint32_t)(fr * ROWB);
-      foff[4 * q + 2] = (uint32_t)v.z * 2u + (uint32_t)(fr * ROWB);
-      foff[4 * q + 3] = (uint32_t)v.w * 2u + (uint32_t)(fr * ROWB);
+      foff[4 * q + 0] = (uint32_t)v.x * 2u + (uint32_t)(fr * ROWP);
+      foff[4 * q + 1] = (uint32_t)v.y * 2u + (uint32_t)(fr * ROWP);
+      foff[4 * q + 2] = (uint32_t)v.z * 2u + (uint32_t)(fr * ROWP);
+      foff[4 * q + 3] = (uint32_t)v.w * 2u + (uint32_t)(fr * ROWP);
     }
   }
   const int fpb = phys_block(nb + fjb, nb, ns, p.layout);
@@ -396,8 +437,9 @@ __global__ void __launch_bounds__(1024) arc_quant_kernel(QuantArgs p) {
       if (j < my_tiles) {
         mbar_wait(&full[s], (j / ST) & 1);
         if (p.debug != 1) {
-          const int r0 = ((int)blockIdx.x + j * (int)gridDim.x) * R;
-          const int nr = min(R, (int)p.rows - r0);
+          const int base = tile_base<R>((int)blockIdx.x + j * (int)gridDim.x);
+          const int nr = tile_rows<R>(base, p.rows);
+          uint8_t* st = sfst + s * NU * UB;
           for (int it = rl; it < nitems; it += nrw * 32) {
             int r = fr, jb = fjb, pb = fpb;
             uint32_t off[16];
@@ -411,20 +453,21 @@ __global__ void __launch_bounds__(1024) arc_quant_kernel(QuantArgs p) {
 #pragma unroll
               for (int q = 0; q < 4; ++q) {
                 const int4 v = __ldg(pp + q);
-                off[4 * q + 0] = (uint32_t)v.x * 2u + (uint32_t)(r * ROWB);
-                off[4 * q + 1] = (uint32_t)v.y * 2u + (uint32_t)(r * ROWB);
-                off[4 * q + 2] = (uint32_t)v.z * 2u + (uint32_t)(r * ROWB);
-                off[4 * q + 3] = (uint32_t)v.w * 2u + (uint32_t)(r * ROWB);
+                off[4 * q + 0] = (uint32_t)v.x * 2u + (uint32_t)(r * ROWP);
+                off[4 * q + 1] = (uint32_t)v.y * 2u + (uint32_t)(r * ROWP);
+                off[4 * q + 2] = (uint32_t)v.z * 2u + (uint32_t)(r * ROWP);
+                off[4 * q + 3] = (uint32_t)v.w * 2u + (uint32_t)(r * ROWP);
               }
             }
+            uint32_t sfb = 0;
             if (r < nr) {
-              const int m = r0 + r;
+              const int m = base + 32 * r;
               float z[16];
               gather16(smem + s * SLOT, off, z);
               const uint32_t sf1 = e4m3_ceil_nb(__fmul_rn(absmax16(z), c6g));
               float t[16];
               uint2 packed = encode16(z, k1tab[sf1], t);
-              uint32_t sfb = sf1;
+              sfb = sf1;
               if (!p.weight_mode) {
                 // residual of the encoded primary in units of d1/gs, exact (Q6): e = t - v(q1);
                 // stage 2 with base d1: c6 = RN(d1/6) (table), k2 = RN(d1/d2)
@@ -435,9 +478,8 @@ __global__ void __launch_bounds__(1024) arc_quant_kernel(QuantArgs p) {
                 sfb = sf2;
               }  // weight mode: bitwise duplicate of the primary block
               *reinterpret_cast<uint2*>(p.codes + (int64_t)m * code_row + pb * 8) = packed;
-              p.sf[(int64_t)(m >> 7) * sf_rb_stride + (pb >> 2) * 512 + (pb & 3) + (m & 31) * 16 +
-                   ((m >> 5) & 3) * 4] = (uint8_t)sfb;
             }
+            st[(pb >> 2) * UB + 4 * r + (pb & 3)] = (uint8_t)sfb;
           }
         }
         __syncwarp();
@@ -502,7 +544,7 @@ template <int IPT, int R, int ROWB, int ST>
 static cudaError_t launch_quant_cfg(QuantArgs a, int threads, cudaStream_t stream) {
   a.rows_per_tile = R;
   a.stages = ST;
-  const size_t smem = (size_t)ST * R * ROWB + (128 + 128 + 64) * 4 + 2 * ST * 8;
+  const size_t smem = (size_t)ST * R * (ROWB + 16) + (size_t)ST * (a.Kp / 64) * (R * 4) + (128 + 128 + 64) * 4 + 2 * ST * 8;
   struct Cfg { int dev, threads; size_t smem; int occ; };
   static thread_local Cfg cache[8];
   static thread_local int ncache = 0;
@@ -524,7 +566,7 @@ static cudaError_t launch_quant_cfg(QuantArgs a, int threads, cudaStream_t strea
     cache[ncache % 8] = Cfg{dev, threads, smem, occ};
     ++ncache;
   }
-  const int64_t ntile = (a.rows + R - 1) / R;
+  const int64_t ntile = (a.rows + 127) / 128 * (128 / R);
   const int64_t grid = imin64(ntile, (int64_t)num_sms() * occ);
   cudaLaunchConfig_t cfg;
   memset(&cfg, 0, sizeof(cfg));
