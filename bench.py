@@ -340,7 +340,7 @@ def main():
         out["roofline"]["traffic"] = tr.get("gemm_bytes_per_launch")
         out["roofline"]["traffic_note"] = "profiles/ncu_traffic.json (committed ncu capture); algorithmic " \
             f"{tr.get('gemm_algorithmic_bytes_per_launch', 0):.3g} B per launch"
-        out["quantize"]["traffic"] = tr.get("quant_bytes_per_launch_qkv_fullset")
+        out["quantize"]["traffic"] = tr.get("quant_bytes_per_launch")
 
     # decode-size step (BASELINE configs[1] decode M): the same 4 sites at M=16 tokens through
     # arc_linear (quantize + split-K GEMM + fixed-order reduction), CUDA-graph replay; the

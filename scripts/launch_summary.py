@@ -46,6 +46,28 @@ for k, v in sorted(agg.items(), key=lambda kv: -kv[1]["t_ns"])[:12]:
     out[k] = {"launches": v["n"], "mean_us": v["t_ns"] / v["n"] / 1e3, "total_us": v["t_ns"] / 1e3,
               "mean_dram_bytes": (v["rd"] + v["wr"]) / v["n"],
               "share_of_arc_time": v["t_ns"] / tot if k in ours else None}
+# the prefill step's launches (bench.py's timed region: 4 x (quant, GEMM) at M = 8192) vs the
+# decode section's (M = 16): prefill GEMMs run > 40 us; each follows its site's quantize launch
+pre = defaultdict(lambda: {"n": 0, "t_ns": 0.0, "bytes": 0.0})
+ids = sorted(per, key=int)
+for pos, i in enumerate(ids):
+    k = names[i]
+    t = per[i].get("gpu__time_duration.sum", 0)
+    if not ("arc_gemm" in k and "reduce" not in k and t > 40e3):
+        continue
+    # a prefill GEMM and the quantize launch right before it (its site's activation)
+    picks = [("arc_gemm_kernel", i)]
+    if pos > 0 and "arc_quant_kernel" in names[ids[pos - 1]]:
+        picks.append(("arc_quant_kernel", ids[pos - 1]))
+    for key, j in picks:
+        m = per[j]
+        pre[key]["n"] += 1
+        pre[key]["t_ns"] += m.get("gpu__time_duration.sum", 0)
+        pre[key]["bytes"] += m.get("dram__bytes_read.sum", 0) + m.get("dram__bytes_write.sum", 0)
+ptot = sum(v["t_ns"] for v in pre.values())
+out["prefill_step"] = {k: {"launches": v["n"], "mean_us": v["t_ns"] / max(v["n"], 1) / 1e3,
+                           "mean_dram_bytes": v["bytes"] / max(v["n"], 1), "share_of_step": v["t_ns"] / ptot}
+                       for k, v in pre.items()}
 print(json.dumps(out, indent=1))
 if "--json" in sys.argv:
     json.dump(out, open(sys.argv[sys.argv.index("--json") + 1], "w"), indent=1)
