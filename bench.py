@@ -342,43 +342,52 @@ def main():
             f"{tr.get('gemm_algorithmic_bytes_per_launch', 0):.3g} B per launch"
         out["quantize"]["traffic"] = tr.get("quant_bytes_per_launch")
 
-    # decode-size step (BASELINE configs[1] decode M): the same 4 sites at M=16 tokens through
-    # arc_linear (quantize + split-K GEMM + fixed-order reduction), CUDA-graph replay; the
-    # weights (~126 MB for the 4 sites) stream from HBM/L2 every step.
+    # decode-size step (BASELINE configs[1] decode M): the same 4 sites at M=16 tokens, CUDA-graph
+    # replay; the weights (~128 MB for the 4 sites, > L2) stream from HBM every step.  Default =
+    # arc_linear (quantize kernel + split-K GEMM + reduce kernel); the one-kernel fused decode
+    # linear (quantize + stream-K GEMM + fixed-order reduction) beside it.
     if not args.no_decode and world == 1:
         Md = 16
         xd = [synth.activation(Md, s.K, synth.Structure(s.K, 8, seed=5), seed=9, device=device) for s in sites]
         yd = [torch.empty(Md, s.N, dtype=torch.bfloat16, device=device) for s in sites]
         wsd = [A.Workspace(device) for _ in sites]
-        for s, x_, y_, w_ in zip(sites, xd, yd, wsd):
-            A.linear(x_, s.prof, s.qw, out=y_, ws=w_)
-        torch.cuda.synchronize()
-        g = torch.cuda.CUDAGraph()
-        gs_ = torch.cuda.Stream()
-        with torch.cuda.stream(gs_):
-            with torch.cuda.graph(g, stream=gs_):
-                for s, x_, y_, w_ in zip(sites, xd, yd, wsd):
-                    A.linear(x_, s.prof, s.qw, out=y_, ws=w_)
-        torch.cuda.synchronize()
-        for _ in range(3):
-            g.replay()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        reps = 50
-        torch.cuda.synchronize()
-        e0.record()
-        for _ in range(reps):
-            g.replay()
-        e1.record()
-        torch.cuda.synchronize()
-        dms = e0.elapsed_time(e1) / reps
+        dec = {}
+        for mode in ("fused", "unfused"):
+            for s, x_, y_, w_ in zip(sites, xd, yd, wsd):
+                A.linear(x_, s.prof, s.qw, out=y_, ws=w_, mode=mode)
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            gs_ = torch.cuda.Stream()
+            with torch.cuda.stream(gs_):
+                with torch.cuda.graph(g, stream=gs_):
+                    for s, x_, y_, w_ in zip(sites, xd, yd, wsd):
+                        A.linear(x_, s.prof, s.qw, out=y_, ws=w_, mode=mode)
+            torch.cuda.synchronize()
+            for _ in range(3):
+                g.replay()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            reps = 50
+            torch.cuda.synchronize()
+            e0.record()
+            for _ in range(reps):
+                g.replay()
+            e1.record()
+            torch.cuda.synchronize()
+            dec[mode] = e0.elapsed_time(e1) / reps
+            del g
+        dms = dec["unfused"]
         wbytes = sum(s.N * s.Kp * 9 // 16 for s in sites)
         dbytes = wbytes + sum(Md * s.K * 2 + Md * s.N * 2 for s in sites)
         out["decode"] = {"M_tokens": Md, "us_per_layer_step": dms * 1e3, "tflops": sum(2.0 * Md * s.N * (s.K + s.S)
                          for s in sites) / (dms * 1e-3) / 1e12,
                          "bytes_per_step": dbytes, "achieved_gbs": dbytes / (dms * 1e-3) / 1e9,
                          "hbm_frac": dbytes / (dms * 1e-3) / 1e9 / peaks["hbm"],
-                         "note": "4 sites x (quant + split-K GEMM + reduce) = 12 launches per step in one CUDA graph; "
-                                 "bound = weight bytes / HBM"}
+                         "fused_us_per_layer_step": dec["fused"] * 1e3,
+                         "fused_hbm_frac": dbytes / (dec["fused"] * 1e-3) / 1e9 / peaks["hbm"],
+                         "note": "4 sites x (quantize + split-K GEMM + reduce, PDL-chained) per step in one CUDA "
+                                 "graph (arc_linear default); fused_* = the one-kernel fused decode linear "
+                                 "(ARC_LINEAR_FUSED: quantize phase + grid barrier + stream-K GEMM + in-kernel "
+                                 "reduction); bound = weight bytes / HBM"}
 
     # e2e through the public C-ABI host-buffer call (H2D of x and D2H of y inside the timed region)
     if not args.no_e2e:

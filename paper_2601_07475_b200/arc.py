@@ -72,6 +72,11 @@ _sig("arc_quantize_activation", [_P, _i64, _i64, ctypes.POINTER(ArcProfile), _P,
 _sig("arc_gemm", [_P, _P, _P, _i64, ctypes.POINTER(ArcQWeight), _P, ctypes.c_int, _i64, _P, ctypes.c_size_t, _P])
 _sig("arc_linear", [_P, _i64, _i64, ctypes.POINTER(ArcProfile), ctypes.POINTER(ArcQWeight), _P, ctypes.c_int,
                     _i64, _P, ctypes.c_size_t, _P])
+_sig("arc_linear_ex", [_P, _i64, _i64, ctypes.POINTER(ArcProfile), ctypes.POINTER(ArcQWeight), _P, ctypes.c_int,
+                       _i64, _P, ctypes.c_size_t, ctypes.c_int, _P])
+_sig("arc_linear_ex_workspace_size", [_i64, ctypes.POINTER(ArcQWeight), ctypes.c_int, ctypes.POINTER(ctypes.c_size_t)])
+_sig("arc_linear_fused_operand_offsets", [_i64, ctypes.POINTER(ArcQWeight), ctypes.POINTER(ctypes.c_size_t),
+                                          ctypes.POINTER(ctypes.c_size_t)])
 _sig("arc_linear_hostio_workspace_size", [_i64, ctypes.POINTER(ArcQWeight), ctypes.c_int,
                                          ctypes.POINTER(ctypes.c_size_t)])
 _sig("arc_linear_hostio", [_P, _i64, ctypes.POINTER(ArcProfile), ctypes.POINTER(ArcQWeight), _P, ctypes.c_int, _P,
@@ -86,8 +91,9 @@ EXPORTED = [
     "arc_status_string", "arc_last_error", "arc_device_supported", "arc_buffer_sizes", "arc_gemm_workspace_size",
     "arc_linear_workspace_size",
     "arc_calib_absmax", "arc_select_outliers", "arc_gather_order", "arc_tensor_scale", "arc_quantize_weight",
-    "arc_quantize_activation", "arc_gemm", "arc_linear", "arc_linear_hostio_workspace_size", "arc_linear_hostio",
-    "arc_probe_e2m1", "arc_probe_e2m1_bits", "arc_probe_e2m1_raw_bits", "arc_probe_e4m3_ceil",
+    "arc_quantize_activation", "arc_gemm", "arc_linear", "arc_linear_ex", "arc_linear_ex_workspace_size",
+    "arc_linear_fused_operand_offsets", "arc_linear_hostio_workspace_size", "arc_linear_hostio",
+    "arc_probe_e2m1", "arc_probe_e2m1_bits", "arc_probe_e2m1_raw_bits", "arc_probe_e4m3_ceil", "arc_debug_fused_trace",
 ]
 
 
@@ -286,8 +292,8 @@ def _dtype_code(dt) -> int:
 
 class Workspace:
     """Grow-only device workspace for arc_gemm / arc_linear (256-byte aligned by the
-    allocator, zero-filled on allocation: the split-K tile counters must start at 0,
-    and the kernels leave them at 0)."""
+    allocator, zero-filled on allocation: the sync words of the fused kernel (grid barrier,
+    per-tile counters) must start at 0, and every call leaves them at 0)."""
 
     def __init__(self, device="cuda"):
         self.device = device
@@ -320,20 +326,41 @@ def gemm(a_codes, a_sf, gs_x: torch.Tensor, qw: QWeight, out_dtype=torch.bfloat1
     return out
 
 
+LINEAR_MODES = {"auto": 0, "fused": 1, "unfused": 2}  # arc.h ARC_LINEAR_AUTO / _FUSED / _UNFUSED
+
+
+def linear_workspace_size_ex(M: int, qw, mode: str = "auto") -> int:
+    b = ctypes.c_size_t()
+    _check(_lib.arc_linear_ex_workspace_size(M, ctypes.byref(qw.c()), LINEAR_MODES[mode], ctypes.byref(b)),
+           "arc_linear_ex_workspace_size")
+    return b.value
+
+
+def fused_operand_offsets(M: int, qw):
+    """Byte offsets (codes, scales) of the quantized activation the fused kernel leaves in its workspace."""
+    c, f = ctypes.c_size_t(), ctypes.c_size_t()
+    _check(_lib.arc_linear_fused_operand_offsets(M, ctypes.byref(qw.c()), ctypes.byref(c), ctypes.byref(f)),
+           "arc_linear_fused_operand_offsets")
+    return c.value, f.value
+
+
 def linear(x: torch.Tensor, prof: Profile, qw: QWeight, out_dtype=torch.bfloat16, out=None, ws: Workspace = None,
-           stream=None):
-    """The ARC linear layer: fused activation quantize + augmented NVFP4 GEMM (two launches)."""
+           stream=None, mode: str = "auto"):
+    """The ARC linear layer (Eq.2): activation quantize + augmented NVFP4 GEMM.  mode "unfused" = two
+    launches (quantize kernel, GEMM kernel); "fused" (M <= 128) = one kernel that quantizes, multiplies
+    and reduces (slower on B200, see decode.cu); "auto" = unfused."""
     assert x.dtype == torch.bfloat16 and x.is_cuda
     M = x.shape[0]
     if out is None:
         out = _alloc_out(M, qw.N, out_dtype, x.device)
-    need = linear_workspace_size(M, qw)
+    need = linear_workspace_size_ex(M, qw, mode)
     if ws is None:
         ws = _default_ws.setdefault(x.device, Workspace(x.device))
     buf = ws.get(need)
-    _check(_lib.arc_linear(_ptr(x), M, x.stride(0), ctypes.byref(prof.c()), ctypes.byref(qw.c()), _ptr(out),
-                           _dtype_code(out.dtype), out.stride(0), _ptr(buf), buf.numel(), _stream(stream)),
-           "arc_linear")
+    _check(_lib.arc_linear_ex(_ptr(x), M, x.stride(0), ctypes.byref(prof.c()), ctypes.byref(qw.c()), _ptr(out),
+                              _dtype_code(out.dtype), out.stride(0), _ptr(buf), buf.numel(), LINEAR_MODES[mode],
+                              _stream(stream)),
+           "arc_linear_ex")
     return out
 
 

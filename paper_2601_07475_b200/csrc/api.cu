@@ -136,11 +136,27 @@ arc_status_t arc_gemm_workspace_size(int64_t M, const arc_qweight_t* qw, size_t*
   return ARC_OK;
 }
 
+// arc_linear workspace: [sync words | quantized A + arc_gemm workspace] (unfused) or
+// [sync words | fused-kernel workspace] (fused, M <= 128); the sync words sit at offset 0
+// in both so a workspace shared by both paths keeps them zero.
+static size_t linear_rest_bytes(int64_t M, const arc_qweight_t* qw, int flags) {
+  size_t rest = 0;
+  if (flags != ARC_LINEAR_FUSED) {
+    rest = act_ws_bytes(M, qw->K, qw->S) + (size_t)round_up((int64_t)plan_gemm(M, qw->N, qw->Kp).ws_bytes, 256);
+  }
+  if (flags != ARC_LINEAR_UNFUSED) {
+    const FusedPlan fp = plan_fused(M, qw->N, qw->Kp);
+    if (fp.ok) rest = std::max(rest, (size_t)round_up((int64_t)fp.ws_bytes, 256));
+  }
+  return rest;
+}
+
 arc_status_t arc_linear_workspace_size(int64_t M, const arc_qweight_t* qw, size_t* bytes) {
-  size_t g = 0;
-  arc_status_t s = arc_gemm_workspace_size(M, qw, &g);
+  arc_status_t s = check_qweight(qw);
   if (s != ARC_OK) return s;
-  *bytes = act_ws_bytes(M, qw->K, qw->S) + (size_t)round_up((int64_t)g, 256);
+  if (!bytes) return fail(ARC_ERR_NULL, "null bytes");
+  if (M < 0) return fail(ARC_ERR_SHAPE, "M < 0");
+  *bytes = sync_bytes_of(qw->N) + (M == 0 ? 0 : linear_rest_bytes(M, qw, ARC_LINEAR_AUTO));
   return ARC_OK;
 }
 
@@ -328,29 +344,95 @@ arc_status_t arc_gemm(const uint8_t* a_codes, const uint8_t* a_sf, const float* 
   return e == cudaSuccess ? ARC_OK : cuda_fail(e, "arc_gemm", detail);
 }
 
-arc_status_t arc_linear(const void* x, int64_t M, int64_t ldx, const arc_profile_t* prof, const arc_qweight_t* qw,
-                        void* y, arc_dtype_t y_dtype, int64_t ldy, void* ws, size_t ws_bytes, void* stream) {
+arc_status_t arc_linear_ex(const void* x, int64_t M, int64_t ldx, const arc_profile_t* prof, const arc_qweight_t* qw,
+                           void* y, arc_dtype_t y_dtype, int64_t ldy, void* ws, size_t ws_bytes, int flags,
+                           void* stream) {
   arc_status_t s = check_profile(prof);
   if (s != ARC_OK) return s;
   s = check_qweight(qw);
   if (s != ARC_OK) return s;
   if (qw->K != prof->K || qw->S != prof->S || qw->layout != prof->layout)
     return fail(ARC_ERR_SHAPE, "profile and qweight disagree on K / S / layout");
-  if (M < 0) return fail(ARC_ERR_SHAPE, "M < 0");
+  if (flags != ARC_LINEAR_AUTO && flags != ARC_LINEAR_FUSED && flags != ARC_LINEAR_UNFUSED)
+    return fail(ARC_ERR_SHAPE, "bad flags");
+  if (M < 0 || M > (1 << 30)) return fail(ARC_ERR_SHAPE, "bad M");
+  if (flags == ARC_LINEAR_FUSED && M > 128) return fail(ARC_ERR_SHAPE, "ARC_LINEAR_FUSED needs M <= 128");
   if (M == 0) return ARC_OK;
-  if (!ws) return fail(ARC_ERR_NULL, "null workspace");
-  size_t need = 0;
-  s = arc_linear_workspace_size(M, qw, &need);
-  if (s != ARC_OK) return s;
-  if (ws_bytes < need) return fail(ARC_ERR_WORKSPACE, "workspace too small");
+  if (!ws || !x || !y) return fail(ARC_ERR_NULL, "null x / y / workspace");
+  if (ldx < prof->K || ldx % 8) return fail(ARC_ERR_SHAPE, "bad ldx");
+  if (y_dtype != ARC_BF16 && y_dtype != ARC_FP32) return fail(ARC_ERR_SHAPE, "y_dtype must be ARC_BF16 or ARC_FP32");
+  if (ldy < qw->N || ldy % (y_dtype == ARC_FP32 ? 4 : 8))
+    return fail(ARC_ERR_SHAPE, "ldy must be >= N and a multiple of 16 bytes");
+  const size_t sync = sync_bytes_of(qw->N);
+  if (ws_bytes < sync + linear_rest_bytes(M, qw, flags)) return fail(ARC_ERR_WORKSPACE, "workspace too small");
   if ((reinterpret_cast<uintptr_t>(ws) & 255u) != 0) return fail(ARC_ERR_ALIGN, "workspace not 256B aligned");
-  uint8_t* codes = static_cast<uint8_t*>(ws);
+  if (!aligned16(x) || !aligned16(y)) return fail(ARC_ERR_ALIGN, "x / y not 16B aligned");
+  uint8_t* rest = static_cast<uint8_t*>(ws) + sync;
+  const size_t rest_bytes = ws_bytes - sync;
+  // AUTO = unfused: the one-kernel fused path measured slower on B200 at every M (decode.cu)
+  const bool fused = flags == ARC_LINEAR_FUSED;
+  if (fused) {
+    s = check_device();
+    if (s != ARC_OK) return s;
+    FusedProblem p;
+    p.x = x;
+    p.ldx = ldx;
+    p.perm = prof->perm;
+    p.gs_x = prof->gs;
+    p.M = M;
+    p.N = qw->N;
+    p.K = qw->K;
+    p.S = qw->S;
+    p.Kp = qw->Kp;
+    p.layout = (int)qw->layout;
+    p.b_codes = qw->codes;
+    p.b_sf = qw->sf;
+    p.gs_w = qw->gs;
+    p.y = y;
+    p.ldy = ldy;
+    p.y_fp32 = y_dtype == ARC_FP32;
+    p.sync = reinterpret_cast<unsigned*>(ws);
+    p.ws = rest;
+    p.ws_bytes = rest_bytes;
+    const char* detail = nullptr;
+    cudaError_t e = launch_linear_fused(p, (cudaStream_t)stream, &detail);
+    return e == cudaSuccess ? ARC_OK : cuda_fail(e, "arc_linear (fused)", detail);
+  }
+  uint8_t* codes = rest;
   uint8_t* sf = codes + round_up(M * (qw->Kp / 2), 256);
   const size_t act = act_ws_bytes(M, qw->K, qw->S);
   s = arc_quantize_activation(x, M, ldx, prof, codes, sf, stream);
   if (s != ARC_OK) return s;
-  return arc_gemm(codes, sf, prof->gs, M, qw, y, y_dtype, ldy, static_cast<uint8_t*>(ws) + act, ws_bytes - act,
-                  stream);
+  return arc_gemm(codes, sf, prof->gs, M, qw, y, y_dtype, ldy, rest + act, rest_bytes - act, stream);
+}
+
+arc_status_t arc_linear(const void* x, int64_t M, int64_t ldx, const arc_profile_t* prof, const arc_qweight_t* qw,
+                        void* y, arc_dtype_t y_dtype, int64_t ldy, void* ws, size_t ws_bytes, void* stream) {
+  return arc_linear_ex(x, M, ldx, prof, qw, y, y_dtype, ldy, ws, ws_bytes, ARC_LINEAR_AUTO, stream);
+}
+
+arc_status_t arc_linear_ex_workspace_size(int64_t M, const arc_qweight_t* qw, int flags, size_t* bytes) {
+  arc_status_t s = check_qweight(qw);
+  if (s != ARC_OK) return s;
+  if (!bytes) return fail(ARC_ERR_NULL, "null bytes");
+  if (M < 0) return fail(ARC_ERR_SHAPE, "M < 0");
+  if (flags != ARC_LINEAR_AUTO && flags != ARC_LINEAR_FUSED && flags != ARC_LINEAR_UNFUSED)
+    return fail(ARC_ERR_SHAPE, "bad flags");
+  if (flags == ARC_LINEAR_FUSED && M > 128) return fail(ARC_ERR_SHAPE, "ARC_LINEAR_FUSED needs M <= 128");
+  *bytes = sync_bytes_of(qw->N) + (M == 0 ? 0 : linear_rest_bytes(M, qw, flags));
+  return ARC_OK;
+}
+
+arc_status_t arc_linear_fused_operand_offsets(int64_t M, const arc_qweight_t* qw, size_t* code_off,
+                                              size_t* sf_off) {
+  arc_status_t s = check_qweight(qw);
+  if (s != ARC_OK) return s;
+  if (!code_off || !sf_off) return fail(ARC_ERR_NULL, "null offset");
+  const FusedPlan fp = plan_fused(M, qw->N, qw->Kp);
+  if (!fp.ok) return fail(ARC_ERR_SHAPE, "fused path needs 1 <= M <= 128");
+  *code_off = sync_bytes_of(qw->N);
+  *sf_off = *code_off + fp.a_code_bytes;
+  return ARC_OK;
 }
 
 arc_status_t arc_linear_hostio_workspace_size(int64_t M, const arc_qweight_t* qw, arc_dtype_t y_dtype,

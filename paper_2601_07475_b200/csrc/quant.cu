@@ -21,6 +21,7 @@
 // stage 2 with base = d1.
 #include "arc_device.cuh"
 #include "arc_internal.h"
+#include "quant_dev.cuh"
 
 #include <cuda_fp16.h>
 
@@ -54,145 +55,12 @@ struct QuantArgs {
   int32_t debug;   // perf experiments only (env ARC_QUANT_DEBUG): 1 = skip compute, 2 = skip loads
 };
 
-// Two fp32 products z*k with one FMUL2 (mul.rn.f32x2: two IEEE RN multiplies).
-ARC_DEV float2 mul2(float a, float b, float k) {
-  unsigned long long x, y, r;
-  asm("mov.b64 %0, {%1, %2};" : "=l"(x) : "f"(a), "f"(b));
-  asm("mov.b64 %0, {%1, %1};" : "=l"(y) : "f"(k));
-  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(x), "l"(y));
-  float2 o;
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(o.x), "=f"(o.y) : "l"(r));
-  return o;
-}
-
-// One NVFP4 stage on 16 values (oracle C4) given the block's multiplier k:
-// t = z*k (mul.rn.f32x2), q = rne_e2m1(t) (cvt.rn.satfinite.e2m1x2), packed with
-// element 2i in the low nibble of byte i (bytes assembled by the PTX byte-vector mov).
-ARC_DEV uint2 encode16(const float (&z)[16], float k) {
-  float t[16];
-#pragma unroll
-  for (int i = 0; i < 16; i += 2) {
-    const float2 p = mul2(z[i], z[i + 1], k);
-    t[i] = p.x;
-    t[i + 1] = p.y;
-  }
-  uint32_t w0, w1;
-  asm("{\n\t.reg .b8 b<8>;\n\t"
-      "cvt.rn.satfinite.e2m1x2.f32 b0, %3, %2;\n\t"
-      "cvt.rn.satfinite.e2m1x2.f32 b1, %5, %4;\n\t"
-      "cvt.rn.satfinite.e2m1x2.f32 b2, %7, %6;\n\t"
-      "cvt.rn.satfinite.e2m1x2.f32 b3, %9, %8;\n\t"
-      "cvt.rn.satfinite.e2m1x2.f32 b4, %11, %10;\n\t"
-      "cvt.rn.satfinite.e2m1x2.f32 b5, %13, %12;\n\t"
-      "cvt.rn.satfinite.e2m1x2.f32 b6, %15, %14;\n\t"
-      "cvt.rn.satfinite.e2m1x2.f32 b7, %17, %16;\n\t"
-      "mov.b32 %0, {b0, b1, b2, b3};\n\t"
-      "mov.b32 %1, {b4, b5, b6, b7};\n\t}"
-      : "=r"(w0), "=r"(w1)
-      : "f"(t[0]), "f"(t[1]), "f"(t[2]), "f"(t[3]), "f"(t[4]), "f"(t[5]), "f"(t[6]), "f"(t[7]), "f"(t[8]),
-        "f"(t[9]), "f"(t[10]), "f"(t[11]), "f"(t[12]), "f"(t[13]), "f"(t[14]), "f"(t[15]));
-#if ARC_E2M1_SIGN_FIXUP
-  uint32_t s0 = 0, s1 = 0;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    s0 |= (__float_as_uint(t[i]) >> 31) << (4 * i + 3);
-    s1 |= (__float_as_uint(t[i + 8]) >> 31) << (4 * i + 3);
-  }
-  w0 = (w0 & 0x77777777u) | s0;
-  w1 = (w1 & 0x77777777u) | s1;
-#endif
-  return make_uint2(w0, w1);
-}
-
-ARC_DEV uint2 encode16(const float (&z)[16], float k, float (&t)[16]) {
-#pragma unroll
-  for (int i = 0; i < 16; i += 2) {
-    const float2 p = mul2(z[i], z[i + 1], k);
-    t[i] = p.x;
-    t[i + 1] = p.y;
-  }
-  uint32_t w0, w1;
-  asm("{\n\t.reg .b8 b<8>;\n\t"
-      "cvt.rn.satfinite.e2m1x2.f32 b0, %3, %2;\n\t"
-      "cvt.rn.satfinite.e2m1x2.f32 b1, %5, %4;\n\t"
-      "cvt.rn.satfinite.e2m1x2.f32 b2, %7, %6;\n\t"
-      "cvt.rn.satfinite.e2m1x2.f32 b3, %9, %8;\n\t"
-      "cvt.rn.satfinite.e2m1x2.f32 b4, %11, %10;\n\t"
-      "cvt.rn.satfinite.e2m1x2.f32 b5, %13, %12;\n\t"
-      "cvt.rn.satfinite.e2m1x2.f32 b6, %15, %14;\n\t"
-      "cvt.rn.satfinite.e2m1x2.f32 b7, %17, %16;\n\t"
-      "mov.b32 %0, {b0, b1, b2, b3};\n\t"
-      "mov.b32 %1, {b4, b5, b6, b7};\n\t}"
-      : "=r"(w0), "=r"(w1)
-      : "f"(t[0]), "f"(t[1]), "f"(t[2]), "f"(t[3]), "f"(t[4]), "f"(t[5]), "f"(t[6]), "f"(t[7]), "f"(t[8]),
-        "f"(t[9]), "f"(t[10]), "f"(t[11]), "f"(t[12]), "f"(t[13]), "f"(t[14]), "f"(t[15]));
-  return make_uint2(w0, w1);
-}
-
-// e = t - v(q) for 16 codes (exact: t and v(q) are multiples of ulp(t)).  The
-// E2M1 values come from the hardware decoder cvt.rn.f16x2.e2m1x2 (exact in f16).
-ARC_DEV void residual16(const float (&t)[16], uint2 packed, float (&e)[16]) {
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const uint32_t w = i < 4 ? packed.x : packed.y;
-    const uint32_t byte = (w >> (8 * (i & 3))) & 0xFFu;
-    uint32_t h2;
-    asm("{\n\t.reg .b8 b;\n\t.reg .b16 lo, hi;\n\t"
-        "cvt.u8.u32 b, %1;\n\t"
-        "cvt.rn.f16x2.e2m1x2 %0, b;\n\t}"
-        : "=r"(h2)
-        : "r"(byte));
-    const float2 v = __half22float2(*reinterpret_cast<const __half2*>(&h2));
-    e[2 * i] = __fsub_rn(t[2 * i], v.x);
-    e[2 * i + 1] = __fsub_rn(t[2 * i + 1], v.y);
-  }
-}
-
-// k2 = RN(d1 / d2) for scale codes c1, c2 (oracle STAGE's k with base d1).  For two
-// normal E4M3 values the quotient is 2^(e1-e2) * (8+m1)/(8+m2), so RN commutes with
-// the power of two: k2 = RN((8+m1)/(8+m2)) scaled by 2^(e1-e2) (exact exponent add).
-// Subnormal codes take the IEEE division.
-ARC_DEV float ratio_k(uint32_t c1, uint32_t c2, const float* rat) {
-  if (c2 == 0u) return 0.0f;
-  if (c1 < 8u || c2 < 8u) return __fdiv_rn(e4m3_value(c1), e4m3_value(c2));
-  const float r = rat[((c1 & 7u) << 3) | (c2 & 7u)];
-  return __uint_as_float(__float_as_uint(r) + ((int)(c1 >> 3) - (int)(c2 >> 3)) * (1 << 23));
-}
-
-// max |z| over 16 values as a shallow tree (exact; order-independent)
-ARC_DEV float absmax16(const float (&z)[16]) {
-  float m[8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) m[i] = fmaxf(fabsf(z[2 * i]), fabsf(z[2 * i + 1]));
-#pragma unroll
-  for (int i = 0; i < 4; ++i) m[i] = fmaxf(m[i], m[i + 4]);
-  return fmaxf(fmaxf(m[0], m[2]), fmaxf(m[1], m[3]));
-}
-
-// Branch-free smallest E4M3 code >= v (v >= 0), saturating at 0x7E (Q2); same
-// result as arc::e4m3_ceil (probe-tested).
-ARC_DEV uint32_t e4m3_ceil_nb(float v) {
-  const uint32_t b = __float_as_uint(v);
-  const uint32_t cn = min((b >> 20) - 960u + ((b & 0xFFFFFu) != 0u), 126u);  // normal grid, saturated
-  const uint32_t cs = (uint32_t)ceilf(__fmul_rn(v, 512.0f));                 // subnormal grid (v < 2^-6)
-  return v < 0.015625f ? cs : cn;
-}
-
 ARC_DEV void cp_async16(uint32_t dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
 }
 // arrive on `bar` once all of this thread's prior cp.async copies completed
 ARC_DEV void cp_async_arrive(uint64_t* bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-
-// physical block of logical block l (App.D P:591-597 interleaved, or the
-// logical concatenation of P:138): primaries l < K/16, residual j = K/16 + j
-ARC_DEV int phys_block(int l, int nb, int ns, int layout) {
-  if (layout != 0) return l;
-  if (l < ns) return 2 * l;
-  if (l < nb) return l + ns;
-  return 2 * (l - nb) + 1;
 }
 
 // gather 16 channels of one staged row (byte offsets into smem) as fp32 (exact)
