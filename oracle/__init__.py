@@ -79,6 +79,10 @@ def lib():
         L.or_gemm_exact.argtypes = [P, P, P, P, i64, i64, P, i64, P, P]
         L.or_mxfp8_block.restype = None
         L.or_mxfp8_block.argtypes = [P, P, P]
+        L.or_rmsnorm.restype = i32
+        L.or_rmsnorm.argtypes = [P, i64, i32, i64, P, f32, P, i64]
+        L.or_rmsnorm_scale.restype = f32
+        L.or_rmsnorm_scale.argtypes = [P, i32, f32]
         for n in ("or_e2m1_encode_n", "or_e4m3_ceil_n", "or_e4m3_rn_n"):
             getattr(L, n).restype = None
             getattr(L, n).argtypes = [P, i64, P]
@@ -225,6 +229,24 @@ def quantize_weight(w_bits, perm, S: int, gs: float, layout: int = INTERLEAVED):
     perm = np.ascontiguousarray(perm, np.int32)
     _check(lib().or_quantize_weight(_p(w), N, K, K, _p(perm), S, gs, layout, _p(codes), _p(sf)))
     return codes, sf
+
+
+# ----------------------------------------------------------------------------- RMSNorm
+def rmsnorm(x_bits, gamma_bits, eps: float) -> np.ndarray:
+    """RMSNorm stage of the fused kernel, reading Q23: bf16 bits [M][K] -> bf16 bits."""
+    x = as_bf16_bits(x_bits)
+    g = np.ascontiguousarray(as_bf16_bits(gamma_bits).reshape(-1))
+    M, K = x.shape
+    assert g.size == K
+    y = np.zeros((M, K), np.uint16)
+    _check(lib().or_rmsnorm(_p(x), M, K, K, _p(g), np.float32(eps), _p(y), K))
+    return y
+
+
+def rmsnorm_scale(x_row_bits, eps: float) -> float:
+    """r = 1/sqrt(ss/K + eps) of one row in the pinned order (Q23)."""
+    x = np.ascontiguousarray(as_bf16_bits(x_row_bits).reshape(-1))
+    return float(lib().or_rmsnorm_scale(_p(x), x.size, np.float32(eps)))
 
 
 # ----------------------------------------------------------------------------- calibration

@@ -30,9 +30,13 @@
  *   calibration   S:188 example; perm prefix = {j : max_j > tau}.
  *   gemm_exact    Eq.2 identity as an integer equality; brute
  *                 float64 dequantized product on small shapes.
+ *   rmsnorm       float64 formula within two bf16 roundings; exact invariance
+ *                 under power-of-two scaling of a row (eps = 0); constant rows
+ *                 -> +-1 exactly; torch's fp32 RMSNorm within one bf16 ulp.
  * Parity unpinned (decisions, not values the paper prints): Q2 ceil-rounded
  * E4M3 block scales, Q4 static activation tensor scale, Q6/Q7 residual domain
- * and op order, Q12 default layout.  See DESIGN.md.
+ * and op order, Q12 default layout, Q23 RMSNorm reduction order and roundings.
+ * See DESIGN.md.
  */
 #include <math.h>
 #include <stdint.h>
@@ -385,4 +389,62 @@ void or_e4m3_ceil_n(const float* v, int64_t n, uint8_t* c) {
 }
 void or_e4m3_rn_n(const float* v, int64_t n, uint8_t* c) {
     for (int64_t i = 0; i < n; ++i) c[i] = or_e4m3_rn(v[i]);
+}
+
+/* ------------------------------------------------------------------------- */
+/* RMSNorm -- the "RMSNorm" stage of the paper's Fused Quantization Kernel    */
+/* ("integrates Channel Reordering, RMSNorm, Primary Quantization, and        */
+/* Residual Quantization into a single operation"; Fig.8b), in   */
+/* the LLaMA form y = g * x / sqrt(mean(x^2) + eps), with the roundings of an */
+/* unfused bf16 implementation and a pinned reduction order (reading Q23):    */
+/*   s_b = x_{16b}^2 + ... + x_{16b+15}^2, sequential fmaf, original channel  */
+/*         order (block b = channels 16b..16b+15);                            */
+/*   ss  = pairwise tree over s_0 .. s_{K/16-1} zero-padded to a power of two */
+/*         (left + right at every level);                                     */
+/*   r   = 1 / sqrt(ss / K + eps)          (IEEE div, sqrt, div);             */
+/*   y_j = bf16( g_j * bf16( x_j * r ) )   (RNE; g_j * t is exact in fp32).   */
+/* ------------------------------------------------------------------------- */
+static uint16_t f32_to_bf16_rne(float f) {
+    uint32_t u;
+    memcpy(&u, &f, 4);
+    u += 0x7FFFu + ((u >> 16) & 1u);   /* finite inputs only (checked by the caller) */
+    return (uint16_t)(u >> 16);
+}
+
+float or_rmsnorm_scale(const uint16_t* x, int K, float eps) {
+    const int nb = K / 16;
+    int P = 1;
+    while (P < nb) P *= 2;
+    float* t = (float*)calloc((size_t)P, sizeof(float));
+    for (int b = 0; b < nb; ++b) {
+        float acc = 0.0f;
+        for (int i = 0; i < 16; ++i) {
+            const float v = bf16_to_f32(x[16 * b + i]);
+            acc = fmaf(v, v, acc);
+        }
+        t[b] = acc;
+    }
+    for (int w = P; w > 1; w /= 2)
+        for (int i = 0; i < w / 2; ++i) t[i] = t[2 * i] + t[2 * i + 1];
+    const float ss = t[0];
+    free(t);
+    const float mean = ss / (float)K;
+    return 1.0f / sqrtf(mean + eps);
+}
+
+int or_rmsnorm(const uint16_t* x, int64_t M, int K, int64_t ldx, const uint16_t* gamma, float eps, uint16_t* y,
+               int64_t ldy) {
+    if (K <= 0 || K % 16 || M < 0 || ldx < K || ldy < K || !(eps >= 0.0f)) return OR_ERR_SHAPE;
+    for (int64_t m = 0; m < M; ++m) {
+        const uint16_t* xr = x + m * ldx;
+        for (int j = 0; j < K; ++j)
+            if (!isfinite(bf16_to_f32(xr[j]))) return OR_ERR_NONFINITE;
+        const float r = or_rmsnorm_scale(xr, K, eps);
+        if (!isfinite(r)) return OR_ERR_NONFINITE;  /* all-zero row with eps = 0 */
+        for (int j = 0; j < K; ++j) {
+            const float tj = bf16_to_f32(f32_to_bf16_rne(bf16_to_f32(xr[j]) * r));
+            y[m * ldy + j] = f32_to_bf16_rne(bf16_to_f32(gamma[j]) * tj);
+        }
+    }
+    return OR_OK;
 }
