@@ -170,6 +170,31 @@ ARC_API arc_status_t arc_quantize_weight(const void* w, int64_t N, int64_t K, in
 ARC_API arc_status_t arc_quantize_activation(const void* x, int64_t M, int64_t ldx, const arc_profile_t* prof,
                                      uint8_t* codes, uint8_t* sf, void* stream);
 
+/* ---------------------------------------------------------------- RMSNorm (fused producer) */
+/* The RMSNorm stage of the paper's "Fused Quantization Kernel that integrates Channel
+ * Reordering, RMSNorm, Primary Quantization, and Residual Quantization into a single
+ * operation" (Fig.8b), in the LLaMA form with the roundings of a bf16 model
+ * and a pinned reduction order (reading Q23):
+ *   r   = 1 / sqrt(ss / K + eps), ss = pairwise tree over the K/16 sums of 16 consecutive
+ *         squares (each a sequential fp32 fma), zero-padded to a power of two;
+ *   y_j = bf16(gamma_j * bf16(x_j * r)).
+ * x: bf16 [M][ldx]; gamma: bf16 [K]; eps >= 0 (fp32); y: bf16 [M][ldy].  All-zero rows with
+ * eps = 0 and non-finite inputs give unspecified output. */
+ARC_API arc_status_t arc_rmsnorm(const void* x, int64_t M, int64_t K, int64_t ldx, const void* gamma, float eps,
+                                 void* y, int64_t ldy, void* stream);
+/* arc_quantize_activation of arc_rmsnorm(x) in ONE pass over x: each staged row is normalized
+ * in shared memory, then reordered and quantized (primary + residual).  Bit-identical to
+ * arc_rmsnorm followed by arc_quantize_activation; the normalized row never reaches HBM. */
+ARC_API arc_status_t arc_rmsnorm_quantize_activation(const void* x, int64_t M, int64_t ldx, const void* gamma,
+                                                     float eps, const arc_profile_t* prof, uint8_t* codes,
+                                                     uint8_t* sf, void* stream);
+/* arc_linear with the RMSNorm folded into its quantize pass (the attention / MLP input sites
+ * of a decoder layer, Fig.5): y = arc_gemm(arc_rmsnorm_quantize_activation(x)).
+ * Workspace: arc_linear_workspace_size(M, qw). */
+ARC_API arc_status_t arc_linear_rmsnorm(const void* x, int64_t M, int64_t ldx, const void* gamma, float eps,
+                                        const arc_profile_t* prof, const arc_qweight_t* qw, void* y,
+                                        arc_dtype_t y_dtype, int64_t ldy, void* ws, size_t ws_bytes, void* stream);
+
 /* ---------------------------------------------------------------- GEMM */
 /* y[M][N] (row stride ldy elements) = (1/(gs_x*gs_w)) * sum over the Kp physical
  * elements of A_aug * B_aug^T (Eq.2), FP32 accumulation in tensor

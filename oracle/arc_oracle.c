@@ -399,8 +399,10 @@ void or_e4m3_rn_n(const float* v, int64_t n, uint8_t* c) {
 /* unfused bf16 implementation and a pinned reduction order (reading Q23):    */
 /*   s_b = x_{16b}^2 + ... + x_{16b+15}^2, sequential fmaf, original channel  */
 /*         order (block b = channels 16b..16b+15);                            */
-/*   ss  = pairwise tree over s_0 .. s_{K/16-1} zero-padded to a power of two */
-/*         (left + right at every level);                                     */
+/*   the K/16 block sums, zero-padded to P = a power of two >= max(K/16, 32), */
+/*   are dealt round-robin to 32 partials (block b -> partial b mod 32); each */
+/*   partial is a pairwise tree over its P/32 blocks in increasing b, and ss  */
+/*   is a pairwise tree over the 32 partials (left + right at every level);   */
 /*   r   = 1 / sqrt(ss / K + eps)          (IEEE div, sqrt, div);             */
 /*   y_j = bf16( g_j * bf16( x_j * r ) )   (RNE; g_j * t is exact in fp32).   */
 /* ------------------------------------------------------------------------- */
@@ -411,23 +413,35 @@ static uint16_t f32_to_bf16_rne(float f) {
     return (uint16_t)(u >> 16);
 }
 
+static float pairwise_tree(float* t, int n) {  /* n a power of two; destroys t */
+    for (int w = n; w > 1; w /= 2)
+        for (int i = 0; i < w / 2; ++i) t[i] = t[2 * i] + t[2 * i + 1];
+    return t[0];
+}
+
 float or_rmsnorm_scale(const uint16_t* x, int K, float eps) {
     const int nb = K / 16;
-    int P = 1;
+    int P = 32;
     while (P < nb) P *= 2;
-    float* t = (float*)calloc((size_t)P, sizeof(float));
+    const int per = P / 32;
+    float* s = (float*)calloc((size_t)P, sizeof(float));
+    float* u = (float*)calloc((size_t)per, sizeof(float));
+    float part[32];
     for (int b = 0; b < nb; ++b) {
         float acc = 0.0f;
         for (int i = 0; i < 16; ++i) {
             const float v = bf16_to_f32(x[16 * b + i]);
             acc = fmaf(v, v, acc);
         }
-        t[b] = acc;
+        s[b] = acc;
     }
-    for (int w = P; w > 1; w /= 2)
-        for (int i = 0; i < w / 2; ++i) t[i] = t[2 * i] + t[2 * i + 1];
-    const float ss = t[0];
-    free(t);
+    for (int t = 0; t < 32; ++t) {
+        for (int j = 0; j < per; ++j) u[j] = s[t + 32 * j];
+        part[t] = pairwise_tree(u, per);
+    }
+    const float ss = pairwise_tree(part, 32);
+    free(s);
+    free(u);
     const float mean = ss / (float)K;
     return 1.0f / sqrtf(mean + eps);
 }

@@ -77,6 +77,10 @@ _sig("arc_linear_ex", [_P, _i64, _i64, ctypes.POINTER(ArcProfile), ctypes.POINTE
 _sig("arc_linear_ex_workspace_size", [_i64, ctypes.POINTER(ArcQWeight), ctypes.c_int, ctypes.POINTER(ctypes.c_size_t)])
 _sig("arc_linear_fused_operand_offsets", [_i64, ctypes.POINTER(ArcQWeight), ctypes.POINTER(ctypes.c_size_t),
                                           ctypes.POINTER(ctypes.c_size_t)])
+_sig("arc_rmsnorm", [_P, _i64, _i64, _i64, _P, _f32, _P, _i64, _P])
+_sig("arc_rmsnorm_quantize_activation", [_P, _i64, _i64, _P, _f32, ctypes.POINTER(ArcProfile), _P, _P, _P])
+_sig("arc_linear_rmsnorm", [_P, _i64, _i64, _P, _f32, ctypes.POINTER(ArcProfile), ctypes.POINTER(ArcQWeight), _P,
+                            ctypes.c_int, _i64, _P, ctypes.c_size_t, _P])
 _sig("arc_linear_hostio_workspace_size", [_i64, ctypes.POINTER(ArcQWeight), ctypes.c_int,
                                          ctypes.POINTER(ctypes.c_size_t)])
 _sig("arc_linear_hostio", [_P, _i64, ctypes.POINTER(ArcProfile), ctypes.POINTER(ArcQWeight), _P, ctypes.c_int, _P,
@@ -92,7 +96,8 @@ EXPORTED = [
     "arc_linear_workspace_size",
     "arc_calib_absmax", "arc_select_outliers", "arc_gather_order", "arc_tensor_scale", "arc_quantize_weight",
     "arc_quantize_activation", "arc_gemm", "arc_linear", "arc_linear_ex", "arc_linear_ex_workspace_size",
-    "arc_linear_fused_operand_offsets", "arc_linear_hostio_workspace_size", "arc_linear_hostio",
+    "arc_linear_fused_operand_offsets", "arc_linear_hostio_workspace_size", "arc_rmsnorm",
+    "arc_rmsnorm_quantize_activation", "arc_linear_rmsnorm", "arc_linear_hostio",
     "arc_probe_e2m1", "arc_probe_e2m1_bits", "arc_probe_e2m1_raw_bits", "arc_probe_e4m3_ceil", "arc_debug_fused_trace",
 ]
 
@@ -361,6 +366,50 @@ def linear(x: torch.Tensor, prof: Profile, qw: QWeight, out_dtype=torch.bfloat16
                               _dtype_code(out.dtype), out.stride(0), _ptr(buf), buf.numel(), LINEAR_MODES[mode],
                               _stream(stream)),
            "arc_linear_ex")
+    return out
+
+
+def rmsnorm(x: torch.Tensor, gamma: torch.Tensor, eps: float, out=None, stream=None) -> torch.Tensor:
+    """The RMSNorm stage of the fused quantization kernel, reading Q23: bf16 -> bf16."""
+    assert x.dtype == torch.bfloat16 and gamma.dtype == torch.bfloat16 and x.is_cuda
+    M, K = x.shape
+    if out is None:
+        out = torch.empty(M, K, dtype=torch.bfloat16, device=x.device)
+    _check(_lib.arc_rmsnorm(_ptr(x), M, K, x.stride(0), _ptr(gamma), float(eps), _ptr(out), out.stride(0),
+                            _stream(stream)), "arc_rmsnorm")
+    return out
+
+
+def rmsnorm_quantize_activation(x: torch.Tensor, gamma: torch.Tensor, eps: float, prof: Profile, codes=None,
+                                sf=None, stream=None):
+    """quantize_activation(rmsnorm(x)) in one pass over x (the paper's fused kernel)."""
+    assert x.dtype == torch.bfloat16 and x.is_cuda and x.shape[1] == prof.K
+    M = x.shape[0]
+    Kp, cb, sb = buffer_sizes(M, prof.K, prof.S)
+    if codes is None:
+        codes = torch.empty(M, Kp // 2, dtype=torch.uint8, device=x.device)
+    if sf is None:
+        sf = torch.empty(sb, dtype=torch.uint8, device=x.device)
+    _check(_lib.arc_rmsnorm_quantize_activation(_ptr(x), M, x.stride(0), _ptr(gamma), float(eps),
+                                                ctypes.byref(prof.c()), _ptr(codes), _ptr(sf), _stream(stream)),
+           "arc_rmsnorm_quantize_activation")
+    return codes, sf
+
+
+def linear_rmsnorm(x: torch.Tensor, gamma: torch.Tensor, eps: float, prof: Profile, qw: QWeight,
+                   out_dtype=torch.bfloat16, out=None, ws: Workspace = None, stream=None):
+    """ARC linear of rmsnorm(x): the normalizing quantize pass + the augmented NVFP4 GEMM."""
+    assert x.dtype == torch.bfloat16 and x.is_cuda
+    M = x.shape[0]
+    if out is None:
+        out = _alloc_out(M, qw.N, out_dtype, x.device)
+    need = linear_workspace_size(M, qw)
+    if ws is None:
+        ws = _default_ws.setdefault(x.device, Workspace(x.device))
+    buf = ws.get(need)
+    _check(_lib.arc_linear_rmsnorm(_ptr(x), M, x.stride(0), _ptr(gamma), float(eps), ctypes.byref(prof.c()),
+                                   ctypes.byref(qw.c()), _ptr(out), _dtype_code(out.dtype), out.stride(0), _ptr(buf),
+                                   buf.numel(), _stream(stream)), "arc_linear_rmsnorm")
     return out
 
 

@@ -306,6 +306,37 @@ arc_status_t arc_quantize_activation(const void* x, int64_t M, int64_t ldx, cons
   return e == cudaSuccess ? ARC_OK : cuda_fail(e, "arc_quantize_activation");
 }
 
+arc_status_t arc_rmsnorm(const void* x, int64_t M, int64_t K, int64_t ldx, const void* gamma, float eps, void* y,
+                         int64_t ldy, void* stream) {
+  if (K <= 0 || K % 16 || K > 32768 || M < 0 || ldx < K || ldx % 8 || ldy < K || ldy % 8)
+    return fail(ARC_ERR_SHAPE, "bad M/K/ldx/ldy");
+  if (!(eps >= 0.0f) || eps > 3.4e38f) return fail(ARC_ERR_SHAPE, "eps must be finite and >= 0");
+  if (M == 0) return ARC_OK;
+  if (!x || !gamma || !y) return fail(ARC_ERR_NULL, "null x / gamma / y");
+  if (!aligned16(x) || !aligned16(gamma) || !aligned16(y)) return fail(ARC_ERR_ALIGN, "buffer not 16B aligned");
+  arc_status_t s = check_device();
+  if (s != ARC_OK) return s;
+  cudaError_t e = launch_rmsnorm(x, M, (int)K, ldx, gamma, eps, y, ldy, (cudaStream_t)stream);
+  return e == cudaSuccess ? ARC_OK : cuda_fail(e, "arc_rmsnorm");
+}
+
+arc_status_t arc_rmsnorm_quantize_activation(const void* x, int64_t M, int64_t ldx, const void* gamma, float eps,
+                                             const arc_profile_t* prof, uint8_t* codes, uint8_t* sf, void* stream) {
+  arc_status_t s = check_profile(prof);
+  if (s != ARC_OK) return s;
+  if (M < 0 || ldx < prof->K || ldx % 8) return fail(ARC_ERR_SHAPE, "bad M/ldx");
+  if (!(eps >= 0.0f) || eps > 3.4e38f) return fail(ARC_ERR_SHAPE, "eps must be finite and >= 0");
+  if (M == 0) return ARC_OK;
+  if (!x || !gamma || !codes || !sf) return fail(ARC_ERR_NULL, "null x / gamma / codes / sf");
+  if (!aligned16(x) || !aligned16(gamma) || !aligned16(codes) || !aligned16(sf))
+    return fail(ARC_ERR_ALIGN, "buffer not 16B aligned");
+  s = check_device();
+  if (s != ARC_OK) return s;
+  cudaError_t e = launch_quant(x, M, (int)prof->K, ldx, prof->perm, prof->S, prof->gs, (int)prof->layout, 0, codes,
+                               sf, (cudaStream_t)stream, gamma, eps);
+  return e == cudaSuccess ? ARC_OK : cuda_fail(e, "arc_rmsnorm_quantize_activation");
+}
+
 arc_status_t arc_gemm(const uint8_t* a_codes, const uint8_t* a_sf, const float* gs_x, int64_t M,
                       const arc_qweight_t* qw, void* y, arc_dtype_t y_dtype, int64_t ldy, void* ws, size_t ws_bytes,
                       void* stream) {
@@ -404,6 +435,29 @@ arc_status_t arc_linear_ex(const void* x, int64_t M, int64_t ldx, const arc_prof
   s = arc_quantize_activation(x, M, ldx, prof, codes, sf, stream);
   if (s != ARC_OK) return s;
   return arc_gemm(codes, sf, prof->gs, M, qw, y, y_dtype, ldy, rest + act, rest_bytes - act, stream);
+}
+
+arc_status_t arc_linear_rmsnorm(const void* x, int64_t M, int64_t ldx, const void* gamma, float eps,
+                                const arc_profile_t* prof, const arc_qweight_t* qw, void* y, arc_dtype_t y_dtype,
+                                int64_t ldy, void* ws, size_t ws_bytes, void* stream) {
+  arc_status_t s = check_profile(prof);
+  if (s != ARC_OK) return s;
+  s = check_qweight(qw);
+  if (s != ARC_OK) return s;
+  if (qw->K != prof->K || qw->S != prof->S || qw->layout != prof->layout)
+    return fail(ARC_ERR_SHAPE, "profile and qweight disagree on K / S / layout");
+  if (M < 0 || M > (1 << 30)) return fail(ARC_ERR_SHAPE, "bad M");
+  if (M == 0) return ARC_OK;
+  if (!ws) return fail(ARC_ERR_NULL, "null workspace");
+  const size_t sync = sync_bytes_of(qw->N);
+  if (ws_bytes < sync + linear_rest_bytes(M, qw, ARC_LINEAR_UNFUSED)) return fail(ARC_ERR_WORKSPACE, "workspace too small");
+  if ((reinterpret_cast<uintptr_t>(ws) & 255u) != 0) return fail(ARC_ERR_ALIGN, "workspace not 256B aligned");
+  uint8_t* codes = static_cast<uint8_t*>(ws) + sync;
+  uint8_t* sf = codes + round_up(M * (qw->Kp / 2), 256);
+  const size_t act = act_ws_bytes(M, qw->K, qw->S);
+  s = arc_rmsnorm_quantize_activation(x, M, ldx, gamma, eps, prof, codes, sf, stream);
+  if (s != ARC_OK) return s;
+  return arc_gemm(codes, sf, prof->gs, M, qw, y, y_dtype, ldy, codes + act, ws_bytes - sync - act, stream);
 }
 
 arc_status_t arc_linear(const void* x, int64_t M, int64_t ldx, const arc_profile_t* prof, const arc_qweight_t* qw,

@@ -52,7 +52,11 @@ struct QuantArgs {
   int32_t npw;     // primary warps
   int32_t nrw;     // residual warps
   int32_t bulk;    // producer uses one cp.async.bulk per row (else 16-byte cp.async per lane)
-  int32_t debug;   // perf experiments only (env ARC_QUANT_DEBUG): 1 = skip compute, 2 = skip loads
+  int32_t debug;   // perf experiments only (env ARC_QUANT_DEBUG): 1 = skip compute, 2 = skip loads,
+                   // 3 = quantizing warps do not wait for the norm warps, 4 = norm warps skip the RMS
+  const uint16_t* gamma;  // RMSNorm weight bf16[K] (norm mode)
+  float eps;
+  int32_t norm;    // 1: RMSNorm the staged rows in place before quantizing (R norm warps)
 };
 
 ARC_DEV void cp_async16(uint32_t dst, const void* src) {
@@ -67,6 +71,26 @@ ARC_DEV void cp_async_arrive(uint64_t* bar) {
 ARC_DEV void gather16(const uint8_t* base, const uint32_t (&off)[16], float (&z)[16]) {
 #pragma unroll
   for (int q = 0; q < 16; ++q) z[q] = bf16_bits_to_f32(*reinterpret_cast<const uint16_t*>(base + off[q]));
+}
+
+// RMSNorm of the 16 gathered channels of logical block l (reading Q23): z = bf16(g * bf16(z * r)).
+// gperm holds gamma in reordered order (gperm[16 l + q] = gamma[perm[16 l + q]], staged once per
+// CTA), so a lane's 16 gains are two conflict-free 16-byte loads at gperm + 32 l.  Pairs:
+// mul.rn.f32x2, one cvt.rn.bf16x2.f32, one bf16x2 multiply (the product of two bf16 is exact in
+// fp32, so its single rounding equals the oracle's).
+ARC_DEV void norm16(float (&z)[16], const uint8_t* gblk, float r) {
+  const uint4 g0 = *reinterpret_cast<const uint4*>(gblk);
+  const uint4 g1 = *reinterpret_cast<const uint4*>(gblk + 16);
+  const uint32_t gw[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+#pragma unroll
+  for (int i = 0; i < 16; i += 2) {
+    const float2 p = mul2(z[i], z[i + 1], r);
+    const __nv_bfloat162 t = __floats2bfloat162_rn(p.x, p.y);
+    const __nv_bfloat162 y = __hmul2(*reinterpret_cast<const __nv_bfloat162*>(&gw[i >> 1]), t);
+    const uint32_t yw = *reinterpret_cast<const uint32_t*>(&y);
+    z[i] = __uint_as_float(yw << 16);
+    z[i + 1] = __uint_as_float(yw & 0xFFFF0000u);
+  }
 }
 
 // Rows of a tile.  Tile t of the 128-row group g holds rows base + 32 i, i < R, with
@@ -104,7 +128,7 @@ ARC_DEV int tile_rows(int base, int64_t rows) {  // valid rows base + 32 i < row
 // Rows sit at a fixed ROWP stride (ROWB + 16: rows of one tile fall in different
 // banks for the residual warp's cross-row gathers) and the tile loop is unrolled
 // over the ring so the gathers are `LDS [off + const]`.
-template <int IPT, int R, int ROWB, int ST>
+template <int IPT, int R, int ROWB, int ST, bool NORM>
 __global__ void __launch_bounds__(1024) arc_quant_kernel(QuantArgs p) {
   extern __shared__ __align__(16) uint8_t smem[];
   constexpr int ROWP = ROWB + 16;
@@ -119,6 +143,10 @@ __global__ void __launch_bounds__(1024) arc_quant_kernel(QuantArgs p) {
   float* rat = c6tab + 128;    // RN((8+m1)/(8+m2)): mantissa ratio of two normal E4M3 scales
   uint64_t* full = reinterpret_cast<uint64_t*>(rat + 64);
   uint64_t* empty = full + ST;
+  uint64_t* normed = empty + ST;  // norm mode: the RMS scales of slot s's rows are ready
+  float* rscale = reinterpret_cast<float*>(normed + ST);  // [ST][R] 1/rms of each staged row
+  uint8_t* gam = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(rscale + ST * R) + 15) & ~uintptr_t(15));
+  // gam: gamma in reordered channel order, bf16[K], staged once per CTA (norm mode)
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
@@ -135,6 +163,7 @@ __global__ void __launch_bounds__(1024) arc_quant_kernel(QuantArgs p) {
     for (int s = 0; s < ST; ++s) {
       mbar_init(&full[s], p.bulk ? 1 : 32);
       mbar_init(&empty[s], npw + nrw);
+      mbar_init(&normed[s], R);
     }
     fence_mbar_init();
   }
@@ -145,6 +174,10 @@ __global__ void __launch_bounds__(1024) arc_quant_kernel(QuantArgs p) {
     c6tab[c] = __fdiv_rn(e4m3_value((uint32_t)c), 6.0f);
     if (c < 64) rat[c] = __fdiv_rn((float)(8 + (c >> 3)), (float)(8 + (c & 7)));
   }
+  if (NORM)
+    for (int c = tid; c < K; c += blockDim.x)
+      reinterpret_cast<uint16_t*>(gam)[c] = __ldg(reinterpret_cast<const unsigned short*>(p.gamma) + __ldg(p.perm + c));
+
   __syncthreads();
 
   if (warp == npw + nrw) {
@@ -210,8 +243,34 @@ __global__ void __launch_bounds__(1024) arc_quant_kernel(QuantArgs p) {
     return;
   }
 
+  if (NORM && warp > npw + nrw) {
+    // ---------------------------------------------------------------- norm warps (RMSNorm)
+    // norm warp r owns row r of every tile: its RMS scale 1/sqrt(mean(x^2)+eps) in the pinned
+    // order (Q23), published in smem; the quantizing warps apply y = bf16(g * bf16(x * r)) to
+    // the 16 channels they gather (norm16)
+    const int r = warp - (npw + nrw + 1);
+    for (int j0 = 0; j0 < my_tiles; j0 += ST) {
+#pragma unroll
+      for (int s = 0; s < ST; ++s) {
+        const int j = j0 + s;
+        if (j < my_tiles) {
+          mbar_wait(&full[s], (j / ST) & 1);
+          const int base = tile_base<R>((int)blockIdx.x + j * (int)gridDim.x);
+          if (r < tile_rows<R>(base, p.rows) && p.debug != 1 && p.debug != 4) {
+            const float sc = rms_scale_any(smem + s * SLOT + r * ROWP, K, p.eps, lane);
+            if (lane == 0) rscale[s * R + r] = sc;
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&normed[s]);
+        }
+      }
+    }
+    return;
+  }
+
   const int nb = K >> 4, ns = p.S >> 4;
   const int ka16 = nb + ns, NB = p.Kp >> 4;
+  uint64_t* ready = (NORM && p.debug != 3) ? normed : full;  // what the quantizing warps wait for
   const float c6g = __fdiv_rn(gs, 6.0f);
 
   if (warp < npw) {
@@ -241,7 +300,7 @@ __global__ void __launch_bounds__(1024) arc_quant_kernel(QuantArgs p) {
       for (int s = 0; s < ST; ++s) {
         const int j = j0 + s;
         if (j < my_tiles) {
-          mbar_wait(&full[s], (j / ST) & 1);
+          mbar_wait(&ready[s], (j / ST) & 1);
           if (p.debug != 1) {
             const int base = tile_base<R>((int)blockIdx.x + j * (int)gridDim.x);
             const int nr = tile_rows<R>(base, p.rows);
@@ -260,6 +319,7 @@ __global__ void __launch_bounds__(1024) arc_quant_kernel(QuantArgs p) {
                     if (kind[i] == 1) {
                       float z[16];
                       gather16(smem + s * SLOT + r * ROWP, off[i], z);
+                      if (NORM) norm16(z, gam + 32 * (tid + i * npw * 32), rscale[s * R + r]);
                       // stage 1 (Eq.1 with the NVFP4 two-level scale, Q7 op order)
                       sfb = e4m3_ceil_nb(__fmul_rn(absmax16(z), c6g));
                       packed = encode16(z, k1tab[sfb]);
@@ -303,7 +363,7 @@ __global__ void __launch_bounds__(1024) arc_quant_kernel(QuantArgs p) {
     for (int s = 0; s < ST; ++s) {
       const int j = j0 + s;
       if (j < my_tiles) {
-        mbar_wait(&full[s], (j / ST) & 1);
+        mbar_wait(&ready[s], (j / ST) & 1);
         if (p.debug != 1) {
           const int base = tile_base<R>((int)blockIdx.x + j * (int)gridDim.x);
           const int nr = tile_rows<R>(base, p.rows);
@@ -332,6 +392,7 @@ __global__ void __launch_bounds__(1024) arc_quant_kernel(QuantArgs p) {
               const int m = base + 32 * r;
               float z[16];
               gather16(smem + s * SLOT, off, z);
+              if (NORM) norm16(z, gam + 32 * jb, rscale[s * R + r]);
               const uint32_t sf1 = e4m3_ceil_nb(__fmul_rn(absmax16(z), c6g));
               float t[16];
               uint2 packed = encode16(z, k1tab[sf1], t);
@@ -408,11 +469,12 @@ __global__ void arc_finalize_scale_kernel(float* gs) {
 // Per-(kernel, threads, smem) launch configuration, computed once per process:
 // the attribute calls and the occupancy query cost more host time than the
 // kernel itself at decode sizes.
-template <int IPT, int R, int ROWB, int ST>
+template <int IPT, int R, int ROWB, int ST, bool NORM>
 static cudaError_t launch_quant_cfg(QuantArgs a, int threads, cudaStream_t stream) {
   a.rows_per_tile = R;
   a.stages = ST;
-  const size_t smem = (size_t)ST * R * (ROWB + 16) + (size_t)ST * (a.Kp / 64) * (R * 4) + (128 + 128 + 64) * 4 + 2 * ST * 8;
+  const size_t smem = (size_t)ST * R * (ROWB + 16) + (size_t)ST * (a.Kp / 64) * (R * 4) + (128 + 128 + 64) * 4 + 3 * ST * 8 +
+                      (size_t)ST * R * 4 + (NORM ? 16 + (size_t)a.K * 2 : 0);
   struct Cfg { int dev, threads; size_t smem; int occ; };
   static thread_local Cfg cache[8];
   static thread_local int ncache = 0;
@@ -422,13 +484,13 @@ static cudaError_t launch_quant_cfg(QuantArgs a, int threads, cudaStream_t strea
   for (int i = 0; i < ncache && i < 8; ++i)
     if (cache[i].dev == dev && cache[i].threads == threads && cache[i].smem == smem) occ = cache[i].occ;
   if (occ == 0) {
-    cudaError_t e = cudaFuncSetAttribute(arc_quant_kernel<IPT, R, ROWB, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(arc_quant_kernel<IPT, R, ROWB, ST, NORM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          227 * 1024);
     if (e != cudaSuccess) return e;
     // the full shared-memory carveout so several CTAs' rings fit per SM
-    e = cudaFuncSetAttribute(arc_quant_kernel<IPT, R, ROWB, ST>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    e = cudaFuncSetAttribute(arc_quant_kernel<IPT, R, ROWB, ST, NORM>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e != cudaSuccess) return e;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, arc_quant_kernel<IPT, R, ROWB, ST>, threads, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, arc_quant_kernel<IPT, R, ROWB, ST, NORM>, threads, smem);
     if (e != cudaSuccess) return e;
     if (occ < 1) occ = 1;
     cache[ncache % 8] = Cfg{dev, threads, smem, occ};
@@ -447,14 +509,18 @@ static cudaError_t launch_quant_cfg(QuantArgs a, int threads, cudaStream_t strea
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, arc_quant_kernel<IPT, R, ROWB, ST>, a);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, arc_quant_kernel<IPT, R, ROWB, ST, NORM>, a);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
 cudaError_t launch_quant(const void* x, int64_t rows, int K, int64_t ld, const int32_t* perm, int S, const float* gs,
-                         int layout, int weight_mode, uint8_t* codes, uint8_t* sf, cudaStream_t stream) {
+                         int layout, int weight_mode, uint8_t* codes, uint8_t* sf, cudaStream_t stream,
+                         const void* gamma, float eps) {
   QuantArgs a;
+  a.gamma = static_cast<const uint16_t*>(gamma);
+  a.eps = eps;
+  a.norm = gamma != nullptr ? 1 : 0;
   a.x = static_cast<const uint16_t*>(x);
   a.rows = rows;
   a.K = K;
@@ -474,26 +540,74 @@ cudaError_t launch_quant(const void* x, int64_t rows, int K, int64_t ld, const i
   a.bulk = bulk_env >= 0 ? bulk_env : 1;
   const int NB = a.Kp / 16, ns = S / 16;
   const int nprim = NB - ns;                 // primary + pad blocks per row
-  const int ipt = (nprim + 28 * 32 - 1) / (28 * 32);  // <= 28 primary warps
-  a.npw = (nprim + ipt * 32 - 1) / (ipt * 32);
   const int64_t rowb = (int64_t)K * 2;
-  a.nrw = ns == 0 ? 0 : (int)imin64(2, (ns + 31) / 32);  // ipt == 2 configuration: R = 1
-  const int threads = (a.npw + a.nrw + 1) * 32;
-  if (threads > 1024) return cudaErrorInvalidValue;
   // ring configurations (rows per tile R, row slot bytes, stages), tuned on B200:
   // K <= 4096: R=4 (the residual warp gets a full 32 items per tile), 3 x 32 KB slots
   // -> 2 CTAs/SM; K <= 8192: R=2, 3 x 32 KB; K <= 16384: R=2, 3 x 64 KB (1 CTA/SM).
+  // Norm mode adds R norm warps (one per row of a tile).
+  int ipt = (nprim + 28 * 32 - 1) / (28 * 32);  // <= 28 primary warps
   if (ipt == 1) {
     const int R = rowb <= 8192 ? 4 : 2;
+    a.npw = (nprim + 31) / 32;
     a.nrw = ns == 0 ? 0 : (int)imin64(2, (R * ns + 31) / 32);
-    const int th = (a.npw + a.nrw + 1) * 32;
-    if (th > 1024) return cudaErrorInvalidValue;
-    if (rowb <= 8192) return launch_quant_cfg<1, 4, 8192, 3>(a, th, stream);
-    if (rowb <= 16384) return launch_quant_cfg<1, 2, 16384, 3>(a, th, stream);
-    return launch_quant_cfg<1, 2, 32768, 3>(a, th, stream);
+    const int th = (a.npw + a.nrw + 1 + (a.norm ? R : 0)) * 32;
+    if (th <= 1024) {
+      if (a.norm) {  // gamma takes 2K bytes of shared memory: 2-stage rings above K = 8192
+        if (rowb <= 8192) return launch_quant_cfg<1, 4, 8192, 3, true>(a, th, stream);
+        if (rowb <= 16384) return launch_quant_cfg<1, 2, 16384, 3, true>(a, th, stream);
+        return launch_quant_cfg<1, 2, 32768, 2, true>(a, th, stream);
+      }
+      if (rowb <= 8192) return launch_quant_cfg<1, 4, 8192, 3, false>(a, th, stream);
+      if (rowb <= 16384) return launch_quant_cfg<1, 2, 16384, 3, false>(a, th, stream);
+      return launch_quant_cfg<1, 2, 32768, 3, false>(a, th, stream);
+    }
+    ipt = 2;  // norm mode with 28 primary warps: two blocks per primary lane instead
   }
-  if (ipt == 2) return launch_quant_cfg<2, 1, 65536, 3>(a, threads, stream);
+  if (ipt == 2) {
+    a.npw = (nprim + 63) / 64;
+    a.nrw = ns == 0 ? 0 : (int)imin64(2, (ns + 31) / 32);  // R = 1
+    const int threads = (a.npw + a.nrw + 1 + (a.norm ? 1 : 0)) * 32;
+    if (threads > 1024) return cudaErrorInvalidValue;
+    if (a.norm) return launch_quant_cfg<2, 1, 65536, 2, true>(a, threads, stream);
+    return launch_quant_cfg<2, 1, 65536, 3, false>(a, threads, stream);
+  }
   return cudaErrorInvalidValue;  // K + S > 32768 is rejected in api.cu
+}
+
+// Standalone RMSNorm (the unfused comparison and the calibration input of a normed site):
+// one warp per row, the same device functions (and so the same bits) as the fused kernel.
+__global__ void __launch_bounds__(128) arc_rmsnorm_kernel(const uint16_t* x, int64_t rows, int K, int64_t ldx,
+                                                          const uint16_t* gamma, float eps, uint16_t* y, int64_t ldy) {
+  pdl_launch_dependents();
+  pdl_wait();
+  const int lane = threadIdx.x & 31;
+  for (int64_t m = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5); m < rows; m += (int64_t)gridDim.x * 4) {
+    const uint8_t* row = reinterpret_cast<const uint8_t*>(x + m * ldx);
+    const float sc = rms_scale_any(row, K, eps, lane);
+    for (int c0 = lane * 8; c0 < K; c0 += 256) {
+      const uint4 g = __ldg(reinterpret_cast<const uint4*>(gamma + c0));
+      *reinterpret_cast<uint4*>(y + m * ldy + c0) = rms_apply8(*reinterpret_cast<const uint4*>(row + c0 * 2), g, sc);
+    }
+  }
+}
+
+cudaError_t launch_rmsnorm(const void* x, int64_t rows, int K, int64_t ldx, const void* gamma, float eps, void* y,
+                           int64_t ldy, cudaStream_t s) {
+  const int64_t grid = imax64(1, imin64((rows + 3) / 4, (int64_t)num_sms() * 16));
+  cudaLaunchConfig_t cfg;
+  memset(&cfg, 0, sizeof(cfg));
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(128);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, arc_rmsnorm_kernel, static_cast<const uint16_t*>(x), rows, K, ldx,
+                                     static_cast<const uint16_t*>(gamma), eps, static_cast<uint16_t*>(y), ldy);
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
 }
 
 cudaError_t launch_calib_absmax(const void* x, int64_t rows, int K, int64_t ld, float* chan_max, cudaStream_t s) {

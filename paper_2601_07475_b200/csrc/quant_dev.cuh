@@ -6,6 +6,7 @@
 #pragma once
 #include "arc_device.cuh"
 
+#include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
 namespace arc {
@@ -141,6 +142,80 @@ ARC_DEV int phys_block(int l, int nb, int ns, int layout) {
   if (l < ns) return 2 * l;
   if (l < nb) return l + ns;
   return 2 * (l - nb) + 1;
+}
+
+// ------------------------------------------------------------------ RMSNorm (reading Q23)
+// 1/sqrt(ss/K + eps) of one bf16 row (generic pointer: shared or global), computed by one warp
+// in the oracle's pinned order (reading Q23): per 16-channel block a sequential fma over its 16
+// squares; block b goes to lane b mod 32 (so a warp's loads at each step are 1 KB contiguous:
+// no shared-memory bank conflicts), each lane reduces its BPL blocks as a pairwise tree in
+// increasing b, and the 32 lane partials as a pairwise tree over the lanes (xor shuffles).
+template <int BPL>
+ARC_DEV float rms_scale_warp(const uint8_t* row, int K, float eps, int lane) {
+  const int nb = K >> 4;
+  // local pairwise tree over this lane's BPL leaves as a binary counter: lv[l] holds the
+  // pending left subtree of size 2^l; indices are compile-time (unrolled), so registers only
+  float lv[7];
+  float c = 0.0f;
+#pragma unroll
+  for (int j = 0; j < BPL; ++j) {
+    const int b = j * 32 + lane;
+    float acc = 0.0f;
+    if (b < nb) {
+      const uint4 w0 = *reinterpret_cast<const uint4*>(row + b * 32);
+      const uint4 w1 = *reinterpret_cast<const uint4*>(row + b * 32 + 16);
+      const uint32_t w[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float lo = __uint_as_float(w[i] << 16), hi = __uint_as_float(w[i] & 0xFFFF0000u);
+        acc = __fmaf_rn(lo, lo, acc);
+        acc = __fmaf_rn(hi, hi, acc);
+      }
+    }
+    c = acc;
+#pragma unroll
+    for (int l = 0; (1 << l) < BPL; ++l) {
+      if (j & (1 << l)) {
+        c = __fadd_rn(lv[l], c);  // left + right
+      } else {
+        lv[l] = c;
+        break;
+      }
+    }
+  }
+  float ss = c;  // the root of the lane's subtree (BPL a power of two)
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) ss = __fadd_rn(ss, __shfl_xor_sync(0xffffffffu, ss, o));
+  const float mean = __fdiv_rn(ss, (float)K);
+  return __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(mean, eps)));
+}
+
+ARC_DEV float rms_scale_any(const uint8_t* row, int K, float eps, int lane) {
+  const int nb = K >> 4;
+  if (nb <= 32) return rms_scale_warp<1>(row, K, eps, lane);
+  if (nb <= 64) return rms_scale_warp<2>(row, K, eps, lane);
+  if (nb <= 128) return rms_scale_warp<4>(row, K, eps, lane);
+  if (nb <= 256) return rms_scale_warp<8>(row, K, eps, lane);
+  if (nb <= 512) return rms_scale_warp<16>(row, K, eps, lane);
+  if (nb <= 1024) return rms_scale_warp<32>(row, K, eps, lane);
+  return rms_scale_warp<64>(row, K, eps, lane);
+}
+
+// y_j = bf16(g_j * bf16(x_j * r)) for 8 channels (one 16-byte word of x and of gamma)
+ARC_DEV uint4 rms_apply8(uint4 x, uint4 g, float r) {
+  const uint32_t xw[4] = {x.x, x.y, x.z, x.w}, gw[4] = {g.x, g.y, g.z, g.w};
+  uint32_t o[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const __nv_bfloat162 t = __floats2bfloat162_rn(__fmul_rn(__uint_as_float(xw[i] << 16), r),
+                                                   __fmul_rn(__uint_as_float(xw[i] & 0xFFFF0000u), r));
+    const uint32_t tw = *reinterpret_cast<const uint32_t*>(&t);
+    const __nv_bfloat162 y = __floats2bfloat162_rn(
+        __fmul_rn(__uint_as_float(gw[i] << 16), __uint_as_float(tw << 16)),
+        __fmul_rn(__uint_as_float(gw[i] & 0xFFFF0000u), __uint_as_float(tw & 0xFFFF0000u)));
+    o[i] = *reinterpret_cast<const uint32_t*>(&y);
+  }
+  return make_uint4(o[0], o[1], o[2], o[3]);
 }
 
 }  // namespace arc

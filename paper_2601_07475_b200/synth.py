@@ -9,6 +9,7 @@ recipe:
   structure(K, S_inj, seed): idx = S_inj distinct channels, gain ~ logU[32, 128]
   activation(M, K, st, seed): X = N(0,1) * exp(0.5 N(0,1))[row] ; X[:, idx] *= gain
   weight(N, K, seed): N(0,1) / sqrt(K)
+  rmsnorm_weight(K, seed): exp(0.3 N(0,1))  (positive per-channel RMSNorm gains around 1)
 """
 from __future__ import annotations
 
@@ -40,6 +41,12 @@ def weight(N: int, K: int, seed: int, device="cpu") -> torch.Tensor:
     g = torch.Generator(device=device).manual_seed(int(seed) + 7919)
     w = torch.randn(N, K, generator=g, device=device, dtype=torch.float32) / math.sqrt(K)
     return w.to(torch.bfloat16)
+
+
+def rmsnorm_weight(K: int, seed: int, device="cpu") -> torch.Tensor:
+    """bf16 [K] RMSNorm gain vector (the gamma of the attention / MLP input norms)."""
+    g = torch.Generator(device=device).manual_seed(int(seed) + 104729)
+    return torch.exp(0.3 * torch.randn(K, generator=g, device=device, dtype=torch.float32)).to(torch.bfloat16)
 
 
 def random_perm(K: int, seed: int) -> np.ndarray:

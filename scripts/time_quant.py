@@ -13,24 +13,31 @@ ap.add_argument("--K", type=int, default=4096)
 ap.add_argument("--M", type=int, default=8192)
 ap.add_argument("--S", type=int, default=128)
 ap.add_argument("--iters", type=int, default=20)
+ap.add_argument("--norm", action="store_true", help="time arc_rmsnorm_quantize_activation (fused RMSNorm)")
 args = ap.parse_args()
 K, M, S = args.K, args.M, args.S
 st = synth.Structure(K, S, seed=0)
 prof = A.calibrate([synth.activation(1024, K, st, seed=1000, device="cuda")], s_override=S)
 nrot = max(2, int(4 * 126e6 // (M * K * 2)) + 1)
 xs = [synth.activation(M, K, st, seed=i, device="cuda") for i in range(nrot)]
-codes, sf = A.quantize_activation(xs[0], prof)
+gamma = synth.rmsnorm_weight(K, seed=0, device="cuda")
+if args.norm:
+    def quant(x, prof, codes=None, sf=None):
+        return A.rmsnorm_quantize_activation(x, gamma, 1e-5, prof, codes, sf)
+else:
+    quant = A.quantize_activation
+codes, sf = quant(xs[0], prof)
 for i in range(3):
-    A.quantize_activation(xs[i % nrot], prof, codes, sf)
+    quant(xs[i % nrot], prof, codes, sf)
 torch.cuda.synchronize()
 g = torch.cuda.CUDAGraph()
 s = torch.cuda.Stream()
 with torch.cuda.stream(s):
-    A.quantize_activation(xs[0], prof, codes, sf)
+    quant(xs[0], prof, codes, sf)
     torch.cuda.synchronize()
     with torch.cuda.graph(g, stream=s):
         for i in range(nrot):
-            A.quantize_activation(xs[i], prof, codes, sf)
+            quant(xs[i], prof, codes, sf)
 torch.cuda.synchronize()
 ts = []
 for it in range(max(3, args.iters // nrot)):
@@ -44,7 +51,7 @@ ts.sort()
 Kp = codes.shape[1] * 2
 byts = M * (2 * K + Kp // 2 + Kp // 16)
 med = ts[len(ts) // 2]
-print(f"K={K} M={M} S={S}: median {med*1e3:.1f} us  {byts/med/1e6:.0f} GB/s  (min {ts[0]*1e3:.1f} us)")
+print(f"{'rmsnorm+quant' if args.norm else 'quant'} K={K} M={M} S={S}: median {med*1e3:.1f} us  {byts/med/1e6:.0f} GB/s  (min {ts[0]*1e3:.1f} us)")
 
 # reference: plain torch streaming kernels on the same rotated buffers
 def _t(fn):
