@@ -83,6 +83,10 @@ def lib():
         L.or_rmsnorm.argtypes = [P, i64, i32, i64, P, f32, P, i64]
         L.or_rmsnorm_scale.restype = f32
         L.or_rmsnorm_scale.argtypes = [P, i32, f32]
+        L.or_silu_f32_n.restype = None
+        L.or_silu_f32_n.argtypes = [P, i64, P]
+        L.or_silu_mul.restype = i32
+        L.or_silu_mul.argtypes = [P, i64, i32, i64, i64, P, i64]
         for n in ("or_e2m1_encode_n", "or_e4m3_ceil_n", "or_e4m3_rn_n"):
             getattr(L, n).restype = None
             getattr(L, n).argtypes = [P, i64, P]
@@ -247,6 +251,29 @@ def rmsnorm_scale(x_row_bits, eps: float) -> float:
     """r = 1/sqrt(ss/K + eps) of one row in the pinned order (Q23)."""
     x = np.ascontiguousarray(as_bf16_bits(x_row_bits).reshape(-1))
     return float(lib().or_rmsnorm_scale(_p(x), x.size, np.float32(eps)))
+
+
+# ----------------------------------------------------------------------------- SiLU-mul
+def silu_f32(g_bits) -> np.ndarray:
+    """fp32 SiLU of bf16 inputs in the pinned op sequence of reading Q24 (before the bf16 rounding)."""
+    g = np.ascontiguousarray(as_bf16_bits(g_bits).reshape(-1))
+    out = np.zeros(g.size, np.float32)
+    lib().or_silu_f32_n(_p(g), g.size, _p(out))
+    return out
+
+
+def silu_mul(gu_bits, K: int | None = None, up_off: int | None = None) -> np.ndarray:
+    """Down-proj input h = bf16(bf16(SiLU(gate)) * up) (Fig.5, reading Q24).
+
+    gu: bf16 bits [M][ld] holding gate in columns [0, K) and up in [up_off, up_off + K)
+    (default: the fused gate_up output, K = ld / 2, up_off = K).  Returns bf16 bits [M][K]."""
+    gu = as_bf16_bits(gu_bits)
+    M, ld = gu.shape
+    K = ld // 2 if K is None else K
+    up_off = K if up_off is None else up_off
+    h = np.zeros((M, K), np.uint16)
+    _check(lib().or_silu_mul(_p(gu), M, K, ld, up_off, _p(h), K))
+    return h
 
 
 # ----------------------------------------------------------------------------- calibration

@@ -33,6 +33,9 @@
  *   rmsnorm       float64 formula within two bf16 roundings; exact invariance
  *                 under power-of-two scaling of a row (eps = 0); constant rows
  *                 -> +-1 exactly; torch's fp32 RMSNorm within one bf16 ulp.
+ *   silu          all 2^16 bf16 gate values: fp32 SiLU within 4 ulp of long
+ *                 double, its bf16 rounding correctly rounded everywhere, torch's
+ *                 bf16 SiLU bit-identical wherever its exp does not overflow.
  * Parity unpinned (decisions, not values the paper prints): Q2 ceil-rounded
  * E4M3 block scales, Q4 static activation tensor scale, Q6/Q7 residual domain
  * and op order, Q12 default layout, Q23 RMSNorm reduction order and roundings.
@@ -458,6 +461,66 @@ int or_rmsnorm(const uint16_t* x, int64_t M, int K, int64_t ldx, const uint16_t*
         for (int j = 0; j < K; ++j) {
             const float tj = bf16_to_f32(f32_to_bf16_rne(bf16_to_f32(xr[j]) * r));
             y[m * ldy + j] = f32_to_bf16_rne(bf16_to_f32(gamma[j]) * tj);
+        }
+    }
+    return OR_OK;
+}
+
+/* ------------------------------------------------------------------------- */
+/* SiLU-mul stage: the producer of the down-projection input site.  The     */
+/* paper's decoder layer (Fig.5) quantizes every linear input; the   */
+/* down_proj input is h = SiLU(gate) * up of the bf16 gate/up outputs.      */
+/* Reading Q24 (the paper is silent on how SiLU is evaluated): the ops of a */
+/* bf16 model -- s = SiLU(g) in fp32, rounded to bf16, then bf16(s * u) --  */
+/* with the fp32 SiLU pinned as this sequence of IEEE RN binary32 ops:      */
+/*   a  = max(-|g|, -104)                                                   */
+/*   n  = rint(a * L2E)              (ties to even)                         */
+/*   r  = fma(n, -LN2_HI, a);  r = fma(n, -LN2_LO, r)     (Cody-Waite)      */
+/*   p  = Horner over C7..C0 = RN(1/k!), one fma per step (Taylor e^r)      */
+/*   E  = (p * 2^n1) * 2^n2,  n1 = trunc(n/2), n2 = n - n1   (= e^-|g|)     */
+/*   d  = 1 + E;  rc = 1 / d                                                */
+/*   s  = (g >= 0 ? g : g * E) * rc  (sigma(g) = 1/(1+e^-g), or E/(1+E))    */
+/*   h  = bf16( bf16(s) * u )        (the product of two bf16 is exact)     */
+/* Pinned (tests/test_oracle_silu.py) against long-double SiLU over every   */
+/* finite bf16 g, against the correctly rounded bf16 SiLU, and against      */
+/* torch's bf16 SiLU and SiLU*mul on CPU.                                   */
+/* ------------------------------------------------------------------------- */
+static const float SILU_L2E = 0x1.715476p+0f;      /* RN(1/ln 2) */
+static const float SILU_LN2_HI = 0x1.62e4p-1f;     /* 15 significant bits: n * LN2_HI exact for |n| <= 150 */
+static const float SILU_LN2_LO = 0x1.7f7d1cp-20f;  /* RN(ln 2 - LN2_HI) */
+static const float SILU_C[8] = {1.0f, 1.0f, 0x1p-1f, 0x1.555556p-3f, 0x1.555556p-5f,
+                                0x1.111112p-7f, 0x1.6c16c2p-10f, 0x1.a01a02p-13f};  /* RN(1/k!) */
+
+float or_silu_f32(float g) {
+    float a = -fabsf(g);
+    if (a < -104.0f) a = -104.0f;
+    const float n = rintf(a * SILU_L2E);
+    float r = fmaf(n, -SILU_LN2_HI, a);
+    r = fmaf(n, -SILU_LN2_LO, r);
+    float p = SILU_C[7];
+    for (int k = 6; k >= 0; --k) p = fmaf(p, r, SILU_C[k]);
+    const int ni = (int)n, n1 = ni / 2, n2 = ni - n1;   /* C division truncates toward zero */
+    const float E = (p * ldexpf(1.0f, n1)) * ldexpf(1.0f, n2);
+    const float d = 1.0f + E;
+    const float rc = 1.0f / d;
+    const float q = g >= 0.0f ? g : g * E;
+    return q * rc;
+}
+
+void or_silu_f32_n(const uint16_t* g, int64_t n, float* out) {
+    for (int64_t i = 0; i < n; ++i) out[i] = or_silu_f32(bf16_to_f32(g[i]));
+}
+
+/* h[m][j] = bf16(bf16(SiLU(gu[m][j])) * gu[m][up_off + j]) for j < K */
+int or_silu_mul(const uint16_t* gu, int64_t M, int K, int64_t ld, int64_t up_off, uint16_t* h, int64_t ldh) {
+    if (K <= 0 || M < 0 || up_off < K || ld < up_off + K || ldh < K) return OR_ERR_SHAPE;
+    for (int64_t m = 0; m < M; ++m) {
+        const uint16_t* row = gu + m * ld;
+        for (int j = 0; j < K; ++j) {
+            const float g = bf16_to_f32(row[j]), u = bf16_to_f32(row[up_off + j]);
+            if (!isfinite(g) || !isfinite(u)) return OR_ERR_NONFINITE;
+            const float s = bf16_to_f32(f32_to_bf16_rne(or_silu_f32(g)));
+            h[m * ldh + j] = f32_to_bf16_rne(s * u);
         }
     }
     return OR_OK;
