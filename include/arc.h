@@ -195,6 +195,33 @@ ARC_API arc_status_t arc_linear_rmsnorm(const void* x, int64_t M, int64_t ldx, c
                                         const arc_profile_t* prof, const arc_qweight_t* qw, void* y,
                                         arc_dtype_t y_dtype, int64_t ldy, void* ws, size_t ws_bytes, void* stream);
 
+/* ---------------------------------------------------------------- SiLU-mul (fused producer, Fig.5) */
+/* The down-projection input of a LLaMA/Qwen decoder layer (Fig.5 P:157 quantizes every linear
+ * input): h = SiLU(gate) * up of the bf16 gate/up projections, with the roundings of a bf16
+ * model and SiLU evaluated by a pinned fp32 op sequence (reading Q24; correctly rounded to
+ * bf16 for every bf16 gate value):
+ *   h_j = bf16( bf16(SiLU(g_j)) * u_j ),  g_j = gu[m][j], u_j = gu[m][up_off + j], j < K.
+ * gu: bf16 [M][ld] (e.g. the fused gate_up output, up_off = K, ld = 2K); h: bf16 [M][ldh].
+ * up_off = ARC_GU_PAIRS instead reads (g_j, u_j) as the adjacent pair gu[m][2j], gu[m][2j+1]
+ * (a gate_up weight whose gate and up rows are interleaved offline); ld >= 2K then.
+ * Requires K % 16 == 0, K <= 32768, up_off >= K (or ARC_GU_PAIRS), ld >= up_off + K, ld,
+ * up_off, ldh multiples of 8 elements, 16-byte aligned buffers.  Non-finite inputs give
+ * unspecified output. */
+#define ARC_GU_PAIRS (-1)
+ARC_API arc_status_t arc_silu_mul(const void* gu, int64_t M, int64_t K, int64_t ld, int64_t up_off, void* h,
+                                  int64_t ldh, void* stream);
+/* arc_quantize_activation of arc_silu_mul(gu) in ONE pass over gu: each staged gate/up row pair
+ * is combined in shared memory and quantized (primary + residual); h never reaches HBM.
+ * Bit-identical to arc_silu_mul followed by arc_quantize_activation.  K = prof->K <= 16384. */
+ARC_API arc_status_t arc_silu_mul_quantize_activation(const void* gu, int64_t M, int64_t ld, int64_t up_off,
+                                                      const arc_profile_t* prof, uint8_t* codes, uint8_t* sf,
+                                                      void* stream);
+/* arc_linear of arc_silu_mul(gu) (the down_proj site): y = arc_gemm(arc_silu_mul_quantize_activation(gu)).
+ * Workspace: arc_linear_workspace_size(M, qw). */
+ARC_API arc_status_t arc_linear_silu_mul(const void* gu, int64_t M, int64_t ld, int64_t up_off,
+                                         const arc_profile_t* prof, const arc_qweight_t* qw, void* y,
+                                         arc_dtype_t y_dtype, int64_t ldy, void* ws, size_t ws_bytes, void* stream);
+
 /* ---------------------------------------------------------------- GEMM */
 /* y[M][N] (row stride ldy elements) = (1/(gs_x*gs_w)) * sum over the Kp physical
  * elements of A_aug * B_aug^T (Eq.2), FP32 accumulation in tensor

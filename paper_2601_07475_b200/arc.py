@@ -81,6 +81,10 @@ _sig("arc_rmsnorm", [_P, _i64, _i64, _i64, _P, _f32, _P, _i64, _P])
 _sig("arc_rmsnorm_quantize_activation", [_P, _i64, _i64, _P, _f32, ctypes.POINTER(ArcProfile), _P, _P, _P])
 _sig("arc_linear_rmsnorm", [_P, _i64, _i64, _P, _f32, ctypes.POINTER(ArcProfile), ctypes.POINTER(ArcQWeight), _P,
                             ctypes.c_int, _i64, _P, ctypes.c_size_t, _P])
+_sig("arc_silu_mul", [_P, _i64, _i64, _i64, _i64, _P, _i64, _P])
+_sig("arc_silu_mul_quantize_activation", [_P, _i64, _i64, _i64, ctypes.POINTER(ArcProfile), _P, _P, _P])
+_sig("arc_linear_silu_mul", [_P, _i64, _i64, _i64, ctypes.POINTER(ArcProfile), ctypes.POINTER(ArcQWeight), _P,
+                             ctypes.c_int, _i64, _P, ctypes.c_size_t, _P])
 _sig("arc_linear_hostio_workspace_size", [_i64, ctypes.POINTER(ArcQWeight), ctypes.c_int,
                                          ctypes.POINTER(ctypes.c_size_t)])
 _sig("arc_linear_hostio", [_P, _i64, ctypes.POINTER(ArcProfile), ctypes.POINTER(ArcQWeight), _P, ctypes.c_int, _P,
@@ -98,6 +102,7 @@ EXPORTED = [
     "arc_quantize_activation", "arc_gemm", "arc_linear", "arc_linear_ex", "arc_linear_ex_workspace_size",
     "arc_linear_fused_operand_offsets", "arc_linear_hostio_workspace_size", "arc_rmsnorm",
     "arc_rmsnorm_quantize_activation", "arc_linear_rmsnorm", "arc_linear_hostio",
+    "arc_silu_mul", "arc_silu_mul_quantize_activation", "arc_linear_silu_mul",
     "arc_probe_e2m1", "arc_probe_e2m1_bits", "arc_probe_e2m1_raw_bits", "arc_probe_e4m3_ceil", "arc_debug_fused_trace",
 ]
 
@@ -410,6 +415,61 @@ def linear_rmsnorm(x: torch.Tensor, gamma: torch.Tensor, eps: float, prof: Profi
     _check(_lib.arc_linear_rmsnorm(_ptr(x), M, x.stride(0), _ptr(gamma), float(eps), ctypes.byref(prof.c()),
                                    ctypes.byref(qw.c()), _ptr(out), _dtype_code(out.dtype), out.stride(0), _ptr(buf),
                                    buf.numel(), _stream(stream)), "arc_linear_rmsnorm")
+    return out
+
+
+GU_PAIRS = -1  # up_off value: gu holds (gate_j, up_j) adjacent pairs (ARC_GU_PAIRS)
+
+
+def _gu_args(gu: torch.Tensor, K: int | None, up_off: int | None):
+    assert gu.dtype == torch.bfloat16 and gu.is_cuda and gu.dim() == 2 and gu.stride(1) == 1
+    K = gu.shape[1] // 2 if K is None else K
+    return K, (K if up_off is None else up_off)
+
+
+def silu_mul(gu: torch.Tensor, K: int | None = None, up_off: int | None = None, out=None, stream=None):
+    """Down-proj input h = bf16(bf16(SiLU(gate)) * up) (Fig.5, reading Q24) of gu = [gate | up]
+    (gate in columns [0, K), up in [up_off, up_off + K); default the fused gate_up output), or of
+    (gate_j, up_j) adjacent pairs with up_off = GU_PAIRS."""
+    K, up_off = _gu_args(gu, K, up_off)
+    M = gu.shape[0]
+    if out is None:
+        out = torch.empty(M, K, dtype=torch.bfloat16, device=gu.device)
+    _check(_lib.arc_silu_mul(_ptr(gu), M, K, gu.stride(0), up_off, _ptr(out), out.stride(0), _stream(stream)),
+           "arc_silu_mul")
+    return out
+
+
+def silu_mul_quantize_activation(gu: torch.Tensor, prof: Profile, up_off: int | None = None, codes=None, sf=None,
+                                 stream=None):
+    """quantize_activation(silu_mul(gu)) in one pass over gu (h never reaches HBM)."""
+    K, up_off = _gu_args(gu, prof.K, up_off)
+    M = gu.shape[0]
+    Kp, cb, sb = buffer_sizes(M, prof.K, prof.S)
+    if codes is None:
+        codes = torch.empty(M, Kp // 2, dtype=torch.uint8, device=gu.device)
+    if sf is None:
+        sf = torch.empty(sb, dtype=torch.uint8, device=gu.device)
+    _check(_lib.arc_silu_mul_quantize_activation(_ptr(gu), M, gu.stride(0), up_off, ctypes.byref(prof.c()),
+                                                 _ptr(codes), _ptr(sf), _stream(stream)),
+           "arc_silu_mul_quantize_activation")
+    return codes, sf
+
+
+def linear_silu_mul(gu: torch.Tensor, prof: Profile, qw: QWeight, up_off: int | None = None,
+                    out_dtype=torch.bfloat16, out=None, ws: Workspace = None, stream=None):
+    """ARC linear of silu_mul(gu) (the down_proj site): the SiLU-mul quantize pass + the augmented NVFP4 GEMM."""
+    K, up_off = _gu_args(gu, prof.K, up_off)
+    M = gu.shape[0]
+    if out is None:
+        out = _alloc_out(M, qw.N, out_dtype, gu.device)
+    need = linear_workspace_size(M, qw)
+    if ws is None:
+        ws = _default_ws.setdefault(gu.device, Workspace(gu.device))
+    buf = ws.get(need)
+    _check(_lib.arc_linear_silu_mul(_ptr(gu), M, gu.stride(0), up_off, ctypes.byref(prof.c()), ctypes.byref(qw.c()),
+                                    _ptr(out), _dtype_code(out.dtype), out.stride(0), _ptr(buf), buf.numel(),
+                                    _stream(stream)), "arc_linear_silu_mul")
     return out
 
 

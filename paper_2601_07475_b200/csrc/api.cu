@@ -337,6 +337,40 @@ arc_status_t arc_rmsnorm_quantize_activation(const void* x, int64_t M, int64_t l
   return e == cudaSuccess ? ARC_OK : cuda_fail(e, "arc_rmsnorm_quantize_activation");
 }
 
+arc_status_t arc_silu_mul(const void* gu, int64_t M, int64_t K, int64_t ld, int64_t up_off, void* h, int64_t ldh,
+                          void* stream) {
+  const bool pairs = up_off == ARC_GU_PAIRS;
+  if (K <= 0 || K % 16 || K > 32768 || M < 0 || (!pairs && (up_off < K || up_off % 8)) ||
+      ld < (pairs ? 2 * K : up_off + K) || ld % 8 || ldh < K || ldh % 8)
+    return fail(ARC_ERR_SHAPE, "bad M/K/ld/up_off/ldh");
+  if (M == 0) return ARC_OK;
+  if (!gu || !h) return fail(ARC_ERR_NULL, "null gu / h");
+  if (!aligned16(gu) || !aligned16(h)) return fail(ARC_ERR_ALIGN, "buffer not 16B aligned");
+  arc_status_t s = check_device();
+  if (s != ARC_OK) return s;
+  cudaError_t e = launch_silu_mul(gu, M, (int)K, ld, pairs ? -2 : up_off, h, ldh, (cudaStream_t)stream);
+  return e == cudaSuccess ? ARC_OK : cuda_fail(e, "arc_silu_mul");
+}
+
+arc_status_t arc_silu_mul_quantize_activation(const void* gu, int64_t M, int64_t ld, int64_t up_off,
+                                              const arc_profile_t* prof, uint8_t* codes, uint8_t* sf, void* stream) {
+  arc_status_t s = check_profile(prof);
+  if (s != ARC_OK) return s;
+  const int64_t K = prof->K;
+  if (K > 16384) return fail(ARC_ERR_UNSUPPORTED, "SiLU-mul quantize supports K <= 16384");
+  const bool pairs = up_off == ARC_GU_PAIRS;
+  if (M < 0 || (!pairs && (up_off < K || up_off % 8)) || ld < (pairs ? 2 * K : up_off + K) || ld % 8)
+    return fail(ARC_ERR_SHAPE, "bad M/ld/up_off");
+  if (M == 0) return ARC_OK;
+  if (!gu || !codes || !sf) return fail(ARC_ERR_NULL, "null gu / codes / sf");
+  if (!aligned16(gu) || !aligned16(codes) || !aligned16(sf)) return fail(ARC_ERR_ALIGN, "buffer not 16B aligned");
+  s = check_device();
+  if (s != ARC_OK) return s;
+  cudaError_t e = launch_quant(gu, M, (int)K, ld, prof->perm, prof->S, prof->gs, (int)prof->layout, 0, codes, sf,
+                               (cudaStream_t)stream, nullptr, 0.0f, pairs ? -2 : up_off);
+  return e == cudaSuccess ? ARC_OK : cuda_fail(e, "arc_silu_mul_quantize_activation");
+}
+
 arc_status_t arc_gemm(const uint8_t* a_codes, const uint8_t* a_sf, const float* gs_x, int64_t M,
                       const arc_qweight_t* qw, void* y, arc_dtype_t y_dtype, int64_t ldy, void* ws, size_t ws_bytes,
                       void* stream) {
@@ -456,6 +490,29 @@ arc_status_t arc_linear_rmsnorm(const void* x, int64_t M, int64_t ldx, const voi
   uint8_t* sf = codes + round_up(M * (qw->Kp / 2), 256);
   const size_t act = act_ws_bytes(M, qw->K, qw->S);
   s = arc_rmsnorm_quantize_activation(x, M, ldx, gamma, eps, prof, codes, sf, stream);
+  if (s != ARC_OK) return s;
+  return arc_gemm(codes, sf, prof->gs, M, qw, y, y_dtype, ldy, codes + act, ws_bytes - sync - act, stream);
+}
+
+arc_status_t arc_linear_silu_mul(const void* gu, int64_t M, int64_t ld, int64_t up_off, const arc_profile_t* prof,
+                                 const arc_qweight_t* qw, void* y, arc_dtype_t y_dtype, int64_t ldy, void* ws,
+                                 size_t ws_bytes, void* stream) {
+  arc_status_t s = check_profile(prof);
+  if (s != ARC_OK) return s;
+  s = check_qweight(qw);
+  if (s != ARC_OK) return s;
+  if (qw->K != prof->K || qw->S != prof->S || qw->layout != prof->layout)
+    return fail(ARC_ERR_SHAPE, "profile and qweight disagree on K / S / layout");
+  if (M < 0 || M > (1 << 30)) return fail(ARC_ERR_SHAPE, "bad M");
+  if (M == 0) return ARC_OK;
+  if (!ws) return fail(ARC_ERR_NULL, "null workspace");
+  const size_t sync = sync_bytes_of(qw->N);
+  if (ws_bytes < sync + linear_rest_bytes(M, qw, ARC_LINEAR_UNFUSED)) return fail(ARC_ERR_WORKSPACE, "workspace too small");
+  if ((reinterpret_cast<uintptr_t>(ws) & 255u) != 0) return fail(ARC_ERR_ALIGN, "workspace not 256B aligned");
+  uint8_t* codes = static_cast<uint8_t*>(ws) + sync;
+  uint8_t* sf = codes + round_up(M * (qw->Kp / 2), 256);
+  const size_t act = act_ws_bytes(M, qw->K, qw->S);
+  s = arc_silu_mul_quantize_activation(gu, M, ld, up_off, prof, codes, sf, stream);
   if (s != ARC_OK) return s;
   return arc_gemm(codes, sf, prof->gs, M, qw, y, y_dtype, ldy, codes + act, ws_bytes - sync - act, stream);
 }

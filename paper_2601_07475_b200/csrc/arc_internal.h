@@ -12,9 +12,12 @@ inline int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
 int num_sms();  // SM count of the current device (cached per device)
 
 // gamma != nullptr: RMSNorm (reading Q23) each row in place before quantizing it.
+// up_off >= 0: SiLU-mul mode (reading Q24): quantize bf16(bf16(SiLU(x)) * x[up_off..]) per row.
 cudaError_t launch_quant(const void* x, int64_t rows, int K, int64_t ld, const int32_t* perm, int S, const float* gs,
                          int layout, int weight_mode, uint8_t* codes, uint8_t* sf, cudaStream_t stream,
-                         const void* gamma = nullptr, float eps = 0.0f);
+                         const void* gamma = nullptr, float eps = 0.0f, int64_t up_off = -1);
+cudaError_t launch_silu_mul(const void* gu, int64_t rows, int K, int64_t ld, int64_t up_off, void* h, int64_t ldh,
+                            cudaStream_t s);
 cudaError_t launch_rmsnorm(const void* x, int64_t rows, int K, int64_t ldx, const void* gamma, float eps, void* y,
                            int64_t ldy, cudaStream_t s);
 cudaError_t launch_calib_absmax(const void* x, int64_t rows, int K, int64_t ld, float* chan_max, cudaStream_t s);

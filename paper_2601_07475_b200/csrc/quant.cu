@@ -57,6 +57,7 @@ struct QuantArgs {
   const uint16_t* gamma;  // RMSNorm weight bf16[K] (norm mode)
   float eps;
   int32_t norm;    // 1: RMSNorm the staged rows in place before quantizing (R norm warps)
+  int64_t up_off;  // SiLU-mul mode (Fig.5, reading Q24): x holds gate, x + up_off holds up
 };
 
 ARC_DEV void cp_async16(uint32_t dst, const void* src) {
@@ -90,6 +91,76 @@ ARC_DEV void norm16(float (&z)[16], const uint8_t* gblk, float r) {
     const uint32_t yw = *reinterpret_cast<const uint32_t*>(&y);
     z[i] = __uint_as_float(yw << 16);
     z[i + 1] = __uint_as_float(yw & 0xFFFF0000u);
+  }
+}
+
+// SiLU (reading Q24) of a bf16 gate pattern gb -> bf16 pattern of bf16(SiLU(g)).  Patterns with
+// |g| in [2^-9, 128) -- magnitude bits [SILU_LO, SILU_LO + SILU_N) -- read a per-CTA table at
+// index (mag - SILU_LO) | (sign << 11), built with silu_f32 itself; the rest follow from the
+// pinned sequence in closed form (checked against the oracle over all 2^16 patterns):
+//   |g| < 2^-125 (exponent field 0 or 1): E = 1, d = 2, s = g/2 exactly, bf16 ties to even;
+//   2^-125 <= |g| < 2^-9: bf16(SiLU(g)) = g/2 (exponent - 1);
+//   g >= 128: g;  g <= -128: -0.
+constexpr uint32_t SILU_LO = 0x3B00u, SILU_N = 0x800u;
+constexpr int SILU_TAB = 4096;
+
+ARC_DEV uint32_t silu_bf16_bits(uint32_t gb, const uint16_t* tab) {
+  const uint32_t mag = gb & 0x7FFFu;
+  const uint32_t t = mag - SILU_LO;
+  if (t < SILU_N) return tab[t | ((gb >> 4) & 0x800u)];
+  const uint32_t neg = gb & 0x8000u;
+  if (mag < 0x100u) return ((mag + ((mag >> 1) & 1u)) >> 1) | neg;
+  if (mag < SILU_LO) return (mag - 0x80u) | neg;
+  return neg ? 0x8000u : mag;
+}
+
+// h = bf16(s * u) for two (SiLU bits, up-in-high-half word) pairs: one mul.rn.f32x2 + one
+// cvt.rn.bf16x2.f32 (s * u of two bf16 values is exact in fp32 unless it underflows, where the
+// fp32 rounding happens exactly as in the oracle's fp32 multiply)
+ARC_DEV void silu_prod2(uint32_t s0, uint32_t s1, uint32_t w0, uint32_t w1, float& z0, float& z1) {
+  unsigned long long a, b, r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(a) : "r"(s0 << 16), "r"(s1 << 16));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(b) : "r"(w0 & 0xFFFF0000u), "r"(w1 & 0xFFFF0000u));
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  float p0, p1;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(p0), "=f"(p1) : "l"(r));
+  const __nv_bfloat162 h = __floats2bfloat162_rn(p0, p1);
+  const uint32_t hw = *reinterpret_cast<const uint32_t*>(&h);
+  z0 = __uint_as_float(hw << 16);
+  z1 = __uint_as_float(hw & 0xFFFF0000u);
+}
+
+// SiLU-mul of one 16-channel block (reading Q24): z = bf16(bf16(SiLU(g)) * u) for the 16
+// gathered (g, u) pairs.  MODE 1: gate row at `row`, up row at row + upb (two LDS.U16 per
+// channel); MODE 2: (g, u) adjacent bf16 pairs, one LDS.32 per channel (off = 4 * channel).
+// The block's 16 gate patterns are first checked against the table range (one branch per
+// block, rarely divergent).
+template <int MODE>
+ARC_DEV void silu_mul_block16(float (&z)[16], const uint8_t* row, const uint32_t (&off)[16], int upb,
+                              const uint16_t* tab) {
+#pragma unroll
+  for (int hb = 0; hb < 16; hb += 8) {  // two halves of 8 channels: 8 live (g, u) words
+    uint32_t w[8];  // gate bits | up bits << 16
+    uint32_t tmax = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      if (MODE == 2) w[q] = *reinterpret_cast<const uint32_t*>(row + off[hb + q]);
+      else w[q] = *reinterpret_cast<const uint16_t*>(row + off[hb + q]) |
+                  ((uint32_t)*reinterpret_cast<const uint16_t*>(row + upb + off[hb + q]) << 16);
+      tmax = max(tmax, (w[q] & 0x7FFFu) - SILU_LO);
+    }
+    if (tmax < SILU_N) {
+#pragma unroll
+      for (int q = 0; q < 8; q += 2)
+        silu_prod2(tab[((w[q] & 0x7FFFu) - SILU_LO) | ((w[q] >> 4) & 0x800u)],
+                   tab[((w[q + 1] & 0x7FFFu) - SILU_LO) | ((w[q + 1] >> 4) & 0x800u)], w[q], w[q + 1], z[hb + q],
+                   z[hb + q + 1]);
+    } else {
+#pragma unroll
+      for (int q = 0; q < 8; q += 2)
+        silu_prod2(silu_bf16_bits(w[q] & 0xFFFFu, tab), silu_bf16_bits(w[q + 1] & 0xFFFFu, tab), w[q], w[q + 1],
+                   z[hb + q], z[hb + q + 1]);
+    }
   }
 }
 
@@ -128,7 +199,12 @@ ARC_DEV int tile_rows(int base, int64_t rows) {  // valid rows base + 32 i < row
 // Rows sit at a fixed ROWP stride (ROWB + 16: rows of one tile fall in different
 // banks for the residual warp's cross-row gathers) and the tile loop is unrolled
 // over the ring so the gathers are `LDS [off + const]`.
-template <int IPT, int R, int ROWB, int ST, bool NORM>
+//
+// SILU mode (the down-proj input site; ROWB then holds 4K bytes): SILU = 1, a staged row is the
+// gate row [0, 2K) bytes followed by the up row [2K, 4K); SILU = 2, the row holds (g_j, u_j)
+// bf16 pairs (an interleaved gate_up output).  The quantizing warps gather each of their 16
+// channels' (g, u) and quantize h = bf16(bf16(SiLU(g)) * u) (silu_mul_block16, reading Q24).
+template <int IPT, int R, int ROWB, int ST, bool NORM, int SILU>
 __global__ void __launch_bounds__(1024) arc_quant_kernel(QuantArgs p) {
   extern __shared__ __align__(16) uint8_t smem[];
   constexpr int ROWP = ROWB + 16;
@@ -136,6 +212,7 @@ __global__ void __launch_bounds__(1024) arc_quant_kernel(QuantArgs p) {
   constexpr int UB = R * 4;  // staged scale bytes per 4-block unit per tile
   const int K = p.K;
   const int npw = p.npw, nrw = p.nrw;
+  constexpr uint32_t OSC = SILU == 2 ? 4u : 2u;  // staged bytes per channel index
   const int NU = p.Kp >> 6;  // 4-block units per row
   uint8_t* sfst = smem + ST * SLOT;  // [ST][NU][UB]
   float* k1tab = reinterpret_cast<float*>(sfst + ST * NU * UB);
@@ -146,6 +223,8 @@ __global__ void __launch_bounds__(1024) arc_quant_kernel(QuantArgs p) {
   uint64_t* normed = empty + ST;  // norm mode: the RMS scales of slot s's rows are ready
   float* rscale = reinterpret_cast<float*>(normed + ST);  // [ST][R] 1/rms of each staged row
   uint8_t* gam = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(rscale + ST * R) + 15) & ~uintptr_t(15));
+  // SiLU table at the same place, addressed from `smem` so loads stay in the shared window
+  const uint16_t* stab = reinterpret_cast<const uint16_t*>(smem + (gam - smem));
   // gam: gamma in reordered channel order, bf16[K], staged once per CTA (norm mode)
 
   const int tid = threadIdx.x;
@@ -174,6 +253,11 @@ __global__ void __launch_bounds__(1024) arc_quant_kernel(QuantArgs p) {
     c6tab[c] = __fdiv_rn(e4m3_value((uint32_t)c), 6.0f);
     if (c < 64) rat[c] = __fdiv_rn((float)(8 + (c >> 3)), (float)(8 + (c & 7)));
   }
+  if (SILU)
+    for (int c = tid; c < SILU_TAB; c += blockDim.x) {
+      const uint32_t gb = (((uint32_t)c & 2047u) + SILU_LO) | (((uint32_t)c & 2048u) << 4);
+      reinterpret_cast<uint16_t*>(gam)[c] = __bfloat16_as_ushort(__float2bfloat16_rn(silu_f32(__uint_as_float(gb << 16))));
+    }
   if (NORM)
     for (int c = tid; c < K; c += blockDim.x)
       reinterpret_cast<uint16_t*>(gam)[c] = __ldg(reinterpret_cast<const unsigned short*>(p.gamma) + __ldg(p.perm + c));
@@ -184,6 +268,7 @@ __global__ void __launch_bounds__(1024) arc_quant_kernel(QuantArgs p) {
     // ---------------------------------------------------------------- producer warp
     const uint32_t ring = smem_u32(smem) + (uint32_t)lane * 16u;
     const int kc = K >> 3;  // 16-byte chunks per row
+    const uint32_t rowbytes = (uint32_t)K * (SILU ? 4u : 2u);
     const uint64_t x_policy = policy_evict_first();
     // scales staged for tile jt (slot s) -> global, one UB-byte word per unit
     auto flush_sf = [&](int s, int jt) {
@@ -211,13 +296,17 @@ __global__ void __launch_bounds__(1024) arc_quant_kernel(QuantArgs p) {
           if (p.bulk) {
             // one cp.async.bulk per row (TMA engine, no LSU/MIO traffic); lane 0 only
             if (lane == 0) {
-              mbar_expect_tx(&full[s], (uint32_t)(nr * K * 2));
+              mbar_expect_tx(&full[s], (uint32_t)nr * rowbytes);
               if (p.debug != 2)
-                for (int r = 0; r < nr; ++r)  // X is read once: evict-first
-                  bulk_load_hint(smem + s * SLOT + r * ROWP, p.x + (int64_t)(base + 32 * r) * p.ld, (uint32_t)K * 2,
-                                 &full[s], x_policy);
+                for (int r = 0; r < nr; ++r) {  // X is read once: evict-first
+                  bulk_load_hint(smem + s * SLOT + r * ROWP, p.x + (int64_t)(base + 32 * r) * p.ld,
+                                 (uint32_t)K * (SILU == 2 ? 4 : 2), &full[s], x_policy);
+                  if (SILU == 1)
+                    bulk_load_hint(smem + s * SLOT + r * ROWP + K * 2, p.x + (int64_t)(base + 32 * r) * p.ld + p.up_off,
+                                   (uint32_t)K * 2, &full[s], x_policy);
+                }
               else
-                mbar_complete_tx_self(&full[s], (uint32_t)(nr * K * 2));
+                mbar_complete_tx_self(&full[s], (uint32_t)nr * rowbytes);
             }
           } else {
             if (p.debug != 2) {
@@ -289,10 +378,10 @@ __global__ void __launch_bounds__(1024) arc_quant_kernel(QuantArgs p) {
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int4 v = __ldg(pp + q);
-        off[i][4 * q + 0] = (uint32_t)v.x * 2u;
-        off[i][4 * q + 1] = (uint32_t)v.y * 2u;
-        off[i][4 * q + 2] = (uint32_t)v.z * 2u;
-        off[i][4 * q + 3] = (uint32_t)v.w * 2u;
+        off[i][4 * q + 0] = (uint32_t)v.x * OSC;
+        off[i][4 * q + 1] = (uint32_t)v.y * OSC;
+        off[i][4 * q + 2] = (uint32_t)v.z * OSC;
+        off[i][4 * q + 3] = (uint32_t)v.w * OSC;
       }
     }
     for (int j0 = 0; j0 < my_tiles; j0 += ST) {
@@ -318,8 +407,12 @@ __global__ void __launch_bounds__(1024) arc_quant_kernel(QuantArgs p) {
                     uint2 packed = make_uint2(0u, 0u);
                     if (kind[i] == 1) {
                       float z[16];
-                      gather16(smem + s * SLOT + r * ROWP, off[i], z);
-                      if (NORM) norm16(z, gam + 32 * (tid + i * npw * 32), rscale[s * R + r]);
+                      if (SILU) {
+                        silu_mul_block16<SILU>(z, smem + s * SLOT + r * ROWP, off[i], K * 2, stab);
+                      } else {
+                        gather16(smem + s * SLOT + r * ROWP, off[i], z);
+                        if (NORM) norm16(z, gam + 32 * (tid + i * npw * 32), rscale[s * R + r]);
+                      }
                       // stage 1 (Eq.1 with the NVFP4 two-level scale, Q7 op order)
                       sfb = e4m3_ceil_nb(__fmul_rn(absmax16(z), c6g));
                       packed = encode16(z, k1tab[sfb]);
@@ -351,10 +444,10 @@ __global__ void __launch_bounds__(1024) arc_quant_kernel(QuantArgs p) {
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const int4 v = __ldg(pp + q);
-      foff[4 * q + 0] = (uint32_t)v.x * 2u + (uint32_t)(fr * ROWP);
-      foff[4 * q + 1] = (uint32_t)v.y * 2u + (uint32_t)(fr * ROWP);
-      foff[4 * q + 2] = (uint32_t)v.z * 2u + (uint32_t)(fr * ROWP);
-      foff[4 * q + 3] = (uint32_t)v.w * 2u + (uint32_t)(fr * ROWP);
+      foff[4 * q + 0] = (uint32_t)v.x * OSC + (uint32_t)(fr * ROWP);
+      foff[4 * q + 1] = (uint32_t)v.y * OSC + (uint32_t)(fr * ROWP);
+      foff[4 * q + 2] = (uint32_t)v.z * OSC + (uint32_t)(fr * ROWP);
+      foff[4 * q + 3] = (uint32_t)v.w * OSC + (uint32_t)(fr * ROWP);
     }
   }
   const int fpb = phys_block(nb + fjb, nb, ns, p.layout);
@@ -381,18 +474,22 @@ __global__ void __launch_bounds__(1024) arc_quant_kernel(QuantArgs p) {
 #pragma unroll
               for (int q = 0; q < 4; ++q) {
                 const int4 v = __ldg(pp + q);
-                off[4 * q + 0] = (uint32_t)v.x * 2u + (uint32_t)(r * ROWP);
-                off[4 * q + 1] = (uint32_t)v.y * 2u + (uint32_t)(r * ROWP);
-                off[4 * q + 2] = (uint32_t)v.z * 2u + (uint32_t)(r * ROWP);
-                off[4 * q + 3] = (uint32_t)v.w * 2u + (uint32_t)(r * ROWP);
+                off[4 * q + 0] = (uint32_t)v.x * OSC + (uint32_t)(r * ROWP);
+                off[4 * q + 1] = (uint32_t)v.y * OSC + (uint32_t)(r * ROWP);
+                off[4 * q + 2] = (uint32_t)v.z * OSC + (uint32_t)(r * ROWP);
+                off[4 * q + 3] = (uint32_t)v.w * OSC + (uint32_t)(r * ROWP);
               }
             }
             uint32_t sfb = 0;
             if (r < nr) {
               const int m = base + 32 * r;
               float z[16];
-              gather16(smem + s * SLOT, off, z);
-              if (NORM) norm16(z, gam + 32 * jb, rscale[s * R + r]);
+              if (SILU) {
+                silu_mul_block16<SILU>(z, smem + s * SLOT, off, K * 2, stab);
+              } else {
+                gather16(smem + s * SLOT, off, z);
+                if (NORM) norm16(z, gam + 32 * jb, rscale[s * R + r]);
+              }
               const uint32_t sf1 = e4m3_ceil_nb(__fmul_rn(absmax16(z), c6g));
               float t[16];
               uint2 packed = encode16(z, k1tab[sf1], t);
@@ -469,12 +566,12 @@ __global__ void arc_finalize_scale_kernel(float* gs) {
 // Per-(kernel, threads, smem) launch configuration, computed once per process:
 // the attribute calls and the occupancy query cost more host time than the
 // kernel itself at decode sizes.
-template <int IPT, int R, int ROWB, int ST, bool NORM>
+template <int IPT, int R, int ROWB, int ST, bool NORM, int SILU = 0>
 static cudaError_t launch_quant_cfg(QuantArgs a, int threads, cudaStream_t stream) {
   a.rows_per_tile = R;
   a.stages = ST;
   const size_t smem = (size_t)ST * R * (ROWB + 16) + (size_t)ST * (a.Kp / 64) * (R * 4) + (128 + 128 + 64) * 4 + 3 * ST * 8 +
-                      (size_t)ST * R * 4 + (NORM ? 16 + (size_t)a.K * 2 : 0);
+                      (size_t)ST * R * 4 + (NORM ? 16 + (size_t)a.K * 2 : 0) + (SILU ? 16 + SILU_TAB * 2 : 0);
   struct Cfg { int dev, threads; size_t smem; int occ; };
   static thread_local Cfg cache[8];
   static thread_local int ncache = 0;
@@ -484,13 +581,13 @@ static cudaError_t launch_quant_cfg(QuantArgs a, int threads, cudaStream_t strea
   for (int i = 0; i < ncache && i < 8; ++i)
     if (cache[i].dev == dev && cache[i].threads == threads && cache[i].smem == smem) occ = cache[i].occ;
   if (occ == 0) {
-    cudaError_t e = cudaFuncSetAttribute(arc_quant_kernel<IPT, R, ROWB, ST, NORM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(arc_quant_kernel<IPT, R, ROWB, ST, NORM, SILU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          227 * 1024);
     if (e != cudaSuccess) return e;
     // the full shared-memory carveout so several CTAs' rings fit per SM
-    e = cudaFuncSetAttribute(arc_quant_kernel<IPT, R, ROWB, ST, NORM>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    e = cudaFuncSetAttribute(arc_quant_kernel<IPT, R, ROWB, ST, NORM, SILU>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e != cudaSuccess) return e;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, arc_quant_kernel<IPT, R, ROWB, ST, NORM>, threads, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, arc_quant_kernel<IPT, R, ROWB, ST, NORM, SILU>, threads, smem);
     if (e != cudaSuccess) return e;
     if (occ < 1) occ = 1;
     cache[ncache % 8] = Cfg{dev, threads, smem, occ};
@@ -509,15 +606,27 @@ static cudaError_t launch_quant_cfg(QuantArgs a, int threads, cudaStream_t strea
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, arc_quant_kernel<IPT, R, ROWB, ST, NORM>, a);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, arc_quant_kernel<IPT, R, ROWB, ST, NORM, SILU>, a);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
+template <int SILU>
+static cudaError_t launch_silu_cfg(QuantArgs a, int th, int ipt, int64_t rb, cudaStream_t stream) {
+  if (ipt == 1) {
+    if (rb <= 8192) return launch_quant_cfg<1, 4, 8192, 3, false, SILU>(a, th, stream);
+    if (rb <= 16384) return launch_quant_cfg<1, 2, 16384, 3, false, SILU>(a, th, stream);
+    if (rb <= 32768) return launch_quant_cfg<1, 2, 32768, 3, false, SILU>(a, th, stream);
+    return launch_quant_cfg<1, 1, 65536, 3, false, SILU>(a, th, stream);
+  }
+  return launch_quant_cfg<2, 1, 65536, 3, false, SILU>(a, th, stream);
+}
+
 cudaError_t launch_quant(const void* x, int64_t rows, int K, int64_t ld, const int32_t* perm, int S, const float* gs,
                          int layout, int weight_mode, uint8_t* codes, uint8_t* sf, cudaStream_t stream,
-                         const void* gamma, float eps) {
+                         const void* gamma, float eps, int64_t up_off) {
   QuantArgs a;
+  a.up_off = up_off;
   a.gamma = static_cast<const uint16_t*>(gamma);
   a.eps = eps;
   a.norm = gamma != nullptr ? 1 : 0;
@@ -541,6 +650,20 @@ cudaError_t launch_quant(const void* x, int64_t rows, int K, int64_t ld, const i
   const int NB = a.Kp / 16, ns = S / 16;
   const int nprim = NB - ns;                 // primary + pad blocks per row
   const int64_t rowb = (int64_t)K * 2;
+  if (up_off >= 0 || up_off == -2) {
+    // SiLU-mul mode: a staged row is gate + up (4K bytes); always whole-row bulk copies.
+    // up_off == -2: (g, u) pairs (SILU = 2); else up at x + up_off (SILU = 1).
+    a.bulk = 1;
+    const int64_t rb = 2 * rowb;
+    const int R = rb <= 8192 ? 4 : rb <= 32768 ? 2 : 1;
+    const int ipt2 = (nprim + 28 * 32 - 1) / (28 * 32);
+    a.npw = (nprim + 32 * ipt2 - 1) / (32 * ipt2);
+    a.nrw = ns == 0 ? 0 : (int)imin64(2, (R * ns + 31) / 32);
+    const int th = (a.npw + a.nrw + 1) * 32;
+    if (th > 1024 || rb > 65536) return cudaErrorInvalidValue;
+    if (up_off == -2) return launch_silu_cfg<2>(a, th, ipt2, rb, stream);
+    return launch_silu_cfg<1>(a, th, ipt2, rb, stream);
+  }
   // ring configurations (rows per tile R, row slot bytes, stages), tuned on B200:
   // K <= 4096: R=4 (the residual warp gets a full 32 items per tile), 3 x 32 KB slots
   // -> 2 CTAs/SM; K <= 8192: R=2, 3 x 32 KB; K <= 16384: R=2, 3 x 64 KB (1 CTA/SM).
@@ -606,6 +729,53 @@ cudaError_t launch_rmsnorm(const void* x, int64_t rows, int K, int64_t ldx, cons
   cfg.numAttrs = 1;
   cudaError_t e = cudaLaunchKernelEx(&cfg, arc_rmsnorm_kernel, static_cast<const uint16_t*>(x), rows, K, ldx,
                                      static_cast<const uint16_t*>(gamma), eps, static_cast<uint16_t*>(y), ldy);
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
+// Standalone SiLU-mul (the unfused comparison and the calibration input of the down-proj site):
+// 8 channels per thread, the same device function (and so the same bits) as the fused kernel.
+__global__ void __launch_bounds__(256) arc_silu_mul_kernel(const uint16_t* gu, int64_t rows, int K, int64_t ld,
+                                                           int64_t up_off, uint16_t* h, int64_t ldh) {
+  pdl_launch_dependents();
+  pdl_wait();
+  const int k8 = K >> 3;
+  const int64_t n = rows * k8;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t m = i / k8;
+    const int c = (int)(i - m * k8) * 8;
+    uint4 g, u;
+    if (up_off == -2) {  // (g_j, u_j) pairs: 8 channels = 32 bytes
+      const uint4 a = __ldg(reinterpret_cast<const uint4*>(gu + m * ld + 2 * c));
+      const uint4 b = __ldg(reinterpret_cast<const uint4*>(gu + m * ld + 2 * c + 8));
+      g = make_uint4(__byte_perm(a.x, a.y, 0x5410), __byte_perm(a.z, a.w, 0x5410), __byte_perm(b.x, b.y, 0x5410),
+                     __byte_perm(b.z, b.w, 0x5410));
+      u = make_uint4(__byte_perm(a.x, a.y, 0x7632), __byte_perm(a.z, a.w, 0x7632), __byte_perm(b.x, b.y, 0x7632),
+                     __byte_perm(b.z, b.w, 0x7632));
+    } else {
+      g = __ldg(reinterpret_cast<const uint4*>(gu + m * ld + c));
+      u = __ldg(reinterpret_cast<const uint4*>(gu + m * ld + up_off + c));
+    }
+    *reinterpret_cast<uint4*>(h + m * ldh + c) = silu_mul8(g, u);
+  }
+}
+
+cudaError_t launch_silu_mul(const void* gu, int64_t rows, int K, int64_t ld, int64_t up_off, void* h, int64_t ldh,
+                            cudaStream_t s) {
+  const int64_t n = rows * (K / 8);
+  const int64_t grid = imax64(1, imin64((n + 255) / 256, (int64_t)num_sms() * 8));
+  cudaLaunchConfig_t cfg;
+  memset(&cfg, 0, sizeof(cfg));
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(256);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, arc_silu_mul_kernel, static_cast<const uint16_t*>(gu), rows, K, ld, up_off,
+                                     static_cast<uint16_t*>(h), ldh);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }

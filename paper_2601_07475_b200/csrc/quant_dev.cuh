@@ -218,4 +218,50 @@ ARC_DEV uint4 rms_apply8(uint4 x, uint4 g, float r) {
   return make_uint4(o[0], o[1], o[2], o[3]);
 }
 
+// ------------------------------------------------------------------ SiLU-mul (Fig.5, reading Q24)
+// fp32 SiLU of a bf16 gate value as the pinned sequence of IEEE RN ops of reading Q24
+// (DESIGN.md): Cody-Waite reduction of e^-|g|, degree-7 Taylor in Horner form (one fma per
+// step), exact power-of-two scaling in two halves, then sigma = 1/(1+E) or E/(1+E).
+ARC_DEV float exp2i(int n) { return __int_as_float((n + 127) << 23); }  // 2^n, -126 <= n <= 127
+
+ARC_DEV float silu_f32(float g) {
+  const float a = fmaxf(-fabsf(g), -104.0f);
+  const float n = rintf(__fmul_rn(a, 0x1.715476p+0f));
+  float r = __fmaf_rn(n, -0x1.62e4p-1f, a);
+  r = __fmaf_rn(n, -0x1.7f7d1cp-20f, r);
+  float p = 0x1.a01a02p-13f;
+  p = __fmaf_rn(p, r, 0x1.6c16c2p-10f);
+  p = __fmaf_rn(p, r, 0x1.111112p-7f);
+  p = __fmaf_rn(p, r, 0x1.555556p-5f);
+  p = __fmaf_rn(p, r, 0x1.555556p-3f);
+  p = __fmaf_rn(p, r, 0.5f);
+  p = __fmaf_rn(p, r, 1.0f);
+  p = __fmaf_rn(p, r, 1.0f);
+  const int ni = (int)n, n1 = ni / 2, n2 = ni - n1;
+  const float E = __fmul_rn(__fmul_rn(p, exp2i(n1)), exp2i(n2));
+  const float rc = __frcp_rn(__fadd_rn(1.0f, E));
+  const float q = g >= 0.0f ? g : __fmul_rn(g, E);
+  return __fmul_rn(q, rc);
+}
+
+// h = bf16(bf16(SiLU(g)) * u) of one gate/up pair, as fp32 (exact: h is a bf16 value)
+ARC_DEV float silu_mul1(float g, float u) {
+  const float s = __bfloat162float(__float2bfloat16_rn(silu_f32(g)));
+  return __bfloat162float(__float2bfloat16_rn(__fmul_rn(s, u)));
+}
+
+// 8 channels: one 16-byte word of gate and of up -> one 16-byte word of h (bf16)
+ARC_DEV uint4 silu_mul8(uint4 g, uint4 u) {
+  const uint32_t gw[4] = {g.x, g.y, g.z, g.w}, uw[4] = {u.x, u.y, u.z, u.w};
+  uint32_t o[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const __nv_bfloat162 h = __floats2bfloat162_rn(
+        silu_mul1(__uint_as_float(gw[i] << 16), __uint_as_float(uw[i] << 16)),
+        silu_mul1(__uint_as_float(gw[i] & 0xFFFF0000u), __uint_as_float(uw[i] & 0xFFFF0000u)));
+    o[i] = *reinterpret_cast<const uint32_t*>(&h);
+  }
+  return make_uint4(o[0], o[1], o[2], o[3]);
+}
+
 }  // namespace arc

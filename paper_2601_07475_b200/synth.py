@@ -10,6 +10,9 @@ recipe:
   activation(M, K, st, seed): X = N(0,1) * exp(0.5 N(0,1))[row] ; X[:, idx] *= gain
   weight(N, K, seed): N(0,1) / sqrt(K)
   rmsnorm_weight(K, seed): exp(0.3 N(0,1))  (positive per-channel RMSNorm gains around 1)
+  gate_up(M, K, st, seed): bf16 [M, 2K] = [gate | up] with gate = 2 N(0,1) (pre-activation spread
+      that covers SiLU's negative lobe and linear tail) and up = activation(M, K, st) (the
+      down-proj input's outlier channels, Fig.2, come through the up half)
 """
 from __future__ import annotations
 
@@ -47,6 +50,14 @@ def rmsnorm_weight(K: int, seed: int, device="cpu") -> torch.Tensor:
     """bf16 [K] RMSNorm gain vector (the gamma of the attention / MLP input norms)."""
     g = torch.Generator(device=device).manual_seed(int(seed) + 104729)
     return torch.exp(0.3 * torch.randn(K, generator=g, device=device, dtype=torch.float32)).to(torch.bfloat16)
+
+
+def gate_up(M: int, K: int, st: Structure, seed: int, device="cpu") -> torch.Tensor:
+    """bf16 [M, 2K] fused gate_up output: gate in columns [0, K), up in [K, 2K)."""
+    g = torch.Generator(device=device).manual_seed(int(seed) + 15485863)
+    gate = 2.0 * torch.randn(M, K, generator=g, device=device, dtype=torch.float32)
+    up = activation(M, K, st, seed, device=device).float()
+    return torch.cat([gate, up], dim=1).to(torch.bfloat16)
 
 
 def random_perm(K: int, seed: int) -> np.ndarray:

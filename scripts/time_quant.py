@@ -14,16 +14,25 @@ ap.add_argument("--M", type=int, default=8192)
 ap.add_argument("--S", type=int, default=128)
 ap.add_argument("--iters", type=int, default=20)
 ap.add_argument("--norm", action="store_true", help="time arc_rmsnorm_quantize_activation (fused RMSNorm)")
+ap.add_argument("--silu", action="store_true", help="time arc_silu_mul_quantize_activation (fused SiLU-mul)")
+ap.add_argument("--pairs", action="store_true", help="with --silu: gate/up as adjacent pairs (ARC_GU_PAIRS)")
 args = ap.parse_args()
 K, M, S = args.K, args.M, args.S
 st = synth.Structure(K, S, seed=0)
 prof = A.calibrate([synth.activation(1024, K, st, seed=1000, device="cuda")], s_override=S)
 nrot = max(2, int(4 * 126e6 // (M * K * 2)) + 1)
-xs = [synth.activation(M, K, st, seed=i, device="cuda") for i in range(nrot)]
+if args.silu:
+    nrot = max(2, int(4 * 126e6 // (M * K * 4)) + 1)
+    xs = [synth.gate_up(M, K, st, seed=i, device="cuda") for i in range(nrot)]
+else:
+    xs = [synth.activation(M, K, st, seed=i, device="cuda") for i in range(nrot)]
 gamma = synth.rmsnorm_weight(K, seed=0, device="cuda")
 if args.norm:
     def quant(x, prof, codes=None, sf=None):
         return A.rmsnorm_quantize_activation(x, gamma, 1e-5, prof, codes, sf)
+elif args.silu:
+    def quant(x, prof, codes=None, sf=None):
+        return A.silu_mul_quantize_activation(x, prof, up_off=A.GU_PAIRS if args.pairs else None, codes=codes, sf=sf)
 else:
     quant = A.quantize_activation
 codes, sf = quant(xs[0], prof)
@@ -49,9 +58,9 @@ for it in range(max(3, args.iters // nrot)):
     ts.append(e0.elapsed_time(e1) / nrot)
 ts.sort()
 Kp = codes.shape[1] * 2
-byts = M * (2 * K + Kp // 2 + Kp // 16)
+byts = M * ((4 if args.silu else 2) * K + Kp // 2 + Kp // 16)
 med = ts[len(ts) // 2]
-print(f"{'rmsnorm+quant' if args.norm else 'quant'} K={K} M={M} S={S}: median {med*1e3:.1f} us  {byts/med/1e6:.0f} GB/s  (min {ts[0]*1e3:.1f} us)")
+print(f"{'rmsnorm+quant' if args.norm else 'silu+quant' if args.silu else 'quant'} K={K} M={M} S={S}: median {med*1e3:.1f} us  {byts/med/1e6:.0f} GB/s  (min {ts[0]*1e3:.1f} us)")
 
 # reference: plain torch streaming kernels on the same rotated buffers
 def _t(fn):

@@ -1,0 +1,141 @@
+"""GPU parity of the SiLU-mul producer of the down-projection input site (Fig.5 P:157;
+SiLU op sequence = DESIGN.md reading Q24):
+
+* arc_silu_mul is bit-exact against the oracle's silu_mul for EVERY finite bf16 gate value
+  (all 2^16 patterns, each against several up values) and on the synthetic gate_up recipe;
+* arc_silu_mul_quantize_activation (SiLU-mul + reorder + primary + residual NVFP4 in one pass)
+  is bit-exact against the oracle's quantize_activation of the oracle's silu_mul, in both
+  layouts, across the ring configurations (R = 4 / 2 / 1 rows per tile, 28 primary warps, the
+  two-blocks-per-lane variant) and with a gate_up buffer whose up half sits at an offset;
+* it equals the unfused GPU chain arc_quantize_activation(arc_silu_mul(gu)) bit for bit;
+* arc_linear_silu_mul is within the GEMM tolerance of the oracle's exact GEMM."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2601_07475_b200 import synth
+from _helpers import dev_bits, valid_sf_mask
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def A():
+    from paper_2601_07475_b200 import arc
+    assert arc.device_supported()
+    return arc
+
+
+def _kp(K, S):
+    return (K + S + 63) // 64 * 64
+
+
+def test_silu_mul_every_bf16_gate(A):
+    b = np.arange(65536, dtype=np.uint32).astype(np.uint16)
+    g = b[((b >> 7) & 0xFF) != 0xFF]                      # finite bf16 patterns
+    n = g.size
+    K = 512
+    rows = (n + K - 1) // K
+    gate = np.zeros(rows * K, np.uint16)
+    gate[:n] = g
+    gen = torch.Generator().manual_seed(1)
+    for trial in range(3):
+        up = (torch.randn(rows, K, generator=gen) * (4.0 ** trial)).to(torch.bfloat16)
+        gu_bits = np.concatenate([gate.reshape(rows, K), dev_bits(up)], axis=1)
+        gu = torch.from_numpy(gu_bits.astype(np.int16)).view(torch.bfloat16).cuda()
+        h = A.silu_mul(gu)
+        torch.cuda.synchronize()
+        assert np.array_equal(dev_bits(h), oracle.silu_mul(gu_bits))
+
+
+@pytest.mark.parametrize("M,K", [(1, 16), (37, 256), (64, 4096), (9, 14336)])
+def test_silu_mul_recipe(A, M, K):
+    st = synth.Structure(K, 16, seed=K)
+    gu = synth.gate_up(M, K, st, seed=M + K, device="cuda")
+    h = A.silu_mul(gu)
+    torch.cuda.synchronize()
+    assert np.array_equal(dev_bits(h), oracle.silu_mul(dev_bits(gu)))
+
+
+# K = 256 (R = 4), 4096 (R = 2), 8192 (R = 2, 32 KB rows), 14336 (R = 1, 28 primary warps),
+# 16384 (two blocks per primary lane), ragged M / K
+@pytest.mark.parametrize("M,K,S", [(16, 256, 16), (300, 4096, 128), (70, 8192, 64), (77, 14336, 128),
+                                   (12, 16384, 256), (130, 1024, 0), (5, 112, 48)])
+@pytest.mark.parametrize("layout", [0, 1])
+@pytest.mark.parametrize("pairs", [False, True])
+def test_silu_mul_quantize_bit_exact(A, M, K, S, layout, pairs):
+    st = synth.Structure(K, max(S, 16), seed=K + S)
+    gu = synth.gate_up(M, K, st, seed=M * 3 + K + layout, device="cuda")
+    cal = A.silu_mul(synth.gate_up(256, K, st, seed=99, device="cuda"))
+    prof = A.calibrate([cal], s_override=S, layout=layout)
+    if pairs:  # the same gate/up values as (g_j, u_j) adjacent pairs
+        gp = torch.stack([gu[:, :K], gu[:, K:]], dim=2).reshape(M, 2 * K).contiguous()
+        codes, sf = A.silu_mul_quantize_activation(gp, prof, up_off=A.GU_PAIRS)
+        assert torch.equal(A.silu_mul(gp, up_off=A.GU_PAIRS), A.silu_mul(gu))
+    else:
+        codes, sf = A.silu_mul_quantize_activation(gu, prof)
+    c2, s2 = A.quantize_activation(A.silu_mul(gu), prof)
+    torch.cuda.synchronize()
+    h_or = oracle.silu_mul(dev_bits(gu))
+    oc, osf = oracle.quantize_activation(h_or, prof.perm.cpu().numpy(), S, float(prof.gs.item()), layout)
+    mask = valid_sf_mask(M, _kp(K, S))
+    assert np.array_equal(codes.cpu().numpy(), oc), "fused SiLU-mul+quantize codes differ from the oracle"
+    assert np.array_equal(sf.cpu().numpy()[mask], osf[mask]), "fused SiLU-mul+quantize scales differ"
+    mt = torch.from_numpy(mask).cuda()
+    assert torch.equal(codes, c2) and torch.equal(sf.view(-1)[mt], s2.view(-1)[mt])
+
+
+def test_silu_mul_quantize_offset_up(A):
+    """gate in columns [0, K), 64 pad columns, up in [K + 64, 2K + 64); row stride 2K + 128."""
+    M, K, S = 50, 2048, 64
+    st = synth.Structure(K, 64, seed=4)
+    base = synth.gate_up(M, K, st, seed=8, device="cuda")
+    buf = torch.zeros(M, 2 * K + 128, dtype=torch.bfloat16, device="cuda")
+    buf[:, :K] = base[:, :K]
+    buf[:, K + 64:2 * K + 64] = base[:, K:]
+    prof = A.calibrate([A.silu_mul(synth.gate_up(128, K, st, seed=3, device="cuda"))], s_override=S)
+    codes, sf = A.silu_mul_quantize_activation(buf, prof, up_off=K + 64)
+    torch.cuda.synchronize()
+    oc, osf = oracle.quantize_activation(oracle.silu_mul(dev_bits(buf), K=K, up_off=K + 64),
+                                         prof.perm.cpu().numpy(), S, float(prof.gs.item()))
+    assert np.array_equal(codes.cpu().numpy(), oc)
+    mask = valid_sf_mask(M, _kp(K, S))
+    assert np.array_equal(sf.cpu().numpy()[mask], osf[mask])
+
+
+def test_silu_mul_quantize_full_size_sampled_rows(A):
+    """The bench's down-proj input site at full prefill size (M = 8192, K = 14336, S = 128),
+    bit-exact on sampled rows (the oracle runs row by row)."""
+    M, K, S = 8192, 14336, 128
+    st = synth.Structure(K, S, seed=21)
+    gu = synth.gate_up(M, K, st, seed=22, device="cuda")
+    prof = A.calibrate([A.silu_mul(synth.gate_up(1024, K, st, seed=23, device="cuda"))], s_override=S)
+    codes, sf = A.silu_mul_quantize_activation(gu, prof)
+    torch.cuda.synchronize()
+    rows = np.array([0, 1, 31, 32, 127, 128, 129, 4095, 5000, 8191])
+    oc, osf = oracle.quantize_activation(oracle.silu_mul(dev_bits(gu[torch.from_numpy(rows).cuda()])),
+                                         prof.perm.cpu().numpy(), S, float(prof.gs.item()))
+    assert np.array_equal(codes.cpu().numpy()[rows], oc)
+    Kp = _kp(K, S)
+    sfn = sf.cpu().numpy()
+    for i, m in enumerate(rows):
+        for c in range(Kp // 16):
+            assert sfn[oracle.sf_offset(int(m), c, Kp)] == osf[oracle.sf_offset(i, c, Kp)]
+
+
+@pytest.mark.parametrize("M,N,K,S", [(16, 256, 256, 16), (200, 600, 4096, 128), (16, 4096, 14336, 128)])
+def test_linear_silu_mul_parity(A, M, N, K, S):
+    st = synth.Structure(K, S, seed=N)
+    gu = synth.gate_up(M, K, st, seed=N + 2, device="cuda")
+    w = synth.weight(N, K, seed=N + 1, device="cuda")
+    prof = A.calibrate([A.silu_mul(synth.gate_up(256, K, st, seed=5, device="cuda"))], s_override=S)
+    qw = A.quantize_weight(w, prof)
+    y = A.linear_silu_mul(gu, prof, qw, out_dtype=torch.float32)
+    torch.cuda.synchronize()
+    perm, gs, gs_w = prof.perm.cpu().numpy(), float(prof.gs.item()), float(qw.gs.item())
+    ac, asf = oracle.quantize_activation(oracle.silu_mul(dev_bits(gu)), perm, S, gs)
+    bc, bsf = oracle.quantize_weight(dev_bits(w), perm, S, gs_w)
+    yref, bound = oracle.gemm_reference(ac, asf, bc, bsf, gs, gs_w)
+    err = np.abs(y.cpu().numpy().astype(np.float64) - yref)
+    assert (err <= bound).all(), f"worst err/bound {np.max(err / np.maximum(bound, 1e-300))}"
