@@ -234,6 +234,17 @@ ARC_API arc_status_t arc_linear_silu_mul(const void* gu, int64_t M, int64_t ld, 
 ARC_API arc_status_t arc_gemm(const uint8_t* a_codes, const uint8_t* a_sf, const float* gs_x, int64_t M,
                               const arc_qweight_t* qw, void* y, arc_dtype_t y_dtype, int64_t ldy, void* ws,
                               size_t ws_bytes, void* stream);
+/* arc_gemm with the SwiGLU activation in its epilogue (the MLP gate_up site, Fig.5):
+ * qw is the fused gate_up weight with its rows interleaved in groups of 16 -- rows 32j..32j+15
+ * are gate rows 16j..16j+15 and rows 32j+16..32j+31 the matching up rows (qw->N = 2I, I % 16
+ * == 0) -- and instead of the bf16 GEMM output the kernel stores
+ *   h[m][i] = bf16( bf16(SiLU(g)) * u ),  g = y[m][32(i/16) + i%16], u = y[m][32(i/16) + 16 + i%16],
+ * y the bf16 output arc_gemm would write (reading Q24 for SiLU), into h: bf16 [M][ldh],
+ * ldh >= N/2.  Bit-identical to arc_silu_mul applied to the de-interleaved arc_gemm output;
+ * the gate/up output never reaches HBM.  Workspace as arc_gemm (split-K at decode sizes). */
+ARC_API arc_status_t arc_gemm_swiglu(const uint8_t* a_codes, const uint8_t* a_sf, const float* gs_x, int64_t M,
+                                     const arc_qweight_t* qw, void* h, int64_t ldh, void* ws, size_t ws_bytes,
+                                     void* stream);
 /* The full ARC linear layer Y = X W^T computed as Eq.2: online activation
  * quantization feeding the augmented NVFP4 GEMM (two launches, PDL-chained).  x: bf16 [M][ldx]; y: [M][ldy] of
  * y_dtype.  ws: arc_linear_workspace_size(M, qw) bytes, 256-byte aligned, sync words zero

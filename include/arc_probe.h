@@ -21,6 +21,9 @@ ARC_API arc_status_t arc_probe_e2m1_bits(uint32_t start_bits, int64_t n, uint8_t
 ARC_API arc_status_t arc_probe_e2m1_raw_bits(uint32_t start_bits, int64_t n, uint8_t* out, void* stream);
 /* out[i] = the kernel's ceil-rounded E4M3 scale code of in[i] >= 0 (reading Q2). */
 ARC_API arc_status_t arc_probe_e4m3_ceil(const float* in, int64_t n, uint8_t* out, void* stream);
+/* out[i] = the bf16 pattern of bf16(SiLU(g[i])) as the fused SiLU-mul quantize kernel computes
+ * it (per-CTA table + closed-form tails, reading Q24), for bf16 patterns g[i]. */
+ARC_API arc_status_t arc_probe_silu(const uint16_t* g, int64_t n, uint16_t* out, void* stream);
 /* Timing experiments only: with env ARC_FUSED_TRACE set, the fused linear kernel records 8
  * globaltimer stamps per CTA of its last launch (entry, prologue, griddepcontrol.wait,
  * quantize phase, grid barrier, first full stage, last MMA, exit); copies up to max_ctas rows

@@ -81,6 +81,7 @@ _sig("arc_rmsnorm", [_P, _i64, _i64, _i64, _P, _f32, _P, _i64, _P])
 _sig("arc_rmsnorm_quantize_activation", [_P, _i64, _i64, _P, _f32, ctypes.POINTER(ArcProfile), _P, _P, _P])
 _sig("arc_linear_rmsnorm", [_P, _i64, _i64, _P, _f32, ctypes.POINTER(ArcProfile), ctypes.POINTER(ArcQWeight), _P,
                             ctypes.c_int, _i64, _P, ctypes.c_size_t, _P])
+_sig("arc_gemm_swiglu", [_P, _P, _P, _i64, ctypes.POINTER(ArcQWeight), _P, _i64, _P, ctypes.c_size_t, _P])
 _sig("arc_silu_mul", [_P, _i64, _i64, _i64, _i64, _P, _i64, _P])
 _sig("arc_silu_mul_quantize_activation", [_P, _i64, _i64, _i64, ctypes.POINTER(ArcProfile), _P, _P, _P])
 _sig("arc_linear_silu_mul", [_P, _i64, _i64, _i64, ctypes.POINTER(ArcProfile), ctypes.POINTER(ArcQWeight), _P,
@@ -93,6 +94,7 @@ _sig("arc_probe_e2m1", [_P, _i64, _P, _P])
 _sig("arc_probe_e2m1_bits", [ctypes.c_uint32, _i64, _P, _P])
 _sig("arc_probe_e2m1_raw_bits", [ctypes.c_uint32, _i64, _P, _P])
 _sig("arc_probe_e4m3_ceil", [_P, _i64, _P, _P])
+_sig("arc_probe_silu", [_P, _i64, _P, _P])
 
 # every symbol include/arc.h and include/arc_probe.h declare (checked by tests)
 EXPORTED = [
@@ -102,8 +104,8 @@ EXPORTED = [
     "arc_quantize_activation", "arc_gemm", "arc_linear", "arc_linear_ex", "arc_linear_ex_workspace_size",
     "arc_linear_fused_operand_offsets", "arc_linear_hostio_workspace_size", "arc_rmsnorm",
     "arc_rmsnorm_quantize_activation", "arc_linear_rmsnorm", "arc_linear_hostio",
-    "arc_silu_mul", "arc_silu_mul_quantize_activation", "arc_linear_silu_mul",
-    "arc_probe_e2m1", "arc_probe_e2m1_bits", "arc_probe_e2m1_raw_bits", "arc_probe_e4m3_ceil", "arc_debug_fused_trace",
+    "arc_silu_mul", "arc_silu_mul_quantize_activation", "arc_linear_silu_mul", "arc_gemm_swiglu",
+    "arc_probe_e2m1", "arc_probe_e2m1_bits", "arc_probe_e2m1_raw_bits", "arc_probe_e4m3_ceil", "arc_debug_fused_trace", "arc_probe_silu",
 ]
 
 
@@ -336,6 +338,39 @@ def gemm(a_codes, a_sf, gs_x: torch.Tensor, qw: QWeight, out_dtype=torch.bfloat1
     return out
 
 
+def gemm_swiglu(a_codes, a_sf, gs_x: torch.Tensor, qw: QWeight, out=None, ws: Workspace = None, stream=None):
+    """arc_gemm with the SwiGLU epilogue: qw = a gate_up weight prepared from interleave_gate_up(...);
+    out = h [M][N/2] bf16 = bf16(bf16(SiLU(g)) * u) of the bf16 GEMM output (Fig.5, reading Q24)."""
+    M = a_codes.shape[0]
+    if out is None:
+        out = torch.empty(M, qw.N // 2, dtype=torch.bfloat16, device=a_codes.device)
+    need = gemm_workspace_size(M, qw)
+    buf = None
+    if need:
+        if ws is None:
+            ws = _default_ws.setdefault(("gemm", a_codes.device), Workspace(a_codes.device))
+        buf = ws.get(need)
+    _check(_lib.arc_gemm_swiglu(_ptr(a_codes), _ptr(a_sf), _ptr(gs_x), M, ctypes.byref(qw.c()), _ptr(out),
+                                out.stride(0), _ptr(buf), 0 if buf is None else buf.numel(), _stream(stream)),
+           "arc_gemm_swiglu")
+    return out
+
+
+def interleave_gate_up(w_gate: torch.Tensor, w_up: torch.Tensor) -> torch.Tensor:
+    """Offline weight layout for arc_gemm_swiglu: gate/up rows interleaved in groups of 16
+    (rows 32j..32j+15 = gate rows 16j.., rows 32j+16..32j+31 = up rows 16j..).  Layout only."""
+    I, K = w_gate.shape
+    assert w_up.shape == (I, K) and I % 16 == 0
+    return torch.stack([w_gate.view(I // 16, 16, K), w_up.view(I // 16, 16, K)], dim=1).reshape(2 * I, K).contiguous()
+
+
+def deinterleave_gate_up(y: torch.Tensor) -> torch.Tensor:
+    """Columns of a GEMM output over interleave_gate_up weights back to [gate | up].  Layout only."""
+    M, N = y.shape
+    v = y.reshape(M, N // 32, 2, 16)
+    return torch.cat([v[:, :, 0, :].reshape(M, N // 2), v[:, :, 1, :].reshape(M, N // 2)], dim=1)
+
+
 LINEAR_MODES = {"auto": 0, "fused": 1, "unfused": 2}  # arc.h ARC_LINEAR_AUTO / _FUSED / _UNFUSED
 
 
@@ -512,4 +547,12 @@ def probe_e2m1_raw_bits(start: int, n: int, device="cuda") -> torch.Tensor:
 def probe_e4m3_ceil(x: torch.Tensor) -> torch.Tensor:
     out = torch.empty(x.numel(), dtype=torch.uint8, device=x.device)
     _check(_lib.arc_probe_e4m3_ceil(_ptr(x), x.numel(), _ptr(out), _stream()), "arc_probe_e4m3_ceil")
+    return out
+
+
+def probe_silu(g_bits: torch.Tensor) -> torch.Tensor:
+    """bf16 patterns of bf16(SiLU(g)) as the fused SiLU-mul quantize kernel computes them
+    (g_bits: int16/uint16-viewed bf16 patterns on the device)."""
+    out = torch.empty(g_bits.numel(), dtype=torch.int16, device=g_bits.device)
+    _check(_lib.arc_probe_silu(_ptr(g_bits), g_bits.numel(), _ptr(out), _stream()), "arc_probe_silu")
     return out

@@ -409,6 +409,42 @@ arc_status_t arc_gemm(const uint8_t* a_codes, const uint8_t* a_sf, const float* 
   return e == cudaSuccess ? ARC_OK : cuda_fail(e, "arc_gemm", detail);
 }
 
+arc_status_t arc_gemm_swiglu(const uint8_t* a_codes, const uint8_t* a_sf, const float* gs_x, int64_t M,
+                             const arc_qweight_t* qw, void* h, int64_t ldh, void* ws, size_t ws_bytes, void* stream) {
+  arc_status_t s = check_qweight(qw);
+  if (s != ARC_OK) return s;
+  if (M < 0 || M > (1 << 30)) return fail(ARC_ERR_SHAPE, "bad M");
+  if (qw->N % 32) return fail(ARC_ERR_SHAPE, "SwiGLU weight N must be a multiple of 32 (16-row gate/up groups)");
+  if (ldh < qw->N / 2 || ldh % 8) return fail(ARC_ERR_SHAPE, "ldh must be >= N/2 and a multiple of 8");
+  if (M == 0) return ARC_OK;
+  if (!a_codes || !a_sf || !gs_x || !h) return fail(ARC_ERR_NULL, "null a_codes / a_sf / gs_x / h");
+  if (!aligned16(a_codes) || !aligned16(a_sf) || !aligned16(h)) return fail(ARC_ERR_ALIGN, "buffer not 16B aligned");
+  const GemmPlan pl = plan_gemm(M, qw->N, qw->Kp);
+  if (pl.ws_bytes > 0 && (!ws || ws_bytes < pl.ws_bytes)) return fail(ARC_ERR_WORKSPACE, "split-K workspace too small");
+  if (ws && !aligned16(ws)) return fail(ARC_ERR_ALIGN, "ws not 16B aligned");
+  s = check_device();
+  if (s != ARC_OK) return s;
+  GemmProblem p;
+  p.M = M;
+  p.N = qw->N;
+  p.Kp = qw->Kp;
+  p.a_codes = a_codes;
+  p.a_sf = a_sf;
+  p.b_codes = qw->codes;
+  p.b_sf = qw->sf;
+  p.gs_x = gs_x;
+  p.gs_w = qw->gs;
+  p.y = h;
+  p.ldy = ldh;
+  p.y_fp32 = 0;
+  p.swiglu = 1;
+  p.ws = ws;
+  p.ws_bytes = ws_bytes;
+  const char* detail = nullptr;
+  cudaError_t e = launch_gemm(p, (cudaStream_t)stream, &detail);
+  return e == cudaSuccess ? ARC_OK : cuda_fail(e, "arc_gemm_swiglu", detail);
+}
+
 arc_status_t arc_linear_ex(const void* x, int64_t M, int64_t ldx, const arc_profile_t* prof, const arc_qweight_t* qw,
                            void* y, arc_dtype_t y_dtype, int64_t ldy, void* ws, size_t ws_bytes, int flags,
                            void* stream) {

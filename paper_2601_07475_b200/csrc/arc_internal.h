@@ -34,6 +34,7 @@ struct GemmProblem {
   void* y;
   int64_t ldy;
   int y_fp32;
+  int swiglu = 0;    // SwiGLU epilogue (gate/up rows interleaved in groups of 16): y = h [M][N/2] bf16
   void* ws;          // split-K partials (decode-size M), may be null when plan.ws_bytes == 0
   size_t ws_bytes;
 };

@@ -24,6 +24,7 @@
 // [192,448)) + SFA 16 + SFB 32; the epilogue of tile t overlaps the MMAs of t+1.
 #include "arc_device.cuh"
 #include "arc_internal.h"
+#include "quant_dev.cuh"
 
 #include <cuda.h>
 #include <cstdlib>
@@ -71,6 +72,7 @@ struct Args {
   int nsplit;   // split-K factor (decode-size M): > 1 -> fp32 partials into ws[nsplit][M][N]
   int kbs;      // K-blocks per split
   float* ws;
+  int swiglu;   // SwiGLU epilogue: y = h [M][N/2] bf16 from 16-row-interleaved gate/up weight rows
   int raster;   // tile order: 0 = M-tile groups fastest (the A panel stays in L2), 1 = N tiles fastest (B stays)
   int debug;  // perf experiments only (env ARC_GEMM_DEBUG): 1 = no epilogue work, 2 = no scale copies, 3 = no stores, 4 = no TMEM loads,
               // 5 = STG stores, 6 = no TMA store, 7 = MMA ignores the accumulator-free barriers,
@@ -147,6 +149,35 @@ __device__ __forceinline__ void epilogue_tile(const Args& args, const CUtensorMa
         for (int j = 0; j < 32; ++j)
           if (n0 + j < N) yr[j] = __fmul_rn(__uint_as_float(r[j]), alpha);
       }
+    }
+    if (args.swiglu && nsplit == 1 && mb * BM + q * 32 < M && n0 < N) {
+      // SwiGLU (Fig.5, reading Q24): chunk c holds gate channels 16(n0/32) + [0,16) in
+      // its first 16 columns and the matching up channels in the last 16 (weight rows
+      // interleaved offline in groups of 16).  g, u = bf16(alpha * acc) -- exactly the bf16
+      // GEMM output -- then h = bf16(bf16(SiLU(g)) * u); 32 rows x 16 h staged (32 B per row)
+      // and TMA-stored into h [M][N/2].
+      if (lane == 0) bulk_wait_read0();
+      __syncwarp();
+      uint32_t hw[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const __nv_bfloat162 g2 = __floats2bfloat162_rn(__fmul_rn(__uint_as_float(r[2 * i]), alpha),
+                                                        __fmul_rn(__uint_as_float(r[2 * i + 1]), alpha));
+        const __nv_bfloat162 u2 = __floats2bfloat162_rn(__fmul_rn(__uint_as_float(r[16 + 2 * i]), alpha),
+                                                        __fmul_rn(__uint_as_float(r[16 + 2 * i + 1]), alpha));
+        const __nv_bfloat162 h2 = __floats2bfloat162_rn(silu_mul1(__low2float(g2), __low2float(u2)),
+                                                        silu_mul1(__high2float(g2), __high2float(u2)));
+        hw[i] = *reinterpret_cast<const uint32_t*>(&h2);
+      }
+      *reinterpret_cast<uint4*>(st + lane * 32) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+      *reinterpret_cast<uint4*>(st + lane * 32 + 16) = make_uint4(hw[4], hw[5], hw[6], hw[7]);
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) {
+        tma_store_2d_hint(tmY, st, n0 / 2, mb * BM + q * 32, y_policy);
+        bulk_commit();
+      }
+      continue;
     }
     if (!args.y_fp32 && nsplit == 1 && mb * BM + q * 32 < M && n0 < N && args.debug != 3) {
       // bf16: stage the 32x32 sub-tile in smem (64B swizzle: 16-byte unit u of row
@@ -539,10 +570,27 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
 // Deterministic split-K reduction: y[m][n] = sum_ks ws[ks][m][n] in ks order.
 __global__ void arc_splitk_reduce_kernel(const float* __restrict__ ws, int nsplit, int M, int N, void* y,
-                                         int64_t ldy, int y_fp32) {
+                                         int64_t ldy, int y_fp32, int swiglu) {
   pdl_launch_dependents();
   pdl_wait();
   const int64_t total = (int64_t)M * N;
+  if (swiglu) {  // h[m][j] from gate column 32(j/16) + j%16 and up column +16 (see epilogue_tile)
+    const int NH = N / 2;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (int64_t)M * NH;
+         i += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t m = i / NH;
+      const int j = (int)(i - m * NH);
+      const int64_t ig = m * N + 32 * (j >> 4) + (j & 15), iu = ig + 16;
+      float g = ws[ig], u = ws[iu];
+      for (int k = 1; k < nsplit; ++k) {
+        g = __fadd_rn(g, ws[(int64_t)k * total + ig]);
+        u = __fadd_rn(u, ws[(int64_t)k * total + iu]);
+      }
+      static_cast<__nv_bfloat16*>(y)[m * ldy + j] = __float2bfloat16_rn(
+          silu_mul1(__bfloat162float(__float2bfloat16_rn(g)), __bfloat162float(__float2bfloat16_rn(u))));
+    }
+    return;
+  }
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     float acc = ws[i];
     for (int k = 1; k < nsplit; ++k) acc = __fadd_rn(acc, ws[(int64_t)k * total + i]);
@@ -590,15 +638,17 @@ bool make_sf_map(CUtensorMap* m, const uint8_t* sf, int64_t row_blocks, int64_t 
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-bool make_y_map(CUtensorMap* m, void* y, int64_t rows, int64_t cols, int64_t ldy) {
+// box_cols 32: 64B-swizzled 32x32 sub-tiles; 16: the SwiGLU epilogue's unswizzled 32 rows x 16 h
+bool make_y_map(CUtensorMap* m, void* y, int64_t rows, int64_t cols, int64_t ldy, int box_cols) {
   EncodeTiledFn enc = get_encode_fn();
   if (!enc) return false;
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)(ldy * 2)};
-  cuuint32_t box[2] = {32, 32};
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, 32};
   cuuint32_t estr[2] = {1, 1};
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, y, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-             CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+             box_cols == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 }  // namespace
@@ -694,7 +744,7 @@ cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t stream, const char** 
   }
   CUtensorMap tmA, tmB, tmY;
   memset(&tmY, 0, sizeof(tmY));
-  if (!p.y_fp32 && !make_y_map(&tmY, p.y, p.M, p.N, p.ldy)) {
+  if (p.swiglu ? !make_y_map(&tmY, p.y, p.M, p.N / 2, p.ldy, 16) : (!p.y_fp32 && !make_y_map(&tmY, p.y, p.M, p.N, p.ldy, 32))) {
     if (detail) *detail = "cuTensorMapEncodeTiled (Y) failed";
     return cudaErrorInvalidValue;
   }
@@ -733,6 +783,7 @@ cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t stream, const char** 
   a.y = p.y;
   a.ldy = p.ldy;
   a.y_fp32 = p.y_fp32;
+  a.swiglu = p.swiglu;
   static const int dbg = getenv("ARC_GEMM_DEBUG") ? atoi(getenv("ARC_GEMM_DEBUG")) : 0;
   a.debug = dbg;
   // Keep the smaller operand L2-resident: sweep the tiles along it fastest so each wave of
@@ -782,7 +833,7 @@ cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t stream, const char** 
     rc.attrs = ra;
     rc.numAttrs = 1;
     e = cudaLaunchKernelEx(&rc, arc_splitk_reduce_kernel, static_cast<const float*>(p.ws), (int)pl.nsplit, (int)p.M,
-                           (int)p.N, p.y, p.ldy, p.y_fp32);
+                           (int)p.N, p.y, p.ldy, p.y_fp32, p.swiglu);
     if (e != cudaSuccess) return e;
   }
   return cudaGetLastError();

@@ -22,9 +22,11 @@
 #include "arc_device.cuh"
 #include "arc_internal.h"
 #include "quant_dev.cuh"
+#include "arc_probe.h"
 
 #include <cuda_fp16.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 
@@ -52,7 +54,8 @@ struct QuantArgs {
   int32_t npw;     // primary warps
   int32_t nrw;     // residual warps
   int32_t bulk;    // producer uses one cp.async.bulk per row (else 16-byte cp.async per lane)
-  int32_t debug;   // perf experiments only (env ARC_QUANT_DEBUG): 1 = skip compute, 2 = skip loads,
+  int32_t debug;   // perf experiments only (env ARC_QUANT_DEBUG): 1 = skip compute, 2 = skip loads, 5 = SiLU mode
+                   // without table lookups, 6 = SiLU mode without the up gather,
                    // 3 = quantizing warps do not wait for the norm warps, 4 = norm warps skip the RMS
   const uint16_t* gamma;  // RMSNorm weight bf16[K] (norm mode)
   float eps;
@@ -135,9 +138,19 @@ ARC_DEV void silu_prod2(uint32_t s0, uint32_t s1, uint32_t w0, uint32_t w1, floa
 // channel); MODE 2: (g, u) adjacent bf16 pairs, one LDS.32 per channel (off = 4 * channel).
 // The block's 16 gate patterns are first checked against the table range (one branch per
 // block, rarely divergent).
+ARC_DEV void build_silu_table(uint16_t* tab, int tid, int nthreads) {
+  for (int c = tid; c < SILU_TAB; c += nthreads) {
+    const uint32_t gb = (((uint32_t)c & 2047u) + SILU_LO) | (((uint32_t)c & 2048u) << 4);
+    tab[c] = __bfloat16_as_ushort(__float2bfloat16_rn(silu_f32(__uint_as_float(gb << 16))));
+  }
+}
+
+// (Measured alternatives: a MUFU fast path -- ex2.approx + rcp.approx with a
+// midpoint-distance check falling back to the table -- is MUFU-bound and 40 % slower; a
+// (g, u)-pair layout with one LDS.32 per channel is no faster.)
 template <int MODE>
 ARC_DEV void silu_mul_block16(float (&z)[16], const uint8_t* row, const uint32_t (&off)[16], int upb,
-                              const uint16_t* tab) {
+                              const uint16_t* tab, int dbg = 0) {
 #pragma unroll
   for (int hb = 0; hb < 16; hb += 8) {  // two halves of 8 channels: 8 live (g, u) words
     uint32_t w[8];  // gate bits | up bits << 16
@@ -145,11 +158,15 @@ ARC_DEV void silu_mul_block16(float (&z)[16], const uint8_t* row, const uint32_t
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       if (MODE == 2) w[q] = *reinterpret_cast<const uint32_t*>(row + off[hb + q]);
+      else if (dbg == 6) w[q] = *reinterpret_cast<const uint16_t*>(row + off[hb + q]) | 0x3F800000u;
       else w[q] = *reinterpret_cast<const uint16_t*>(row + off[hb + q]) |
                   ((uint32_t)*reinterpret_cast<const uint16_t*>(row + upb + off[hb + q]) << 16);
       tmax = max(tmax, (w[q] & 0x7FFFu) - SILU_LO);
     }
-    if (tmax < SILU_N) {
+    if (dbg == 5) {
+#pragma unroll
+      for (int q = 0; q < 8; q += 2) silu_prod2(w[q] & 0xFFFFu, w[q + 1] & 0xFFFFu, w[q], w[q + 1], z[hb + q], z[hb + q + 1]);
+    } else if (tmax < SILU_N) {
 #pragma unroll
       for (int q = 0; q < 8; q += 2)
         silu_prod2(tab[((w[q] & 0x7FFFu) - SILU_LO) | ((w[q] >> 4) & 0x800u)],
@@ -253,11 +270,7 @@ __global__ void __launch_bounds__(1024) arc_quant_kernel(QuantArgs p) {
     c6tab[c] = __fdiv_rn(e4m3_value((uint32_t)c), 6.0f);
     if (c < 64) rat[c] = __fdiv_rn((float)(8 + (c >> 3)), (float)(8 + (c & 7)));
   }
-  if (SILU)
-    for (int c = tid; c < SILU_TAB; c += blockDim.x) {
-      const uint32_t gb = (((uint32_t)c & 2047u) + SILU_LO) | (((uint32_t)c & 2048u) << 4);
-      reinterpret_cast<uint16_t*>(gam)[c] = __bfloat16_as_ushort(__float2bfloat16_rn(silu_f32(__uint_as_float(gb << 16))));
-    }
+  if (SILU) build_silu_table(reinterpret_cast<uint16_t*>(gam), tid, blockDim.x);
   if (NORM)
     for (int c = tid; c < K; c += blockDim.x)
       reinterpret_cast<uint16_t*>(gam)[c] = __ldg(reinterpret_cast<const unsigned short*>(p.gamma) + __ldg(p.perm + c));
@@ -408,7 +421,7 @@ __global__ void __launch_bounds__(1024) arc_quant_kernel(QuantArgs p) {
                     if (kind[i] == 1) {
                       float z[16];
                       if (SILU) {
-                        silu_mul_block16<SILU>(z, smem + s * SLOT + r * ROWP, off[i], K * 2, stab);
+                        silu_mul_block16<SILU>(z, smem + s * SLOT + r * ROWP, off[i], K * 2, stab, p.debug);
                       } else {
                         gather16(smem + s * SLOT + r * ROWP, off[i], z);
                         if (NORM) norm16(z, gam + 32 * (tid + i * npw * 32), rscale[s * R + r]);
@@ -485,7 +498,7 @@ __global__ void __launch_bounds__(1024) arc_quant_kernel(QuantArgs p) {
               const int m = base + 32 * r;
               float z[16];
               if (SILU) {
-                silu_mul_block16<SILU>(z, smem + s * SLOT, off, K * 2, stab);
+                silu_mul_block16<SILU>(z, smem + s * SLOT, off, K * 2, stab, p.debug);
               } else {
                 gather16(smem + s * SLOT, off, z);
                 if (NORM) norm16(z, gam + 32 * jb, rscale[s * R + r]);
@@ -802,4 +815,40 @@ cudaError_t launch_tensor_scale(const void* x, int64_t rows, int K, int64_t ld, 
   return cudaGetLastError();
 }
 
+// Probe (include/arc_probe.h): the fused kernel's SiLU stage exactly as the quantizing warps
+// run it -- silu_mul_block16 over a staged 16-channel (gate, up = 1.0) row -- so tests can pin
+// bf16(SiLU(g)) of the fused path against the oracle for every bf16 pattern.
+__global__ void __launch_bounds__(128) probe_silu_block_kernel(const uint16_t* g, int64_t n, uint16_t* out) {
+  __shared__ __align__(16) uint16_t tab[SILU_TAB];
+  __shared__ __align__(16) uint8_t rows[128 * 64];
+  build_silu_table(tab, threadIdx.x, blockDim.x);
+  __syncthreads();
+  uint8_t* row = rows + threadIdx.x * 64;  // gate bf16[16] | up bf16[16]
+  uint32_t off[16];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) off[q] = 2u * q;
+  for (int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 16; b < n; b += (int64_t)gridDim.x * blockDim.x * 16) {
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      reinterpret_cast<uint16_t*>(row)[q] = b + q < n ? g[b + q] : 0;
+      reinterpret_cast<uint16_t*>(row)[16 + q] = 0x3F80;  // up = 1.0: h = bf16(SiLU(g))
+    }
+    float z[16];
+    silu_mul_block16<1>(z, row, off, 32, tab);
+#pragma unroll
+    for (int q = 0; q < 16; ++q)
+      if (b + q < n) out[b + q] = (uint16_t)(__float_as_uint(z[q]) >> 16);
+  }
+}
+
 }  // namespace arc
+
+extern "C" arc_status_t arc_probe_silu(const uint16_t* g, int64_t n, uint16_t* out, void* stream) {
+  if (!g || !out) return ARC_ERR_NULL;
+  if (n < 0) return ARC_ERR_SHAPE;
+  if (!arc_device_supported()) return ARC_ERR_UNSUPPORTED;
+  if (n == 0) return ARC_OK;
+  const int64_t blocks = std::min<int64_t>((n + 128 * 16 - 1) / (128 * 16), 1024);
+  arc::probe_silu_block_kernel<<<(unsigned)blocks, 128, 0, (cudaStream_t)stream>>>(g, n, out);
+  return cudaGetLastError() == cudaSuccess ? ARC_OK : ARC_ERR_CUDA;
+}

@@ -1,0 +1,180 @@
+"""Config 5 (BASELINE.json configs[4]): the linear chain of one LLaMA-3-8B decoder layer at
+batch x seq = 16 x 2048 (M = 32768 tokens), all four activation sites with their producers
+(Fig.5), timed as one CUDA graph per variant (CUDA events; inputs > 4x L2):
+
+  arc_fused    RMSNorm+quantize -> qkv GEMM | quantize -> o GEMM | RMSNorm+quantize -> gate_up
+               GEMM | SiLU-mul+quantize -> down GEMM        (S = 128 per site, producers fused)
+  arc_swiglu   as arc_fused, but SiLU-mul in the gate_up GEMM epilogue and a plain quantize of h
+  arc_unfused  the same with separate arc_rmsnorm / arc_silu_mul kernels (bf16 round trips in HBM)
+  nvfp4_s0     arc_fused with S = 0 (plain NVFP4, no residual channels; same kernels)
+  bf16_cublas  torch: rms_norm + matmul, matmul, rms_norm + matmul, silu * mul + matmul
+
+Attention itself, the residual adds and RoPE are outside the linear chain (not in the paper's
+method); the o-proj input is a synthetic activation.  Writes JSON to stdout."""
+import json
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2601_07475_b200 import arc as A, synth  # noqa: E402
+
+M = int(sys.argv[1]) if len(sys.argv) > 1 else 32768
+H, I, NQKV = 4096, 14336, 6144
+EPS = 1e-5
+
+
+def graph_time(fn, reps=3):
+    fn()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        fn()
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g, stream=s):
+            for _ in range(reps):
+                fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1) / reps)
+    return sorted(ts)[2] * 1e3  # us
+
+
+st_h = synth.Structure(H, 128, seed=1)
+st_i = synth.Structure(I, 128, seed=2)
+x = synth.activation(M, H, st_h, seed=3, device="cuda")        # residual stream into the layer
+attn = synth.activation(M, H, st_h, seed=4, device="cuda")     # attention output (o-proj input)
+x2 = synth.activation(M, H, st_h, seed=5, device="cuda")       # residual stream into the MLP
+g1 = synth.rmsnorm_weight(H, seed=6, device="cuda")
+g2 = synth.rmsnorm_weight(H, seed=7, device="cuda")
+w_qkv = synth.weight(NQKV, H, seed=8, device="cuda")
+w_o = synth.weight(H, H, seed=9, device="cuda")
+w_g = synth.weight(I, H, seed=10, device="cuda")
+w_u = synth.weight(I, H, seed=11, device="cuda")
+w_d = synth.weight(H, I, seed=12, device="cuda")
+w_gu = torch.cat([w_g, w_u])
+
+out = {"M_tokens": M, "shape": "LLaMA-3-8B layer: qkv 4096->6144, o 4096->4096, gate_up 4096->28672, down 14336->4096",
+       "us": {}}
+
+
+def arc_chain(S):
+    cal = 2048
+    p_qkv = A.calibrate([A.rmsnorm(synth.activation(cal, H, st_h, seed=20, device="cuda"), g1, EPS)], s_override=S)
+    p_o = A.calibrate([synth.activation(cal, H, st_h, seed=21, device="cuda")], s_override=S)
+    p_gu = A.calibrate([A.rmsnorm(synth.activation(cal, H, st_h, seed=22, device="cuda"), g2, EPS)], s_override=S)
+    p_d = A.calibrate([A.silu_mul(synth.gate_up(cal, I, st_i, seed=23, device="cuda"))], s_override=S)
+    q_qkv, q_o = A.quantize_weight(w_qkv, p_qkv), A.quantize_weight(w_o, p_o)
+    q_gu, q_d = A.quantize_weight(w_gu, p_gu), A.quantize_weight(w_d, p_d)
+    q_gui = A.quantize_weight(A.interleave_gate_up(w_g, w_u), p_gu)
+    bufs = {}
+
+    def act(name, prof, rows):
+        if name not in bufs:
+            bufs[name] = A.quantize_activation(torch.zeros(rows, prof.K, dtype=torch.bfloat16, device="cuda"), prof)
+        return bufs[name]
+
+    c1, s1 = act("qkv", p_qkv, M)
+    c2, s2 = act("o", p_o, M)
+    c3, s3 = act("gu", p_gu, M)
+    c4, s4 = act("d", p_d, M)
+    y_qkv = torch.empty(M, NQKV, dtype=torch.bfloat16, device="cuda")
+    y_o = torch.empty(M, H, dtype=torch.bfloat16, device="cuda")
+    gu = torch.empty(M, 2 * I, dtype=torch.bfloat16, device="cuda")
+    h = torch.empty(M, I, dtype=torch.bfloat16, device="cuda")
+    y_d = torch.empty(M, H, dtype=torch.bfloat16, device="cuda")
+    xn = torch.empty(M, H, dtype=torch.bfloat16, device="cuda")
+    ws = A.Workspace("cuda")
+
+    def fused():
+        A.rmsnorm_quantize_activation(x, g1, EPS, p_qkv, c1, s1)
+        A.gemm(c1, s1, p_qkv.gs, q_qkv, out=y_qkv, ws=ws)
+        A.quantize_activation(attn, p_o, c2, s2)
+        A.gemm(c2, s2, p_o.gs, q_o, out=y_o, ws=ws)
+        A.rmsnorm_quantize_activation(x2, g2, EPS, p_gu, c3, s3)
+        A.gemm(c3, s3, p_gu.gs, q_gu, out=gu, ws=ws)
+        A.silu_mul_quantize_activation(gu, p_d, codes=c4, sf=s4)
+        A.gemm(c4, s4, p_d.gs, q_d, out=y_d, ws=ws)
+
+    def swiglu():
+        A.rmsnorm_quantize_activation(x, g1, EPS, p_qkv, c1, s1)
+        A.gemm(c1, s1, p_qkv.gs, q_qkv, out=y_qkv, ws=ws)
+        A.quantize_activation(attn, p_o, c2, s2)
+        A.gemm(c2, s2, p_o.gs, q_o, out=y_o, ws=ws)
+        A.rmsnorm_quantize_activation(x2, g2, EPS, p_gu, c3, s3)
+        A.gemm_swiglu(c3, s3, p_gu.gs, q_gui, out=h, ws=ws)
+        A.quantize_activation(h, p_d, c4, s4)
+        A.gemm(c4, s4, p_d.gs, q_d, out=y_d, ws=ws)
+
+    def unfused():
+        A.rmsnorm(x, g1, EPS, out=xn)
+        A.quantize_activation(xn, p_qkv, c1, s1)
+        A.gemm(c1, s1, p_qkv.gs, q_qkv, out=y_qkv, ws=ws)
+        A.quantize_activation(attn, p_o, c2, s2)
+        A.gemm(c2, s2, p_o.gs, q_o, out=y_o, ws=ws)
+        A.rmsnorm(x2, g2, EPS, out=xn)
+        A.quantize_activation(xn, p_gu, c3, s3)
+        A.gemm(c3, s3, p_gu.gs, q_gu, out=gu, ws=ws)
+        A.silu_mul(gu, out=h)
+        A.quantize_activation(h, p_d, c4, s4)
+        A.gemm(c4, s4, p_d.gs, q_d, out=y_d, ws=ws)
+
+    parts = {
+        "rmsnorm_quant_qkv": lambda: A.rmsnorm_quantize_activation(x, g1, EPS, p_qkv, c1, s1),
+        "gemm_qkv": lambda: A.gemm(c1, s1, p_qkv.gs, q_qkv, out=y_qkv, ws=ws),
+        "quant_o": lambda: A.quantize_activation(attn, p_o, c2, s2),
+        "gemm_o": lambda: A.gemm(c2, s2, p_o.gs, q_o, out=y_o, ws=ws),
+        "rmsnorm_quant_gate_up": lambda: A.rmsnorm_quantize_activation(x2, g2, EPS, p_gu, c3, s3),
+        "gemm_gate_up": lambda: A.gemm(c3, s3, p_gu.gs, q_gu, out=gu, ws=ws),
+        "gemm_gate_up_swiglu": lambda: A.gemm_swiglu(c3, s3, p_gu.gs, q_gui, out=h, ws=ws),
+        "silu_mul_quant_down": lambda: A.silu_mul_quantize_activation(gu, p_d, codes=c4, sf=s4),
+        "quant_down_h": lambda: A.quantize_activation(h, p_d, c4, s4),
+        "gemm_down": lambda: A.gemm(c4, s4, p_d.gs, q_d, out=y_d, ws=ws),
+        "rmsnorm_alone": lambda: A.rmsnorm(x, g1, EPS, out=xn),
+        "silu_mul_alone": lambda: A.silu_mul(gu, out=h),
+    }
+    return fused, swiglu, unfused, parts
+
+
+fused, swiglu, unfused, parts = arc_chain(128)
+out["us"]["arc_fused"] = graph_time(fused)
+out["us"]["arc_swiglu_epilogue"] = graph_time(swiglu)
+out["us"]["arc_unfused"] = graph_time(unfused)
+out["arc_parts_us"] = {k: graph_time(f) for k, f in parts.items()}
+del fused, swiglu, unfused, parts
+torch.cuda.empty_cache()
+fused0, _, _, _ = arc_chain(0)
+out["us"]["nvfp4_s0_fused"] = graph_time(fused0)
+del fused0
+torch.cuda.empty_cache()
+
+xn = torch.empty(M, H, dtype=torch.bfloat16, device="cuda")
+y_qkv = torch.empty(M, NQKV, dtype=torch.bfloat16, device="cuda")
+y_o = torch.empty(M, H, dtype=torch.bfloat16, device="cuda")
+gu = torch.empty(M, 2 * I, dtype=torch.bfloat16, device="cuda")
+y_d = torch.empty(M, H, dtype=torch.bfloat16, device="cuda")
+
+
+def bf16_chain():
+    torch.matmul(torch.nn.functional.rms_norm(x, (H,), g1, EPS), w_qkv.t(), out=y_qkv)
+    torch.matmul(attn, w_o.t(), out=y_o)
+    torch.matmul(torch.nn.functional.rms_norm(x2, (H,), g2, EPS), w_gu.t(), out=gu)
+    torch.matmul(torch.nn.functional.silu(gu[:, :I]) * gu[:, I:], w_d.t(), out=y_d)
+
+
+out["us"]["bf16_cublas"] = graph_time(bf16_chain)
+flops = 2.0 * M * (H * NQKV + H * H + H * 2 * I + I * H)
+u = out["us"]
+out["tflops_effective"] = {k: flops / (v * 1e-6) / 1e12 for k, v in u.items()}
+out["arc_vs_nvfp4_overhead"] = u["arc_fused"] / u["nvfp4_s0_fused"] - 1.0
+out["arc_speedup_vs_bf16"] = u["bf16_cublas"] / min(u["arc_fused"], u["arc_swiglu_epilogue"])
+out["fusion_saving_vs_unfused"] = 1.0 - min(u["arc_fused"], u["arc_swiglu_epilogue"]) / u["arc_unfused"]
+print(json.dumps(out))
