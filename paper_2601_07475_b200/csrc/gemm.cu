@@ -92,7 +92,7 @@ template <bool PAIR>
 __device__ __forceinline__ void epilogue_tile(const Args& args, const CUtensorMap* tmY, uint32_t tmem, int b, int mb,
                                               int nbk, int ks, float alpha, uint64_t y_policy, uint8_t* st,
                                               uint64_t* ovl_free, uint64_t* buf_free, int warp, int lane,
-                                              uint32_t leader = 0) {
+                                              uint32_t leader = 0, const uint16_t* stab = nullptr) {
   const int q = warp & 3;  // TMEM lane quadrant this warp may access
   const int M = args.M, N = args.N, nsplit = args.nsplit;
   const int m = mb * BM + q * 32 + lane;
@@ -156,25 +156,66 @@ __device__ __forceinline__ void epilogue_tile(const Args& args, const CUtensorMa
       // interleaved offline in groups of 16).  g, u = bf16(alpha * acc) -- exactly the bf16
       // GEMM output -- then h = bf16(bf16(SiLU(g)) * u); 32 rows x 16 h staged (32 B per row)
       // and TMA-stored into h [M][N/2].
-      if (lane == 0) bulk_wait_read0();
+      // two 1 KB staging buffers per warp (alternating chunks): only the store issued two chunks
+      // ago must have finished reading its buffer
+      uint8_t* sth = st + (cc & 1) * 1024;
+      if (lane == 0) bulk_wait_read1();
       __syncwarp();
       uint32_t hw[8];
+      if (stab) {
+        // per-CTA SiLU table (the 2-SM kernel has the shared memory for it): all 16 gate
+        // patterns first, one range check, then 16 independent table loads (pipelined)
+        uint32_t gw[8], uw[8];
+        uint32_t tmax = 0;
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const __nv_bfloat162 g2 = __floats2bfloat162_rn(__fmul_rn(__uint_as_float(r[2 * i]), alpha),
-                                                        __fmul_rn(__uint_as_float(r[2 * i + 1]), alpha));
-        const __nv_bfloat162 u2 = __floats2bfloat162_rn(__fmul_rn(__uint_as_float(r[16 + 2 * i]), alpha),
-                                                        __fmul_rn(__uint_as_float(r[16 + 2 * i + 1]), alpha));
-        const __nv_bfloat162 h2 = __floats2bfloat162_rn(silu_mul1(__low2float(g2), __low2float(u2)),
-                                                        silu_mul1(__high2float(g2), __high2float(u2)));
-        hw[i] = *reinterpret_cast<const uint32_t*>(&h2);
+        for (int i = 0; i < 8; ++i) {
+          const __nv_bfloat162 g2 = __floats2bfloat162_rn(__fmul_rn(__uint_as_float(r[2 * i]), alpha),
+                                                          __fmul_rn(__uint_as_float(r[2 * i + 1]), alpha));
+          const __nv_bfloat162 u2 = __floats2bfloat162_rn(__fmul_rn(__uint_as_float(r[16 + 2 * i]), alpha),
+                                                          __fmul_rn(__uint_as_float(r[16 + 2 * i + 1]), alpha));
+          gw[i] = *reinterpret_cast<const uint32_t*>(&g2);
+          uw[i] = *reinterpret_cast<const uint32_t*>(&u2);
+          tmax = max(tmax, max((gw[i] & 0x7FFFu) - SILU_LO, ((gw[i] >> 16) & 0x7FFFu) - SILU_LO));
+        }
+        uint32_t sb[16];
+        if (tmax < SILU_N) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            sb[2 * i] = stab[((gw[i] & 0x7FFFu) - SILU_LO) | ((gw[i] >> 4) & 0x800u)];
+            sb[2 * i + 1] = stab[(((gw[i] >> 16) & 0x7FFFu) - SILU_LO) | ((gw[i] >> 20) & 0x800u)];
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            sb[2 * i] = silu_bf16_bits(gw[i] & 0xFFFFu, stab);
+            sb[2 * i + 1] = silu_bf16_bits(gw[i] >> 16, stab);
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const __nv_bfloat162 h2 = __floats2bfloat162_rn(
+              __fmul_rn(__uint_as_float(sb[2 * i] << 16), __uint_as_float(uw[i] << 16)),
+              __fmul_rn(__uint_as_float(sb[2 * i + 1] << 16), __uint_as_float(uw[i] & 0xFFFF0000u)));
+          hw[i] = *reinterpret_cast<const uint32_t*>(&h2);
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const __nv_bfloat162 g2 = __floats2bfloat162_rn(__fmul_rn(__uint_as_float(r[2 * i]), alpha),
+                                                          __fmul_rn(__uint_as_float(r[2 * i + 1]), alpha));
+          const __nv_bfloat162 u2 = __floats2bfloat162_rn(__fmul_rn(__uint_as_float(r[16 + 2 * i]), alpha),
+                                                          __fmul_rn(__uint_as_float(r[16 + 2 * i + 1]), alpha));
+          const __nv_bfloat162 h2 = __floats2bfloat162_rn(silu_mul1(__low2float(g2), __low2float(u2)),
+                                                          silu_mul1(__high2float(g2), __high2float(u2)));
+          hw[i] = *reinterpret_cast<const uint32_t*>(&h2);
+        }
       }
-      *reinterpret_cast<uint4*>(st + lane * 32) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
-      *reinterpret_cast<uint4*>(st + lane * 32 + 16) = make_uint4(hw[4], hw[5], hw[6], hw[7]);
+      *reinterpret_cast<uint4*>(sth + lane * 32) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+      *reinterpret_cast<uint4*>(sth + lane * 32 + 16) = make_uint4(hw[4], hw[5], hw[6], hw[7]);
       fence_proxy_async();
       __syncwarp();
       if (lane == 0) {
-        tma_store_2d_hint(tmY, st, n0 / 2, mb * BM + q * 32, y_policy);
+        tma_store_2d_hint(tmY, sth, n0 / 2, mb * BM + q * 32, y_policy);
         bulk_commit();
       }
       continue;
@@ -403,6 +444,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 constexpr int P_B_BYTES = (BN / 2) * BKB;                                     // 16 KB
 constexpr int P_STAGE_BYTES = A_BYTES + P_B_BYTES + SFA_BYTES + SFB_BYTES;  // 38 KB
 constexpr int p_smem_bytes(int stages) { return stages * P_STAGE_BYTES + 4 * EPI_STAGE_BYTES + 1024 + 256; }
+constexpr int P_SILU_TAB_BYTES = SILU_TAB * 2;  // SwiGLU epilogue: bf16 SiLU table after the barriers
 constexpr uint32_t kIdescPair = (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(2 * BM >> 4) << 24);
 constexpr uint32_t kPeerBitMask = 0xFEFFFFFFu;  // shared::cluster address bit selecting the odd CTA of a pair
 
@@ -420,6 +462,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* ovl_free = tfull + 1;
   uint64_t* buf_free = ovl_free + 1;  // [2]
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(buf_free + 2);
+  uint16_t* stab = reinterpret_cast<uint16_t*>(reinterpret_cast<uint8_t*>(full) + 256);
+  if (args.swiglu) build_silu_table(stab, threadIdx.x, NUM_THREADS);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -554,7 +598,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       mbar_wait(tfull, t & 1);
       tc_fence_after();
       epilogue_tile<true>(args, &tmY, tmem, t & 1, mb, nbk, ks, alpha, y_policy,
-                          epi_stage + (warp - 2) * EPI_STAGE_BYTES, ovl_free, &buf_free[t & 1], warp, lane, leader);
+                          epi_stage + (warp - 2) * EPI_STAGE_BYTES, ovl_free, &buf_free[t & 1], warp, lane, leader,
+                          args.swiglu ? stab : nullptr);
     }
     if (lane == 0) bulk_wait_all();
   }
@@ -736,7 +781,11 @@ GemmPlan plan_gemm(int64_t M, int64_t N, int64_t Kp) {
 }
 
 cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t stream, const char** detail) {
-  const GemmPlan pl = plan_gemm(p.M, p.N, p.Kp);
+  GemmPlan pl = plan_gemm(p.M, p.N, p.Kp);
+  // SwiGLU epilogue: the 2-SM kernel leaves shared memory for the SiLU table (the 1-SM kernel's
+  // 4 x 54 KB ring does not), so prefill-size SwiGLU GEMMs run as CTA pairs
+  static const int env_swp = getenv("ARC_GEMM_SWIGLU_PAIR") ? atoi(getenv("ARC_GEMM_SWIGLU_PAIR")) : 1;
+  if (p.swiglu && env_swp && pl.CL == 2 && pl.nsplit == 1) pl.pair = 1;
   const int CL = pl.CL;
   if (pl.nsplit > 1 && (p.ws == nullptr || p.ws_bytes < pl.ws_bytes)) {
     if (detail) *detail = "split-K workspace too small";
@@ -765,7 +814,8 @@ cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t stream, const char** 
     if (attr_err == cudaSuccess)
       attr_err = cudaFuncSetAttribute(arc_gemm_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     if (attr_err == cudaSuccess)
-      attr_err = cudaFuncSetAttribute(arc_gemm_pair_kernel<2, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, p_smem_bytes(5));
+      attr_err = cudaFuncSetAttribute(arc_gemm_pair_kernel<2, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      p_smem_bytes(5) + P_SILU_TAB_BYTES);
     if (attr_err == cudaSuccess)
       attr_err = cudaFuncSetAttribute(arc_gemm_pair_kernel<4, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, p_smem_bytes(5));
     if (attr_err == cudaSuccess)
@@ -802,7 +852,7 @@ cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t stream, const char** 
   cfg.blockDim = dim3(NUM_THREADS);
   static const int env_st = getenv("ARC_GEMM_STAGES") ? atoi(getenv("ARC_GEMM_STAGES")) : 5;
   const bool st4 = pl.pair && CL == 2 && env_st == 4;  // experiment only
-  cfg.dynamicSmemBytes = pl.pair ? p_smem_bytes(st4 ? 4 : 5) : SMEM_BYTES;
+  cfg.dynamicSmemBytes = pl.pair ? p_smem_bytes(st4 ? 4 : 5) + (p.swiglu ? P_SILU_TAB_BYTES : 0) : SMEM_BYTES;
   cfg.stream = stream;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;

@@ -97,26 +97,6 @@ ARC_DEV void norm16(float (&z)[16], const uint8_t* gblk, float r) {
   }
 }
 
-// SiLU (reading Q24) of a bf16 gate pattern gb -> bf16 pattern of bf16(SiLU(g)).  Patterns with
-// |g| in [2^-9, 128) -- magnitude bits [SILU_LO, SILU_LO + SILU_N) -- read a per-CTA table at
-// index (mag - SILU_LO) | (sign << 11), built with silu_f32 itself; the rest follow from the
-// pinned sequence in closed form (checked against the oracle over all 2^16 patterns):
-//   |g| < 2^-125 (exponent field 0 or 1): E = 1, d = 2, s = g/2 exactly, bf16 ties to even;
-//   2^-125 <= |g| < 2^-9: bf16(SiLU(g)) = g/2 (exponent - 1);
-//   g >= 128: g;  g <= -128: -0.
-constexpr uint32_t SILU_LO = 0x3B00u, SILU_N = 0x800u;
-constexpr int SILU_TAB = 4096;
-
-ARC_DEV uint32_t silu_bf16_bits(uint32_t gb, const uint16_t* tab) {
-  const uint32_t mag = gb & 0x7FFFu;
-  const uint32_t t = mag - SILU_LO;
-  if (t < SILU_N) return tab[t | ((gb >> 4) & 0x800u)];
-  const uint32_t neg = gb & 0x8000u;
-  if (mag < 0x100u) return ((mag + ((mag >> 1) & 1u)) >> 1) | neg;
-  if (mag < SILU_LO) return (mag - 0x80u) | neg;
-  return neg ? 0x8000u : mag;
-}
-
 // h = bf16(s * u) for two (SiLU bits, up-in-high-half word) pairs: one mul.rn.f32x2 + one
 // cvt.rn.bf16x2.f32 (s * u of two bf16 values is exact in fp32 unless it underflows, where the
 // fp32 rounding happens exactly as in the oracle's fp32 multiply)
@@ -138,13 +118,6 @@ ARC_DEV void silu_prod2(uint32_t s0, uint32_t s1, uint32_t w0, uint32_t w1, floa
 // channel); MODE 2: (g, u) adjacent bf16 pairs, one LDS.32 per channel (off = 4 * channel).
 // The block's 16 gate patterns are first checked against the table range (one branch per
 // block, rarely divergent).
-ARC_DEV void build_silu_table(uint16_t* tab, int tid, int nthreads) {
-  for (int c = tid; c < SILU_TAB; c += nthreads) {
-    const uint32_t gb = (((uint32_t)c & 2047u) + SILU_LO) | (((uint32_t)c & 2048u) << 4);
-    tab[c] = __bfloat16_as_ushort(__float2bfloat16_rn(silu_f32(__uint_as_float(gb << 16))));
-  }
-}
-
 // (Measured alternatives: a MUFU fast path -- ex2.approx + rcp.approx with a
 // midpoint-distance check falling back to the table -- is MUFU-bound and 40 % slower; a
 // (g, u)-pair layout with one LDS.32 per channel is no faster.)
