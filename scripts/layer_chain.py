@@ -25,7 +25,7 @@ H, I, NQKV = 4096, 14336, 6144
 EPS = 1e-5
 
 
-def graph_time(fn, reps=3):
+def make_graph(fn, reps=3):
     fn()
     torch.cuda.synchronize()
     g = torch.cuda.CUDAGraph()
@@ -37,15 +37,27 @@ def graph_time(fn, reps=3):
             for _ in range(reps):
                 fn()
     torch.cuda.synchronize()
-    ts = []
-    for _ in range(5):
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        g.replay()
-        e1.record()
-        torch.cuda.synchronize()
-        ts.append(e0.elapsed_time(e1) / reps)
-    return sorted(ts)[2] * 1e3  # us
+    return g, reps
+
+
+def graph_times(fns: dict, rounds=7):
+    """Median per-call time (us) of each variant, replayed round-robin so that clock / power drift over
+    the run affects every variant alike."""
+    graphs = {k: make_graph(f) for k, f in fns.items()}
+    ts = {k: [] for k in fns}
+    for _ in range(rounds):
+        for k, (g, reps) in graphs.items():
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            g.replay()
+            e1.record()
+            torch.cuda.synchronize()
+            ts[k].append(e0.elapsed_time(e1) / reps)
+    return {k: sorted(v)[len(v) // 2] * 1e3 for k, v in ts.items()}
+
+
+def graph_time(fn, reps=3):
+    return graph_times({"x": fn})["x"]
 
 
 st_h = synth.Structure(H, 128, seed=1)
@@ -145,10 +157,8 @@ def arc_chain(S):
 
 
 fused, swiglu, unfused, parts = arc_chain(128)
-out["us"]["arc_fused"] = graph_time(fused)
-out["us"]["arc_swiglu_epilogue"] = graph_time(swiglu)
-out["us"]["arc_unfused"] = graph_time(unfused)
-out["arc_parts_us"] = {k: graph_time(f) for k, f in parts.items()}
+out["us"].update(graph_times({"arc_fused": fused, "arc_swiglu_epilogue": swiglu, "arc_unfused": unfused}))
+out["arc_parts_us"] = graph_times(parts)
 del fused, swiglu, unfused, parts
 torch.cuda.empty_cache()
 fused0, _, _, _ = arc_chain(0)
