@@ -17,6 +17,16 @@ ARC linear:
   (NCCL over NVLink/NVSwitch on GPUs).  Per-rank block groupings differ from the
   unsharded layer, so the result equals sum_r linear_r, not the 1-GPU layer.
 
+* SequenceParallelColumnLinear: the Megatron sequence-parallel layout.
+  The previous row-parallel layer reduce-scatters its output over tokens (RowParallelLinear
+  with reduce="scatter"), so each rank holds M/P rows of the residual stream; the next
+  column-parallel layer quantizes only ITS rows (optionally with the fused RMSNorm)
+  and all-gathers the packed NVFP4 codes + block scales -- Kp/2 + Kp/16 bytes per row
+  instead of 2K for a bf16 all-gather (0.28x at K = 4096) -- then runs its N-shard GEMM over
+  all M rows.  The redundant per-rank quantize of the replicated input disappears.  The
+  gathered codes are bit-identical to quantizing the full activation (quantization is
+  per row), so the outputs equal the column-parallel layer's.
+
 The compute backend is the ctypes binding of libarc.so by default; tests inject a
 CPU backend to exercise this host logic with the gloo backend on CPU.
 """
@@ -40,6 +50,34 @@ def shard_range(total: int, rank: int, world: int, align: int = 16):
 def _default_backend():
     from paper_2601_07475_b200 import arc  # fails loudly if libarc.so is missing
     return arc
+
+
+def _all_gather_rows(t: torch.Tensor, group=None) -> torch.Tensor:
+    """Every rank's t concatenated along dim 0 in rank order (NCCL all_gather_into_tensor on GPUs)."""
+    world = dist.get_world_size(group)
+    t = t.contiguous()
+    out = torch.empty((world * t.shape[0],) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+    if t.is_cuda:
+        dist.all_gather_into_tensor(out, t, group=group)
+    else:  # gloo
+        dist.all_gather(list(out.chunk(world)), t, group=group)
+    return out
+
+
+def _reduce_scatter_rows(y: torch.Tensor, group=None) -> torch.Tensor:
+    """Sum over ranks, rank r keeps rows [r M/P, (r+1) M/P) (NCCL reduce_scatter_tensor on GPUs)."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    m = y.shape[0]
+    if m % world:
+        raise ValueError(f"M = {m} not divisible by {world} ranks")
+    if y.is_cuda:
+        out = torch.empty((m // world,) + tuple(y.shape[1:]), dtype=y.dtype, device=y.device)
+        dist.reduce_scatter_tensor(out, y.contiguous(), op=dist.ReduceOp.SUM, group=group)
+        return out
+    y = y.clone()  # gloo has no reduce-scatter: all-reduce, keep this rank's rows
+    dist.all_reduce(y, op=dist.ReduceOp.SUM, group=group)
+    return y[rank * (m // world):(rank + 1) * (m // world)].contiguous()
 
 
 @dataclass
@@ -80,9 +118,46 @@ class RowParallelLinear:
                                               layout=layout)
         self.qweight = self.backend.quantize_weight(weight_full[:, lo:hi].contiguous(), self.profile)
 
-    def forward(self, x_shard: torch.Tensor, out_dtype=torch.float32, reduce: bool = True) -> torch.Tensor:
-        """x_shard: this rank's [M, K/P] slice of the activation."""
+    def forward(self, x_shard: torch.Tensor, out_dtype=torch.float32, reduce="all") -> torch.Tensor:
+        """x_shard: this rank's [M, K/P] slice of the activation.  reduce: "all" (all-reduce, every rank
+        gets Y), "scatter" (reduce-scatter over tokens, rank r gets rows [r M/P, (r+1) M/P): the
+        sequence-parallel layout) or None (the partial Y_r)."""
         y = self.backend.linear(x_shard, self.profile, self.qweight, out_dtype=out_dtype)
-        if reduce and self.shard.world > 1:
-            dist.all_reduce(y, op=dist.ReduceOp.SUM, group=self.group)
+        if reduce is True or reduce == "all":
+            if self.shard.world > 1 or self.group is not None:
+                dist.all_reduce(y, op=dist.ReduceOp.SUM, group=self.group)
+        elif reduce == "scatter":
+            y = _reduce_scatter_rows(y, self.group)
         return y
+
+
+class SequenceParallelColumnLinear:
+    """Column-parallel ARC linear fed from M/P token rows per rank: quantize the local rows (optionally
+    RMSNorm-fused), all-gather the packed codes + block scales, GEMM over all M rows for this N shard."""
+
+    def __init__(self, weight_full: torch.Tensor, profile, rank: int, world: int, backend=None, group=None):
+        self.backend = backend or _default_backend()
+        N = weight_full.shape[0]
+        lo, hi = shard_range(N, rank, world, align=8)
+        self.shard = ShardInfo(rank, world, lo, hi)
+        self.group = group
+        self.profile = profile
+        self.qweight = self.backend.quantize_weight(weight_full[lo:hi].contiguous(), profile)
+
+    def gather_quantized(self, x_rows: torch.Tensor, gamma=None, eps: float = 1e-5):
+        """(codes [M][Kp/2], scales) of all ranks' rows: each rank quantizes its M/P rows; the 128x4 scale
+        tiles of 128-row blocks concatenate, so M/P must be a multiple of 128."""
+        m_loc = x_rows.shape[0]
+        if m_loc % 128:
+            raise ValueError(f"sequence-parallel rows per rank ({m_loc}) must be a multiple of 128")
+        if gamma is not None:
+            codes, sf = self.backend.rmsnorm_quantize_activation(x_rows, gamma, eps, self.profile)
+        else:
+            codes, sf = self.backend.quantize_activation(x_rows, self.profile)
+        codes_all = _all_gather_rows(codes, self.group)
+        sf_all = _all_gather_rows(sf.reshape(m_loc // 128, -1), self.group).reshape(-1)
+        return codes_all, sf_all
+
+    def forward(self, x_rows: torch.Tensor, gamma=None, eps: float = 1e-5, out_dtype=torch.bfloat16):
+        codes, sf = self.gather_quantized(x_rows, gamma, eps)
+        return self.backend.gemm(codes, sf, self.profile.gs, self.qweight, out_dtype=out_dtype)

@@ -42,6 +42,19 @@ class OracleBackend:
         y, _ = oracle.gemm_reference(ac, asf, qw.codes, qw.sf, prof.gs, qw.gs)
         return torch.from_numpy(y).to(out_dtype)
 
+    def quantize_activation(self, x, prof):
+        ac, asf = oracle.quantize_activation(oracle.as_bf16_bits(x), prof.perm, prof.S, prof.gs, prof.layout)
+        return torch.from_numpy(ac), torch.from_numpy(asf)
+
+    def rmsnorm_quantize_activation(self, x, gamma, eps, prof):
+        y = oracle.rmsnorm(oracle.as_bf16_bits(x), oracle.as_bf16_bits(gamma), eps)
+        ac, asf = oracle.quantize_activation(y, prof.perm, prof.S, prof.gs, prof.layout)
+        return torch.from_numpy(ac), torch.from_numpy(asf)
+
+    def gemm(self, codes, sf, gs, qw, out_dtype=torch.float32):
+        y, _ = oracle.gemm_reference(codes.numpy(), sf.numpy(), qw.codes, qw.sf, gs, qw.gs)
+        return torch.from_numpy(y).to(out_dtype)
+
     def linear_bound(self, x, prof, qw):
         ac, asf = oracle.quantize_activation(oracle.as_bf16_bits(x), prof.perm, prof.S, prof.gs, prof.layout)
         return oracle.gemm_reference(ac, asf, qw.codes, qw.sf, prof.gs, qw.gs)

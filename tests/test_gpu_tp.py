@@ -53,3 +53,31 @@ def test_tp_layers_world1_nccl(pg):
         bc, bsf = oracle.quantize_weight(dev_bits(w), perm, p.S, gs_w)
         yref, bound = oracle.gemm_reference(ac, asf, bc, bsf, gs, gs_w)
         assert np.all(np.abs(y.cpu().numpy().astype(np.float64) - yref) <= bound)
+
+
+def test_sequence_parallel_world1_nccl(pg):
+    """SURVEY f2 path on the GPU (NCCL all_gather_into_tensor / reduce_scatter_tensor at world 1):
+    the gathered codes and scales equal the direct quantization, the SP column output equals
+    arc.gemm on them, the RMSNorm-fused variant equals arc.linear_rmsnorm."""
+    from paper_2601_07475_b200 import arc, tp
+    M, K, N = 256, 1024, 512
+    st = synth.Structure(K, 32, seed=3)
+    x = synth.activation(M, K, st, seed=4, device="cuda")
+    cal = synth.activation(512, K, st, seed=1001, device="cuda")
+    w = synth.weight(N, K, seed=5, device="cuda")
+    gamma = synth.rmsnorm_weight(K, seed=6, device="cuda")
+    prof = arc.calibrate([cal])
+    sp = tp.SequenceParallelColumnLinear(w, prof, 0, 1, group=pg)
+    codes, sf = sp.gather_quantized(x)
+    c0, s0 = arc.quantize_activation(x, prof)
+    y = sp.forward(x, out_dtype=torch.float32)
+    y0 = arc.gemm(c0, s0, prof.gs, sp.qweight, out_dtype=torch.float32)
+    yn = sp.forward(x, gamma=gamma, eps=1e-5, out_dtype=torch.float32)
+    yn0 = arc.linear_rmsnorm(x, gamma, 1e-5, prof, sp.qweight, out_dtype=torch.float32)
+    row = tp.RowParallelLinear(w, cal, 0, 1, group=pg)
+    y_all = row.forward(x, out_dtype=torch.float32, reduce="all")
+    y_sc = row.forward(x, out_dtype=torch.float32, reduce="scatter")
+    torch.cuda.synchronize()
+    assert torch.equal(codes, c0) and torch.equal(sf, s0)
+    assert torch.equal(y, y0) and torch.equal(yn, yn0)
+    assert torch.equal(y_sc, y_all)

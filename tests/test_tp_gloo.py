@@ -100,3 +100,76 @@ def test_shard_range():
     assert tp.shard_range(4096, 3, 8) == (1536, 2048)
     with pytest.raises(ValueError):
         tp.shard_range(4096 + 16, 0, 8)
+
+
+# ----------------------------------------------------------------------------- sequence parallel (f2)
+MS = 256  # 128 token rows per rank at world 2
+
+
+def _sp_inputs():
+    from paper_2601_07475_b200 import synth
+    st = synth.Structure(K, S_INJ, seed=3)
+    x = synth.activation(MS, K, st, seed=4)
+    cal = synth.activation(256, K, st, seed=1001)
+    w = synth.weight(N, K, seed=5)
+    gamma = synth.rmsnorm_weight(K, seed=6)
+    return x, cal, w, gamma
+
+
+def _sp_worker(rank, world, port, outdir):
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, HERE)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2601_07475_b200 import tp
+    from _oracle_backend import OracleBackend
+    be = OracleBackend()
+    x, cal, w, gamma = _sp_inputs()
+    rows = slice(rank * MS // world, (rank + 1) * MS // world)
+    prof = be.calibrate([cal])
+    sp = tp.SequenceParallelColumnLinear(w, prof, rank, world, backend=be)
+    codes, sf = sp.gather_quantized(x[rows].contiguous())
+    y = sp.forward(x[rows].contiguous(), out_dtype=torch.float64)
+    yn = sp.forward(x[rows].contiguous(), gamma=gamma, eps=1e-5, out_dtype=torch.float64)
+    # row-parallel with the sequence-parallel reduce-scatter
+    row = tp.RowParallelLinear(w, cal, rank, world, backend=be)
+    xs = x[:, row.shard.lo:row.shard.hi].contiguous()
+    y_all = row.forward(xs, out_dtype=torch.float64, reduce="all")
+    y_sc = row.forward(xs, out_dtype=torch.float64, reduce="scatter")
+    for name, t in (("codes", codes), ("sf", sf), ("y", y), ("yn", yn), ("yall", y_all), ("ysc", y_sc)):
+        np.save(os.path.join(outdir, f"sp_{name}{rank}.npy"), t.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_sequence_parallel_world2_gloo():
+    """each rank quantizes its M/P token rows (plain or RMSNorm-fused) and all-gathers the
+    packed codes + scales: bit-identical to quantizing all M rows, so each rank's N-shard output equals
+    the oracle's column-parallel shard exactly; the reduce-scatter variant of the row-parallel layer
+    gives every rank its rows of the all-reduce result."""
+    sys.path.insert(0, HERE)
+    import oracle
+    from paper_2601_07475_b200 import tp
+    from _oracle_backend import OracleBackend
+    world = 2
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_sp_worker, args=(world, _free_port(), d), nprocs=world, join=True)
+        be = OracleBackend()
+        x, cal, w, gamma = _sp_inputs()
+        prof = be.calibrate([cal])
+        ac, asf = oracle.quantize_activation(oracle.as_bf16_bits(x), prof.perm, prof.S, prof.gs, prof.layout)
+        xn = oracle.rmsnorm(oracle.as_bf16_bits(x), oracle.as_bf16_bits(gamma), 1e-5)
+        nc, nsf = oracle.quantize_activation(xn, prof.perm, prof.S, prof.gs, prof.layout)
+        for r in range(world):
+            assert np.array_equal(np.load(os.path.join(d, f"sp_codes{r}.npy")), ac)
+            assert np.array_equal(np.load(os.path.join(d, f"sp_sf{r}.npy")).reshape(-1), asf.reshape(-1))
+            lo, hi = tp.shard_range(N, r, world, align=8)
+            qw = be.quantize_weight(w[lo:hi].contiguous(), prof)
+            ref, _ = oracle.gemm_reference(ac, asf, qw.codes, qw.sf, prof.gs, qw.gs)
+            assert np.array_equal(np.load(os.path.join(d, f"sp_y{r}.npy")), ref)
+            refn, _ = oracle.gemm_reference(nc, nsf, qw.codes, qw.sf, prof.gs, qw.gs)
+            assert np.array_equal(np.load(os.path.join(d, f"sp_yn{r}.npy")), refn)
+            y_all = np.load(os.path.join(d, f"sp_yall{r}.npy"))
+            y_sc = np.load(os.path.join(d, f"sp_ysc{r}.npy"))
+            assert np.array_equal(y_sc, y_all[r * MS // world:(r + 1) * MS // world])
