@@ -105,11 +105,15 @@ class Clocks:
 
 # ----------------------------------------------------------------------------- workload
 class Site:
-    def __init__(self, name, K, N, M, S, rank, world, mode, device, A):
+    def __init__(self, name, K, N, M, S, rank, world, mode, device, A, layout="mp"):
         """mode: 'full' (1 GPU), 'col' (column-parallel shard of N), 'row' (row-parallel shard of K).
-        Sharded sites are built with paper_2601_07475_b200.tp (the tested host logic)."""
+        Sharded sites are built with paper_2601_07475_b200.tp (the tested host logic).  layout 'sp'
+        (sequence parallel): a col site quantizes its M/P token rows and all-gathers the
+        packed codes + scales; a row site reduce-scatters its output over tokens.  'mp': a col site
+        quantizes the replicated M rows; a row site all-reduces."""
         from paper_2601_07475_b200 import tp
         self.name, self.M, self.mode = name, M, mode
+        self.sp = layout == "sp" and world > 1
         seed = zlib.crc32(name.encode()) % 1000
         st = synth.Structure(K, S, seed=seed * 31)
         cal = synth.activation(4096, K, st, seed=seed + 1000, device=device)
@@ -137,21 +141,31 @@ class Site:
         self.codes = torch.empty(M, Kp // 2, dtype=torch.uint8, device=device)
         self.sf = torch.empty(sb, dtype=torch.uint8, device=device)
         self.y = torch.empty(M, Nl, dtype=torch.bfloat16, device=device)
+        self.m_q = M  # rows this rank quantizes
+        if self.sp and mode == "col":
+            ml = M // world
+            assert ml % 128 == 0, "sequence-parallel rows per rank must be a multiple of 128"
+            self.x = self.x[rank * ml:(rank + 1) * ml].contiguous()
+            self.codes_loc = torch.empty(ml, Kp // 2, dtype=torch.uint8, device=device)
+            self.sf_loc = torch.empty(ml * Kp // 16, dtype=torch.uint8, device=device)
+            self.m_q = ml
+        if self.sp and mode == "row":
+            self.y_rs = torch.empty(M // world, Nl, dtype=torch.bfloat16, device=device)
         self.ws = A.Workspace(device)
         self.flops = 2.0 * M * Nl * (Kl + S_l)                       # SPEC S:322 cost model, algorithmic
         self.flops_eff = 2.0 * M * Nl * Kl
-        self.q_bytes = M * (2 * Kl + Kp // 2 + Kp // 16) + 4 * Kl     # bf16 read + codes + scales + perm
+        self.q_bytes = self.m_q * (2 * Kl + Kp // 2 + Kp // 16) + 4 * Kl  # bf16 read + codes + scales + perm
         self.g_bytes = Nl * Kp * 9 // 16 + M * Kp * 9 // 16 + M * Nl * 2
 
 
-def build_sites(A, M, rank, world, device):
+def build_sites(A, M, rank, world, device, layout="mp"):
     sites = []
     for name, K, N in SITES:
         if world == 1:
             mode = "full"
         else:
             mode = "col" if name in ("qkv", "gate_up") else "row"
-        sites.append(Site(name, K, N, M, S_AUG, rank, world, mode, device, A))
+        sites.append(Site(name, K, N, M, S_AUG, rank, world, mode, device, A, layout))
     return sites
 
 
@@ -159,14 +173,23 @@ def run_step(A, sites, ev=None, pg=None):
     for i, s in enumerate(sites):
         if ev is not None:
             ev[i][0].record()
-        A.quantize_activation(s.x, s.prof, s.codes, s.sf)
+        if s.sp and s.mode == "col":
+            # sequence parallel: quantize this rank's token rows, all-gather the packed codes + scales
+            A.quantize_activation(s.x, s.prof, s.codes_loc, s.sf_loc)
+            torch.distributed.all_gather_into_tensor(s.codes, s.codes_loc, group=pg)
+            torch.distributed.all_gather_into_tensor(s.sf, s.sf_loc, group=pg)
+        else:
+            A.quantize_activation(s.x, s.prof, s.codes, s.sf)
         if ev is not None:
             ev[i][1].record()
         A.gemm(s.codes, s.sf, s.prof.gs, s.qw, out=s.y, ws=s.ws)
         if ev is not None:
             ev[i][2].record()
         if s.mode == "row" and pg is not None:
-            torch.distributed.all_reduce(s.y, group=pg)
+            if s.sp:
+                torch.distributed.reduce_scatter_tensor(s.y_rs, s.y, group=pg)
+            else:
+                torch.distributed.all_reduce(s.y, group=pg)
 
 
 # ----------------------------------------------------------------------------- oracle (CPU) legs
@@ -222,6 +245,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-decode", action="store_true")
+    ap.add_argument("--tp-layout", default="mp", choices=["mp", "sp"],
+                    help="N>1: sequence-parallel (quantize M/P rows + all-gather packed codes, reduce-scatter) "
+                         "or plain Megatron (replicated quantize, all-reduce)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -241,7 +267,7 @@ def main():
     workload = "llama3-8b-layer-4-arc-linears-prefill"
     config = {"workload": workload, "M_tokens": args.M, "S": S_AUG,
               "sites": [f"{n}:K{k}xN{nn}" for n, k, nn in SITES],
-              "parallelism": "single" if world == 1 else f"tp{world}",
+              "parallelism": "single" if world == 1 else f"tp{world}-{args.tp_layout}",
               "l2": "per-step footprint > 4x L2 (no flush needed)"}
 
     if args.impl == "reference":
@@ -273,7 +299,7 @@ def main():
     from paper_2601_07475_b200 import arc as A
     if not A.device_supported():
         raise SystemExit("bench.py: current device is not sm_100 -- the ARC path has no fallback")
-    sites = build_sites(A, args.M, rank, world, device)
+    sites = build_sites(A, args.M, rank, world, device, args.tp_layout)
     torch.cuda.synchronize()
 
     for _ in range(args.warmup):
