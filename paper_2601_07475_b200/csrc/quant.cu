@@ -212,9 +212,10 @@ __global__ void __launch_bounds__(1024) arc_quant_kernel(QuantArgs p) {
   uint64_t* empty = full + ST;
   uint64_t* normed = empty + ST;  // norm mode: the RMS scales of slot s's rows are ready
   float* rscale = reinterpret_cast<float*>(normed + ST);  // [ST][R] 1/rms of each staged row
-  uint8_t* gam = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(rscale + ST * R) + 15) & ~uintptr_t(15));
+  // gam: addressed from `smem` (an integer offset) so every access stays an LDS/STS, not a generic access
+  uint8_t* gam = smem + ((reinterpret_cast<uint8_t*>(rscale + ST * R) - smem + 15) & ~15);
   // SiLU table at the same place, addressed from `smem` so loads stay in the shared window
-  const uint16_t* stab = reinterpret_cast<const uint16_t*>(smem + (gam - smem));
+  const uint16_t* stab = reinterpret_cast<const uint16_t*>(gam);
   // gam: gamma in reordered channel order, bf16[K], staged once per CTA (norm mode)
 
   const int tid = threadIdx.x;
@@ -244,9 +245,18 @@ __global__ void __launch_bounds__(1024) arc_quant_kernel(QuantArgs p) {
     if (c < 64) rat[c] = __fdiv_rn((float)(8 + (c >> 3)), (float)(8 + (c & 7)));
   }
   if (SILU) build_silu_table(reinterpret_cast<uint16_t*>(gam), tid, blockDim.x);
-  if (NORM)
-    for (int c = tid; c < K; c += blockDim.x)
-      reinterpret_cast<uint16_t*>(gam)[c] = __ldg(reinterpret_cast<const unsigned short*>(p.gamma) + __ldg(p.perm + c));
+  if (NORM) {
+    // gamma in reordered channel order: 8 channels per thread, the 8 perm words and then the 8 gamma
+    // gathers issued back to back (independent loads), one 16-byte shared store
+    const unsigned short* g16 = reinterpret_cast<const unsigned short*>(p.gamma);
+    for (int c8 = tid * 8; c8 < K; c8 += blockDim.x * 8) {
+      const int4 a = __ldg(reinterpret_cast<const int4*>(p.perm + c8));
+      const int4 b = __ldg(reinterpret_cast<const int4*>(p.perm + c8 + 4));
+      const uint32_t v0 = __ldg(g16 + a.x), v1 = __ldg(g16 + a.y), v2 = __ldg(g16 + a.z), v3 = __ldg(g16 + a.w);
+      const uint32_t v4 = __ldg(g16 + b.x), v5 = __ldg(g16 + b.y), v6 = __ldg(g16 + b.z), v7 = __ldg(g16 + b.w);
+      *reinterpret_cast<uint4*>(gam + 2 * c8) = make_uint4(v0 | (v1 << 16), v2 | (v3 << 16), v4 | (v5 << 16), v6 | (v7 << 16));
+    }
+  }
 
   __syncthreads();
 
