@@ -83,6 +83,10 @@ def lib():
         L.or_rmsnorm.argtypes = [P, i64, i32, i64, P, f32, P, i64]
         L.or_rmsnorm_scale.restype = f32
         L.or_rmsnorm_scale.argtypes = [P, i32, f32]
+        L.or_quantize_mx.restype = i32
+        L.or_quantize_mx.argtypes = [P, i64, i32, i64, P, i32, i32, i32, i32, P, P]
+        L.or_mx_offset.restype = i32
+        L.or_mx_offset.argtypes = [f32]
         L.or_silu_f32_n.restype = None
         L.or_silu_f32_n.argtypes = [P, i64, P]
         L.or_silu_mul.restype = i32
@@ -232,6 +236,28 @@ def quantize_weight(w_bits, perm, S: int, gs: float, layout: int = INTERLEAVED):
     sf = np.zeros(sf_rows_padded(N) * Kp // 16, np.uint8)
     perm = np.ascontiguousarray(perm, np.int32)
     _check(lib().or_quantize_weight(_p(w), N, K, K, _p(perm), S, gs, layout, _p(codes), _p(sf)))
+    return codes, sf
+
+
+# ----------------------------------------------------------------------------- MXFP4-ARC (f3)
+def mx_offset(amax: float) -> int:
+    """Tensor offset c (gs = 2^-c): the largest block scale E8M0_up(amax/6) maps to 2^8 (reading Q25)."""
+    return int(lib().or_mx_offset(np.float32(amax)))
+
+
+def quantize_mx(x_bits, perm, S: int, c: int, weight: bool = False, layout: int = INTERLEAVED):
+    """MXFP4-ARC (32-blocks, E8M0 scales; residual or, for weights, duplicated outlier blocks) in the
+    NVFP4 physical format with E4M3 codes of 2^(e - c): packed codes [rows][Kp/2], swizzled scales."""
+    x = as_bf16_bits(x_bits)
+    M, K = x.shape
+    Kp = kp(K, S)
+    codes = np.zeros((M, Kp // 2), np.uint8)
+    sf = np.zeros(sf_rows_padded(M) * Kp // 16, np.uint8)
+    perm = np.ascontiguousarray(perm, np.int32)
+    rc = lib().or_quantize_mx(_p(x), M, K, K, _p(perm), S, int(c), int(bool(weight)), layout, _p(codes), _p(sf))
+    if rc == 8:
+        raise OracleError("block scale outside E4M3's powers of two for this tensor offset")
+    _check(rc)
     return codes, sf
 
 

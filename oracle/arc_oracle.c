@@ -33,6 +33,9 @@
  *   rmsnorm       float64 formula within two bf16 roundings; exact invariance
  *                 under power-of-two scaling of a row (eps = 0); constant rows
  *                 -> +-1 exactly; torch's fp32 RMSNorm within one bf16 ulp.
+ *   mx (f3)       SPEC example 7s -> scale 2; every block = smallest power of
+ *                 two >= amax/6 with brute-force nearest codes; residual stage
+ *                 exact; physical bytes decode to the MX values (GEMM identity).
  *   silu          all 2^16 bf16 gate values: fp32 SiLU within 4 ulp of long
  *                 double, its bf16 rounding correctly rounded everywhere, torch's
  *                 bf16 SiLU bit-identical wherever its exp does not overflow.
@@ -41,6 +44,7 @@
  * and op order, Q12 default layout, Q23 RMSNorm reduction order and roundings.
  * See DESIGN.md.
  */
+#include <limits.h>
 #include <math.h>
 #include <stdint.h>
 #include <stdlib.h>
@@ -525,3 +529,101 @@ int or_silu_mul(const uint16_t* gu, int64_t M, int K, int64_t ld, int64_t up_off
     }
     return OR_OK;
 }
+
+/* ------------------------------------------------------------------------- */
+/* MXFP4-ARC (f3): the paper's generalisation to MXFP4 (Table 6        */
+/* P:509-535; SPEC: MXFP4 => g = 32, E8M0 scale, no tensor scale).  Reading    */
+/* Q25: per 32-channel block (two consecutive logical 16-blocks) of the       */
+/* reordered row:                                                             */
+/*   a = max|z|; a = 0 -> scale "zero" (byte 0x00), t = z (codes 0 / -0)       */
+/*   d = E8M0_up(a / 6) = 2^e (a/6 one fp32 RN division), t = z * 2^-e (exact) */
+/*   q = rne_e2m1_sat(t)                                                      */
+/*   residual (outlier blocks): r = t - v(q) (exact, units of 2^e),           */
+/*   d2 = E8M0_up(max|r| / 6) = 2^e2, u = r * 2^-e2, q2 = rne(u); absolute     */
+/*   residual scale 2^(e+e2) = E8M0_up(max|x - d v(q)| / 6) exactly.           */
+/* Physical format: the NVFP4 one (so the same tcgen05 GEMM consumes it):     */
+/* both 16-halves of a 32-block carry the E4M3 code of 2^(e - c), with the    */
+/* tensor offset gs = 2^-c folded into alpha = 1/(gs_x gs_w); a block scale   */
+/* outside E4M3's powers of two [2^-9, 2^8] is OR_ERR_RANGE.                  */
+/* ------------------------------------------------------------------------- */
+#define OR_ERR_RANGE 8
+
+static int mx_ceil_log2(float raw) {      /* smallest e with 2^e >= raw > 0 */
+    int e;
+    float f = frexpf(raw, &e);            /* raw = f 2^e, f in [0.5, 1) */
+    return f == 0.5f ? e - 1 : e;
+}
+
+static int mx_code(int k, uint8_t* code) { /* E4M3 code of 2^k */
+    if (k < -9 || k > 8) return OR_ERR_RANGE;
+    *code = or_e4m3_ceil(ldexpf(1.0f, k)); /* exact: 2^k is an E4M3 value */
+    return OR_OK;
+}
+
+/* one 32-block: t (E2M1 units), q; *e_out = block exponent (INT32_MIN for an all-zero block) */
+static void mx_stage(const float z[32], float t[32], uint8_t q[32], int* e_out) {
+    float a = 0.0f;
+    for (int i = 0; i < 32; ++i)
+        if (fabsf(z[i]) > a) a = fabsf(z[i]);
+    if (a == 0.0f) {
+        for (int i = 0; i < 32; ++i) { t[i] = z[i]; q[i] = or_e2m1_encode(t[i]); }
+        *e_out = INT32_MIN;
+        return;
+    }
+    const int e = mx_ceil_log2(a / 6.0f);
+    for (int i = 0; i < 32; ++i) { t[i] = ldexpf(z[i], -e); q[i] = or_e2m1_encode(t[i]); }
+    *e_out = e;
+}
+
+/* logical row (as or_arc_row_logical): codes[K+S] one per byte, sf[(K+S)/16] physical E4M3 bytes */
+int or_arc_row_logical_mx(const uint16_t* x_row, const int32_t* perm, int K, int S, int c, int weight,
+                          uint8_t* codes, uint8_t* sf) {
+    if (K <= 0 || K % 32 || S < 0 || S % 32 || S > K) return OR_ERR_SHAPE;
+    const int nb = K / 16;
+    for (int b = 0; b < K / 32; ++b) {
+        float z[32], t[32], r[32], u[32];
+        uint8_t q[32], q2[32], s = 0, s2 = 0;
+        int e, e2;
+        for (int i = 0; i < 32; ++i) {
+            z[i] = bf16_to_f32(x_row[perm[32 * b + i]]);
+            if (!isfinite(z[i])) return OR_ERR_NONFINITE;
+        }
+        mx_stage(z, t, q, &e);
+        if (e != INT32_MIN && mx_code(e - c, &s) != OR_OK) return OR_ERR_RANGE;
+        memcpy(codes + 32 * b, q, 32);
+        sf[2 * b] = sf[2 * b + 1] = s;
+        if (b < S / 32) {
+            if (weight) {                                      /* duplicate */
+                memcpy(codes + K + 32 * b, q, 32);
+                sf[nb + 2 * b] = sf[nb + 2 * b + 1] = s;
+                continue;
+            }
+            for (int i = 0; i < 32; ++i) r[i] = t[i] - or_e2m1_value(q[i]);   /* exact */
+            mx_stage(r, u, q2, &e2);
+            if (e != INT32_MIN && e2 != INT32_MIN && mx_code(e + e2 - c, &s2) != OR_OK) return OR_ERR_RANGE;
+            if (e2 == INT32_MIN) s2 = 0;
+            memcpy(codes + K + 32 * b, q2, 32);
+            sf[nb + 2 * b] = sf[nb + 2 * b + 1] = s2;
+        }
+    }
+    return OR_OK;
+}
+
+int or_quantize_mx(const uint16_t* x, int64_t M, int K, int64_t ldx, const int32_t* perm, int S, int c, int weight,
+                   int layout, uint8_t* codes, uint8_t* sf) {
+    int64_t Kp = or_kp(K, S);
+    uint8_t* lc = (uint8_t*)malloc((size_t)(K + S));
+    uint8_t* ls = (uint8_t*)malloc((size_t)((K + S) / 16 + 1));
+    int rc = OR_OK;
+    for (int64_t m = 0; m < M && rc == OR_OK; ++m) {
+        rc = or_arc_row_logical_mx(x + m * ldx, perm, K, S, c, weight, lc, ls);
+        if (rc == OR_OK) or_pack_row(lc, ls, K, S, layout, m, codes + m * (Kp / 2), sf);
+    }
+    free(lc);
+    free(ls);
+    return rc;
+}
+
+/* tensor offset c for a tensor whose largest |value| is amax: the largest block scale
+ * E8M0_up(amax/6) = 2^E maps to 2^8 (E4M3's largest power of two): c = E - 8; amax = 0 -> 0 */
+int or_mx_offset(float amax) { return amax > 0.0f ? mx_ceil_log2(amax / 6.0f) - 8 : 0; }
