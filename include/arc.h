@@ -195,6 +195,27 @@ ARC_API arc_status_t arc_linear_rmsnorm(const void* x, int64_t M, int64_t ldx, c
                                         const arc_profile_t* prof, const arc_qweight_t* qw, void* y,
                                         arc_dtype_t y_dtype, int64_t ldy, void* ws, size_t ws_bytes, void* stream);
 
+/* ---------------------------------------------------------------- MXFP4-ARC */
+/* The paper's MXFP4 generalisation (Table 6; SPEC: MXFP4 = 32-element blocks,
+ * E8M0 scales, no tensor scale), reading Q25: per 32-channel block of the reordered row,
+ * 2^e = E8M0_up(amax/6) (amax/6 one fp32 RN division), codes rne_e2m1_sat(x * 2^-e); for the S
+ * outlier channels the exact residual x/2^e - v(q) is quantized again the same way (absolute
+ * scale 2^(e+e2)); weights duplicate their outlier blocks.  Output in the NVFP4 physical
+ * format of arc_quantize_activation -- both 16-halves of a 32-block carry the E4M3 code of
+ * 2^(e - c) where gs = 2^-c is the tensor offset -- so arc_gemm multiplies MXFP4-ARC operands
+ * exactly (alpha = 1/(gs_x gs_w) = 2^(c_x + c_w)).  K and S must be multiples of 32; block
+ * scales outside [2^-9, 2^8] * 2^c (E4M3's powers of two) give unspecified codes. */
+/* gs = 2^-c with c = ceil(log2(amax/6)) - 8: the largest block scale of a tensor with max |x| =
+ * amax maps to 2^8 (host, no device work). */
+ARC_API arc_status_t arc_mx_tensor_scale(float amax, float* gs);
+/* As arc_quantize_activation; prof->gs must be a power of two (arc_mx_tensor_scale). */
+ARC_API arc_status_t arc_quantize_activation_mx(const void* x, int64_t M, int64_t ldx, const arc_profile_t* prof,
+                                                uint8_t* codes, uint8_t* sf, void* stream);
+/* As arc_quantize_weight (outlier blocks duplicated); gs_w a device power of two. */
+ARC_API arc_status_t arc_quantize_weight_mx(const void* w, int64_t N, int64_t K, int64_t ldw, const int32_t* perm,
+                                            int32_t S, const float* gs_w, arc_layout_t layout, uint8_t* codes,
+                                            uint8_t* sf, void* stream);
+
 /* ---------------------------------------------------------------- SiLU-mul (fused producer, Fig.5) */
 /* The down-projection input of a LLaMA/Qwen decoder layer (Fig.5 P:157 quantizes every linear
  * input): h = SiLU(gate) * up of the bf16 gate/up projections, with the roundings of a bf16

@@ -81,6 +81,9 @@ _sig("arc_rmsnorm", [_P, _i64, _i64, _i64, _P, _f32, _P, _i64, _P])
 _sig("arc_rmsnorm_quantize_activation", [_P, _i64, _i64, _P, _f32, ctypes.POINTER(ArcProfile), _P, _P, _P])
 _sig("arc_linear_rmsnorm", [_P, _i64, _i64, _P, _f32, ctypes.POINTER(ArcProfile), ctypes.POINTER(ArcQWeight), _P,
                             ctypes.c_int, _i64, _P, ctypes.c_size_t, _P])
+_sig("arc_mx_tensor_scale", [_f32, ctypes.POINTER(_f32)])
+_sig("arc_quantize_activation_mx", [_P, _i64, _i64, ctypes.POINTER(ArcProfile), _P, _P, _P])
+_sig("arc_quantize_weight_mx", [_P, _i64, _i64, _i64, _P, _i32, _P, ctypes.c_int, _P, _P, _P])
 _sig("arc_gemm_swiglu", [_P, _P, _P, _i64, ctypes.POINTER(ArcQWeight), _P, _i64, _P, ctypes.c_size_t, _P])
 _sig("arc_silu_mul", [_P, _i64, _i64, _i64, _i64, _P, _i64, _P])
 _sig("arc_silu_mul_quantize_activation", [_P, _i64, _i64, _i64, ctypes.POINTER(ArcProfile), _P, _P, _P])
@@ -105,6 +108,7 @@ EXPORTED = [
     "arc_linear_fused_operand_offsets", "arc_linear_hostio_workspace_size", "arc_rmsnorm",
     "arc_rmsnorm_quantize_activation", "arc_linear_rmsnorm", "arc_linear_hostio",
     "arc_silu_mul", "arc_silu_mul_quantize_activation", "arc_linear_silu_mul", "arc_gemm_swiglu",
+    "arc_mx_tensor_scale", "arc_quantize_activation_mx", "arc_quantize_weight_mx",
     "arc_probe_e2m1", "arc_probe_e2m1_bits", "arc_probe_e2m1_raw_bits", "arc_probe_e4m3_ceil", "arc_debug_fused_trace", "arc_probe_silu",
 ]
 
@@ -454,6 +458,47 @@ def linear_rmsnorm(x: torch.Tensor, gamma: torch.Tensor, eps: float, prof: Profi
 
 
 GU_PAIRS = -1  # up_off value: gu holds (gate_j, up_j) adjacent pairs (ARC_GU_PAIRS)
+
+
+# ----------------------------------------------------------------------------- MXFP4-ARC (f3)
+def mx_tensor_scale(amax: float) -> float:
+    """gs = 2^-c for a tensor with max |x| = amax (reading Q25)."""
+    g = _f32()
+    _check(_lib.arc_mx_tensor_scale(float(amax), ctypes.byref(g)), "arc_mx_tensor_scale")
+    return float(g.value)
+
+
+def mx_profile(prof: "Profile", amax: float) -> "Profile":
+    """The same calibration (perm, S) with the MX tensor offset as gs."""
+    return Profile(K=prof.K, S=prof.S, perm=prof.perm,
+                   gs=torch.tensor([mx_tensor_scale(amax)], dtype=torch.float32, device=prof.perm.device),
+                   layout=prof.layout, S_raw=prof.S_raw, M=prof.M, tau=prof.tau)
+
+
+def quantize_activation_mx(x: torch.Tensor, prof: "Profile", codes=None, sf=None, stream=None):
+    assert x.dtype == torch.bfloat16 and x.is_cuda and x.shape[1] == prof.K
+    M = x.shape[0]
+    Kp, cb, sb = buffer_sizes(M, prof.K, prof.S)
+    if codes is None:
+        codes = torch.empty(M, Kp // 2, dtype=torch.uint8, device=x.device)
+    if sf is None:
+        sf = torch.empty(sb, dtype=torch.uint8, device=x.device)
+    _check(_lib.arc_quantize_activation_mx(_ptr(x), M, x.stride(0), ctypes.byref(prof.c()), _ptr(codes), _ptr(sf),
+                                           _stream(stream)), "arc_quantize_activation_mx")
+    return codes, sf
+
+
+def quantize_weight_mx(w: torch.Tensor, prof: "Profile", stream=None) -> "QWeight":
+    """MXFP4-ARC weight (outlier blocks duplicated) with gs_w = 2^-c_w from max |w|."""
+    assert w.dtype == torch.bfloat16 and w.is_cuda
+    N, K = w.shape
+    Kp, cb, sb = buffer_sizes(N, K, prof.S)
+    codes = torch.empty(N, Kp // 2, dtype=torch.uint8, device=w.device)
+    sf = torch.empty(sb, dtype=torch.uint8, device=w.device)
+    gs = torch.tensor([mx_tensor_scale(float(w.float().abs().max()))], dtype=torch.float32, device=w.device)
+    _check(_lib.arc_quantize_weight_mx(_ptr(w), N, K, w.stride(0), _ptr(prof.perm), prof.S, _ptr(gs), prof.layout,
+                                       _ptr(codes), _ptr(sf), _stream(stream)), "arc_quantize_weight_mx")
+    return QWeight(N=N, K=K, Kp=Kp, S=prof.S, layout=prof.layout, codes=codes, sf=sf, gs=gs)
 
 
 def _gu_args(gu: torch.Tensor, K: int | None, up_off: int | None):

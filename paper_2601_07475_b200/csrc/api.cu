@@ -337,6 +337,63 @@ arc_status_t arc_rmsnorm_quantize_activation(const void* x, int64_t M, int64_t l
   return e == cudaSuccess ? ARC_OK : cuda_fail(e, "arc_rmsnorm_quantize_activation");
 }
 
+// ---------------------------------------------------------------- MXFP4-ARC (f3, reading Q25)
+arc_status_t arc_mx_tensor_scale(float amax, float* gs) {
+  if (!gs) return fail(ARC_ERR_NULL, "null gs");
+  if (!(amax >= 0.0f) || amax > 3.4e38f) return fail(ARC_ERR_NONFINITE, "amax must be finite and >= 0");
+  int c = 0;
+  if (amax > 0.0f) {
+    const float raw = amax / 6.0f;
+    int x;
+    const float f = frexpf(raw, &x);
+    c = (f == 0.5f ? x - 1 : x) - 8;
+  }
+  *gs = ldexpf(1.0f, -c);
+  return ARC_OK;
+}
+
+static arc_status_t check_mx(int64_t K, int32_t S, const float* gs_host_or_null) {
+  if (K % 32 || S % 32) return fail(ARC_ERR_ALIGN, "MXFP4-ARC needs K and S multiples of 32");
+  (void)gs_host_or_null;
+  return ARC_OK;
+}
+
+arc_status_t arc_quantize_activation_mx(const void* x, int64_t M, int64_t ldx, const arc_profile_t* prof,
+                                        uint8_t* codes, uint8_t* sf, void* stream) {
+  arc_status_t s = check_profile(prof);
+  if (s != ARC_OK) return s;
+  s = check_mx(prof->K, prof->S, nullptr);
+  if (s != ARC_OK) return s;
+  if (M < 0 || ldx < prof->K || ldx % 8) return fail(ARC_ERR_SHAPE, "bad M/ldx");
+  if (M == 0) return ARC_OK;
+  if (!x || !codes || !sf) return fail(ARC_ERR_NULL, "null x / codes / sf");
+  if (!aligned16(x) || !aligned16(codes) || !aligned16(sf)) return fail(ARC_ERR_ALIGN, "buffer not 16B aligned");
+  s = check_device();
+  if (s != ARC_OK) return s;
+  cudaError_t e = launch_quant(x, M, (int)prof->K, ldx, prof->perm, prof->S, prof->gs, (int)prof->layout, 0, codes,
+                               sf, (cudaStream_t)stream, nullptr, 0.0f, -1, 1);
+  return e == cudaSuccess ? ARC_OK : cuda_fail(e, "arc_quantize_activation_mx");
+}
+
+arc_status_t arc_quantize_weight_mx(const void* w, int64_t N, int64_t K, int64_t ldw, const int32_t* perm, int32_t S,
+                                    const float* gs_w, arc_layout_t layout, uint8_t* codes, uint8_t* sf,
+                                    void* stream) {
+  if (!w || !perm || !gs_w || !codes || !sf) return fail(ARC_ERR_NULL, "null argument");
+  arc_status_t s = check_ks(K, S);
+  if (s != ARC_OK) return s;
+  s = check_mx(K, S, nullptr);
+  if (s != ARC_OK) return s;
+  if (N < 0 || ldw < K || ldw % 8) return fail(ARC_ERR_SHAPE, "bad N/ldw");
+  if (layout != ARC_LAYOUT_INTERLEAVED && layout != ARC_LAYOUT_CONTIGUOUS) return fail(ARC_ERR_SHAPE, "bad layout");
+  if (!aligned16(w) || !aligned16(codes) || !aligned16(sf)) return fail(ARC_ERR_ALIGN, "buffer not 16B aligned");
+  s = check_device();
+  if (s != ARC_OK) return s;
+  if (N == 0) return ARC_OK;
+  cudaError_t e = launch_quant(w, N, (int)K, ldw, perm, S, gs_w, (int)layout, 1, codes, sf, (cudaStream_t)stream,
+                               nullptr, 0.0f, -1, 1);
+  return e == cudaSuccess ? ARC_OK : cuda_fail(e, "arc_quantize_weight_mx");
+}
+
 arc_status_t arc_silu_mul(const void* gu, int64_t M, int64_t K, int64_t ld, int64_t up_off, void* h, int64_t ldh,
                           void* stream) {
   const bool pairs = up_off == ARC_GU_PAIRS;

@@ -15,7 +15,7 @@ int num_sms();  // SM count of the current device (cached per device)
 // up_off >= 0: SiLU-mul mode (reading Q24): quantize bf16(bf16(SiLU(x)) * x[up_off..]) per row.
 cudaError_t launch_quant(const void* x, int64_t rows, int K, int64_t ld, const int32_t* perm, int S, const float* gs,
                          int layout, int weight_mode, uint8_t* codes, uint8_t* sf, cudaStream_t stream,
-                         const void* gamma = nullptr, float eps = 0.0f, int64_t up_off = -1);
+                         const void* gamma = nullptr, float eps = 0.0f, int64_t up_off = -1, int mx = 0);
 cudaError_t launch_silu_mul(const void* gu, int64_t rows, int K, int64_t ld, int64_t up_off, void* h, int64_t ldh,
                             cudaStream_t s);
 cudaError_t launch_rmsnorm(const void* x, int64_t rows, int K, int64_t ldx, const void* gamma, float eps, void* y,

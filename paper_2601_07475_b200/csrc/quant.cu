@@ -154,6 +154,27 @@ ARC_DEV void silu_mul_block16(float (&z)[16], const uint8_t* row, const uint32_t
   }
 }
 
+// MX block scale (reading Q25): for block abs-max a > 0, e = ceil(log2(RN(a/6))) (exact from the
+// fp32 bits), k = 2^-e (t = z*k exact), code = E4M3 code of 2^(e - c); a = 0 -> code 0, k = 1.
+// Exponents outside what E4M3 / the fp32 multiplier can hold give unspecified codes (the oracle
+// reports a range error there).
+ARC_DEV uint32_t mx_pow2_code(int k) {
+  if (k >= -6) return (uint32_t)min(k + 7, 15) << 3;
+  return 1u << max(k + 9, 0);
+}
+ARC_DEV void mx_scale(float a, int c, uint32_t& code, float& k, int& e) {
+  if (a == 0.0f) {
+    code = 0u;
+    k = 1.0f;
+    e = 0;
+    return;
+  }
+  const uint32_t b = __float_as_uint(__fdiv_rn(a, 6.0f));
+  e = (int)((b >> 23) & 0xFFu) - 127 + ((b & 0x7FFFFFu) != 0u);
+  code = mx_pow2_code(e - c);
+  k = __int_as_float((min(max(127 - e, 1), 254)) << 23);
+}
+
 // Rows of a tile.  Tile t of the 128-row group g holds rows base + 32 i, i < R, with
 // base = 128 g + 32 R h + r (t = g * 128/R + 32 h + r): the R rows share (m & 31) and
 // have consecutive (m >> 5) & 3, so in the 128x4 scale layout the tile's scales of one
@@ -194,7 +215,11 @@ ARC_DEV int tile_rows(int base, int64_t rows) {  // valid rows base + 32 i < row
 // gate row [0, 2K) bytes followed by the up row [2K, 4K); SILU = 2, the row holds (g_j, u_j)
 // bf16 pairs (an interleaved gate_up output).  The quantizing warps gather each of their 16
 // channels' (g, u) and quantize h = bf16(bf16(SiLU(g)) * u) (silu_mul_block16, reading Q24).
-template <int IPT, int R, int ROWB, int ST, bool NORM, int SILU>
+//
+// MX mode (reading Q25): MXFP4-ARC -- 32-channel blocks (the 16-blocks of lanes 2j, 2j+1,
+// max combined with one shuffle), power-of-two scales 2^e = E8M0_up(amax/6), t = z * 2^-e, written in
+// the NVFP4 physical format with the E4M3 code of 2^(e - c) (gs = 2^-c), so arc_gemm consumes it.
+template <int IPT, int R, int ROWB, int ST, bool NORM, int SILU, bool MX>
 __global__ void __launch_bounds__(1024) arc_quant_kernel(QuantArgs p) {
   extern __shared__ __align__(16) uint8_t smem[];
   constexpr int ROWP = ROWB + 16;
@@ -357,6 +382,7 @@ __global__ void __launch_bounds__(1024) arc_quant_kernel(QuantArgs p) {
   const int ka16 = nb + ns, NB = p.Kp >> 4;
   uint64_t* ready = (NORM && p.debug != 3) ? normed : full;  // what the quantizing warps wait for
   const float c6g = __fdiv_rn(gs, 6.0f);
+  const int mx_c = 127 - (int)((__float_as_uint(gs) >> 23) & 0xFFu);  // MX: gs = 2^-c
 
   if (warp < npw) {
     // ---------------------------------------------------------------- primary warps
@@ -392,7 +418,32 @@ __global__ void __launch_bounds__(1024) arc_quant_kernel(QuantArgs p) {
             uint8_t* st = sfst + s * NU * UB;
 #pragma unroll
             for (int i = 0; i < IPT; ++i) {
-              if (kind[i] != 0) {
+              if (MX) {
+                // every lane takes part (the block max is shared by lane pairs); idle lanes store nothing
+                const int pb = pbs[i];
+                uint8_t* cptr = p.codes + (int64_t)base * code_row + pb * 8;
+                uint8_t* sst = st + (pb >> 2) * UB + (pb & 3);
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                  uint32_t sfb = 0;
+                  if (r < nr) {
+                    float z[16];
+                    if (kind[i] == 1) gather16(smem + s * SLOT + r * ROWP, off[i], z);
+                    else
+#pragma unroll
+                      for (int q = 0; q < 16; ++q) z[q] = 0.0f;
+                    float a = absmax16(z);
+                    a = fmaxf(a, __shfl_xor_sync(0xffffffffu, a, 1));
+                    float k;
+                    int e;
+                    mx_scale(a, mx_c, sfb, k, e);
+                    const uint2 packed = encode16(z, k);
+                    if (kind[i] != 0) *reinterpret_cast<uint2*>(cptr + (int64_t)(32 * r) * code_row) = packed;
+                    if (kind[i] != 1) sfb = 0;
+                  }
+                  if (kind[i] != 0) sst[4 * r] = (uint8_t)sfb;
+                }
+              } else if (kind[i] != 0) {
                 const int pb = pbs[i];
                 uint8_t* cptr = p.codes + (int64_t)base * code_row + pb * 8;
                 uint8_t* sst = st + (pb >> 2) * UB + (pb & 3);
@@ -429,6 +480,66 @@ __global__ void __launch_bounds__(1024) arc_quant_kernel(QuantArgs p) {
   }
 
   // ---------------------------------------------------------------- residual warps
+  if (MX) {
+    // warp-uniform item loop (lane pairs share each 32-block's maxima); items (row, outlier 16-block)
+    for (int j0 = 0; j0 < my_tiles; j0 += ST) {
+#pragma unroll
+      for (int s = 0; s < ST; ++s) {
+        const int j = j0 + s;
+        if (j < my_tiles) {
+          mbar_wait(&ready[s], (j / ST) & 1);
+          const int base = tile_base<R>((int)blockIdx.x + j * (int)gridDim.x);
+          const int nr = tile_rows<R>(base, p.rows);
+          uint8_t* st = sfst + s * NU * UB;
+          for (int it0 = (warp - npw) * 32; it0 < R * ns; it0 += nrw * 32) {
+            const int it = it0 + lane;
+            const bool has = it < R * ns;
+            const int r = has ? it / ns : 0, jb = has ? it - (it / ns) * ns : 0;
+            const bool live = has && r < nr;
+            float z[16];
+            if (live) {
+              const int* pp = p.perm + 16 * jb;
+#pragma unroll
+              for (int q = 0; q < 16; ++q)
+                z[q] = bf16_bits_to_f32(*reinterpret_cast<const uint16_t*>(smem + s * SLOT + r * ROWP + 2 * __ldg(pp + q)));
+            } else {
+#pragma unroll
+              for (int q = 0; q < 16; ++q) z[q] = 0.0f;
+            }
+            float a = absmax16(z);
+            a = fmaxf(a, __shfl_xor_sync(0xffffffffu, a, 1));
+            uint32_t c1;
+            float k1;
+            int e1;
+            mx_scale(a, mx_c, c1, k1, e1);
+            float t[16];
+            uint2 packed = encode16(z, k1, t);
+            uint32_t sfb = c1;
+            if (!p.weight_mode) {
+              float ee[16];
+              residual16(t, packed, ee);
+              float a2 = absmax16(ee);
+              a2 = fmaxf(a2, __shfl_xor_sync(0xffffffffu, a2, 1));
+              uint32_t c2;
+              float k2;
+              int e2;
+              mx_scale(a2, 0, c2, k2, e2);           // e2 relative to 2^e1
+              if (a != 0.0f && a2 != 0.0f) c2 = mx_pow2_code(e1 + e2 - mx_c);
+              else c2 = 0u;
+              packed = encode16(ee, k2);
+              sfb = c2;
+            }  // weight mode: bitwise duplicate of the primary block
+            const int pb = phys_block(nb + jb, nb, ns, p.layout);
+            if (live) *reinterpret_cast<uint2*>(p.codes + (int64_t)(base + 32 * r) * code_row + pb * 8) = packed;
+            if (has) st[(pb >> 2) * UB + 4 * r + (pb & 3)] = live ? (uint8_t)sfb : (uint8_t)0;
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[s]);
+        }
+      }
+    }
+    return;
+  }
   const int rl = (warp - npw) * 32 + lane;  // residual lane index
   const int nitems = R * ns;                // (row, outlier block) pairs per tile
   // common case (R*ns <= 32*nrw): one fixed item per lane, offsets in registers
@@ -562,7 +673,7 @@ __global__ void arc_finalize_scale_kernel(float* gs) {
 // Per-(kernel, threads, smem) launch configuration, computed once per process:
 // the attribute calls and the occupancy query cost more host time than the
 // kernel itself at decode sizes.
-template <int IPT, int R, int ROWB, int ST, bool NORM, int SILU = 0>
+template <int IPT, int R, int ROWB, int ST, bool NORM, int SILU = 0, bool MX = false>
 static cudaError_t launch_quant_cfg(QuantArgs a, int threads, cudaStream_t stream) {
   a.rows_per_tile = R;
   a.stages = ST;
@@ -577,13 +688,13 @@ static cudaError_t launch_quant_cfg(QuantArgs a, int threads, cudaStream_t strea
   for (int i = 0; i < ncache && i < 8; ++i)
     if (cache[i].dev == dev && cache[i].threads == threads && cache[i].smem == smem) occ = cache[i].occ;
   if (occ == 0) {
-    cudaError_t e = cudaFuncSetAttribute(arc_quant_kernel<IPT, R, ROWB, ST, NORM, SILU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(arc_quant_kernel<IPT, R, ROWB, ST, NORM, SILU, MX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          227 * 1024);
     if (e != cudaSuccess) return e;
     // the full shared-memory carveout so several CTAs' rings fit per SM
-    e = cudaFuncSetAttribute(arc_quant_kernel<IPT, R, ROWB, ST, NORM, SILU>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    e = cudaFuncSetAttribute(arc_quant_kernel<IPT, R, ROWB, ST, NORM, SILU, MX>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e != cudaSuccess) return e;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, arc_quant_kernel<IPT, R, ROWB, ST, NORM, SILU>, threads, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, arc_quant_kernel<IPT, R, ROWB, ST, NORM, SILU, MX>, threads, smem);
     if (e != cudaSuccess) return e;
     if (occ < 1) occ = 1;
     cache[ncache % 8] = Cfg{dev, threads, smem, occ};
@@ -602,7 +713,7 @@ static cudaError_t launch_quant_cfg(QuantArgs a, int threads, cudaStream_t strea
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, arc_quant_kernel<IPT, R, ROWB, ST, NORM, SILU>, a);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, arc_quant_kernel<IPT, R, ROWB, ST, NORM, SILU, MX>, a);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
@@ -620,7 +731,7 @@ static cudaError_t launch_silu_cfg(QuantArgs a, int th, int ipt, int64_t rb, cud
 
 cudaError_t launch_quant(const void* x, int64_t rows, int K, int64_t ld, const int32_t* perm, int S, const float* gs,
                          int layout, int weight_mode, uint8_t* codes, uint8_t* sf, cudaStream_t stream,
-                         const void* gamma, float eps, int64_t up_off) {
+                         const void* gamma, float eps, int64_t up_off, int mx) {
   QuantArgs a;
   a.up_off = up_off;
   a.gamma = static_cast<const uint16_t*>(gamma);
@@ -676,6 +787,11 @@ cudaError_t launch_quant(const void* x, int64_t rows, int K, int64_t ld, const i
         if (rowb <= 16384) return launch_quant_cfg<1, 2, 16384, 3, true>(a, th, stream);
         return launch_quant_cfg<1, 2, 32768, 2, true>(a, th, stream);
       }
+      if (mx) {
+        if (rowb <= 8192) return launch_quant_cfg<1, 4, 8192, 3, false, 0, true>(a, th, stream);
+        if (rowb <= 16384) return launch_quant_cfg<1, 2, 16384, 3, false, 0, true>(a, th, stream);
+        return launch_quant_cfg<1, 2, 32768, 3, false, 0, true>(a, th, stream);
+      }
       if (rowb <= 8192) return launch_quant_cfg<1, 4, 8192, 3, false>(a, th, stream);
       if (rowb <= 16384) return launch_quant_cfg<1, 2, 16384, 3, false>(a, th, stream);
       return launch_quant_cfg<1, 2, 32768, 3, false>(a, th, stream);
@@ -688,6 +804,7 @@ cudaError_t launch_quant(const void* x, int64_t rows, int K, int64_t ld, const i
     const int threads = (a.npw + a.nrw + 1 + (a.norm ? 1 : 0)) * 32;
     if (threads > 1024) return cudaErrorInvalidValue;
     if (a.norm) return launch_quant_cfg<2, 1, 65536, 2, true>(a, threads, stream);
+    if (mx) return launch_quant_cfg<2, 1, 65536, 3, false, 0, true>(a, threads, stream);
     return launch_quant_cfg<2, 1, 65536, 3, false>(a, threads, stream);
   }
   return cudaErrorInvalidValue;  // K + S > 32768 is rejected in api.cu

@@ -16,6 +16,7 @@ ap.add_argument("--iters", type=int, default=20)
 ap.add_argument("--norm", action="store_true", help="time arc_rmsnorm_quantize_activation (fused RMSNorm)")
 ap.add_argument("--silu", action="store_true", help="time arc_silu_mul_quantize_activation (fused SiLU-mul)")
 ap.add_argument("--pairs", action="store_true", help="with --silu: gate/up as adjacent pairs (ARC_GU_PAIRS)")
+ap.add_argument("--mx", action="store_true", help="time arc_quantize_activation_mx (MXFP4-ARC)")
 args = ap.parse_args()
 K, M, S = args.K, args.M, args.S
 st = synth.Structure(K, S, seed=0)
@@ -30,6 +31,9 @@ gamma = synth.rmsnorm_weight(K, seed=0, device="cuda")
 if args.norm:
     def quant(x, prof, codes=None, sf=None):
         return A.rmsnorm_quantize_activation(x, gamma, 1e-5, prof, codes, sf)
+elif args.mx:
+    prof = A.mx_profile(prof, float(xs[0].float().abs().max()))
+    quant = A.quantize_activation_mx
 elif args.silu:
     def quant(x, prof, codes=None, sf=None):
         return A.silu_mul_quantize_activation(x, prof, up_off=A.GU_PAIRS if args.pairs else None, codes=codes, sf=sf)
@@ -60,7 +64,7 @@ ts.sort()
 Kp = codes.shape[1] * 2
 byts = M * ((4 if args.silu else 2) * K + Kp // 2 + Kp // 16)
 med = ts[len(ts) // 2]
-print(f"{'rmsnorm+quant' if args.norm else 'silu+quant' if args.silu else 'quant'} K={K} M={M} S={S}: median {med*1e3:.1f} us  {byts/med/1e6:.0f} GB/s  (min {ts[0]*1e3:.1f} us)")
+print(f"{'rmsnorm+quant' if args.norm else 'silu+quant' if args.silu else 'mx-quant' if args.mx else 'quant'} K={K} M={M} S={S}: median {med*1e3:.1f} us  {byts/med/1e6:.0f} GB/s  (min {ts[0]*1e3:.1f} us)")
 
 # reference: plain torch streaming kernels on the same rotated buffers
 def _t(fn):

@@ -1,0 +1,65 @@
+"""GPU parity of MXFP4-ARC (reading Q25): arc_quantize_activation_mx /
+arc_quantize_weight_mx are bit-exact against the oracle (codes and the scales of every valid row)
+in both layouts and across the kernel's ring configurations, and arc_gemm over the MX operands is
+within the north_star tolerance of the oracle's exact GEMM (which equals the float64 MX dot
+products, tests/test_oracle_mx.py)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2601_07475_b200 import synth
+from _helpers import dev_bits, valid_sf_mask
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def A():
+    from paper_2601_07475_b200 import arc
+    assert arc.device_supported()
+    return arc
+
+
+def _kp(K, S):
+    return (K + S + 63) // 64 * 64
+
+
+@pytest.mark.parametrize("M,K,S", [(16, 256, 32), (300, 4096, 128), (77, 14336, 128), (130, 1024, 0),
+                                   (5, 96, 64), (12, 16384, 256)])
+@pytest.mark.parametrize("layout", [0, 1])
+def test_mx_quantize_bit_exact(A, M, K, S, layout):
+    st = synth.Structure(K, max(S, 32), seed=K + S)
+    x = synth.activation(M, K, st, seed=M + K + layout, device="cuda")
+    prof = A.calibrate([synth.activation(256, K, st, seed=9, device="cuda")], s_override=S, layout=layout)
+    mprof = A.mx_profile(prof, float(x.float().abs().max()))
+    c = -int(np.log2(float(mprof.gs.item())))
+    codes, sf = A.quantize_activation_mx(x, mprof)
+    torch.cuda.synchronize()
+    oc, osf = oracle.quantize_mx(dev_bits(x), prof.perm.cpu().numpy(), S, c, layout=layout)
+    mask = valid_sf_mask(M, _kp(K, S))
+    assert np.array_equal(codes.cpu().numpy(), oc)
+    assert np.array_equal(sf.cpu().numpy()[mask], osf[mask])
+
+
+@pytest.mark.parametrize("M,N,K,S", [(16, 256, 256, 32), (200, 600, 4096, 128), (1000, 512, 1024, 64)])
+def test_mx_weight_and_gemm(A, M, N, K, S):
+    st = synth.Structure(K, max(S, 32), seed=N)
+    x = synth.activation(M, K, st, seed=N + 1, device="cuda")
+    w = synth.weight(N, K, seed=N + 2, device="cuda")
+    prof = A.calibrate([synth.activation(256, K, st, seed=3, device="cuda")], s_override=S)
+    mprof = A.mx_profile(prof, float(x.float().abs().max()))
+    qw = A.quantize_weight_mx(w, prof)
+    codes, sf = A.quantize_activation_mx(x, mprof)
+    y = A.gemm(codes, sf, mprof.gs, qw, out_dtype=torch.float32)
+    torch.cuda.synchronize()
+    perm = prof.perm.cpu().numpy()
+    cx, cw = -int(np.log2(float(mprof.gs.item()))), -int(np.log2(float(qw.gs.item())))
+    bc, bsf = oracle.quantize_mx(dev_bits(w), perm, S, cw, weight=True)
+    assert np.array_equal(qw.codes.cpu().numpy(), bc)
+    mask = valid_sf_mask(N, _kp(K, S))
+    assert np.array_equal(qw.sf.cpu().numpy()[mask], bsf[mask])
+    ac, asf = oracle.quantize_mx(dev_bits(x), perm, S, cx)
+    yref, bound = oracle.gemm_reference(ac, asf, bc, bsf, 2.0 ** -cx, 2.0 ** -cw)
+    err = np.abs(y.cpu().numpy().astype(np.float64) - yref)
+    assert (err <= bound).all(), f"worst err/bound {np.max(err / np.maximum(bound, 1e-300))}"
