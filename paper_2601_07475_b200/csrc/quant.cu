@@ -481,7 +481,22 @@ __global__ void __launch_bounds__(1024) arc_quant_kernel(QuantArgs p) {
 
   // ---------------------------------------------------------------- residual warps
   if (MX) {
-    // warp-uniform item loop (lane pairs share each 32-block's maxima); items (row, outlier 16-block)
+    // warp-uniform item loop (lane pairs share each 32-block's maxima); items (row, outlier 16-block).
+    // The lane's first item's 16 gather offsets are kept in registers (the common case R*ns <= 32*nrw).
+    uint32_t moff[16];
+    {
+      const int it = (warp - npw) * 32 + lane;
+      const int jb = it < R * ns ? it % ns : 0, r = it < R * ns ? it / ns : 0;
+      const int4* pp = reinterpret_cast<const int4*>(p.perm + 16 * jb);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int4 v = __ldg(pp + q);
+        moff[4 * q + 0] = (uint32_t)v.x * 2u + (uint32_t)(r * ROWP);
+        moff[4 * q + 1] = (uint32_t)v.y * 2u + (uint32_t)(r * ROWP);
+        moff[4 * q + 2] = (uint32_t)v.z * 2u + (uint32_t)(r * ROWP);
+        moff[4 * q + 3] = (uint32_t)v.w * 2u + (uint32_t)(r * ROWP);
+      }
+    }
     for (int j0 = 0; j0 < my_tiles; j0 += ST) {
 #pragma unroll
       for (int s = 0; s < ST; ++s) {
@@ -497,7 +512,9 @@ __global__ void __launch_bounds__(1024) arc_quant_kernel(QuantArgs p) {
             const int r = has ? it / ns : 0, jb = has ? it - (it / ns) * ns : 0;
             const bool live = has && r < nr;
             float z[16];
-            if (live) {
+            if (live && it0 == (warp - npw) * 32) {
+              gather16(smem + s * SLOT, moff, z);
+            } else if (live) {
               const int* pp = p.perm + 16 * jb;
 #pragma unroll
               for (int q = 0; q < 16; ++q)
