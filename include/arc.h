@@ -149,6 +149,9 @@ ARC_API arc_status_t arc_select_outliers(const float* chan_max_host, int64_t K, 
  * possible.  Use perm_out for BOTH arc_quantize_weight and the activation
  * profile.  K must be a multiple of 16; perm_host must be a permutation. */
 ARC_API arc_status_t arc_gather_order(const int32_t* perm_host, int64_t K, int32_t* perm_out_host);
+/* As arc_gather_order for staged rows of elem_bytes per channel: 2 = bf16 rows (the default), 4 =
+ * (gate, up) bf16 pairs (ARC_GU_PAIRS rows of arc_silu_mul_quantize_activation). */
+ARC_API arc_status_t arc_gather_order_ex(const int32_t* perm_host, int64_t K, int elem_bytes, int32_t* perm_out_host);
 /* gs_out[0] = 2688 / max|x| over a rows x K bf16 matrix (1.0 if the max is 0):
  * the NVFP4 encode tensor scale (reading Q3).  gs_out is a device float. */
 ARC_API arc_status_t arc_tensor_scale(const void* x, int64_t rows, int64_t K, int64_t ldx, float* gs_out,

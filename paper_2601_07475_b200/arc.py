@@ -81,6 +81,7 @@ _sig("arc_rmsnorm", [_P, _i64, _i64, _i64, _P, _f32, _P, _i64, _P])
 _sig("arc_rmsnorm_quantize_activation", [_P, _i64, _i64, _P, _f32, ctypes.POINTER(ArcProfile), _P, _P, _P])
 _sig("arc_linear_rmsnorm", [_P, _i64, _i64, _P, _f32, ctypes.POINTER(ArcProfile), ctypes.POINTER(ArcQWeight), _P,
                             ctypes.c_int, _i64, _P, ctypes.c_size_t, _P])
+_sig("arc_gather_order_ex", [_P, _i64, ctypes.c_int, _P])
 _sig("arc_mx_tensor_scale", [_f32, ctypes.POINTER(_f32)])
 _sig("arc_quantize_activation_mx", [_P, _i64, _i64, ctypes.POINTER(ArcProfile), _P, _P, _P])
 _sig("arc_quantize_weight_mx", [_P, _i64, _i64, _i64, _P, _i32, _P, ctypes.c_int, _P, _P, _P])
@@ -108,7 +109,7 @@ EXPORTED = [
     "arc_linear_fused_operand_offsets", "arc_linear_hostio_workspace_size", "arc_rmsnorm",
     "arc_rmsnorm_quantize_activation", "arc_linear_rmsnorm", "arc_linear_hostio",
     "arc_silu_mul", "arc_silu_mul_quantize_activation", "arc_linear_silu_mul", "arc_gemm_swiglu",
-    "arc_mx_tensor_scale", "arc_quantize_activation_mx", "arc_quantize_weight_mx",
+    "arc_mx_tensor_scale", "arc_quantize_activation_mx", "arc_quantize_weight_mx", "arc_gather_order_ex",
     "arc_probe_e2m1", "arc_probe_e2m1_bits", "arc_probe_e2m1_raw_bits", "arc_probe_e4m3_ceil", "arc_debug_fused_trace", "arc_probe_silu",
 ]
 
@@ -225,16 +226,18 @@ def select_outliers(chan_max_host: np.ndarray, s_override: int = -1) -> dict:
     return dict(perm=perm, S=S.value, S_raw=S_raw.value, M=M.value, tau=tau.value, gs=gs.value)
 
 
-def gather_order(perm: np.ndarray) -> np.ndarray:
-    """Bank-conflict-aware channel order inside each 16-channel block (same block sets)."""
+def gather_order(perm: np.ndarray, elem_bytes: int = 2) -> np.ndarray:
+    """Bank-conflict-aware channel order inside each 16-channel block (same block sets); elem_bytes 4
+    for (gate, up) pair rows (ARC_GU_PAIRS)."""
     p = np.ascontiguousarray(perm, dtype=np.int32)
     out = np.empty_like(p)
-    _check(_lib.arc_gather_order(p.ctypes.data_as(_P), p.size, out.ctypes.data_as(_P)), "arc_gather_order")
+    _check(_lib.arc_gather_order_ex(p.ctypes.data_as(_P), p.size, int(elem_bytes), out.ctypes.data_as(_P)),
+           "arc_gather_order_ex")
     return out
 
 
 def calibrate(batches, s_override: int = -1, layout: int = INTERLEAVED, device=None,
-              optimize_gather: bool = True) -> Profile:
+              optimize_gather: bool = True, gather_bytes: int = 2) -> Profile:
     """Offline calibration of one activation site over an iterable of bf16 [rows, K] batches.
     With optimize_gather the channel order inside each 16-block is re-arranged for
     conflict-free shared-memory gathers (arc_gather_order; block sets unchanged)."""
@@ -244,7 +247,7 @@ def calibrate(batches, s_override: int = -1, layout: int = INTERLEAVED, device=N
     torch.cuda.current_stream().synchronize()
     sel = select_outliers(chan_max.cpu().numpy(), s_override)
     if optimize_gather:
-        sel["perm"] = gather_order(sel["perm"])
+        sel["perm"] = gather_order(sel["perm"], gather_bytes)
     dev = chan_max.device if device is None else device
     return Profile(K=chan_max.numel(), S=sel["S"], perm=torch.from_numpy(sel["perm"]).to(dev),
                    gs=torch.tensor([sel["gs"]], dtype=torch.float32, device=dev), layout=layout,
@@ -360,18 +363,20 @@ def gemm_swiglu(a_codes, a_sf, gs_x: torch.Tensor, qw: QWeight, out=None, ws: Wo
     return out
 
 
-def interleave_gate_up(w_gate: torch.Tensor, w_up: torch.Tensor) -> torch.Tensor:
-    """Offline weight layout for arc_gemm_swiglu: gate/up rows interleaved in groups of 16
-    (rows 32j..32j+15 = gate rows 16j.., rows 32j+16..32j+31 = up rows 16j..).  Layout only."""
+def interleave_gate_up(w_gate: torch.Tensor, w_up: torch.Tensor, group: int = 16) -> torch.Tensor:
+    """Offline weight layout, gate/up rows interleaved in groups: group 16 for arc_gemm_swiglu (rows
+    32j..32j+15 = gate rows 16j.., rows 32j+16..32j+31 = up rows 16j..); group 1 for ARC_GU_PAIRS
+    (the GEMM output then holds (g_j, u_j) adjacent pairs).  Layout only."""
     I, K = w_gate.shape
-    assert w_up.shape == (I, K) and I % 16 == 0
-    return torch.stack([w_gate.view(I // 16, 16, K), w_up.view(I // 16, 16, K)], dim=1).reshape(2 * I, K).contiguous()
+    assert w_up.shape == (I, K) and I % group == 0
+    return torch.stack([w_gate.view(I // group, group, K), w_up.view(I // group, group, K)],
+                       dim=1).reshape(2 * I, K).contiguous()
 
 
-def deinterleave_gate_up(y: torch.Tensor) -> torch.Tensor:
+def deinterleave_gate_up(y: torch.Tensor, group: int = 16) -> torch.Tensor:
     """Columns of a GEMM output over interleave_gate_up weights back to [gate | up].  Layout only."""
     M, N = y.shape
-    v = y.reshape(M, N // 32, 2, 16)
+    v = y.reshape(M, N // (2 * group), 2, group)
     return torch.cat([v[:, :, 0, :].reshape(M, N // 2), v[:, :, 1, :].reshape(M, N // 2)], dim=1)
 
 

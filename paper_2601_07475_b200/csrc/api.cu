@@ -207,12 +207,12 @@ arc_status_t arc_select_outliers(const float* chan_max_host, int64_t K, int32_t 
 // channels in the same 32-bit word are one access.  A step costs the largest
 // number of distinct words any bank receives; a seeded local search over
 // in-block swaps minimizes the sum over the 16 steps for each 32-block chunk.
-static int gather_step_cost(const int32_t* col[32], int n) {
+static int gather_step_cost(const int32_t* col[32], int n, int shift) {
   int words[32][32];
   int cnt[32] = {0};
   int worst = 0;
   for (int i = 0; i < n; ++i) {
-    const int w = *col[i] >> 1, b = w & 31;
+    const int w = *col[i] >> shift, b = w & 31;
     bool dup = false;
     for (int k = 0; k < cnt[b]; ++k) dup |= words[b][k] == w;
     if (!dup) {
@@ -224,7 +224,13 @@ static int gather_step_cost(const int32_t* col[32], int n) {
 }
 
 arc_status_t arc_gather_order(const int32_t* perm_host, int64_t K, int32_t* perm_out_host) {
+  return arc_gather_order_ex(perm_host, K, 2, perm_out_host);
+}
+
+arc_status_t arc_gather_order_ex(const int32_t* perm_host, int64_t K, int elem_bytes, int32_t* perm_out_host) {
   if (!perm_host || !perm_out_host) return fail(ARC_ERR_NULL, "null perm");
+  if (elem_bytes != 2 && elem_bytes != 4) return fail(ARC_ERR_SHAPE, "elem_bytes must be 2 or 4");
+  const int shift = elem_bytes == 2 ? 1 : 0;  // channel -> 4-byte shared-memory word
   if (K <= 0 || K % 16) return fail(ARC_ERR_SHAPE, "K must be a positive multiple of 16");
   std::vector<char> seen((size_t)K, 0);
   for (int64_t j = 0; j < K; ++j) {
@@ -242,7 +248,7 @@ arc_status_t arc_gather_order(const int32_t* perm_host, int64_t K, int32_t* perm
     int cost[16];
     for (int q = 0; q < 16; ++q) {
       for (int i = 0; i < n; ++i) col[i] = &B[i * 16 + q];
-      cost[q] = gather_step_cost(col, n);
+      cost[q] = gather_step_cost(col, n, shift);
     }
     for (int it = 0; it < 4000; ++it) {
       rng ^= rng << 13; rng ^= rng >> 7; rng ^= rng << 17;
@@ -250,9 +256,9 @@ arc_status_t arc_gather_order(const int32_t* perm_host, int64_t K, int32_t* perm
       if (a == b) continue;
       std::swap(B[i * 16 + a], B[i * 16 + b]);
       for (int k = 0; k < n; ++k) col[k] = &B[k * 16 + a];
-      const int ca = gather_step_cost(col, n);
+      const int ca = gather_step_cost(col, n, shift);
       for (int k = 0; k < n; ++k) col[k] = &B[k * 16 + b];
-      const int cb = gather_step_cost(col, n);
+      const int cb = gather_step_cost(col, n, shift);
       if (ca + cb <= cost[a] + cost[b]) {
         cost[a] = ca;
         cost[b] = cb;

@@ -3,7 +3,8 @@ batch x seq = 16 x 2048 (M = 32768 tokens), all four activation sites with their
 (Fig.5), timed as one CUDA graph per variant (CUDA events; inputs > 4x L2):
 
   arc_fused    RMSNorm+quantize -> qkv GEMM | quantize -> o GEMM | RMSNorm+quantize -> gate_up
-               GEMM | SiLU-mul+quantize -> down GEMM        (S = 128 per site, producers fused)
+               GEMM (pairwise-interleaved gate/up rows) | SiLU-mul+quantize of the (g, u) pairs -> down
+               GEMM                                          (S = 128 per site, producers fused)
   arc_swiglu   as arc_fused, but SiLU-mul in the gate_up GEMM epilogue and a plain quantize of h
   arc_unfused  the same with separate arc_rmsnorm / arc_silu_mul kernels (bf16 round trips in HBM)
   nvfp4_s0     arc_fused with S = 0 (plain NVFP4, no residual channels; same kernels)
@@ -84,9 +85,15 @@ def arc_chain(S):
     p_o = A.calibrate([synth.activation(cal, H, st_h, seed=21, device="cuda")], s_override=S)
     p_gu = A.calibrate([A.rmsnorm(synth.activation(cal, H, st_h, seed=22, device="cuda"), g2, EPS)], s_override=S)
     p_d = A.calibrate([A.silu_mul(synth.gate_up(cal, I, st_i, seed=23, device="cuda"))], s_override=S)
+    # the fused down-site producer reads (g_j, u_j) pairs: gate/up weight rows interleaved pairwise,
+    # gather order for 4-byte channels
+    p_dp = A.calibrate([A.silu_mul(synth.gate_up(cal, I, st_i, seed=23, device="cuda"))], s_override=S,
+                       gather_bytes=4)
+    q_dp = A.quantize_weight(w_d, p_dp)
     q_qkv, q_o = A.quantize_weight(w_qkv, p_qkv), A.quantize_weight(w_o, p_o)
     q_gu, q_d = A.quantize_weight(w_gu, p_gu), A.quantize_weight(w_d, p_d)
     q_gui = A.quantize_weight(A.interleave_gate_up(w_g, w_u), p_gu)
+    q_gup = A.quantize_weight(A.interleave_gate_up(w_g, w_u, group=1), p_gu)
     bufs = {}
 
     def act(name, prof, rows):
@@ -112,9 +119,9 @@ def arc_chain(S):
         A.quantize_activation(attn, p_o, c2, s2)
         A.gemm(c2, s2, p_o.gs, q_o, out=y_o, ws=ws)
         A.rmsnorm_quantize_activation(x2, g2, EPS, p_gu, c3, s3)
-        A.gemm(c3, s3, p_gu.gs, q_gu, out=gu, ws=ws)
-        A.silu_mul_quantize_activation(gu, p_d, codes=c4, sf=s4)
-        A.gemm(c4, s4, p_d.gs, q_d, out=y_d, ws=ws)
+        A.gemm(c3, s3, p_gu.gs, q_gup, out=gu, ws=ws)
+        A.silu_mul_quantize_activation(gu, p_dp, up_off=A.GU_PAIRS, codes=c4, sf=s4)
+        A.gemm(c4, s4, p_dp.gs, q_dp, out=y_d, ws=ws)
 
     def swiglu():
         A.rmsnorm_quantize_activation(x, g1, EPS, p_qkv, c1, s1)
@@ -148,6 +155,8 @@ def arc_chain(S):
         "gemm_gate_up": lambda: A.gemm(c3, s3, p_gu.gs, q_gu, out=gu, ws=ws),
         "gemm_gate_up_swiglu": lambda: A.gemm_swiglu(c3, s3, p_gu.gs, q_gui, out=h, ws=ws),
         "silu_mul_quant_down": lambda: A.silu_mul_quantize_activation(gu, p_d, codes=c4, sf=s4),
+        "silu_mul_quant_down_pairs": lambda: A.silu_mul_quantize_activation(gu, p_dp, up_off=A.GU_PAIRS, codes=c4,
+                                                                            sf=s4),
         "quant_down_h": lambda: A.quantize_activation(h, p_d, c4, s4),
         "gemm_down": lambda: A.gemm(c4, s4, p_d.gs, q_d, out=y_d, ws=ws),
         "rmsnorm_alone": lambda: A.rmsnorm(x, g1, EPS, out=xn),

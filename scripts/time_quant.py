@@ -20,11 +20,14 @@ ap.add_argument("--mx", action="store_true", help="time arc_quantize_activation_
 args = ap.parse_args()
 K, M, S = args.K, args.M, args.S
 st = synth.Structure(K, S, seed=0)
-prof = A.calibrate([synth.activation(1024, K, st, seed=1000, device="cuda")], s_override=S)
+prof = A.calibrate([synth.activation(1024, K, st, seed=1000, device="cuda")], s_override=S,
+                  gather_bytes=4 if args.pairs else 2)
 nrot = max(2, int(4 * 126e6 // (M * K * 2)) + 1)
 if args.silu:
     nrot = max(2, int(4 * 126e6 // (M * K * 4)) + 1)
     xs = [synth.gate_up(M, K, st, seed=i, device="cuda") for i in range(nrot)]
+    if args.pairs:  # (g_j, u_j) adjacent
+        xs = [torch.stack([x[:, :K], x[:, K:]], dim=2).reshape(M, 2 * K).contiguous() for x in xs]
 else:
     xs = [synth.activation(M, K, st, seed=i, device="cuda") for i in range(nrot)]
 gamma = synth.rmsnorm_weight(K, seed=0, device="cuda")

@@ -79,7 +79,7 @@ def test_silu_mul_quantize_bit_exact(A, M, K, S, layout, pairs):
     st = synth.Structure(K, max(S, 16), seed=K + S)
     gu = synth.gate_up(M, K, st, seed=M * 3 + K + layout, device="cuda")
     cal = A.silu_mul(synth.gate_up(256, K, st, seed=99, device="cuda"))
-    prof = A.calibrate([cal], s_override=S, layout=layout)
+    prof = A.calibrate([cal], s_override=S, layout=layout, gather_bytes=4 if pairs else 2)
     if pairs:  # the same gate/up values as (g_j, u_j) adjacent pairs
         gp = torch.stack([gu[:, :K], gu[:, K:]], dim=2).reshape(M, 2 * K).contiguous()
         codes, sf = A.silu_mul_quantize_activation(gp, prof, up_off=A.GU_PAIRS)
