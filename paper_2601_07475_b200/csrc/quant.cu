@@ -82,10 +82,7 @@ ARC_DEV void gather16(const uint8_t* base, const uint32_t (&off)[16], float (&z)
 // CTA), so a lane's 16 gains are two conflict-free 16-byte loads at gperm + 32 l.  Pairs:
 // mul.rn.f32x2, one cvt.rn.bf16x2.f32, one bf16x2 multiply (the product of two bf16 is exact in
 // fp32, so its single rounding equals the oracle's).
-ARC_DEV void norm16(float (&z)[16], const uint8_t* gblk, float r) {
-  const uint4 g0 = *reinterpret_cast<const uint4*>(gblk);
-  const uint4 g1 = *reinterpret_cast<const uint4*>(gblk + 16);
-  const uint32_t gw[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+ARC_DEV void norm16w(float (&z)[16], const uint32_t (&gw)[8], float r) {
 #pragma unroll
   for (int i = 0; i < 16; i += 2) {
     const float2 p = mul2(z[i], z[i + 1], r);
@@ -95,6 +92,12 @@ ARC_DEV void norm16(float (&z)[16], const uint8_t* gblk, float r) {
     z[i] = __uint_as_float(yw << 16);
     z[i + 1] = __uint_as_float(yw & 0xFFFF0000u);
   }
+}
+ARC_DEV void norm16(float (&z)[16], const uint8_t* gblk, float r) {
+  const uint4 g0 = *reinterpret_cast<const uint4*>(gblk);
+  const uint4 g1 = *reinterpret_cast<const uint4*>(gblk + 16);
+  const uint32_t gw[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+  norm16w(z, gw, r);
 }
 
 // h = bf16(s * u) for two (SiLU bits, up-in-high-half word) pairs: one mul.rn.f32x2 + one
@@ -387,6 +390,7 @@ __global__ void __launch_bounds__(1024) arc_quant_kernel(QuantArgs p) {
   if (warp < npw) {
     // ---------------------------------------------------------------- primary warps
     uint32_t off[IPT][16];
+    uint32_t greg[IPT][8];    // norm mode: the lane's 16 gains (reordered order), kept in registers
     int pbs[IPT], kind[IPT];  // kind: 0 idle, 1 primary, 3 zero pad block
 #pragma unroll
     for (int i = 0; i < IPT; ++i) {
@@ -396,6 +400,12 @@ __global__ void __launch_bounds__(1024) arc_quant_kernel(QuantArgs p) {
       else if (t < nb + (NB - ka16)) { k = 3; pb = ka16 + (t - nb); }
       kind[i] = k;
       pbs[i] = pb;
+      if (NORM) {
+        const uint4 g0 = *reinterpret_cast<const uint4*>(gam + 32 * l);
+        const uint4 g1 = *reinterpret_cast<const uint4*>(gam + 32 * l + 16);
+        greg[i][0] = g0.x; greg[i][1] = g0.y; greg[i][2] = g0.z; greg[i][3] = g0.w;
+        greg[i][4] = g1.x; greg[i][5] = g1.y; greg[i][6] = g1.z; greg[i][7] = g1.w;
+      }
       const int4* pp = reinterpret_cast<const int4*>(p.perm + 16 * l);
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
@@ -458,7 +468,7 @@ __global__ void __launch_bounds__(1024) arc_quant_kernel(QuantArgs p) {
                         silu_mul_block16<SILU>(z, smem + s * SLOT + r * ROWP, off[i], K * 2, stab, p.debug);
                       } else {
                         gather16(smem + s * SLOT + r * ROWP, off[i], z);
-                        if (NORM) norm16(z, gam + 32 * (tid + i * npw * 32), rscale[s * R + r]);
+                        if (NORM) norm16w(z, greg[i], rscale[s * R + r]);
                       }
                       // stage 1 (Eq.1 with the NVFP4 two-level scale, Q7 op order)
                       sfb = e4m3_ceil_nb(__fmul_rn(absmax16(z), c6g));
