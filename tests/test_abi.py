@@ -114,3 +114,36 @@ def test_gather_order_keeps_block_sets(arc):
         assert np.array_equal(out, arc.gather_order(perm))  # deterministic
     with pytest.raises(arc.ArcError):
         arc.gather_order(np.zeros(32, np.int32))
+
+
+def test_validation_of_producer_and_mx_entry_points(arc):
+    """Argument checks of the fused-producer, SwiGLU, MXFP4-ARC and gather-order entry points run
+    before any device work (no GPU needed)."""
+    lib = arc.lib()
+    P = ctypes.c_void_p
+    fake = P(0x10000)
+    prof = arc.ArcProfile(256, 16, 0x10000, 0x10000, 0)
+    # SiLU-mul: up_off < K -> ARC_ERR_SHAPE; pairs need ld >= 2K
+    assert lib.arc_silu_mul(fake, 4, 256, 512, 128, fake, 256, None) == 2
+    assert lib.arc_silu_mul(fake, 4, 256, 256, -1, fake, 256, None) == 2
+    assert lib.arc_silu_mul_quantize_activation(fake, 4, 512, 128, ctypes.byref(prof), fake, fake, None) == 2
+    big = arc.ArcProfile(16400, 16, 0x10000, 0x10000, 0)
+    assert lib.arc_silu_mul_quantize_activation(fake, 4, 32800, 16400, ctypes.byref(big), fake, fake, None) == 4
+    # SwiGLU GEMM: N not a multiple of 32 -> ARC_ERR_SHAPE
+    qw = arc.ArcQWeight(48, 256, 320, 16, 0, 0x10000, 0x10000, 0x10000)
+    assert lib.arc_gemm_swiglu(fake, fake, fake, 4, ctypes.byref(qw), fake, 24, None, 0, None) == 2
+    # MXFP4-ARC: K or S not a multiple of 32 -> ARC_ERR_ALIGN
+    assert lib.arc_quantize_activation_mx(fake, 4, 256, ctypes.byref(prof), fake, fake, None) == 3
+    prof48 = arc.ArcProfile(272, 32, 0x10000, 0x10000, 0)
+    assert lib.arc_quantize_activation_mx(fake, 4, 272, ctypes.byref(prof48), fake, fake, None) == 3
+    # the MX tensor offset: largest block scale E8M0_up(amax/6) maps to 2^8
+    assert arc.mx_tensor_scale(6.0 * 256) == 1.0
+    assert arc.mx_tensor_scale(7.0) == 2.0 ** -(1 - 8)
+    assert arc.mx_tensor_scale(0.0) == 1.0
+    # gather order for 4-byte channels: still a within-block permutation; bad width refused
+    perm = np.random.default_rng(1).permutation(4096).astype(np.int32)
+    out = arc.gather_order(perm, 4)
+    for b in range(256):
+        assert set(out[16 * b:16 * b + 16]) == set(perm[16 * b:16 * b + 16])
+    with pytest.raises(arc.ArcError):
+        arc.gather_order(perm, 3)
