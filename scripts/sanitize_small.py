@@ -16,3 +16,26 @@ for (M, K, N, S) in [(16, 256, 256, 16), (129, 512, 520, 64), (300, 1024, 1024, 
     y32 = A.linear(x, prof, qw, out_dtype=torch.float32)
     torch.cuda.synchronize()
     print("ok", M, K, N, S, float(y32.abs().max()))
+
+# fused producers, SwiGLU epilogue, MXFP4-ARC (small shapes)
+for (M, K, S) in [(16, 256, 32), (130, 1024, 64)]:
+    st = synth.Structure(K, S, seed=3)
+    g = synth.rmsnorm_weight(K, seed=4, device="cuda")
+    x = synth.activation(M, K, st, seed=5, device="cuda")
+    prof = A.calibrate([synth.activation(256, K, st, seed=6, device="cuda")], s_override=S)
+    A.rmsnorm_quantize_activation(x, g, 1e-5, prof)
+    gu = synth.gate_up(M, K, st, seed=7, device="cuda")
+    A.silu_mul_quantize_activation(gu, prof)
+    pp = A.calibrate([synth.activation(256, K, st, seed=6, device="cuda")], s_override=S, gather_bytes=4)
+    gp = torch.stack([gu[:, :K], gu[:, K:]], dim=2).reshape(M, 2 * K).contiguous()
+    A.silu_mul_quantize_activation(gp, pp, up_off=A.GU_PAIRS)
+    mprof = A.mx_profile(prof, float(x.float().abs().max()))
+    qmx = A.quantize_weight_mx(synth.weight(256, K, seed=8, device="cuda"), prof)
+    c, sf = A.quantize_activation_mx(x, mprof)
+    A.gemm(c, sf, mprof.gs, qmx)
+    qgu = A.quantize_weight(A.interleave_gate_up(synth.weight(256, K, seed=9, device="cuda"),
+                                                 synth.weight(256, K, seed=10, device="cuda")), prof)
+    c1, s1 = A.quantize_activation(x, prof)
+    A.gemm_swiglu(c1, s1, prof.gs, qgu)
+    torch.cuda.synchronize()
+    print("ok producers/mx/swiglu", M, K, S)
