@@ -72,6 +72,9 @@ struct Args {
   int nsplit;   // split-K factor (decode-size M): > 1 -> fp32 partials into ws[nsplit][M][N]
   int kbs;      // K-blocks per split
   float* ws;
+  int a_rows;   // rows of the A (activation) TMA box: BM, or 16/32/64 at decode-size M (rows >= M of the
+                // 128-row MMA operand then hold stale shared memory -- harmless: an output row depends
+                // only on its own A row, and rows >= M are never stored)
   int swiglu;   // SwiGLU epilogue: y = h [M][N/2] bf16 from 16-row-interleaved gate/up weight rows
   int raster;   // tile order: 0 = M-tile groups fastest (the A panel stays in L2), 1 = N tiles fastest (B stays)
   int debug;  // perf experiments only (env ARC_GEMM_DEBUG): 1 = no epilogue work, 2 = no scale copies, 3 = no stores, 4 = no TMEM loads,
@@ -339,7 +342,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           uint8_t* sB = sA + A_BYTES;
           uint8_t* sSFA = sB + B_BYTES;
           uint8_t* sSFB = sSFA + SFA_BYTES;
-          mbar_expect_tx(&full[stage], (uint32_t)(A_BYTES + B_BYTES + nk * 512 * ((a_ok ? 1 : 0) + nrb)));
+          mbar_expect_tx(&full[stage], (uint32_t)(args.a_rows * BKB + B_BYTES + nk * 512 * ((a_ok ? 1 : 0) + nrb)));
           tma_load_2d(sA, &tmA, &full[stage], kb * BKB, mb * BM, pol);
           if (a_ok) bulk_load(sSFA, args.sfa + ((int64_t)mb * kc_total + kb * 4) * 512, nk * 512, &full[stage]);
           if (CL == 1) {
@@ -765,7 +768,8 @@ GemmPlan plan_gemm(int64_t M, int64_t N, int64_t Kp) {
     // t_kb ~ one 48 KB stage at an SM's share of HBM bandwidth.
     const double t_kb = 48e3 / 44e9, hbm = 6.0e12;
     double best = 1e30;
-    for (int64_t s = 1; s <= std::min<int64_t>(nkb / 2, 32); ++s) {
+    static const int env_smax = getenv("ARC_GEMM_SPLIT_MAX") ? atoi(getenv("ARC_GEMM_SPLIT_MAX")) : 32;
+    for (int64_t s = 1; s <= std::min<int64_t>(nkb / 2, env_smax); ++s) {
       const int64_t kbs = (nkb + s - 1) / s, ns = (nkb + kbs - 1) / kbs;
       const int64_t it = items * ns, waves = (it + clusters - 1) / clusters;
       const double cost = (double)waves * (double)kbs * t_kb + (ns > 1 ? (double)ns * M * N * 8.0 / hbm : 0.0);
@@ -801,7 +805,10 @@ cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t stream, const char** 
   // B box rows: the 1-SM kernel loads 256 (CL 1) or 128 (CL 2, multicast halves); the pair
   // kernel 128 (one pair) or 64 (two pairs, multicast quarters).  SFB box: 4 / 2 chunks.
   const int b_rows = pl.pair ? (CL == 2 ? 128 : 64) : BN / CL;
-  if (!make_map(&tmA, p.a_codes, p.M, p.Kp / 2, BM) || !make_map(&tmB, p.b_codes, p.N, p.Kp / 2, b_rows) ||
+  // decode-size M on the 1-SM kernel: a 16/32/64-row A box instead of 128 rows of TMA zero fill
+  static const int env_abox = getenv("ARC_GEMM_ABOX") ? atoi(getenv("ARC_GEMM_ABOX")) : 1;
+  const int a_rows = (!pl.pair && CL == 1 && env_abox && p.M <= 64) ? (p.M <= 16 ? 16 : p.M <= 32 ? 32 : 64) : BM;
+  if (!make_map(&tmA, p.a_codes, p.M, p.Kp / 2, a_rows) || !make_map(&tmB, p.b_codes, p.N, p.Kp / 2, b_rows) ||
       (pl.pair && (!make_sf_map(&tmSFA, p.a_sf, (p.M + 127) / 128, p.Kp / 64, 4, 1) ||
                    !make_sf_map(&tmSFB, p.b_sf, (p.N + 127) / 128, p.Kp / 64, CL == 2 ? 4 : 2, 1)))) {
     if (detail) *detail = "cuTensorMapEncodeTiled failed";
@@ -834,6 +841,7 @@ cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t stream, const char** 
   a.ldy = p.ldy;
   a.y_fp32 = p.y_fp32;
   a.swiglu = p.swiglu;
+  a.a_rows = a_rows;
   static const int dbg = getenv("ARC_GEMM_DEBUG") ? atoi(getenv("ARC_GEMM_DEBUG")) : 0;
   a.debug = dbg;
   // Keep the smaller operand L2-resident: sweep the tiles along it fastest so each wave of
