@@ -233,7 +233,8 @@ __global__ void __launch_bounds__(1024) arc_quant_kernel(QuantArgs p) {
   constexpr uint32_t OSC = SILU == 2 ? 4u : 2u;  // staged bytes per channel index
   const int NU = p.Kp >> 6;  // 4-block units per row
   uint8_t* sfst = smem + ST * SLOT;  // [ST][NU][UB]
-  float* k1tab = reinterpret_cast<float*>(sfst + ST * NU * UB);
+  // tables and mbarriers start 16-byte aligned: ST * NU * UB is only a multiple of 4 when Kp/64 is odd
+  float* k1tab = reinterpret_cast<float*>(smem + ((ST * SLOT + ST * NU * UB + 15) & ~15));
   float* c6tab = k1tab + 128;  // RN(e4m3(c) / 6): the residual stage's c6 for base d1 = e4m3(c)
   float* rat = c6tab + 128;    // RN((8+m1)/(8+m2)): mantissa ratio of two normal E4M3 scales
   uint64_t* full = reinterpret_cast<uint64_t*>(rat + 64);
@@ -704,7 +705,7 @@ template <int IPT, int R, int ROWB, int ST, bool NORM, int SILU = 0, bool MX = f
 static cudaError_t launch_quant_cfg(QuantArgs a, int threads, cudaStream_t stream) {
   a.rows_per_tile = R;
   a.stages = ST;
-  const size_t smem = (size_t)ST * R * (ROWB + 16) + (size_t)ST * (a.Kp / 64) * (R * 4) + (128 + 128 + 64) * 4 + 3 * ST * 8 +
+  const size_t smem = (size_t)ST * R * (ROWB + 16) + (size_t)ST * (a.Kp / 64) * (R * 4) + 16 + (128 + 128 + 64) * 4 + 3 * ST * 8 +
                       (size_t)ST * R * 4 + (NORM ? 16 + (size_t)a.K * 2 : 0) + (SILU ? 16 + SILU_TAB * 2 : 0);
   struct Cfg { int dev, threads; size_t smem; int occ; };
   static thread_local Cfg cache[8];

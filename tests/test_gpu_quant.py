@@ -133,3 +133,24 @@ def test_empty_batch_is_noop(A):
     x = torch.empty(0, 256, dtype=torch.bfloat16, device="cuda")
     codes, sf = A.quantize_activation(x, prof)
     assert codes.shape == (0, 160)
+
+
+@pytest.mark.parametrize("K,S", [(18944, 64), (17408, 0)])
+def test_odd_scale_units_with_one_row_tiles(K, S):
+    """Regression: one-row tiles (R = 1) with an odd number of 64-column scale units (Kp/64) used to
+    leave the kernel's mbarriers 4-byte aligned (misaligned-address fault); activation and weight
+    quantization at such shapes are bit-exact."""
+    from paper_2601_07475_b200 import arc as A
+    M, N = 37, 96
+    st = synth.Structure(K, max(S, 16), seed=K)
+    x = synth.activation(M, K, st, seed=1, device="cuda")
+    w = synth.weight(N, K, seed=2, device="cuda")
+    prof = A.calibrate([synth.activation(128, K, st, seed=3, device="cuda")], s_override=S)
+    codes, sf = A.quantize_activation(x, prof)
+    qw = A.quantize_weight(w, prof)
+    torch.cuda.synchronize()
+    perm, gs = prof.perm.cpu().numpy(), float(prof.gs.item())
+    oc, osf = oracle.quantize_activation(dev_bits(x), perm, S, gs)
+    assert np.array_equal(codes.cpu().numpy(), oc)
+    bc, bsf = oracle.quantize_weight(dev_bits(w), perm, S, float(qw.gs.item()))
+    assert np.array_equal(qw.codes.cpu().numpy(), bc)

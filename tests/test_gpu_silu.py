@@ -177,3 +177,16 @@ def test_gemm_swiglu_matches_silu_of_gemm(A, M, I, K, S):
                                             qw.sf.cpu().numpy(), float(prof.gs.item()), float(qw.gs.item()))
         y32 = A.gemm(codes, sf, prof.gs, qw, out_dtype=torch.float32).cpu().numpy().astype(np.float64)
         assert (np.abs(y32 - yref) <= bound).all()
+
+
+def test_silu_mul_quantize_odd_scale_units(A):
+    """Regression (one-row tiles, odd Kp/64): K = 14336, S = 64 -> Kp/64 = 225."""
+    M, K, S = 20, 14336, 64
+    st = synth.Structure(K, S, seed=5)
+    gu = synth.gate_up(M, K, st, seed=6, device="cuda")
+    prof = A.calibrate([A.silu_mul(synth.gate_up(128, K, st, seed=7, device="cuda"))], s_override=S)
+    codes, sf = A.silu_mul_quantize_activation(gu, prof)
+    torch.cuda.synchronize()
+    oc, osf = oracle.quantize_activation(oracle.silu_mul(dev_bits(gu)), prof.perm.cpu().numpy(), S,
+                                         float(prof.gs.item()))
+    assert np.array_equal(codes.cpu().numpy(), oc)
