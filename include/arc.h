@@ -206,11 +206,18 @@ ARC_API arc_status_t arc_linear_rmsnorm(const void* x, int64_t M, int64_t ldx, c
  * scale 2^(e+e2)); weights duplicate their outlier blocks.  Output in the NVFP4 physical
  * format of arc_quantize_activation -- both 16-halves of a 32-block carry the E4M3 code of
  * 2^(e - c) where gs = 2^-c is the tensor offset -- so arc_gemm multiplies MXFP4-ARC operands
- * exactly (alpha = 1/(gs_x gs_w) = 2^(c_x + c_w)).  K and S must be multiples of 32; block
- * scales outside [2^-9, 2^8] * 2^c (E4M3's powers of two) give unspecified codes. */
+ * exactly (alpha = 1/(gs_x gs_w) = 2^(c_x + c_w)).  K and S must be multiples of 32.  A block
+ * exponent e outside [c - 9, c + 8] (E4M3's powers of two for this offset) is clamped into it
+ * (reading Q25b): such a block flushes toward 0 or saturates at +-6 * 2^(c+8), with a scale byte
+ * that matches its codes. */
 /* gs = 2^-c with c = ceil(log2(amax/6)) - 8: the largest block scale of a tensor with max |x| =
  * amax maps to 2^8 (host, no device work). */
 ARC_API arc_status_t arc_mx_tensor_scale(float amax, float* gs);
+/* The same offset computed on the device from max |x| of a rows x K bf16 matrix (the weight's
+ * tensor offset, P:140's offline weight preparation): gs_out[0] = 2^-c, a device float (1.0 if the
+ * max is 0).  K % 16 == 0, ldx >= K, ldx % 8 == 0, x 16-byte aligned; errors as arc_tensor_scale. */
+ARC_API arc_status_t arc_mx_tensor_scale_device(const void* x, int64_t rows, int64_t K, int64_t ldx, float* gs_out,
+                                                void* stream);
 /* As arc_quantize_activation; prof->gs must be a power of two (arc_mx_tensor_scale). */
 ARC_API arc_status_t arc_quantize_activation_mx(const void* x, int64_t M, int64_t ldx, const arc_profile_t* prof,
                                                 uint8_t* codes, uint8_t* sf, void* stream);

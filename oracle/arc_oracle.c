@@ -543,8 +543,12 @@ int or_silu_mul(const uint16_t* gu, int64_t M, int K, int64_t ld, int64_t up_off
 /*   residual scale 2^(e+e2) = E8M0_up(max|x - d v(q)| / 6) exactly.           */
 /* Physical format: the NVFP4 one (so the same tcgen05 GEMM consumes it):     */
 /* both 16-halves of a 32-block carry the E4M3 code of 2^(e - c), with the    */
-/* tensor offset gs = 2^-c folded into alpha = 1/(gs_x gs_w); a block scale   */
-/* outside E4M3's powers of two [2^-9, 2^8] is OR_ERR_RANGE.                  */
+/* tensor offset gs = 2^-c folded into alpha = 1/(gs_x gs_w).  Reading Q25b:  */
+/* a block exponent outside E4M3's powers of two (e - c outside [-9, 8]) is   */
+/* clamped into that range before t is formed (the residual's absolute       */
+/* exponent e + e2 likewise), so such a block flushes toward 0 or saturates  */
+/* at +-6 with a scale that matches its codes -- as NVFP4's saturating E4M3  */
+/* scale does (P:118 names the tensor scale as what keeps blocks in range).  */
 /* ------------------------------------------------------------------------- */
 #define OR_ERR_RANGE 8
 
@@ -554,14 +558,15 @@ static int mx_ceil_log2(float raw) {      /* smallest e with 2^e >= raw > 0 */
     return f == 0.5f ? e - 1 : e;
 }
 
-static int mx_code(int k, uint8_t* code) { /* E4M3 code of 2^k */
-    if (k < -9 || k > 8) return OR_ERR_RANGE;
-    *code = or_e4m3_ceil(ldexpf(1.0f, k)); /* exact: 2^k is an E4M3 value */
-    return OR_OK;
+static uint8_t mx_code(int k) {          /* E4M3 code of 2^k, k in [-9, 8] */
+    return or_e4m3_ceil(ldexpf(1.0f, k)); /* exact: 2^k is an E4M3 value */
 }
 
-/* one 32-block: t (E2M1 units), q; *e_out = block exponent (INT32_MIN for an all-zero block) */
-static void mx_stage(const float z[32], float t[32], uint8_t q[32], int* e_out) {
+static int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
+
+/* one 32-block: t (E2M1 units), q; *e_out = block exponent, clamped to [lo, hi] (Q25b),
+ * INT32_MIN for an all-zero block */
+static void mx_stage(const float z[32], int lo, int hi, float t[32], uint8_t q[32], int* e_out) {
     float a = 0.0f;
     for (int i = 0; i < 32; ++i)
         if (fabsf(z[i]) > a) a = fabsf(z[i]);
@@ -570,7 +575,7 @@ static void mx_stage(const float z[32], float t[32], uint8_t q[32], int* e_out) 
         *e_out = INT32_MIN;
         return;
     }
-    const int e = mx_ceil_log2(a / 6.0f);
+    const int e = clampi(mx_ceil_log2(a / 6.0f), lo, hi);
     for (int i = 0; i < 32; ++i) { t[i] = ldexpf(z[i], -e); q[i] = or_e2m1_encode(t[i]); }
     *e_out = e;
 }
@@ -588,8 +593,8 @@ int or_arc_row_logical_mx(const uint16_t* x_row, const int32_t* perm, int K, int
             z[i] = bf16_to_f32(x_row[perm[32 * b + i]]);
             if (!isfinite(z[i])) return OR_ERR_NONFINITE;
         }
-        mx_stage(z, t, q, &e);
-        if (e != INT32_MIN && mx_code(e - c, &s) != OR_OK) return OR_ERR_RANGE;
+        mx_stage(z, c - 9, c + 8, t, q, &e);
+        if (e != INT32_MIN) s = mx_code(e - c);
         memcpy(codes + 32 * b, q, 32);
         sf[2 * b] = sf[2 * b + 1] = s;
         if (b < S / 32) {
@@ -599,9 +604,12 @@ int or_arc_row_logical_mx(const uint16_t* x_row, const int32_t* perm, int K, int
                 continue;
             }
             for (int i = 0; i < 32; ++i) r[i] = t[i] - or_e2m1_value(q[i]);   /* exact */
-            mx_stage(r, u, q2, &e2);
-            if (e != INT32_MIN && e2 != INT32_MIN && mx_code(e + e2 - c, &s2) != OR_OK) return OR_ERR_RANGE;
-            if (e2 == INT32_MIN) s2 = 0;
+            if (e == INT32_MIN) {                               /* zero block: zero residual */
+                mx_stage(r, 0, 0, u, q2, &e2);
+            } else {
+                mx_stage(r, c - 9 - e, c + 8 - e, u, q2, &e2);  /* e + e2 in [c-9, c+8] */
+            }
+            s2 = (e != INT32_MIN && e2 != INT32_MIN) ? mx_code(e + e2 - c) : 0;
             memcpy(codes + K + 32 * b, q2, 32);
             sf[nb + 2 * b] = sf[nb + 2 * b + 1] = s2;
         }

@@ -83,6 +83,7 @@ _sig("arc_linear_rmsnorm", [_P, _i64, _i64, _P, _f32, ctypes.POINTER(ArcProfile)
                             ctypes.c_int, _i64, _P, ctypes.c_size_t, _P])
 _sig("arc_gather_order_ex", [_P, _i64, ctypes.c_int, _P])
 _sig("arc_mx_tensor_scale", [_f32, ctypes.POINTER(_f32)])
+_sig("arc_mx_tensor_scale_device", [_P, _i64, _i64, _i64, _P, _P])
 _sig("arc_quantize_activation_mx", [_P, _i64, _i64, ctypes.POINTER(ArcProfile), _P, _P, _P])
 _sig("arc_quantize_weight_mx", [_P, _i64, _i64, _i64, _P, _i32, _P, ctypes.c_int, _P, _P, _P])
 _sig("arc_gemm_swiglu", [_P, _P, _P, _i64, ctypes.POINTER(ArcQWeight), _P, _i64, _P, ctypes.c_size_t, _P])
@@ -109,7 +110,7 @@ EXPORTED = [
     "arc_linear_fused_operand_offsets", "arc_linear_hostio_workspace_size", "arc_rmsnorm",
     "arc_rmsnorm_quantize_activation", "arc_linear_rmsnorm", "arc_linear_hostio",
     "arc_silu_mul", "arc_silu_mul_quantize_activation", "arc_linear_silu_mul", "arc_gemm_swiglu",
-    "arc_mx_tensor_scale", "arc_quantize_activation_mx", "arc_quantize_weight_mx", "arc_gather_order_ex",
+    "arc_mx_tensor_scale", "arc_mx_tensor_scale_device", "arc_quantize_activation_mx", "arc_quantize_weight_mx", "arc_gather_order_ex",
     "arc_probe_e2m1", "arc_probe_e2m1_bits", "arc_probe_e2m1_raw_bits", "arc_probe_e4m3_ceil", "arc_debug_fused_trace", "arc_probe_silu",
 ]
 
@@ -312,7 +313,8 @@ def _dtype_code(dt) -> int:
 class Workspace:
     """Grow-only device workspace for arc_gemm / arc_linear (256-byte aligned by the
     allocator, zero-filled on allocation: the sync words of the fused kernel (grid barrier,
-    per-tile counters) must start at 0, and every call leaves them at 0)."""
+    per-tile counters) must start at 0, and every call leaves them at 0).  A Workspace belongs to
+    one stream: calls that share one must be ordered on that stream (the defaults are per stream)."""
 
     def __init__(self, device="cuda"):
         self.device = device
@@ -327,6 +329,12 @@ class Workspace:
 _default_ws = {}
 
 
+def _default_workspace(kind, device, stream=None) -> "Workspace":
+    """Per-(kind, device, stream) default workspace: calls on different streams never share (and so
+    never race on) one buffer, and a buffer grown on one stream is not freed under another's kernel."""
+    return _default_ws.setdefault((kind, str(device), _stream(stream)), Workspace(device))
+
+
 def gemm(a_codes, a_sf, gs_x: torch.Tensor, qw: QWeight, out_dtype=torch.bfloat16, out=None, ws: Workspace = None,
          stream=None):
     """The augmented NVFP4 GEMM (Eq.2): out = A_aug B_aug^T / (gs_x gs_w)."""
@@ -337,7 +345,7 @@ def gemm(a_codes, a_sf, gs_x: torch.Tensor, qw: QWeight, out_dtype=torch.bfloat1
     buf = None
     if need:
         if ws is None:
-            ws = _default_ws.setdefault(("gemm", a_codes.device), Workspace(a_codes.device))
+            ws = _default_workspace("gemm", a_codes.device, stream)
         buf = ws.get(need)
     _check(_lib.arc_gemm(_ptr(a_codes), _ptr(a_sf), _ptr(gs_x), M, ctypes.byref(qw.c()), _ptr(out),
                          _dtype_code(out.dtype), out.stride(0), _ptr(buf), 0 if buf is None else buf.numel(),
@@ -355,7 +363,7 @@ def gemm_swiglu(a_codes, a_sf, gs_x: torch.Tensor, qw: QWeight, out=None, ws: Wo
     buf = None
     if need:
         if ws is None:
-            ws = _default_ws.setdefault(("gemm", a_codes.device), Workspace(a_codes.device))
+            ws = _default_workspace("gemm", a_codes.device, stream)
         buf = ws.get(need)
     _check(_lib.arc_gemm_swiglu(_ptr(a_codes), _ptr(a_sf), _ptr(gs_x), M, ctypes.byref(qw.c()), _ptr(out),
                                 out.stride(0), _ptr(buf), 0 if buf is None else buf.numel(), _stream(stream)),
@@ -409,7 +417,7 @@ def linear(x: torch.Tensor, prof: Profile, qw: QWeight, out_dtype=torch.bfloat16
         out = _alloc_out(M, qw.N, out_dtype, x.device)
     need = linear_workspace_size_ex(M, qw, mode)
     if ws is None:
-        ws = _default_ws.setdefault(x.device, Workspace(x.device))
+        ws = _default_workspace("linear", x.device, stream)
     buf = ws.get(need)
     _check(_lib.arc_linear_ex(_ptr(x), M, x.stride(0), ctypes.byref(prof.c()), ctypes.byref(qw.c()), _ptr(out),
                               _dtype_code(out.dtype), out.stride(0), _ptr(buf), buf.numel(), LINEAR_MODES[mode],
@@ -454,7 +462,7 @@ def linear_rmsnorm(x: torch.Tensor, gamma: torch.Tensor, eps: float, prof: Profi
         out = _alloc_out(M, qw.N, out_dtype, x.device)
     need = linear_workspace_size(M, qw)
     if ws is None:
-        ws = _default_ws.setdefault(x.device, Workspace(x.device))
+        ws = _default_workspace("linear", x.device, stream)
     buf = ws.get(need)
     _check(_lib.arc_linear_rmsnorm(_ptr(x), M, x.stride(0), _ptr(gamma), float(eps), ctypes.byref(prof.c()),
                                    ctypes.byref(qw.c()), _ptr(out), _dtype_code(out.dtype), out.stride(0), _ptr(buf),
@@ -473,8 +481,11 @@ def mx_tensor_scale(amax: float) -> float:
     return float(g.value)
 
 
-def mx_profile(prof: "Profile", amax: float) -> "Profile":
-    """The same calibration (perm, S) with the MX tensor offset as gs."""
+def mx_profile(prof: "Profile", amax: float | None = None) -> "Profile":
+    """The same calibration (perm, S) with the MX tensor offset as gs (static: from the calibration
+    max prof.M unless amax is given)."""
+    if amax is None:
+        amax = prof.M
     return Profile(K=prof.K, S=prof.S, perm=prof.perm,
                    gs=torch.tensor([mx_tensor_scale(amax)], dtype=torch.float32, device=prof.perm.device),
                    layout=prof.layout, S_raw=prof.S_raw, M=prof.M, tau=prof.tau)
@@ -500,7 +511,9 @@ def quantize_weight_mx(w: torch.Tensor, prof: "Profile", stream=None) -> "QWeigh
     Kp, cb, sb = buffer_sizes(N, K, prof.S)
     codes = torch.empty(N, Kp // 2, dtype=torch.uint8, device=w.device)
     sf = torch.empty(sb, dtype=torch.uint8, device=w.device)
-    gs = torch.tensor([mx_tensor_scale(float(w.float().abs().max()))], dtype=torch.float32, device=w.device)
+    gs = torch.empty(1, dtype=torch.float32, device=w.device)
+    _check(_lib.arc_mx_tensor_scale_device(_ptr(w), N, K, w.stride(0), _ptr(gs), _stream(stream)),
+           "arc_mx_tensor_scale_device")
     _check(_lib.arc_quantize_weight_mx(_ptr(w), N, K, w.stride(0), _ptr(prof.perm), prof.S, _ptr(gs), prof.layout,
                                        _ptr(codes), _ptr(sf), _stream(stream)), "arc_quantize_weight_mx")
     return QWeight(N=N, K=K, Kp=Kp, S=prof.S, layout=prof.layout, codes=codes, sf=sf, gs=gs)
@@ -550,7 +563,7 @@ def linear_silu_mul(gu: torch.Tensor, prof: Profile, qw: QWeight, up_off: int | 
         out = _alloc_out(M, qw.N, out_dtype, gu.device)
     need = linear_workspace_size(M, qw)
     if ws is None:
-        ws = _default_ws.setdefault(gu.device, Workspace(gu.device))
+        ws = _default_workspace("linear", gu.device, stream)
     buf = ws.get(need)
     _check(_lib.arc_linear_silu_mul(_ptr(gu), M, gu.stride(0), up_off, ctypes.byref(prof.c()), ctypes.byref(qw.c()),
                                     _ptr(out), _dtype_code(out.dtype), out.stride(0), _ptr(buf), buf.numel(),

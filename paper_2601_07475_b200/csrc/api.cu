@@ -358,6 +358,17 @@ arc_status_t arc_mx_tensor_scale(float amax, float* gs) {
   return ARC_OK;
 }
 
+arc_status_t arc_mx_tensor_scale_device(const void* x, int64_t rows, int64_t K, int64_t ldx, float* gs_out,
+                                        void* stream) {
+  if (!x || !gs_out) return fail(ARC_ERR_NULL, "null x / gs_out");
+  if (K <= 0 || K % 16 || rows < 0 || ldx < K || ldx % 8) return fail(ARC_ERR_SHAPE, "bad rows/K/ldx");
+  if (!aligned16(x)) return fail(ARC_ERR_ALIGN, "x not 16B aligned");
+  arc_status_t s = check_device();
+  if (s != ARC_OK) return s;
+  cudaError_t e = launch_tensor_scale(x, rows, (int)K, ldx, gs_out, (cudaStream_t)stream, 1);
+  return e == cudaSuccess ? ARC_OK : cuda_fail(e, "arc_mx_tensor_scale_device");
+}
+
 static arc_status_t check_mx(int64_t K, int32_t S, const float* gs_host_or_null) {
   if (K % 32 || S % 32) return fail(ARC_ERR_ALIGN, "MXFP4-ARC needs K and S multiples of 32");
   (void)gs_host_or_null;

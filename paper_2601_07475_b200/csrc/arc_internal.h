@@ -4,7 +4,31 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <mutex>
+
 namespace arc {
+
+// Runs f() (returning cudaError_t) once per CUDA device and caches its result: function attributes
+// such as the dynamic shared-memory limit are per device, so a process-wide once is not enough.
+struct PerDeviceOnce {
+  static constexpr int kMaxDev = 64;
+  std::mutex mu;
+  bool done[kMaxDev] = {};
+  cudaError_t err[kMaxDev] = {};
+  template <class F>
+  cudaError_t run(F&& f) {
+    int d = 0;
+    cudaError_t e = cudaGetDevice(&d);
+    if (e != cudaSuccess) return e;
+    if (d < 0 || d >= kMaxDev) return cudaErrorInvalidDevice;
+    std::lock_guard<std::mutex> g(mu);
+    if (!done[d]) {
+      err[d] = f();
+      done[d] = true;
+    }
+    return err[d];
+  }
+};
 
 inline int64_t kp_of(int64_t K, int64_t S) { return (K + S + 63) / 64 * 64; }
 inline int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
@@ -21,7 +45,9 @@ cudaError_t launch_silu_mul(const void* gu, int64_t rows, int K, int64_t ld, int
 cudaError_t launch_rmsnorm(const void* x, int64_t rows, int K, int64_t ldx, const void* gamma, float eps, void* y,
                            int64_t ldy, cudaStream_t s);
 cudaError_t launch_calib_absmax(const void* x, int64_t rows, int K, int64_t ld, float* chan_max, cudaStream_t s);
-cudaError_t launch_tensor_scale(const void* x, int64_t rows, int K, int64_t ld, float* gs_out, cudaStream_t s);
+// mx = 0: gs = 2688/amax (reading Q3); mx = 1: the MXFP4-ARC offset gs = 2^-c (reading Q25).
+cudaError_t launch_tensor_scale(const void* x, int64_t rows, int K, int64_t ld, float* gs_out, cudaStream_t s,
+                                int mx = 0);
 
 struct GemmProblem {
   int64_t M, N, Kp;

@@ -546,10 +546,9 @@ cudaError_t launch_linear_fused(const FusedProblem& p, cudaStream_t stream, cons
     if (detail) *detail = "cuTensorMapEncodeTiled failed";
     return cudaErrorInvalidValue;
   }
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(arc_linear_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, F_SMEM);
+  static PerDeviceOnce attr_once;
+  const cudaError_t attr_err = attr_once.run([] {
+    return cudaFuncSetAttribute(arc_linear_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, F_SMEM);
   });
   if (attr_err != cudaSuccess) return attr_err;
   if (getenv("ARC_FUSED_VERBOSE"))

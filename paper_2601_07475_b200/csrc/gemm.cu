@@ -139,7 +139,9 @@ __device__ __forceinline__ void epilogue_tile(const Args& args, const CUtensorMa
     if (cc == BN / 32 - 1) release(buf_free);
     const int n0 = nbk * BN + c * 32;
     if ((args.y_fp32 || nsplit > 1) && m < M && n0 < N) {
-      float* yr = nsplit > 1 ? args.ws + ((int64_t)ks * M + m) * N + n0
+      // split-K partial rows use the stride round_up(N, 4) so the float4 stores stay 16-byte
+      // aligned for any N (plan_gemm sizes the workspace with the same stride)
+      float* yr = nsplit > 1 ? args.ws + ((int64_t)ks * M + m) * ((N + 3) & ~3) + n0
                              : static_cast<float*>(args.y) + (int64_t)m * args.ldy + n0;
       if (n0 + 32 <= N) {
 #pragma unroll
@@ -621,14 +623,15 @@ __global__ void arc_splitk_reduce_kernel(const float* __restrict__ ws, int nspli
                                          int64_t ldy, int y_fp32, int swiglu) {
   pdl_launch_dependents();
   pdl_wait();
-  const int64_t total = (int64_t)M * N;
+  const int ldp = (N + 3) & ~3;  // partial row stride (see epilogue_tile)
+  const int64_t total = (int64_t)M * ldp;
   if (swiglu) {  // h[m][j] from gate column 32(j/16) + j%16 and up column +16 (see epilogue_tile)
     const int NH = N / 2;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (int64_t)M * NH;
          i += (int64_t)gridDim.x * blockDim.x) {
       const int64_t m = i / NH;
       const int j = (int)(i - m * NH);
-      const int64_t ig = m * N + 32 * (j >> 4) + (j & 15), iu = ig + 16;
+      const int64_t ig = m * ldp + 32 * (j >> 4) + (j & 15), iu = ig + 16;
       float g = ws[ig], u = ws[iu];
       for (int k = 1; k < nsplit; ++k) {
         g = __fadd_rn(g, ws[(int64_t)k * total + ig]);
@@ -639,10 +642,11 @@ __global__ void arc_splitk_reduce_kernel(const float* __restrict__ ws, int nspli
     }
     return;
   }
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    float acc = ws[i];
-    for (int k = 1; k < nsplit; ++k) acc = __fadd_rn(acc, ws[(int64_t)k * total + i]);
-    const int64_t m = i / N, n = i - m * N;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (int64_t)M * N;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t m = i / N, n = i - m * N, ip = m * ldp + n;
+    float acc = ws[ip];
+    for (int k = 1; k < nsplit; ++k) acc = __fadd_rn(acc, ws[(int64_t)k * total + ip]);
     if (y_fp32) static_cast<float*>(y)[m * ldy + n] = acc;
     else static_cast<__nv_bfloat16*>(y)[m * ldy + n] = __float2bfloat16_rn(acc);
   }
@@ -716,10 +720,11 @@ bool make_operand_map(CUtensorMap* m, const void* base, int64_t rows, int64_t ro
 // Co-resident clusters of the persistent grid (clusters of 4 may not tile every GPC's SMs).
 int64_t max_clusters(int CL, bool pair) {
   if (CL == 1) return num_sms();
-  static int cache[2][5] = {};
+  static int cache[PerDeviceOnce::kMaxDev][2][5] = {};
   int dev = 0;
   cudaGetDevice(&dev);
-  int& c = cache[pair ? 1 : 0][CL];
+  if (dev < 0 || dev >= PerDeviceOnce::kMaxDev) dev = 0;
+  int& c = cache[dev][pair ? 1 : 0][CL];
   if (c == 0) {
     cudaLaunchConfig_t cfg;
     memset(&cfg, 0, sizeof(cfg));
@@ -780,7 +785,7 @@ GemmPlan plan_gemm(int64_t M, int64_t N, int64_t Kp) {
       }
     }
   }
-  pl.ws_bytes = pl.nsplit > 1 ? (size_t)pl.nsplit * (size_t)M * (size_t)N * sizeof(float) : 0;
+  pl.ws_bytes = pl.nsplit > 1 ? (size_t)pl.nsplit * (size_t)M * (size_t)round_up(N, 4) * sizeof(float) : 0;
   return pl;
 }
 
@@ -814,10 +819,9 @@ cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t stream, const char** 
     if (detail) *detail = "cuTensorMapEncodeTiled failed";
     return cudaErrorInvalidValue;
   }
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(arc_gemm_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+  static PerDeviceOnce attr_once;
+  const cudaError_t attr_err = attr_once.run([] {
+    cudaError_t attr_err = cudaFuncSetAttribute(arc_gemm_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     if (attr_err == cudaSuccess)
       attr_err = cudaFuncSetAttribute(arc_gemm_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     if (attr_err == cudaSuccess)
@@ -827,6 +831,7 @@ cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t stream, const char** 
       attr_err = cudaFuncSetAttribute(arc_gemm_pair_kernel<4, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, p_smem_bytes(5));
     if (attr_err == cudaSuccess)
       attr_err = cudaFuncSetAttribute(arc_gemm_pair_kernel<2, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, p_smem_bytes(4));
+    return attr_err;
   });
   if (attr_err != cudaSuccess) return attr_err;
   Args a;

@@ -158,13 +158,24 @@ ARC_DEV void silu_mul_block16(float (&z)[16], const uint8_t* row, const uint32_t
 }
 
 // MX block scale (reading Q25): for block abs-max a > 0, e = ceil(log2(RN(a/6))) (exact from the
-// fp32 bits), k = 2^-e (t = z*k exact), code = E4M3 code of 2^(e - c); a = 0 -> code 0, k = 1.
-// Exponents outside what E4M3 / the fp32 multiplier can hold give unspecified codes (the oracle
-// reports a range error there).
+// fp32 bits), clamped to [lo, hi] -- the exponents whose 2^(e - c) E4M3 can hold -- so a block far
+// below the tensor's range flushes toward 0 and one above it saturates at +-6 with a scale that
+// matches its codes (reading Q25b); k = 2^-e (t = z*k exact), code = E4M3 code of 2^(e - c);
+// a = 0 -> code 0, k = 1.
 ARC_DEV uint32_t mx_pow2_code(int k) {
   if (k >= -6) return (uint32_t)min(k + 7, 15) << 3;
   return 1u << max(k + 9, 0);
 }
+ARC_DEV int mx_ceil_exp(float a) {  // ceil(log2(RN(a / 6))) for a > 0
+  const uint32_t b = __float_as_uint(__fdiv_rn(a, 6.0f));
+  const int ex = (int)((b >> 23) & 0xFFu);
+  if (ex == 0) {  // subnormal RN(a/6): value = m 2^-149, ceil(log2) = 32 - clz(m - 1) - 149
+    const uint32_t m = b & 0x7FFFFFu;
+    return (m <= 1u ? 0 : 32 - __clz(m - 1u)) - 149;
+  }
+  return ex - 127 + ((b & 0x7FFFFFu) != 0u);
+}
+ARC_DEV float mx_pow2_inv(int e) { return __int_as_float((min(max(127 - e, 1), 254)) << 23); }
 ARC_DEV void mx_scale(float a, int c, uint32_t& code, float& k, int& e) {
   if (a == 0.0f) {
     code = 0u;
@@ -172,10 +183,9 @@ ARC_DEV void mx_scale(float a, int c, uint32_t& code, float& k, int& e) {
     e = 0;
     return;
   }
-  const uint32_t b = __float_as_uint(__fdiv_rn(a, 6.0f));
-  e = (int)((b >> 23) & 0xFFu) - 127 + ((b & 0x7FFFFFu) != 0u);
+  e = min(max(mx_ceil_exp(a), c - 9), c + 8);
   code = mx_pow2_code(e - c);
-  k = __int_as_float((min(max(127 - e, 1), 254)) << 23);
+  k = mx_pow2_inv(e);
 }
 
 // Rows of a tile.  Tile t of the 128-row group g holds rows base + 32 i, i < R, with
@@ -548,12 +558,14 @@ __global__ void __launch_bounds__(1024) arc_quant_kernel(QuantArgs p) {
               residual16(t, packed, ee);
               float a2 = absmax16(ee);
               a2 = fmaxf(a2, __shfl_xor_sync(0xffffffffu, a2, 1));
-              uint32_t c2;
-              float k2;
-              int e2;
-              mx_scale(a2, 0, c2, k2, e2);           // e2 relative to 2^e1
-              if (a != 0.0f && a2 != 0.0f) c2 = mx_pow2_code(e1 + e2 - mx_c);
-              else c2 = 0u;
+              // stage 2 in units of 2^e1: absolute exponent e1 + e2 clamped like the primary's
+              uint32_t c2 = 0u;
+              float k2 = 1.0f;
+              if (a != 0.0f && a2 != 0.0f) {
+                const int ea = min(max(e1 + mx_ceil_exp(a2), mx_c - 9), mx_c + 8);
+                c2 = mx_pow2_code(ea - mx_c);
+                k2 = mx_pow2_inv(ea - e1);
+              }
               packed = encode16(ee, k2);
               sfb = c2;
             }  // weight mode: bitwise duplicate of the primary block
@@ -694,6 +706,19 @@ __global__ void arc_absmax_all_kernel(const uint16_t* x, int64_t rows, int K, in
 __global__ void arc_finalize_scale_kernel(float* gs) {
   const float amax = *gs;
   *gs = amax > 0.0f ? __fdiv_rn(2688.0f, amax) : 1.0f;
+}
+
+// MXFP4-ARC tensor offset (reading Q25): gs = 2^-c, c = ceil(log2(RN(amax/6))) - 8, in place over the
+// amax bits; amax = 0 -> 1.  Same arithmetic as arc_mx_tensor_scale on the host.
+__global__ void arc_finalize_mx_scale_kernel(float* gs) {
+  const float amax = *gs;
+  int c = 0;
+  if (amax > 0.0f) {
+    int x;
+    const float f = frexpf(__fdiv_rn(amax, 6.0f), &x);
+    c = (f == 0.5f ? x - 1 : x) - 8;
+  }
+  *gs = ldexpf(1.0f, -c);
 }
 
 // ------------------------------------------------------------------ launchers
@@ -930,7 +955,8 @@ cudaError_t launch_calib_absmax(const void* x, int64_t rows, int K, int64_t ld, 
   return cudaGetLastError();
 }
 
-cudaError_t launch_tensor_scale(const void* x, int64_t rows, int K, int64_t ld, float* gs_out, cudaStream_t s) {
+cudaError_t launch_tensor_scale(const void* x, int64_t rows, int K, int64_t ld, float* gs_out, cudaStream_t s,
+                                int mx) {
   cudaError_t e = cudaMemsetAsync(gs_out, 0, sizeof(float), s);
   if (e != cudaSuccess) return e;
   const int64_t n8 = rows * (K / 8);
@@ -939,7 +965,8 @@ cudaError_t launch_tensor_scale(const void* x, int64_t rows, int K, int64_t ld, 
                                                       reinterpret_cast<unsigned int*>(gs_out));
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  arc_finalize_scale_kernel<<<1, 1, 0, s>>>(gs_out);
+  if (mx) arc_finalize_mx_scale_kernel<<<1, 1, 0, s>>>(gs_out);
+  else arc_finalize_scale_kernel<<<1, 1, 0, s>>>(gs_out);
   return cudaGetLastError();
 }
 

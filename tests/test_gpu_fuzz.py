@@ -7,7 +7,7 @@ import torch
 
 import oracle
 from paper_2601_07475_b200 import synth
-from _helpers import dev_bits
+from _helpers import dev_bits, valid_sf_mask
 
 pytestmark = pytest.mark.gpu
 
@@ -31,20 +31,26 @@ def test_quantize_fuzz(M, K, S, layout):
     qw = A.quantize_weight(w, prof)
     torch.cuda.synchronize()
     perm, gs = prof.perm.cpu().numpy(), float(prof.gs.item())
-    oc, _ = oracle.quantize_activation(dev_bits(x), perm, S, gs, layout)
+    Kp = oracle.kp(K, S)
+    ma, mw = valid_sf_mask(M, Kp), valid_sf_mask(40, Kp)
+    oc, osf = oracle.quantize_activation(dev_bits(x), perm, S, gs, layout)
     assert np.array_equal(codes.cpu().numpy(), oc)
-    bc, _ = oracle.quantize_weight(dev_bits(w), perm, S, float(qw.gs.item()), layout)
+    assert np.array_equal(sf.cpu().numpy()[ma], osf[ma]), "activation scale bytes differ"
+    bc, bsf = oracle.quantize_weight(dev_bits(w), perm, S, float(qw.gs.item()), layout)
     assert np.array_equal(qw.codes.cpu().numpy(), bc)
+    assert np.array_equal(qw.sf.cpu().numpy()[mw], bsf[mw]), "weight scale bytes differ"
     if K <= 16384 and M <= 64:
         g = synth.rmsnorm_weight(K, seed=3, device="cuda")
-        cn, _ = A.rmsnorm_quantize_activation(x, g, 1e-5, prof)
+        cn, sn = A.rmsnorm_quantize_activation(x, g, 1e-5, prof)
         gu = synth.gate_up(M, K, st, seed=4, device="cuda")
-        cs, _ = A.silu_mul_quantize_activation(gu, prof)
+        cs, ss = A.silu_mul_quantize_activation(gu, prof)
         torch.cuda.synchronize()
-        on, _ = oracle.quantize_activation(oracle.rmsnorm(dev_bits(x), dev_bits(g), 1e-5), perm, S, gs, layout)
+        on, osn = oracle.quantize_activation(oracle.rmsnorm(dev_bits(x), dev_bits(g), 1e-5), perm, S, gs, layout)
         assert np.array_equal(cn.cpu().numpy(), on)
-        os_, _ = oracle.quantize_activation(oracle.silu_mul(dev_bits(gu)), perm, S, gs, layout)
+        assert np.array_equal(sn.cpu().numpy()[ma], osn[ma]), "RMSNorm-quantize scale bytes differ"
+        os_, oss = oracle.quantize_activation(oracle.silu_mul(dev_bits(gu)), perm, S, gs, layout)
         assert np.array_equal(cs.cpu().numpy(), os_)
+        assert np.array_equal(ss.cpu().numpy()[ma], oss[ma]), "SiLU-mul-quantize scale bytes differ"
 
 
 _rng2 = np.random.default_rng(7)

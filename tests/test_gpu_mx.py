@@ -63,3 +63,33 @@ def test_mx_weight_and_gemm(A, M, N, K, S):
     yref, bound = oracle.gemm_reference(ac, asf, bc, bsf, 2.0 ** -cx, 2.0 ** -cw)
     err = np.abs(y.cpu().numpy().astype(np.float64) - yref)
     assert (err <= bound).all(), f"worst err/bound {np.max(err / np.maximum(bound, 1e-300))}"
+
+
+@pytest.mark.parametrize("layout", [0, 1])
+def test_mx_wide_dynamic_range_bit_exact(A, layout):
+    """blocks whose exponent leaves E4M3's powers of two for the tensor offset (dynamic
+    range > 2^17, runtime values above the calibrated max) are clamped as reading Q25b says -- codes
+    and scales bit-exact against the oracle, activation and weight mode."""
+    M, K, S = 64, 1024, 64
+    st = synth.Structure(K, S, seed=3)
+    x = synth.activation(M, K, st, seed=4, device="cuda").float()
+    g = torch.Generator(device="cuda").manual_seed(5)
+    x = x * torch.exp2(torch.randint(-24, 9, (1, K), generator=g, device="cuda").float())
+    x = x.to(torch.bfloat16)
+    prof = A.calibrate([synth.activation(256, K, st, seed=9, device="cuda")], s_override=S, layout=layout)
+    mprof = A.mx_profile(prof, prof.M)      # offset from the calibration max, below the runtime max
+    c = -int(np.log2(float(mprof.gs.item())))
+    codes, sf = A.quantize_activation_mx(x, mprof)
+    qw = A.quantize_weight_mx(x[:40].contiguous(), prof)
+    torch.cuda.synchronize()
+    perm = prof.perm.cpu().numpy()
+    oc, osf = oracle.quantize_mx(dev_bits(x), perm, S, c, layout=layout)
+    mask = valid_sf_mask(M, _kp(K, S))
+    assert np.array_equal(codes.cpu().numpy(), oc)
+    assert np.array_equal(sf.cpu().numpy()[mask], osf[mask])
+    cw = -int(np.log2(float(qw.gs.item())))
+    assert cw == oracle.mx_offset(float(x[:40].float().abs().max()))
+    bc, bsf = oracle.quantize_mx(dev_bits(x[:40]), perm, S, cw, weight=True, layout=layout)
+    mw = valid_sf_mask(40, _kp(K, S))
+    assert np.array_equal(qw.codes.cpu().numpy(), bc)
+    assert np.array_equal(qw.sf.cpu().numpy()[mw], bsf[mw])

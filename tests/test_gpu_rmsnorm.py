@@ -114,3 +114,27 @@ def test_linear_rmsnorm_parity(A, M, N, K, S):
     yref, bound = oracle.gemm_reference(ac, asf, bc, bsf, gs, gs_w)
     err = np.abs(y.cpu().numpy().astype(np.float64) - yref)
     assert (err <= bound).all(), f"worst err/bound {np.max(err / np.maximum(bound, 1e-300))}"
+
+
+@pytest.mark.parametrize("M,K", [(7, 48), (64, 4096), (20, 14336)])
+@pytest.mark.parametrize("eps", [1e-5, 0.0])
+def test_rmsnorm_vs_float64_formula(A, M, K, eps):
+    """arc_rmsnorm against the float64 LLaMA RMSNorm of the same bf16 inputs, independent of any
+    reduction order: within the two bf16 roundings (2^-8 each) plus fp32 rounding of the scale."""
+    st, h, g = _inputs(M, K, 16, seed=5 * K + M)
+    y = A.rmsnorm(h, g, eps).float().cpu().numpy().astype(np.float64)
+    hf, gf = h.float().cpu().numpy().astype(np.float64), g.float().cpu().numpy().astype(np.float64)
+    ref = gf * hf / np.sqrt((hf ** 2).mean(axis=1, keepdims=True) + np.float64(np.float32(eps)))
+    assert np.all(np.abs(y - ref) <= np.abs(ref) * (2.0 ** -7 + 2.0 ** -15) + 1e-30)
+
+
+@pytest.mark.parametrize("K", [48, 4096, 14336])
+def test_rmsnorm_exact_rows_ieee(A, K):
+    """On rows whose sum of squares is exact in fp32 (any order), arc_rmsnorm's bits equal the
+    order-independent IEEE div / sqrt / div + two bf16 roundings computed with numpy/torch."""
+    from test_oracle_rmsnorm import _exact_rows, _ieee_rmsnorm_of_exact_rows
+    x = _exact_rows(33, K, seed=K + 1)
+    g = synth.rmsnorm_weight(K, seed=K, device="cpu")
+    y = A.rmsnorm(x.cuda(), g.cuda(), 1e-5)
+    torch.cuda.synchronize()
+    assert np.array_equal(dev_bits(y), _ieee_rmsnorm_of_exact_rows(x, g, 1e-5))

@@ -123,10 +123,49 @@ def test_gemm_over_physical_bytes_equals_mx_dot_products():
     assert np.allclose(y, va @ vb.T, rtol=0, atol=1e-9 * np.abs(va).max() * np.abs(vb).max() * 320)
 
 
-def test_range_error():
+def test_out_of_range_blocks_flush():
+    """Reading Q25b: a block 2^-30 below the tensor's range gets the smallest scale 2^(c-9) (E4M3
+    code 0x01) and codes that match it: x / 2^(c-9) rounds to 0 here, so it dequantizes to 0."""
     x = torch.zeros(1, 64)
     x[0, 0] = 1e6
     x[0, 40] = 1e-6
-    with pytest.raises(oracle.OracleError):
-        oracle.quantize_mx(x.to(torch.bfloat16), np.arange(64, dtype=np.int32), 0,
-                           oracle.mx_offset(1e6))
+    c = oracle.mx_offset(1e6)
+    assert c == int(np.ceil(np.log2(np.float32(1e6) / 6))) - 8
+    codes, sf = oracle.quantize_mx(x.to(torch.bfloat16), np.arange(64, dtype=np.int32), 0, c)
+    vals, scales = _decode(codes, sf, 1, 64, 0, c)
+    assert np.all(scales[0, 32:] == 2.0 ** (c - 9)) and np.all(vals[0, 32:] == 0.0)
+    assert vals[0, 0] == _nearest_e2m1(np.array([1e6 / 2.0 ** (c + 8)]))[0] * 2.0 ** (c + 8)
+
+
+def test_out_of_range_blocks_saturate():
+    """Reading Q25b: a block above the offset's range (runtime max above the calibrated one) gets the
+    largest scale 2^(c+8) and saturated codes +-6: every element dequantizes to sign * 6 * 2^(c+8)
+    (clip), never to a shrunken value."""
+    x = torch.zeros(2, 32)
+    x[0, :] = 3e6
+    x[1, ::2] = -5e5
+    xb = x.to(torch.bfloat16)
+    c = oracle.mx_offset(1e3)
+    codes, sf = oracle.quantize_mx(xb, np.arange(32, dtype=np.int32), 0, c)
+    vals, scales = _decode(codes, sf, 2, 32, 0, c)
+    assert np.all(scales == 2.0 ** (c + 8))
+    assert np.all(vals[0] == 6.0 * 2.0 ** (c + 8))
+    assert np.all(vals[1, ::2] == -6.0 * 2.0 ** (c + 8)) and np.all(vals[1, 1::2] == 0.0)
+
+
+def test_out_of_range_residual_clamped():
+    """Outlier (residual) blocks: the residual's absolute exponent e + e2 is clamped too, so the
+    dequantized primary + residual never exceeds what the clamped scales can represent, and an
+    in-range block next to an out-of-range one is unaffected."""
+    x = torch.zeros(1, 64)
+    x[0, :32] = torch.linspace(-3e6, 2e6, 32)
+    x[0, 32:] = torch.linspace(-700, 900, 32)
+    xb = x.to(torch.bfloat16)
+    c = oracle.mx_offset(1e3)
+    codes, sf = oracle.quantize_mx(xb, np.arange(64, dtype=np.int32), 64, c)
+    vals, scales = _decode(codes, sf, 1, 64, 64, c)
+    assert np.all(scales[0] <= 2.0 ** (c + 8)) and np.all(scales[0] >= 2.0 ** (c - 9))
+    xf = xb.float().numpy().astype(np.float64)[0]
+    # in-range block 1: primary + residual within half a residual quantum of x (Q25's definition)
+    rec = vals[0, 32:64] + vals[0, 96:128]
+    assert np.all(np.abs(rec - xf[32:]) <= scales[0, 96:128] * 0.5 + 1e-9 * np.abs(xf[32:]))

@@ -98,3 +98,51 @@ def test_nonfinite_is_an_error():
         oracle.rmsnorm(x, g, 1e-5)
     with pytest.raises(oracle.OracleError):  # all-zero row with eps = 0 -> 1/0
         oracle.rmsnorm(torch.zeros(1, 64, dtype=torch.bfloat16), g, 0.0)
+
+
+def _exact_rows(M, K, seed):
+    """Rows of n * 2^-3 with |n| <= 15: every square is a multiple of 2^-6 and every partial sum of
+    squares stays below 2^24 * 2^-6, so the fp32 sum of squares is exact in ANY order."""
+    rng = np.random.default_rng(seed)
+    n = rng.integers(-15, 16, size=(M, K)).astype(np.float32)
+    n[:, 0] = 7.0  # no all-zero row
+    return torch.from_numpy(n * np.float32(0.125)).to(torch.bfloat16)
+
+
+def _ieee_rmsnorm_of_exact_rows(x: torch.Tensor, g: torch.Tensor, eps: float) -> np.ndarray:
+    """Order-independent definition of reading Q23 on exact rows: ss exact (float64 sum == fp32 sum),
+    mean = RN32(ss / K), r = RN32(1 / RN32(sqrt(RN32(mean + eps)))), y = bf16(g * bf16(x * r)) with
+    RN-even bf16 roundings done by torch's float32 -> bfloat16 cast (a third-party rounding)."""
+    xf = x.float().numpy()
+    K = xf.shape[1]
+    ss64 = (xf.astype(np.float64) ** 2).sum(axis=1)
+    ss = ss64.astype(np.float32)
+    assert np.array_equal(ss.astype(np.float64), ss64)           # the sum really is exact in fp32
+    mean = ss / np.float32(K)
+    r = np.float32(1.0) / np.sqrt(mean + np.float32(eps))
+    assert r.dtype == np.float32
+    t = torch.from_numpy(xf * r[:, None]).to(torch.bfloat16).float()
+    y = (g.float()[None, :] * t).to(torch.bfloat16)
+    return _bits(y)
+
+
+@pytest.mark.parametrize("K", [16, 48, 256, 1040, 4096, 14336])
+@pytest.mark.parametrize("eps", [0.0, 1e-5, 1e-6])
+def test_exact_rows_match_order_independent_ieee(K, eps):
+    """The oracle's reduction order (Q23: 32 round-robin partials + pairwise trees, chosen
+    in 036374d to suit the kernel's conflict-free loads) is a decision; the arithmetic after the
+    reduction is not.  On rows whose sum of squares is exact in fp32 the order cannot matter, so the
+    oracle's bits must equal the IEEE div / sqrt / div and the two bf16 roundings computed here
+    independently with numpy float32 (each op correctly rounded) and torch's bf16 cast."""
+    x = _exact_rows(9, K, seed=K)
+    _, g = _rows(1, K, seed=K + 1)
+    assert np.array_equal(oracle.rmsnorm(x, g, eps), _ieee_rmsnorm_of_exact_rows(x, g, eps))
+
+
+def test_exact_rows_scale_is_ieee_reciprocal_sqrt():
+    x = _exact_rows(4, 4096, seed=5)
+    for i in range(4):
+        xf = x[i].float().numpy()
+        ss = np.float32((xf.astype(np.float64) ** 2).sum())
+        want = np.float32(1.0) / np.sqrt(ss / np.float32(4096) + np.float32(1e-5))
+        assert np.float32(oracle.rmsnorm_scale(_bits(x[i:i + 1])[0], 1e-5)) == want
