@@ -2,30 +2,38 @@
 """Benchmark of the ARC-NVFP4 linear hot path on B200 (BASELINE.json metric:
 "ARC NVFP4 linear TFLOPS (% FP4 tensor peak) + quantize HBM GB/s, 1/2/4/8 GPU").
 
-One step = the four ARC linear sites of one LLaMA-3-8B decoder layer at prefill
-(BASELINE.json configs[1]): fused qkv (K=4096 -> N=6144), o (4096 -> 4096), fused
-gate-up (4096 -> 28672), down (14336 -> 4096), M = 8192 tokens, S = 128 augmented
-channels each; every site = arc_quantize_activation + arc_gemm (what arc_linear
-runs).  Synthetic activations with injected outlier channels, random weights
-(DESIGN.md "Input recipe"); per-step footprint (~0.6 GB) is far above the 126 MB L2.
+One step = the four ARC linear sites of one decoder layer, each = arc_quantize_activation +
+arc_gemm (what arc_linear runs), synthetic activations with injected outlier channels and random
+weights (DESIGN.md "Input recipe"):
 
-N > 1 (torchrun): Megatron-style tensor parallelism of the same layer (strong
-scaling): qkv / gate-up column-parallel over N (no communication), o / down
-row-parallel over K with per-rank calibration and an NCCL all-reduce of Y.
+* N = 1 (default workload llama3-8b, BASELINE configs[1], prefill M = 8192): fused qkv
+  (K=4096 -> N=6144), o (4096 -> 4096), fused gate-up (4096 -> 28672), down (14336 -> 4096),
+  S = 128 augmented channels each.
+* N > 1 (default workload llama3-70b, BASELINE configs[3]): Megatron tensor parallelism of one
+  LLaMA-3-70B layer (strong scaling): qkv (8192 -> 10240) and gate-up (8192 -> 57344)
+  column-parallel over N (replicated input, no communication), o (8192 -> 8192) and down
+  (28672 -> 8192) row-parallel over K with per-rank calibration (S_r = max(16, 128/P), outliers
+  injected balanced over the K shards) and an NCCL all-reduce of Y.  `--workload llama3-70b` at
+  N = 1 gives the same layer unsharded.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl arc|reference] [--M 8192]
+                    [--workload auto|llama3-8b|llama3-70b] [--tp-layout mp|sp]
+
+`--gpus N` with N > 1 and no WORLD_SIZE in the environment re-executes itself under
+torch.distributed.run with N ranks (one per GPU); it exits non-zero if fewer than N GPUs are visible.
 """
 from __future__ import annotations
 
 import argparse
 import json
-import zlib
 import math
 import os
+import socket
 import subprocess
 import sys
 import threading
 import time
+import zlib
 
 import numpy as np
 import torch
@@ -35,8 +43,13 @@ sys.path.insert(0, ROOT)
 
 from paper_2601_07475_b200 import synth  # noqa: E402
 
-SITES = synth.LLAMA3_8B_SITES
 S_AUG = 128
+COL_SITES = ("qkv", "gate_up")
+WORKLOADS = {
+    "llama3-8b": (synth.LLAMA3_8B_SITES, "llama3-8b-layer-4-arc-linears-prefill"),
+    "llama3-70b": (synth.LLAMA3_70B_SITES, "llama3-70b-layer-4-arc-linears-tp"),
+}
+CAL_ROWS = 4096
 
 
 def _peaks():
@@ -103,138 +116,317 @@ class Clocks:
         return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def _gs_float(g) -> float:
+    return float(g.item()) if isinstance(g, torch.Tensor) else float(g)
+
+
 # ----------------------------------------------------------------------------- workload
 class Site:
-    def __init__(self, name, K, N, M, S, rank, world, mode, device, A, layout="mp"):
-        """mode: 'full' (1 GPU), 'col' (column-parallel shard of N), 'row' (row-parallel shard of K).
-        Sharded sites are built with paper_2601_07475_b200.tp (the tested host logic).  layout 'sp'
-        (sequence parallel): a col site quantizes its M/P token rows and all-gathers the
-        packed codes + scales; a row site reduce-scatters its output over tokens.  'mp': a col site
-        quantizes the replicated M rows; a row site all-reduces."""
+    """One ARC linear site of the layer on this rank.  mode: 'full' (1 GPU), 'col' (column-parallel
+    shard of N) or 'row' (row-parallel shard of K).  Sharded sites are built with
+    paper_2601_07475_b200.tp (the tested host logic).  layout 'sp' (sequence parallel): a
+    col site quantizes its M/P token rows and all-gathers the packed codes + scales; a row site
+    reduce-scatters its output over tokens.  'mp': col sites quantize the replicated M rows, row sites
+    all-reduce.  B is the compute backend (the libarc binding; tests pass an oracle stand-in)."""
+
+    def __init__(self, B, name, K, N, M, S, rank, world, device, layout="mp", out_dtype=torch.bfloat16,
+                 cal_rows=CAL_ROWS, keep_host=False):
         from paper_2601_07475_b200 import tp
-        self.name, self.M, self.mode = name, M, mode
+        self.name, self.M = name, M
+        self.mode = "full" if world == 1 else ("col" if name in COL_SITES else "row")
         self.sp = layout == "sp" and world > 1
+        self.world, self.rank = world, rank
         seed = zlib.crc32(name.encode()) % 1000
-        st = synth.Structure(K, S, seed=seed * 31)
-        cal = synth.activation(4096, K, st, seed=seed + 1000, device=device)
+        st = synth.Structure(K, S, seed=seed * 31, shards=world if self.mode == "row" else 1)
+        cal = synth.activation(cal_rows, K, st, seed=seed + 1000, device=device)
         w = synth.weight(N, K, seed=seed * 7, device=device)
         x = synth.activation(M, K, st, seed=seed + 1, device=device)
-        if mode == "full":
-            self.prof = A.calibrate([cal], s_override=S)
-            self.qw = A.quantize_weight(w, self.prof)
-            self.x = x
-        elif mode == "col":
-            prof = A.calibrate([cal], s_override=S)
-            lin = tp.ColumnParallelLinear(w, prof, rank, world, backend=A)
+        self.S_target = S
+        if self.mode == "full":
+            self.prof = B.calibrate([cal], s_override=S)
+            self.qw = B.quantize_weight(w, self.prof)
+            self.x, self.w_local, self.cal_local = x, w, cal
+        elif self.mode == "col":
+            prof = B.calibrate([cal], s_override=S)
+            lin = tp.ColumnParallelLinear(w, prof, rank, world, backend=B)
             self.prof, self.qw, self.x = lin.profile, lin.qweight, x
+            self.w_local = w[lin.shard.lo:lin.shard.hi]
+            self.cal_local = cal
         else:
             S_r = max(16, (S // world + 15) // 16 * 16)
-            lin = tp.RowParallelLinear(w, cal, rank, world, s_override=S_r, backend=A)
+            lin = tp.RowParallelLinear(w, cal, rank, world, s_override=S_r, backend=B)
             self.prof, self.qw = lin.profile, lin.qweight
             self.x = x[:, lin.shard.lo:lin.shard.hi].contiguous()
+            self.w_local = w[:, lin.shard.lo:lin.shard.hi]
+            self.cal_local = cal[:, lin.shard.lo:lin.shard.hi]
+        if not keep_host:
+            self.w_local = self.cal_local = None
         del cal, w, x
-        Kl, Nl, S_l = self.prof.K, self.qw.N, self.prof.S
+        Kl, Nl, S_l = self.x.shape[1], self.qw.codes.shape[0], self.prof.S
         self.K, self.N, self.S = Kl, Nl, S_l
-        self.gs_w = float(self.qw.gs.item())
-        Kp, cb, sb = A.buffer_sizes(M, Kl, S_l)
+        Kp, cb, sb = B.buffer_sizes(M, Kl, S_l)
         self.Kp = Kp
         self.codes = torch.empty(M, Kp // 2, dtype=torch.uint8, device=device)
         self.sf = torch.empty(sb, dtype=torch.uint8, device=device)
-        self.y = torch.empty(M, Nl, dtype=torch.bfloat16, device=device)
+        self.y = torch.empty(M, Nl, dtype=out_dtype, device=device)
         self.m_q = M  # rows this rank quantizes
-        if self.sp and mode == "col":
+        self.out_rows = M // world if (self.sp and self.mode == "row") else M
+        if self.sp and self.mode == "col":
             ml = M // world
             assert ml % 128 == 0, "sequence-parallel rows per rank must be a multiple of 128"
             self.x = self.x[rank * ml:(rank + 1) * ml].contiguous()
-            self.codes_loc = torch.empty(ml, Kp // 2, dtype=torch.uint8, device=device)
-            self.sf_loc = torch.empty(ml * Kp // 16, dtype=torch.uint8, device=device)
             self.m_q = ml
-        if self.sp and mode == "row":
-            self.y_rs = torch.empty(M // world, Nl, dtype=torch.bfloat16, device=device)
-        self.ws = A.Workspace(device)
+        self.ws = B.Workspace(device)
         self.flops = 2.0 * M * Nl * (Kl + S_l)                       # SPEC S:322 cost model, algorithmic
         self.flops_eff = 2.0 * M * Nl * Kl
         self.q_bytes = self.m_q * (2 * Kl + Kp // 2 + Kp // 16) + 4 * Kl  # bf16 read + codes + scales + perm
         self.g_bytes = Nl * Kp * 9 // 16 + M * Kp * 9 // 16 + M * Nl * 2
+        self.comm_bytes = M * Nl * self.y.element_size() if self.mode == "row" else (
+            M * (Kp // 2 + Kp // 16) if self.sp else 0)
 
 
-def build_sites(A, M, rank, world, device, layout="mp"):
-    sites = []
-    for name, K, N in SITES:
-        if world == 1:
-            mode = "full"
-        else:
-            mode = "col" if name in ("qkv", "gate_up") else "row"
-        sites.append(Site(name, K, N, M, S_AUG, rank, world, mode, device, A, layout))
-    return sites
+def workload_sites(name):
+    return WORKLOADS[name][0]
 
 
-def run_step(A, sites, ev=None, pg=None):
+def build_sites(B, M, rank, world, device, layout="mp", workload="llama3-8b", out_dtype=torch.bfloat16,
+                S=S_AUG, cal_rows=CAL_ROWS, keep_host=False, sites=None):
+    out = []
+    for name, K, N in (sites or workload_sites(workload)):
+        out.append(Site(B, name, K, N, M, S, rank, world, device, layout, out_dtype, cal_rows, keep_host))
+    return out
+
+
+def run_step(B, sites, ev=None, pg=None):
+    """One pass of the layer's linears on this rank.  ev[i] = 4 CUDA events per site: before quantize,
+    after quantize, after GEMM, after the collective."""
+    from paper_2601_07475_b200 import tp
     for i, s in enumerate(sites):
         if ev is not None:
             ev[i][0].record()
         if s.sp and s.mode == "col":
             # sequence parallel: quantize this rank's token rows, all-gather the packed codes + scales
-            A.quantize_activation(s.x, s.prof, s.codes_loc, s.sf_loc)
-            torch.distributed.all_gather_into_tensor(s.codes, s.codes_loc, group=pg)
-            torch.distributed.all_gather_into_tensor(s.sf, s.sf_loc, group=pg)
+            c_loc, sf_loc = B.quantize_activation(s.x, s.prof)
+            s.codes.copy_(tp._all_gather_rows(c_loc, pg))
+            s.sf.copy_(tp._all_gather_rows(sf_loc.reshape(s.m_q // 128, -1), pg).reshape(-1))
         else:
-            A.quantize_activation(s.x, s.prof, s.codes, s.sf)
+            B.quantize_activation(s.x, s.prof, s.codes, s.sf)
         if ev is not None:
             ev[i][1].record()
-        A.gemm(s.codes, s.sf, s.prof.gs, s.qw, out=s.y, ws=s.ws)
+        B.gemm(s.codes, s.sf, s.prof.gs, s.qw, out=s.y, ws=s.ws)
         if ev is not None:
             ev[i][2].record()
         if s.mode == "row" and pg is not None:
             if s.sp:
-                torch.distributed.reduce_scatter_tensor(s.y_rs, s.y, group=pg)
+                s.y_out = tp._reduce_scatter_rows(s.y, pg)
             else:
                 torch.distributed.all_reduce(s.y, group=pg)
+        if ev is not None:
+            ev[i][3].record()
 
 
 # ----------------------------------------------------------------------------- oracle (CPU) legs
-def oracle_sample(sites_meta, rows_per_site=4, budget_s=20.0):
-    """Time the oracle (plain C, single thread) on a bounded sample of the same
-    workload: for each site, ARC-quantize `rows_per_site` activation rows and run
-    the exact GEMM of those rows against the site's full weight.  Returns
-    (TFLOP/s in the bench's unit, description, seconds)."""
-    import oracle
-    oracle.build()
-    t_total, flops_total, done = 0.0, 0.0, []
-    for (name, K, N, S, xbits, perm, gs, wcodes, wsf, gs_w) in sites_meta:
-        t0 = time.perf_counter()
-        ac, asf = oracle.quantize_activation(xbits, perm, S, gs)
-        oracle.gemm_reference(ac, asf, wcodes, wsf, gs, gs_w)
-        dt = time.perf_counter() - t0
-        t_total += dt
-        flops_total += 2.0 * xbits.shape[0] * N * (K + S)
-        done.append(f"{name}:{xbits.shape[0]}x{N}x{K}+{S}")
-        if t_total > budget_s:
-            break
-    return flops_total / t_total / 1e12, ";".join(done), t_total
-
-
-def sites_meta_for_oracle(sites, rows):
-    from oracle import as_bf16_bits
-    meta = []
-    for s in sites:
-        xb = as_bf16_bits(s.x[:rows].cpu())
-        meta.append((s.name, s.K, s.N, s.S, xb, s.prof.perm.cpu().numpy(), float(s.prof.gs.item()),
-                     s.qw.codes.cpu().numpy(), s.qw.sf.cpu().numpy(), s.gs_w))
-    return meta
-
-
-def traffic_from_profiles():
-    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(p):
-        try:
-            return json.load(open(p))
-        except Exception:
-            return None
+def lscpu_model():
+    try:
+        for ln in subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout.splitlines():
+            if ln.startswith("Model name:"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
     return None
 
 
-# ----------------------------------------------------------------------------- main
+def oracle_site(name, K, N, S, rows, cal_rows=CAL_ROWS):
+    """Everything the oracle needs for one site, made by the oracle alone on the host: seeded CPU
+    synthetic data of the workload's shapes, calibration (abs-max + outlier selection), the weight's
+    tensor scale and its ARC quantization (outlier blocks duplicated).  Untimed (offline work)."""
+    import oracle
+    seed = zlib.crc32(name.encode()) % 1000
+    st = synth.Structure(K, S, seed=seed * 31)
+    cal = oracle.as_bf16_bits(synth.activation(cal_rows, K, st, seed=seed + 1000))
+    w = synth.weight(N, K, seed=seed * 7)
+    gs_w = oracle.tensor_scale(float(w.float().abs().max()))
+    wb = oracle.as_bf16_bits(w)
+    del w
+    x = oracle.as_bf16_bits(synth.activation(rows, K, st, seed=seed + 1))
+    sel = oracle.select_outliers(oracle.calib_absmax(cal), S)
+    with oracle.openmp():
+        wc, wsf = oracle.quantize_weight(wb, sel["perm"], sel["S"], gs_w)
+    return dict(name=name, K=K, N=N, S=sel["S"], x=x, perm=sel["perm"], gs=sel["gs"], wc=wc, wsf=wsf, gs_w=gs_w)
+
+
+def oracle_step(meta, openmp=True):
+    """One bounded sample of the workload on the oracle: ARC-quantize each site's sample rows and run
+    the exact GEMM of those rows against the site's full weight.  Returns (flops, seconds)."""
+    import oracle
+    ctx = oracle.openmp() if openmp else _Null()
+    flops, t0 = 0.0, time.perf_counter()
+    with ctx:
+        for m in meta:
+            ac, asf = oracle.quantize_activation(m["x"], m["perm"], m["S"], m["gs"])
+            oracle.gemm_exact(ac, asf, m["wc"], m["wsf"])
+            flops += 2.0 * m["x"].shape[0] * m["N"] * (m["K"] + m["S"])
+    return flops, time.perf_counter() - t0
+
+
+class _Null:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        pass
+
+
+def oracle_meta_from_sites(sites, rows):
+    """Oracle-side preparation from the bench's own site inputs (the same bf16 activations, calibration
+    rows and weights, copied to the host): the oracle calibrates and quantizes the weights itself --
+    nothing produced by libarc is used."""
+    import oracle
+    meta = []
+    for s in sites:
+        cal = oracle.as_bf16_bits(s.cal_local.cpu())
+        w = s.w_local.cpu()
+        gs_w = oracle.tensor_scale(float(w.float().abs().max()))
+        sel = oracle.select_outliers(oracle.calib_absmax(cal), s.S)
+        with oracle.openmp():
+            wc, wsf = oracle.quantize_weight(oracle.as_bf16_bits(w), sel["perm"], sel["S"], gs_w)
+        meta.append(dict(name=s.name, K=s.K, N=s.N, S=sel["S"], x=oracle.as_bf16_bits(s.x[:rows].cpu()),
+                         perm=sel["perm"], gs=sel["gs"], wc=wc, wsf=wsf, gs_w=gs_w))
+    return meta
+
+
+def parity_sample(sites, meta):
+    """The timed GPU step's outputs on the sampled rows against the oracle's exact GEMM (north_star
+    bound 1e-5 * sum|ab| + the bf16 rounding of the stored output)."""
+    import oracle
+    out = {}
+    for s, m in zip(sites, meta):
+        rows = m["x"].shape[0]
+        with oracle.openmp():
+            ac, asf = oracle.quantize_activation(m["x"], m["perm"], m["S"], m["gs"])
+            yref, bound = oracle.gemm_reference(ac, asf, m["wc"], m["wsf"], m["gs"], m["gs_w"])
+        y = s.y[:rows].float().cpu().numpy().astype(np.float64)
+        tol = bound + np.abs(yref) * 2.0 ** -8
+        out[s.name] = {"rows": rows, "max_err_over_bound": float(np.max(np.abs(y - yref) / np.maximum(tol, 1e-300))),
+                       "ok": bool(np.all(np.abs(y - yref) <= tol))}
+    return out
+
+
+# ----------------------------------------------------------------------------- GPU side legs
+def time_graph(fn, reps=50, warm=3):
+    g = torch.cuda.CUDAGraph()
+    st = torch.cuda.Stream()
+    fn()
+    torch.cuda.synchronize()
+    with torch.cuda.stream(st):
+        with torch.cuda.graph(g, stream=st):
+            fn()
+    torch.cuda.synchronize()
+    for _ in range(warm):
+        g.replay()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(reps):
+        g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
+def decode_sweep(A, sites, device, peaks, Ms=(1, 4, 16, 32, 64)):
+    """BASELINE configs[1] decode token counts: the same 4 sites at M tokens, CUDA-graph replay.  The
+    weights of the 4 sites (~128 MB at LLaMA-3-8B, > L2) stream from HBM every step.  Bound = weight
+    + activation bytes / HBM."""
+    out = []
+    wbytes = sum(s.N * s.Kp * 9 // 16 for s in sites)
+    for Md in Ms:
+        xd = [synth.activation(Md, s.K, synth.Structure(s.K, 8, seed=5), seed=9, device=device) for s in sites]
+        yd = [torch.empty(Md, s.N, dtype=torch.bfloat16, device=device) for s in sites]
+        wsd = [A.Workspace(device) for _ in sites]
+
+        def step():
+            for s, x_, y_, w_ in zip(sites, xd, yd, wsd):
+                A.linear(x_, s.prof, s.qw, out=y_, ws=w_)
+        ms = time_graph(step)
+        dbytes = wbytes + sum(Md * s.K * 2 + Md * s.N * 2 for s in sites)
+        out.append({"M_tokens": Md, "us_per_layer_step": ms * 1e3, "bytes_per_step": dbytes,
+                    "achieved_gbs": dbytes / (ms * 1e-3) / 1e9, "hbm_frac": dbytes / (ms * 1e-3) / 1e9 / peaks["hbm"],
+                    "tflops": sum(2.0 * Md * s.N * (s.K + s.S) for s in sites) / (ms * 1e-3) / 1e12})
+    return out
+
+
+def quantize_streaming(A, device, peaks, reps=5):
+    """The quantize pass at streaming sizes (footprint >= 4x the 126 MB L2, so every launch reads its
+    input from HBM): M=65536 x K=4096 and M=16384 x K=14336, S = 128."""
+    out = []
+    for M, K in ((65536, 4096), (16384, 14336)):
+        st = synth.Structure(K, S_AUG, seed=K)
+        x = synth.activation(M, K, st, seed=K + 1, device=device)
+        prof = A.calibrate([synth.activation(1024, K, st, seed=K + 2, device=device)], s_override=S_AUG)
+        codes, sf = A.quantize_activation(x, prof)
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+        torch.cuda.synchronize()
+        for e0, e1 in evs:
+            e0.record()
+            A.quantize_activation(x, prof, codes, sf)
+            e1.record()
+        torch.cuda.synchronize()
+        us = float(np.median([e0.elapsed_time(e1) for e0, e1 in evs])) * 1e3
+        Kp = codes.shape[1] * 2
+        nbytes = M * (2 * K + Kp // 2 + Kp // 16) + 4 * K
+        out.append({"M": M, "K": K, "S": S_AUG, "bytes": nbytes, "read_mb": M * K * 2 / 1e6, "us": us,
+                    "achieved_gbs": nbytes / (us * 1e-6) / 1e9, "frac": nbytes / (us * 1e-6) / 1e9 / peaks["hbm"]})
+        del x, codes, sf
+    torch.cuda.empty_cache()
+    return out
+
+
+def nccl_lines(path):
+    keep = []
+    try:
+        for ln in open(path):
+            if any(k in ln for k in ("Init COMPLETE", "NVLS", "nvls", "CollNet", "comm 0x", "Using network",
+                                     "P2P/CUMEM", "Connected all")):
+                keep.append(ln.strip()[:240])
+    except OSError:
+        pass
+    return keep[:40]
+
+
+# ----------------------------------------------------------------------------- arms
+def reference_arm(args, config, metric):
+    """The oracle as the reference arm (there is no reference implementation to install:
+    /root/reference holds only the paper and a spec).  Rank 0 only; self-contained: the oracle
+    builds its own calibration and weights from seeded CPU data, libarc is never loaded."""
+    import oracle
+    oracle.build()
+    rows = 1
+    meta = [oracle_site(name, K, N, S_AUG, rows) for name, K, N in workload_sites(config["_workload"])]
+    for _ in range(min(args.warmup, 1)):
+        oracle_step(meta)
+    flops, secs = 0.0, []
+    for _ in range(args.steps):
+        f, t = oracle_step(meta)
+        flops = f
+        secs.append(t)
+    with oracle.openmp():
+        cores = oracle.num_threads()
+    v = flops / float(np.median(secs)) / 1e12
+    cfg = {k: v_ for k, v_ in config.items() if not k.startswith("_")}
+    sample = f"{rows} activation row per site x full N (quantize + exact int64 GEMM), unsharded layer: " + \
+        ";".join(f"{m['name']}:{rows}x{m['N']}x{m['K']}+{m['S']}" for m in meta)
+    line = {"impl": "reference", "metric": metric, "value": v, "unit": "TFLOP/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": float(np.median(secs)) * 1e3,
+            "higher_is_better": True, "scaling": "strong" if args.gpus > 1 else "weak", "vs_baseline": None,
+            "dtype": "int64-exact (oracle)", "data": "synthetic (seeded, CPU)", "config": cfg,
+            "cpu_baseline": {"value": v, "unit": "TFLOP/s", "cores": cores, "kind": "oracle", "sample": sample,
+                             "nproc": os.cpu_count(), "cpu_model": lscpu_model()},
+            "e2e": {"value": v, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "gpu_launches": 0}
+    print(json.dumps(line))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -242,64 +434,68 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="arc", choices=["arc", "reference"])
     ap.add_argument("--M", type=int, default=8192)
+    ap.add_argument("--workload", default="auto", choices=["auto"] + list(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-decode", action="store_true")
+    ap.add_argument("--no-streaming", action="store_true")
     ap.add_argument("--tp-layout", default="mp", choices=["mp", "sp"],
                     help="N>1: sequence-parallel (quantize M/P rows + all-gather packed codes, reduce-scatter) "
                          "or plain Megatron (replicated quantize, all-reduce)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
+    in_dist = "WORLD_SIZE" in os.environ
+    if args.impl == "arc" and args.gpus > 1 and not in_dist:
+        n = torch.cuda.device_count()
+        if n < args.gpus:
+            raise SystemExit(f"bench.py --gpus {args.gpus}: only {n} CUDA device(s) visible")
+        s = socket.socket()
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+        s.close()
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+        os.execv(sys.executable, cmd)
+
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if in_dist and world != args.gpus:
+        raise SystemExit(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}")
+    workload = args.workload if args.workload != "auto" else ("llama3-8b" if args.gpus == 1 else "llama3-70b")
+    metric = "ARC NVFP4 linear TFLOPS"
+    config = {"workload": WORKLOADS[workload][1], "M_tokens": args.M, "S": S_AUG,
+              "sites": [f"{n}:K{k}xN{nn}" for n, k, nn in workload_sites(workload)],
+              "parallelism": "single" if args.gpus == 1 else f"tp{args.gpus}-{args.tp_layout}",
+              "l2": "per-step footprint > 4x L2 (no flush needed)", "_workload": workload}
+
+    if args.impl == "reference":
+        if rank == 0:
+            reference_arm(args, config, metric)
+        return
+
     pg = None
+    nccl_log = None
     if world > 1:
+        nccl_log = f"/tmp/arc_bench_nccl.{os.getpid()}.log"
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT,NVLS")
+        os.environ.setdefault("NCCL_DEBUG_FILE", nccl_log)
         torch.cuda.set_device(local)
         torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
         pg = torch.distributed.group.WORLD
     device = torch.device("cuda", local)
     torch.cuda.set_device(device)
     peaks = _peaks()
-    fp4_peak_sus = peaks["bf16_sus"] * 4.0   # guide nominal ratio fp4/bf16 = 9/2.25
-    fp4_peak_burst = peaks["bf16"] * 4.0
-    workload = "llama3-8b-layer-4-arc-linears-prefill"
-    config = {"workload": workload, "M_tokens": args.M, "S": S_AUG,
-              "sites": [f"{n}:K{k}xN{nn}" for n, k, nn in SITES],
-              "parallelism": "single" if world == 1 else f"tp{world}-{args.tp_layout}",
-              "l2": "per-step footprint > 4x L2 (no flush needed)"}
-
-    if args.impl == "reference":
-        # the oracle on the host cores, same metric/config, bounded sample per step
-        if rank != 0:
-            return
-        from paper_2601_07475_b200 import arc as A
-        sites = build_sites(A, 64, 0, 1, device)
-        meta = sites_meta_for_oracle(sites, 1)
-        for _ in range(args.warmup if args.warmup < 1 else 0):
-            pass
-        vals = []
-        t0 = time.perf_counter()
-        for _ in range(args.steps):
-            v, desc, secs = oracle_sample(meta, budget_s=30.0)
-            vals.append(v)
-        el = time.perf_counter() - t0
-        v = float(np.median(vals))
-        line = {"impl": "reference", "metric": "ARC NVFP4 linear TFLOPS", "value": v, "unit": "TFLOP/s",
-                "n_gpus": 1, "steps": args.steps, "warmup": 0, "ms_per_step": el / args.steps * 1e3,
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64-exact (oracle)",
-                "data": "synthetic", "config": config,
-                "cpu_baseline": {"value": v, "unit": "TFLOP/s", "cores": 1, "kind": "oracle",
-                                 "sample": f"1 row per site, full N: {desc}"},
-                "e2e": {"value": v, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-        print(json.dumps(line))
-        return
+    fp4_burst = peaks["bf16"] * 4.0     # guide's nominal fp4 / bf16 ratio (9 / 2.25)
+    fp4_sus = peaks["bf16_sus"] * 4.0
 
     from paper_2601_07475_b200 import arc as A
     if not A.device_supported():
         raise SystemExit("bench.py: current device is not sm_100 -- the ARC path has no fallback")
-    sites = build_sites(A, args.M, rank, world, device, args.tp_layout)
+    keep = rank == 0 and world == 1 and not args.no_cpu_baseline
+    sites = build_sites(A, args.M, rank, world, device, args.tp_layout, workload, keep_host=keep)
     torch.cuda.synchronize()
 
     for _ in range(args.warmup):
@@ -307,7 +503,7 @@ def main():
     torch.cuda.synchronize()
 
     nS = len(sites)
-    evs = [[[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(nS)] for _ in range(args.steps)]
+    evs = [[[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(nS)] for _ in range(args.steps)]
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if pg is not None:
         torch.distributed.barrier()
@@ -321,121 +517,123 @@ def main():
     if pg is not None:
         torch.distributed.barrier()
     ms = start.elapsed_time(stop)
-    q_ms = sum(evs[k][i][0].elapsed_time(evs[k][i][1]) for k in range(args.steps) for i in range(nS)) / args.steps
-    g_ms = sum(evs[k][i][1].elapsed_time(evs[k][i][2]) for k in range(args.steps) for i in range(nS)) / args.steps
-    per_site = {s.name: {"gemm_us": 1e3 * sum(evs[k][i][1].elapsed_time(evs[k][i][2]) for k in range(args.steps))
-                         / args.steps,
-                         "quant_us": 1e3 * sum(evs[k][i][0].elapsed_time(evs[k][i][1]) for k in range(args.steps))
-                         / args.steps} for i, s in enumerate(sites)}
+
+    def seg(i, a, b):
+        return sum(evs[k][i][a].elapsed_time(evs[k][i][b]) for k in range(args.steps)) / args.steps
+
+    per_site = {}
+    for i, s in enumerate(sites):
+        per_site[s.name] = {"mode": s.mode, "K": s.K, "N": s.N, "S": s.S, "quant_us": 1e3 * seg(i, 0, 1),
+                            "gemm_us": 1e3 * seg(i, 1, 2), "comm_us": 1e3 * seg(i, 2, 3)}
+    q_ms = sum(v["quant_us"] for v in per_site.values()) / 1e3
+    g_ms = sum(v["gemm_us"] for v in per_site.values()) / 1e3
+    c_ms = sum(v["comm_us"] for v in per_site.values()) / 1e3
     if pg is not None:
-        t = torch.tensor([ms, q_ms, g_ms], dtype=torch.float64, device=device)
+        t = torch.tensor([ms, q_ms, g_ms, c_ms], dtype=torch.float64, device=device)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms, q_ms, g_ms = t.tolist()
+        ms, q_ms, g_ms, c_ms = t.tolist()
 
     flops_rank = sum(s.flops for s in sites)
-    # whole-job units: TP shards one layer; each rank's flops are disjoint parts of it
-    flops_job = flops_rank * world
+    flops_job = flops_rank * world        # TP shards one layer; each rank's flops are disjoint parts of it
     ms_step = ms / args.steps
     value = flops_job / (ms_step * 1e-3) / 1e12
     g_tflops = flops_rank / (g_ms * 1e-3) / 1e12
     q_bytes = sum(s.q_bytes for s in sites)
     q_gbs = q_bytes / (q_ms * 1e-3) / 1e9
     for s in sites:
-        s_ = per_site[s.name]
-        s_["gemm_tflops"] = s.flops / (s_["gemm_us"] * 1e-6) / 1e12
-        s_["quant_gbs"] = s.q_bytes / (s_["quant_us"] * 1e-6) / 1e9
-
-    out = {"metric": "ARC NVFP4 linear TFLOPS", "value": value, "unit": "TFLOP/s", "n_gpus": world,
+        v = per_site[s.name]
+        v["gemm_tflops"] = s.flops / (v["gemm_us"] * 1e-6) / 1e12
+        v["gemm_frac_burst"] = v["gemm_tflops"] / fp4_burst
+        v["quant_gbs"] = s.q_bytes / (v["quant_us"] * 1e-6) / 1e9
+        v["quant_frac"] = v["quant_gbs"] / peaks["hbm"]
+    clocks = clk.summary()
+    power_capped = "sw_power_cap" in clocks.get("reasons", [])
+    peak = fp4_sus if power_capped else fp4_burst
+    out = {"metric": metric, "value": value, "unit": "TFLOP/s", "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-           "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "nvfp4(e2m1+ue4m3)->fp32acc->bf16",
-           "data": "synthetic (LLaMA-3-8B shapes, injected outlier channels, random weights)", "config": config,
+           "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
+           "dtype": "nvfp4(e2m1+ue4m3)->fp32acc->bf16",
+           "data": "synthetic (LLaMA-3 shapes, injected outlier channels, random weights)",
+           "config": {k: v_ for k, v_ in config.items() if not k.startswith("_")},
            "roofline": {"bound": "tensor", "kernel": "arc_gemm_kernel (4 launches/step)",
-                        "achieved": g_tflops, "peak": fp4_peak_sus, "unit": "TFLOP/s", "frac": g_tflops / fp4_peak_sus,
-                        "peak_note": f"{peaks['src']} bf16 sustained {peaks['bf16_sus']} x 4 (fp4/bf16 nominal 9/2.25); "
-                                     f"burst x4 = {fp4_peak_burst:.0f}, frac_burst = {g_tflops / fp4_peak_burst:.3f}",
-                        "traffic": None},
+                        "achieved": g_tflops, "peak": peak, "unit": "TFLOP/s", "frac": g_tflops / peak,
+                        "peak_note": (f"{peaks['src']} bf16 {'sustained' if power_capped else 'burst'} "
+                                      f"{peaks['bf16_sus'] if power_capped else peaks['bf16']} x 4 (fp4/bf16 nominal "
+                                      f"9/2.25; {'sw_power_cap seen' if power_capped else 'clocks at max, no power cap'})"),
+                        "frac_burst": g_tflops / fp4_burst, "frac_sustained": g_tflops / fp4_sus,
+                        "frac_datasheet_9pf": g_tflops / 9000.0, "traffic": None},
            "quantize": {"bound": "hbm", "kernel": "arc_quant_kernel (4 launches/step)", "achieved": q_gbs,
                         "peak": peaks["hbm"], "unit": "GB/s", "frac": q_gbs / peaks["hbm"],
                         "bytes_per_step": q_bytes},
-           "time_split_ms": {"quant": q_ms, "gemm": g_ms, "step": ms_step},
+           "time_split_ms": {"quant": q_ms, "gemm": g_ms, "comm": c_ms, "step": ms_step},
            "per_site": per_site,
            "gpu_launches": args.steps * nS * 2,
-           "clocks": clk.summary()}
-    tr = traffic_from_profiles()
-    if tr:
-        out["roofline"]["traffic"] = tr.get("gemm_bytes_per_launch")
-        out["roofline"]["traffic_note"] = "profiles/ncu_traffic.json (committed ncu capture); algorithmic " \
-            f"{tr.get('gemm_algorithmic_bytes_per_launch', 0):.3g} B per launch"
-        out["quantize"]["traffic"] = tr.get("quant_bytes_per_launch")
+           "clocks": clocks}
+    tr = os.path.join(ROOT, "profiles", "r2_ncu_traffic.json")
+    if os.path.exists(tr):
+        try:
+            d = json.load(open(tr))
+            out["roofline"]["traffic"] = d.get("gemm_bytes_per_launch")
+            out["roofline"]["traffic_note"] = f"ncu --set full capture ({d.get('source', tr)}); algorithmic " \
+                f"{d.get('gemm_algorithmic_bytes_per_launch', 0):.3g} B/launch; per-site: {d.get('per_site')}"
+            out["quantize"]["traffic"] = d.get("quant_bytes_per_launch")
+        except Exception:
+            pass
 
-    # decode-size step (BASELINE configs[1] decode M): the same 4 sites at M=16 tokens, CUDA-graph
-    # replay; the weights (~128 MB for the 4 sites, > L2) stream from HBM every step.  Default =
-    # arc_linear (quantize kernel + split-K GEMM + reduce kernel); the one-kernel fused decode
-    # linear (quantize + stream-K GEMM + fixed-order reduction) beside it.
+    if world > 1:
+        S_r = {}
+        for s in sites:
+            t = torch.tensor([s.S], dtype=torch.int64, device=device)
+            allS = [torch.zeros_like(t) for _ in range(world)]
+            torch.distributed.all_gather(allS, t)
+            S_r[s.name] = [int(a.item()) for a in allS]
+        tp_out = {"layout": args.tp_layout, "gemm_only_ms": q_ms + g_ms, "gemm_plus_comm_ms": ms_step,
+                  "comm_ms": c_ms, "S_r_per_rank": S_r, "sites": {}}
+        for s in sites:
+            v = per_site[s.name]
+            if s.mode == "row":
+                bus = (2.0 if not s.sp else 1.0) * (world - 1) / world * s.comm_bytes / (v["comm_us"] * 1e-6) / 1e9
+                tp_out["sites"][s.name] = {"collective": "reduce_scatter" if s.sp else "all_reduce",
+                                           "bytes": s.comm_bytes, "us": v["comm_us"], "busbw_gbs": bus}
+        out["tp"] = tp_out
+        if rank == 0 and nccl_log:
+            out["nccl"] = nccl_lines(nccl_log)
+
     if not args.no_decode and world == 1:
-        Md = 16
-        xd = [synth.activation(Md, s.K, synth.Structure(s.K, 8, seed=5), seed=9, device=device) for s in sites]
-        yd = [torch.empty(Md, s.N, dtype=torch.bfloat16, device=device) for s in sites]
-        wsd = [A.Workspace(device) for _ in sites]
-        dec = {}
-        for mode in ("fused", "unfused"):
-            for s, x_, y_, w_ in zip(sites, xd, yd, wsd):
-                A.linear(x_, s.prof, s.qw, out=y_, ws=w_, mode=mode)
-            torch.cuda.synchronize()
-            g = torch.cuda.CUDAGraph()
-            gs_ = torch.cuda.Stream()
-            with torch.cuda.stream(gs_):
-                with torch.cuda.graph(g, stream=gs_):
-                    for s, x_, y_, w_ in zip(sites, xd, yd, wsd):
-                        A.linear(x_, s.prof, s.qw, out=y_, ws=w_, mode=mode)
-            torch.cuda.synchronize()
-            for _ in range(3):
-                g.replay()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            reps = 50
-            torch.cuda.synchronize()
-            e0.record()
-            for _ in range(reps):
-                g.replay()
-            e1.record()
-            torch.cuda.synchronize()
-            dec[mode] = e0.elapsed_time(e1) / reps
-            del g
-        dms = dec["unfused"]
-        wbytes = sum(s.N * s.Kp * 9 // 16 for s in sites)
-        dbytes = wbytes + sum(Md * s.K * 2 + Md * s.N * 2 for s in sites)
-        out["decode"] = {"M_tokens": Md, "us_per_layer_step": dms * 1e3, "tflops": sum(2.0 * Md * s.N * (s.K + s.S)
-                         for s in sites) / (dms * 1e-3) / 1e12,
-                         "bytes_per_step": dbytes, "achieved_gbs": dbytes / (dms * 1e-3) / 1e9,
-                         "hbm_frac": dbytes / (dms * 1e-3) / 1e9 / peaks["hbm"],
-                         "fused_us_per_layer_step": dec["fused"] * 1e3,
-                         "fused_hbm_frac": dbytes / (dec["fused"] * 1e-3) / 1e9 / peaks["hbm"],
-                         "note": "4 sites x (quantize + split-K GEMM + reduce, PDL-chained) per step in one CUDA "
-                                 "graph (arc_linear default); fused_* = the one-kernel fused decode linear "
-                                 "(ARC_LINEAR_FUSED: quantize phase + grid barrier + stream-K GEMM + in-kernel "
-                                 "reduction); bound = weight bytes / HBM"}
+        out["decode"] = decode_sweep(A, sites, device, peaks)
+    if not args.no_streaming and world == 1:
+        out["quantize_streaming"] = quantize_streaming(A, device, peaks)
 
-    # e2e through the public C-ABI host-buffer call (H2D of x and D2H of y inside the timed region)
+    # e2e through the public API: every step copies the step's inputs from pinned host memory to the
+    # device and the outputs back (world 1: the C-ABI host-buffer call arc_linear_hostio does both
+    # inside the call; TP: the same copies around the device path incl. its collectives)
     if not args.no_e2e:
         xs = [s.x.cpu().pin_memory() for s in sites]
-        ys = [torch.empty(s.M, s.N, dtype=torch.bfloat16).pin_memory() for s in sites]
-        wss = [torch.zeros(A.linear_hostio_workspace_size(s.M, s.qw), dtype=torch.uint8, device=device)
-               for s in sites]
+        ys = [torch.empty(s.out_rows, s.N, dtype=s.y.dtype).pin_memory() for s in sites]
+        if world == 1:
+            wss = [torch.zeros(A.linear_hostio_workspace_size(s.M, s.qw), dtype=torch.uint8, device=device)
+                   for s in sites]
+
+            def e2e_step():
+                for s, xh, yh, ws in zip(sites, xs, ys, wss):
+                    A.linear_hostio(xh, s.prof, s.qw, yh, ws)
+        else:
+            def e2e_step():
+                for s, xh in zip(sites, xs):
+                    s.x.copy_(xh, non_blocking=True)
+                run_step(A, sites, pg=pg)
+                for s, yh in zip(sites, ys):
+                    yh.copy_(s.y_out if (s.sp and s.mode == "row") else s.y, non_blocking=True)
         for _ in range(2):
-            for s, xh, yh, ws in zip(sites, xs, ys, wss):
-                A.linear_hostio(xh, s.prof, s.qw, yh, ws)
+            e2e_step()
         if pg is not None:
             torch.distributed.barrier()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
         e0.record()
         nE = max(1, min(args.steps, 5))
         for _ in range(nE):
-            for s, xh, yh, ws in zip(sites, xs, ys, wss):
-                A.linear_hostio(xh, s.prof, s.qw, yh, ws)
-                if s.mode == "row" and pg is not None:
-                    pass  # host-buffer variant reports the per-rank partial; reduction is the device path's
+            e2e_step()
         e1.record()
         torch.cuda.synchronize()
         ems = e0.elapsed_time(e1) / nE
@@ -444,15 +642,31 @@ def main():
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
             ems = t.item()
         out["e2e"] = {"value": flops_job / (ems * 1e-3) / 1e12, "unit": "TFLOP/s",
-                      "h2d_bytes_per_step": sum(x.numel() * 2 for x in xs),
-                      "d2h_bytes_per_step": sum(y.numel() * 2 for y in ys),
-                      "ms_per_step": ems, "api": "arc_linear_hostio (C-ABI, pinned host buffers)"}
+                      "h2d_bytes_per_step": sum(x.numel() * x.element_size() for x in xs),
+                      "d2h_bytes_per_step": sum(y.numel() * y.element_size() for y in ys),
+                      "ms_per_step": ems,
+                      "api": "arc_linear_hostio (C-ABI, pinned host buffers)" if world == 1 else
+                             "arc quantize+gemm per rank + NCCL collectives, pinned host copies in the step"}
 
-    if rank == 0 and not args.no_cpu_baseline:
-        meta = sites_meta_for_oracle(sites, 2)
-        v, desc, secs = oracle_sample(meta, budget_s=25.0)
-        out["cpu_baseline"] = {"value": v, "unit": "TFLOP/s", "cores": 1, "kind": "oracle",
-                               "sample": f"2 rows per site x full N (quantize + exact int64 GEMM): {desc}; {secs:.1f}s"}
+    if keep:
+        import oracle
+        oracle.build()
+        rows = 2
+        run_step(A, sites)  # the outputs the parity sample compares
+        torch.cuda.synchronize()
+        meta = oracle_meta_from_sites(sites, rows)
+        out["parity_sample"] = parity_sample(sites, meta)
+        f1, t1 = oracle_step(meta, openmp=False)
+        fN, tN = oracle_step(meta, openmp=True)
+        with oracle.openmp():
+            cores = oracle.num_threads()
+        desc = ";".join(f"{m['name']}:{rows}x{m['N']}x{m['K']}+{m['S']}" for m in meta)
+        out["cpu_baseline"] = {"value": fN / tN / 1e12, "unit": "TFLOP/s", "cores": cores, "kind": "oracle",
+                               "sample": f"{rows} rows per site x full N (quantize + exact int64 GEMM), "
+                                         f"OpenMP over output columns: {desc}; {tN:.2f} s",
+                               "single_thread_value": f1 / t1 / 1e12, "single_thread_s": t1,
+                               "nproc": os.cpu_count(), "cpu_model": lscpu_model(),
+                               "prep": "oracle's own calibration + weight quantization of the same bf16 inputs"}
     if rank == 0:
         print(json.dumps(out))
     if pg is not None:

@@ -20,27 +20,54 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "arc_oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
-_lib = None
+_LIB_OMP = os.path.join(_HERE, "liboracle_omp.so")
+_libs = {}
+_variant = "serial"
 
 INTERLEAVED = 0
 CONTIGUOUS = 1
 
 
+def _compile(out: str, extra) -> None:
+    tmp = out + f".tmp{os.getpid()}"
+    subprocess.check_call(["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-Wno-unknown-pragmas",
+                           *extra, "-fPIC", "-shared", "-o", tmp, _SRC, "-lm"])
+    os.replace(tmp, out)
+
+
 def build(force: bool = False) -> str:
-    """Compile liboracle.so (gcc, -O2 -ffp-contract=off, no fast-math)."""
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        tmp = _LIB + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math",
-                               "-fPIC", "-shared", "-o", tmp, _SRC, "-lm"])
-        os.replace(tmp, _LIB)
+    """Compile liboracle.so (gcc, -O2 -ffp-contract=off, no fast-math) and the same source with
+    -fopenmp as liboracle_omp.so (rows / output columns split over host threads; identical
+    arithmetic per element -- the bench's multi-core CPU baseline)."""
+    for out, extra in ((_LIB, []), (_LIB_OMP, ["-fopenmp"])):
+        if force or not os.path.exists(out) or os.path.getmtime(out) < os.path.getmtime(_SRC):
+            _compile(out, extra)
     return _LIB
 
 
+class openmp:
+    """Context manager: oracle calls inside use the OpenMP build (all host cores unless
+    OMP_NUM_THREADS says otherwise)."""
+
+    def __enter__(self):
+        global _variant
+        self.prev, _variant = _variant, "omp"
+        return self
+
+    def __exit__(self, *a):
+        global _variant
+        _variant = self.prev
+
+
+def num_threads() -> int:
+    """Threads the current variant uses."""
+    return int(lib().or_num_threads())
+
+
 def lib():
-    global _lib
-    if _lib is None:
+    if _variant not in _libs:
         build()
-        L = ctypes.CDLL(_LIB)
+        L = ctypes.CDLL(_LIB_OMP if _variant == "omp" else _LIB)
         P = ctypes.c_void_p
         i64, i32, f32 = ctypes.c_int64, ctypes.c_int, ctypes.c_float
         L.or_e2m1_value.restype = f32
@@ -94,8 +121,10 @@ def lib():
         for n in ("or_e2m1_encode_n", "or_e4m3_ceil_n", "or_e4m3_rn_n"):
             getattr(L, n).restype = None
             getattr(L, n).argtypes = [P, i64, P]
-        _lib = L
-    return _lib
+        L.or_num_threads.restype = i32
+        L.or_num_threads.argtypes = []
+        _libs[_variant] = L
+    return _libs[_variant]
 
 
 def _p(a: np.ndarray):

@@ -257,15 +257,25 @@ void or_pack_row(const uint8_t* lcodes, const uint8_t* lsf, int K, int S, int la
 int or_quantize_activation(const uint16_t* x, int64_t M, int K, int64_t ldx, const int32_t* perm,
                            int S, float gs, int layout, uint8_t* codes, uint8_t* sf) {
     int64_t Kp = or_kp(K, S);
-    uint8_t* lc = (uint8_t*)malloc((size_t)(K + S));
-    uint8_t* ls = (uint8_t*)malloc((size_t)((K + S) / 16 + 1));
     int rc = OR_OK;
-    for (int64_t m = 0; m < M && rc == OR_OK; ++m) {
-        rc = or_arc_row_logical(x + m * ldx, perm, K, S, gs, lc, ls);
-        if (rc == OR_OK) or_pack_row(lc, ls, K, S, layout, m, codes + m * (Kp / 2), sf);
+    /* rows are independent (each writes only its own codes / scale bytes); the OpenMP build
+     * (liboracle_omp.so, the bench's multi-core CPU baseline) splits them over threads */
+    #pragma omp parallel
+    {
+        uint8_t* lc = (uint8_t*)malloc((size_t)(K + S));
+        uint8_t* ls = (uint8_t*)malloc((size_t)((K + S) / 16 + 1));
+        #pragma omp for schedule(static)
+        for (int64_t m = 0; m < M; ++m) {
+            int r = or_arc_row_logical(x + m * ldx, perm, K, S, gs, lc, ls);
+            if (r == OR_OK) or_pack_row(lc, ls, K, S, layout, m, codes + m * (Kp / 2), sf);
+            else {
+                #pragma omp critical
+                rc = r;
+            }
+        }
+        free(lc);
+        free(ls);
     }
-    free(lc);
-    free(ls);
     return rc;
 }
 
@@ -273,15 +283,23 @@ int or_quantize_activation(const uint16_t* x, int64_t M, int K, int64_t ldx, con
 int or_quantize_weight(const uint16_t* w, int64_t N, int K, int64_t ldw, const int32_t* perm, int S,
                        float gs, int layout, uint8_t* codes, uint8_t* sf) {
     int64_t Kp = or_kp(K, S);
-    uint8_t* lc = (uint8_t*)malloc((size_t)(K + S));
-    uint8_t* ls = (uint8_t*)malloc((size_t)((K + S) / 16 + 1));
     int rc = OR_OK;
-    for (int64_t n = 0; n < N && rc == OR_OK; ++n) {
-        rc = or_weight_row_logical(w + n * ldw, perm, K, S, gs, lc, ls);
-        if (rc == OR_OK) or_pack_row(lc, ls, K, S, layout, n, codes + n * (Kp / 2), sf);
+    #pragma omp parallel
+    {
+        uint8_t* lc = (uint8_t*)malloc((size_t)(K + S));
+        uint8_t* ls = (uint8_t*)malloc((size_t)((K + S) / 16 + 1));
+        #pragma omp for schedule(static)
+        for (int64_t n = 0; n < N; ++n) {
+            int r = or_weight_row_logical(w + n * ldw, perm, K, S, gs, lc, ls);
+            if (r == OR_OK) or_pack_row(lc, ls, K, S, layout, n, codes + n * (Kp / 2), sf);
+            else {
+                #pragma omp critical
+                rc = r;
+            }
+        }
+        free(lc);
+        free(ls);
     }
-    free(lc);
-    free(ls);
     return rc;
 }
 
@@ -353,25 +371,38 @@ void or_gemm_exact(const uint8_t* a_codes, const uint8_t* a_sf, const uint8_t* b
                    const uint8_t* b_sf, int64_t N, int64_t Kp, const int64_t* rows, int64_t nrows,
                    int64_t* T, int64_t* Tabs) {
     int64_t* Va = (int64_t*)malloc(sizeof(int64_t) * (size_t)(Kp * nrows));
-    int64_t* Vb = (int64_t*)malloc(sizeof(int64_t) * (size_t)Kp);
     for (int64_t ri = 0; ri < nrows; ++ri)
         for (int64_t p = 0; p < Kp; ++p) Va[ri * Kp + p] = elem_units(a_codes, a_sf, rows[ri], p, Kp);
-    for (int64_t n = 0; n < N; ++n) {
-        for (int64_t p = 0; p < Kp; ++p) Vb[p] = elem_units(b_codes, b_sf, n, p, Kp);
-        for (int64_t ri = 0; ri < nrows; ++ri) {
-            int64_t acc = 0, aabs = 0;
-            for (int64_t p = 0; p < Kp; ++p) {
-                int64_t term = Va[ri * Kp + p] * Vb[p];
-                acc += term;
-                aabs += term < 0 ? -term : term;
+    /* output columns are independent; the OpenMP build splits them over threads */
+    #pragma omp parallel
+    {
+        int64_t* Vb = (int64_t*)malloc(sizeof(int64_t) * (size_t)Kp);
+        #pragma omp for schedule(static)
+        for (int64_t n = 0; n < N; ++n) {
+            for (int64_t p = 0; p < Kp; ++p) Vb[p] = elem_units(b_codes, b_sf, n, p, Kp);
+            for (int64_t ri = 0; ri < nrows; ++ri) {
+                int64_t acc = 0, aabs = 0;
+                for (int64_t p = 0; p < Kp; ++p) {
+                    int64_t term = Va[ri * Kp + p] * Vb[p];
+                    acc += term;
+                    aabs += term < 0 ? -term : term;
+                }
+                T[ri * N + n] = acc;
+                Tabs[ri * N + n] = aabs;
             }
-            T[ri * N + n] = acc;
-            Tabs[ri * N + n] = aabs;
         }
+        free(Vb);
     }
     free(Va);
-    free(Vb);
 }
+
+/* Threads the OpenMP build uses (1 in the plain build). */
+#ifdef _OPENMP
+#include <omp.h>
+int or_num_threads(void) { return omp_get_max_threads(); }
+#else
+int or_num_threads(void) { return 1; }
+#endif
 
 /* ------------------------------------------------------------------------- */
 /* Eq.3 comparator: single-stage MXFP8 -- g = 32, E4M3 elements,  */

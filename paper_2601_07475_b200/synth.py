@@ -22,11 +22,18 @@ import torch
 
 
 class Structure:
-    def __init__(self, K: int, S_inj: int, seed: int = 0):
+    def __init__(self, K: int, S_inj: int, seed: int = 0, shards: int = 1):
+        """shards > 1: S_inj / shards channels inside each of `shards` contiguous K slices (the balanced
+        outliers of a row-parallel layer, SURVEY.md §8(e) "Outlier balance")."""
         rng = np.random.default_rng(seed)
         self.K = K
-        self.idx = np.sort(rng.choice(K, S_inj, replace=False)).astype(np.int64)
-        self.gain = np.exp(rng.uniform(math.log(32.0), math.log(128.0), S_inj)).astype(np.float32)
+        if shards > 1:
+            ks, per = K // shards, max(1, S_inj // shards)
+            self.idx = np.sort(np.concatenate([r * ks + rng.choice(ks, per, replace=False)
+                                               for r in range(shards)])).astype(np.int64)
+        else:
+            self.idx = np.sort(rng.choice(K, S_inj, replace=False)).astype(np.int64)
+        self.gain = np.exp(rng.uniform(math.log(32.0), math.log(128.0), self.idx.size)).astype(np.float32)
 
 
 def activation(M: int, K: int, st: Structure, seed: int, device="cpu") -> torch.Tensor:
@@ -72,4 +79,12 @@ LLAMA3_8B_SITES = [
     ("o", 4096, 4096),
     ("gate_up", 4096, 28672),
     ("down", 14336, 4096),
+]
+
+# LLaMA-3-70B (hidden 8192, intermediate 28672, 64/8 heads x 128), BASELINE configs[3]
+LLAMA3_70B_SITES = [
+    ("qkv", 8192, 10240),
+    ("o", 8192, 8192),
+    ("gate_up", 8192, 57344),
+    ("down", 28672, 8192),
 ]

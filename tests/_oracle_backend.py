@@ -58,3 +58,38 @@ class OracleBackend:
     def linear_bound(self, x, prof, qw):
         ac, asf = oracle.quantize_activation(oracle.as_bf16_bits(x), prof.perm, prof.S, prof.gs, prof.layout)
         return oracle.gemm_reference(ac, asf, qw.codes, qw.sf, prof.gs, qw.gs)
+
+    # --- the buffer-level calls bench.py's step makes (bench.Site / bench.run_step) ---
+    def buffer_sizes(self, rows, K, S):
+        Kp = oracle.kp(K, S)
+        return Kp, rows * Kp // 2, oracle.sf_rows_padded(rows) * Kp // 16
+
+    class Workspace:
+        def __init__(self, device=None):
+            self.device = device
+
+    def quantize_activation_into(self, x, prof, codes, sf):
+        ac, asf = oracle.quantize_activation(oracle.as_bf16_bits(x), prof.perm, prof.S, prof.gs, prof.layout)
+        codes.copy_(torch.from_numpy(ac))
+        sf.copy_(torch.from_numpy(asf.reshape(-1)))
+        return codes, sf
+
+    def gemm_into(self, codes, sf, gs, qw, out):
+        y, _ = oracle.gemm_reference(codes.numpy(), sf.numpy(), qw.codes, qw.sf, gs, qw.gs)
+        out.copy_(torch.from_numpy(y).to(out.dtype))
+        return out
+
+
+class BenchOracleBackend(OracleBackend):
+    """OracleBackend with bench.py's in-place call signatures (quantize_activation(x, prof, codes, sf),
+    gemm(codes, sf, gs, qw, out=, ws=))."""
+
+    def quantize_activation(self, x, prof, codes=None, sf=None):
+        if codes is None:
+            return super().quantize_activation(x, prof)
+        return self.quantize_activation_into(x, prof, codes, sf)
+
+    def gemm(self, codes, sf, gs, qw, out_dtype=torch.float32, out=None, ws=None):
+        if out is None:
+            return super().gemm(codes, sf, gs, qw, out_dtype)
+        return self.gemm_into(codes, sf, gs, qw, out)

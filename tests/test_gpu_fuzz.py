@@ -78,3 +78,26 @@ def test_gemm_fuzz(M, N, K, S):
                                         qw.sf.cpu().numpy(), float(prof.gs.item()), float(qw.gs.item()))
     err = np.abs(y.cpu().numpy().astype(np.float64) - yref)
     assert (err <= bound).all(), f"worst err/bound {np.max(err / np.maximum(bound, 1e-300))}"
+
+
+@pytest.mark.parametrize("M,N,K,S", [(16, 34, 4096, 128), (7, 130, 2048, 64), (64, 1026, 14336, 128),
+                                     (3, 6, 1024, 16)])
+def test_gemm_split_k_ragged_n(M, N, K, S):
+    """decode-size M takes the split-K path; N not a multiple of 4 must not misalign the
+    fp32 partial stores (partial rows are padded to round_up(N, 4)).  fp32 and bf16 outputs."""
+    from paper_2601_07475_b200 import arc as A
+    st = synth.Structure(K, max(S, 16), seed=N)
+    x = synth.activation(M, K, st, seed=M + 11, device="cuda")
+    w = synth.weight(N, K, seed=N + 12, device="cuda")
+    prof = A.calibrate([synth.activation(64, K, st, seed=13, device="cuda")], s_override=S)
+    qw = A.quantize_weight(w, prof)
+    codes, sf = A.quantize_activation(x, prof)
+    y = A.gemm(codes, sf, prof.gs, qw, out_dtype=torch.float32)
+    yb = torch.empty(M, (N + 7) // 8 * 8, dtype=torch.bfloat16, device="cuda")[:, :N]
+    A.gemm(codes, sf, prof.gs, qw, out=yb)
+    torch.cuda.synchronize()
+    yref, bound = oracle.gemm_reference(codes.cpu().numpy(), sf.cpu().numpy(), qw.codes.cpu().numpy(),
+                                        qw.sf.cpu().numpy(), float(prof.gs.item()), float(qw.gs.item()))
+    err = np.abs(y.cpu().numpy().astype(np.float64) - yref)
+    assert (err <= bound).all(), f"worst err/bound {np.max(err / np.maximum(bound, 1e-300))}"
+    assert torch.equal(yb, y.to(torch.bfloat16))

@@ -245,4 +245,16 @@ def test_gemm_swiglu_vs_oracle(A, M, I, K, S):
     wide = ((ghi - glo) > 2) | ((uhi - ulo) > 2)
     bad = ~ok & ~wide
     assert not bad.any(), f"{bad.sum()} of {bad.size} h values match no candidate; first at {np.argwhere(bad)[0]}"
-    assert wide.sum() <= max(2, bad.size // 1000), f"{wide.sum()} wide intervals"
+    # wide intervals (|y| small against sum|ab|): every bf16 pair inside them
+    unchecked = 0
+    for m, i in np.argwhere(wide & ~ok):
+        gk = np.arange(glo[m, i], ghi[m, i] + 1)
+        uk = np.arange(ulo[m, i], uhi[m, i] + 1)
+        if gk.size * uk.size > 1 << 18:
+            unchecked += 1
+            continue
+        G, U = np.meshgrid(gk, uk, indexing="ij")
+        cand = oracle.silu_mul(np.concatenate([_bf16_from_key(G.reshape(1, -1)), _bf16_from_key(U.reshape(1, -1))],
+                                              axis=1))
+        assert (cand == h[m, i]).any(), f"h[{m},{i}] matches no bf16 (g, u) inside the tolerance intervals"
+    assert unchecked <= max(1, h.size // 10000), f"{unchecked} intervals too wide to enumerate"

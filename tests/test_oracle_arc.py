@@ -288,3 +288,22 @@ def test_fig3_qualitative_arc_beats_rtn_100_seeds():
         wins_y += mse_y[0] < mse_y[1]
         wins_q += mse_q[0] < mse_q[1]
     assert wins_x == 100 and wins_y == 100 and wins_q >= 95
+
+
+def test_openmp_build_is_bit_identical():
+    """The OpenMP build (the bench's multi-core CPU baseline) only splits independent rows / output
+    columns over threads: every output equals the plain build's."""
+    from paper_2601_07475_b200 import synth
+    st = synth.Structure(512, 32, seed=4)
+    x = oracle.as_bf16_bits(synth.activation(33, 512, st, seed=5))
+    w = oracle.as_bf16_bits(synth.weight(70, 512, seed=6))
+    sel = oracle.select_outliers(oracle.calib_absmax(x))
+    a = oracle.quantize_activation(x, sel["perm"], sel["S"], sel["gs"])
+    b = oracle.quantize_weight(w, sel["perm"], sel["S"], 3.0)
+    g = oracle.gemm_exact(a[0], a[1], b[0], b[1])
+    with oracle.openmp():
+        a2 = oracle.quantize_activation(x, sel["perm"], sel["S"], sel["gs"])
+        b2 = oracle.quantize_weight(w, sel["perm"], sel["S"], 3.0)
+        g2 = oracle.gemm_exact(a2[0], a2[1], b2[0], b2[1])
+    for u, v in zip(a + b + g, a2 + b2 + g2):
+        assert np.array_equal(u, v)
