@@ -113,7 +113,8 @@ ARC_API int arc_device_supported(void);
 /* Sizes of a quantized operand of `rows` rows (codes / sf bytes, Kp). */
 ARC_API arc_status_t arc_buffer_sizes(int64_t rows, int64_t K, int32_t S, int64_t* Kp, size_t* code_bytes,
                               size_t* sf_bytes);
-/* Workspace arc_gemm needs for M rows against qw: the fp32 split-K partials used at
+/* Workspace arc_gemm needs for M rows against qw (zero it once before the first use): the fp32
+ * split-K / stream-K partials and tile counters used at
  * decode-size M (nsplit*M*N*4 bytes; 0 when the GEMM is not split). */
 ARC_API arc_status_t arc_gemm_workspace_size(int64_t M, const arc_qweight_t* qw, size_t* bytes);
 /* Workspace arc_linear needs (sized for both paths of arc_linear_ex, so one workspace serves
@@ -259,9 +260,13 @@ ARC_API arc_status_t arc_linear_silu_mul(const void* gu, int64_t M, int64_t ld, 
  * memory (tcgen05.mma kind::mxf4nvf4, scale vector 16), stored as y_dtype.
  * a_codes/a_sf: the activation as written by arc_quantize_activation with the
  * same K, S and layout as qw.  ldy * sizeof(y_dtype) must be a multiple of 16.
- * ws: arc_gemm_workspace_size(M, qw) bytes (may be NULL when that is 0); at
- * decode-size M the K range is split over the SMs and the fp32 partials are
- * summed in a fixed order by a second kernel (deterministic). */
+ * ws: arc_gemm_workspace_size(M, qw) bytes (may be NULL when that is 0), ZERO before its
+ * first use (every call leaves it reusable).  At decode-size M (<= 64) one weight-streaming
+ * stream-K kernel runs: every SM streams an equal share of the weight units, a tile split
+ * over several SMs is summed from fp32 partials in a fixed segment order by the last SM to
+ * finish it (deterministic); per-tile arrival counters in ws return to zero.  At other M
+ * below one wave of tiles the K range is split and a second kernel sums the partials in a
+ * fixed order. */
 ARC_API arc_status_t arc_gemm(const uint8_t* a_codes, const uint8_t* a_sf, const float* gs_x, int64_t M,
                               const arc_qweight_t* qw, void* y, arc_dtype_t y_dtype, int64_t ldy, void* ws,
                               size_t ws_bytes, void* stream);

@@ -445,9 +445,22 @@ arc_status_t arc_silu_mul_quantize_activation(const void* gu, int64_t M, int64_t
   return e == cudaSuccess ? ARC_OK : cuda_fail(e, "arc_silu_mul_quantize_activation");
 }
 
+static arc_status_t gemm_impl(const uint8_t* a_codes, const uint8_t* a_sf, const float* gs_x, int64_t M,
+                              const arc_qweight_t* qw, void* y, arc_dtype_t y_dtype, int64_t ldy, void* ws,
+                              size_t ws_bytes, void* stream, int weights_ready);
+
 arc_status_t arc_gemm(const uint8_t* a_codes, const uint8_t* a_sf, const float* gs_x, int64_t M,
                       const arc_qweight_t* qw, void* y, arc_dtype_t y_dtype, int64_t ldy, void* ws, size_t ws_bytes,
                       void* stream) {
+  return gemm_impl(a_codes, a_sf, gs_x, M, qw, y, y_dtype, ldy, ws, ws_bytes, stream, 0);
+}
+
+// weights_ready: the caller knows the weights were complete before the kernel preceding this GEMM
+// started (arc_linear*: that kernel is its own activation quantize), so the decode-size kernel may
+// stream them before griddepcontrol.wait.
+static arc_status_t gemm_impl(const uint8_t* a_codes, const uint8_t* a_sf, const float* gs_x, int64_t M,
+                              const arc_qweight_t* qw, void* y, arc_dtype_t y_dtype, int64_t ldy, void* ws,
+                              size_t ws_bytes, void* stream, int weights_ready) {
   arc_status_t s = check_qweight(qw);
   if (s != ARC_OK) return s;
   if (M < 0 || M > (1 << 30)) return fail(ARC_ERR_SHAPE, "bad M");
@@ -478,6 +491,7 @@ arc_status_t arc_gemm(const uint8_t* a_codes, const uint8_t* a_sf, const float* 
   p.y_fp32 = y_dtype == ARC_FP32;
   p.ws = ws;
   p.ws_bytes = ws_bytes;
+  p.weights_ready = weights_ready;
   const char* detail = nullptr;
   cudaError_t e = launch_gemm(p, (cudaStream_t)stream, &detail);
   return e == cudaSuccess ? ARC_OK : cuda_fail(e, "arc_gemm", detail);
@@ -578,7 +592,7 @@ arc_status_t arc_linear_ex(const void* x, int64_t M, int64_t ldx, const arc_prof
   const size_t act = act_ws_bytes(M, qw->K, qw->S);
   s = arc_quantize_activation(x, M, ldx, prof, codes, sf, stream);
   if (s != ARC_OK) return s;
-  return arc_gemm(codes, sf, prof->gs, M, qw, y, y_dtype, ldy, rest + act, rest_bytes - act, stream);
+  return gemm_impl(codes, sf, prof->gs, M, qw, y, y_dtype, ldy, rest + act, rest_bytes - act, stream, 1);
 }
 
 arc_status_t arc_linear_rmsnorm(const void* x, int64_t M, int64_t ldx, const void* gamma, float eps,
@@ -601,7 +615,7 @@ arc_status_t arc_linear_rmsnorm(const void* x, int64_t M, int64_t ldx, const voi
   const size_t act = act_ws_bytes(M, qw->K, qw->S);
   s = arc_rmsnorm_quantize_activation(x, M, ldx, gamma, eps, prof, codes, sf, stream);
   if (s != ARC_OK) return s;
-  return arc_gemm(codes, sf, prof->gs, M, qw, y, y_dtype, ldy, codes + act, ws_bytes - sync - act, stream);
+  return gemm_impl(codes, sf, prof->gs, M, qw, y, y_dtype, ldy, codes + act, ws_bytes - sync - act, stream, 1);
 }
 
 arc_status_t arc_linear_silu_mul(const void* gu, int64_t M, int64_t ld, int64_t up_off, const arc_profile_t* prof,
@@ -624,7 +638,7 @@ arc_status_t arc_linear_silu_mul(const void* gu, int64_t M, int64_t ld, int64_t 
   const size_t act = act_ws_bytes(M, qw->K, qw->S);
   s = arc_silu_mul_quantize_activation(gu, M, ld, up_off, prof, codes, sf, stream);
   if (s != ARC_OK) return s;
-  return arc_gemm(codes, sf, prof->gs, M, qw, y, y_dtype, ldy, codes + act, ws_bytes - sync - act, stream);
+  return gemm_impl(codes, sf, prof->gs, M, qw, y, y_dtype, ldy, codes + act, ws_bytes - sync - act, stream, 1);
 }
 
 arc_status_t arc_linear(const void* x, int64_t M, int64_t ldx, const arc_profile_t* prof, const arc_qweight_t* qw,

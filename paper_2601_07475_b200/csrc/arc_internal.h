@@ -63,7 +63,21 @@ struct GemmProblem {
   int swiglu = 0;    // SwiGLU epilogue (gate/up rows interleaved in groups of 16): y = h [M][N/2] bf16
   void* ws;          // split-K partials (decode-size M), may be null when plan.ws_bytes == 0
   size_t ws_bytes;
+  // The weights were complete before the kernel preceding this GEMM started (arc_linear: that
+  // kernel is the activation quantize, which lets dependents launch only after its own
+  // griddepcontrol.wait): the decode-size kernel may then stream them before its own wait.
+  int weights_ready = 0;
 };
+// Decode-size M (<= 64): weight-streaming stream-K GEMM (stream_gemm.cu).
+struct StreamPlan {
+  bool ok = false;
+  int a_rows = 0;                 // activation TMA box rows: 16 / 32 / 64
+  int64_t n_tiles = 0, nkb = 0, units = 0, maxseg = 0;
+  int grid = 0;
+  size_t part_bytes = 0, cnt_bytes = 0, ws_bytes = 0;   // workspace: partials + counters (zero before use)
+};
+StreamPlan plan_stream(int64_t M, int64_t N, int64_t Kp);
+cudaError_t launch_stream_gemm(const GemmProblem& p, const StreamPlan& pl, cudaStream_t stream, const char** detail);
 struct GemmPlan {
   int CL;            // CTAs per cluster along M
   int pair;          // CL == 2: 1 = 2-SM tcgen05 MMA (cta_group::2), 0 = two 1-SM CTAs sharing B by multicast

@@ -786,10 +786,18 @@ GemmPlan plan_gemm(int64_t M, int64_t N, int64_t Kp) {
     }
   }
   pl.ws_bytes = pl.nsplit > 1 ? (size_t)pl.nsplit * (size_t)M * (size_t)round_up(N, 4) * sizeof(float) : 0;
+  // decode-size M: the stream-K kernel (stream_gemm.cu); the split-K path stays for the SwiGLU epilogue
+  const StreamPlan sp = plan_stream(M, N, Kp);
+  if (sp.ok) pl.ws_bytes = std::max(pl.ws_bytes, sp.ws_bytes);
   return pl;
 }
 
 cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t stream, const char** detail) {
+  static const int env_stream = getenv("ARC_GEMM_STREAM") ? atoi(getenv("ARC_GEMM_STREAM")) : 1;
+  if (env_stream && !p.swiglu) {
+    const StreamPlan sp = plan_stream(p.M, p.N, p.Kp);
+    if (sp.ok) return launch_stream_gemm(p, sp, stream, detail);
+  }
   GemmPlan pl = plan_gemm(p.M, p.N, p.Kp);
   // SwiGLU epilogue: the 2-SM kernel leaves shared memory for the SiLU table (the 1-SM kernel's
   // 4 x 54 KB ring does not), so prefill-size SwiGLU GEMMs run as CTA pairs

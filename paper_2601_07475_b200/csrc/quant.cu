@@ -263,8 +263,10 @@ __global__ void __launch_bounds__(1024) arc_quant_kernel(QuantArgs p) {
   const int my_tiles = ntile > (int)blockIdx.x ? (ntile - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
   const int sf_rb_stride = (p.Kp >> 6) * 512;
   const int code_row = p.Kp >> 1;
+  // (PDL) wait first, then let the next kernel launch: a dependent launched from here on knows every
+  // kernel before this one has completed (the decode GEMM streams weights before its own wait)
+  pdl_wait();  // the previous kernel's writes are visible from here on
   pdl_launch_dependents();
-  pdl_wait();  // (PDL) the previous kernel's writes are visible from here on
   const float gs = __ldg(p.gs);
 
   if (tid == 0) {
