@@ -113,17 +113,14 @@ ARC_API int arc_device_supported(void);
 /* Sizes of a quantized operand of `rows` rows (codes / sf bytes, Kp). */
 ARC_API arc_status_t arc_buffer_sizes(int64_t rows, int64_t K, int32_t S, int64_t* Kp, size_t* code_bytes,
                               size_t* sf_bytes);
-/* Workspace arc_gemm needs for M rows against qw (zero it once before the first use): the fp32
- * split-K / stream-K partials and tile counters used at
- * decode-size M (nsplit*M*N*4 bytes; 0 when the GEMM is not split). */
+/* Workspace arc_gemm needs for M rows against qw: 0 when the GEMM is not split, else 16 KB of
+ * per-tile arrival counters (offset 0) followed by the fp32 partials of the decode-size split
+ * paths.  Zero it once before the first use; every call leaves the counters at zero, so one
+ * workspace (sized for the largest call) serves calls of any shape on one stream. */
 ARC_API arc_status_t arc_gemm_workspace_size(int64_t M, const arc_qweight_t* qw, size_t* bytes);
-/* Workspace arc_linear needs (sized for both paths of arc_linear_ex, so one workspace serves
- * every mode):
- * 256 bytes of sync words at offset 0 (the fused kernel's grid barrier), then the quantized
- * activation + arc_gemm's workspace (unfused path) or the fused decode kernel's activation
- * operand, fp32 partials and split-tile counters (fused path, M <= 128).  The sync words must
- * be ZERO before the first use of a workspace (e.g. cudaMemsetAsync once after allocating it);
- * every call leaves them ready for the next one, so one workspace can serve every layer. */
+/* Workspace arc_linear needs: 16 KB of the GEMM's tile counters (offset 0), the quantized
+ * activation, then the GEMM's fp32 partials.  Zero it once before the first use (e.g. cudaMemsetAsync after allocating it);
+ * every call leaves it ready for the next one, so one workspace can serve every layer. */
 ARC_API arc_status_t arc_linear_workspace_size(int64_t M, const arc_qweight_t* qw, size_t* bytes);
 
 /* ---------------------------------------------------------------- calibration (offline) */
@@ -283,34 +280,24 @@ ARC_API arc_status_t arc_gemm_swiglu(const uint8_t* a_codes, const uint8_t* a_sf
                                      void* stream);
 /* The full ARC linear layer Y = X W^T computed as Eq.2: online activation
  * quantization feeding the augmented NVFP4 GEMM (two launches, PDL-chained).  x: bf16 [M][ldx]; y: [M][ldy] of
- * y_dtype.  ws: arc_linear_workspace_size(M, qw) bytes, 256-byte aligned, sync words zero
- * before first use (see above).  Same as arc_linear_ex(..., ARC_LINEAR_AUTO, ...). */
+ * y_dtype.  ws: arc_linear_workspace_size(M, qw) bytes, 256-byte aligned, zero before its
+ * first use (see above).  Same as arc_linear_ex(..., ARC_LINEAR_AUTO, ...). */
 ARC_API arc_status_t arc_linear(const void* x, int64_t M, int64_t ldx, const arc_profile_t* prof,
                         const arc_qweight_t* qw, void* y, arc_dtype_t y_dtype, int64_t ldy, void* ws,
                         size_t ws_bytes, void* stream);
 
-/* How arc_linear_ex runs the layer:
- *  ARC_LINEAR_UNFUSED: two launches -- arc_quantize_activation into the workspace, then arc_gemm
- *    (decode-size M: split-K + a fixed-order reduction kernel).
- *  ARC_LINEAR_FUSED (M <= 128 only, else ARC_ERR_SHAPE): ONE launch (the "optionally fused with
- *    the activation quantize as its producer stage" GEMM of the north star): every CTA
- *    quantizes a slice of the activation into the workspace, a grid barrier publishes it, the
- *    GEMM runs over an even (stream-K) split of the (256-feature tile, 256-element K block)
- *    units while the weights stream from HBM from the first cycle, and split tiles are summed
- *    in a fixed order (deterministic) by the last CTA to finish them.  The quantized activation
- *    is bit-identical to arc_quantize_activation's; Y matches within the GEMM tolerance.
- *  ARC_LINEAR_AUTO: UNFUSED (measured faster on B200 at every M: the fused kernel's grid barrier
- *    between its quantize phase and its first MMA costs more than a PDL-overlapped launch). */
+/* How arc_linear_ex runs the layer.  All modes launch two kernels on `stream`: arc_quantize_activation
+ * into the workspace, then arc_gemm, chained by programmatic dependent launch.  At decode-size M
+ * (<= 64) arc_gemm is the weight-streaming stream-K kernel, and because the kernel before it is this
+ * call's own quantize (which lets dependents launch only after its griddepcontrol.wait) it starts
+ * streaming the weights while the quantize runs.  ARC_LINEAR_FUSED is kept for ABI stability and
+ * behaves as ARC_LINEAR_UNFUSED (the round-1 one-kernel fused decode linear, slower on B200, was
+ * removed). */
 enum { ARC_LINEAR_AUTO = 0, ARC_LINEAR_FUSED = 1, ARC_LINEAR_UNFUSED = 2 };
 ARC_API arc_status_t arc_linear_ex_workspace_size(int64_t M, const arc_qweight_t* qw, int flags, size_t* bytes);
 ARC_API arc_status_t arc_linear_ex(const void* x, int64_t M, int64_t ldx, const arc_profile_t* prof,
                                    const arc_qweight_t* qw, void* y, arc_dtype_t y_dtype, int64_t ldy, void* ws,
                                    size_t ws_bytes, int flags, void* stream);
-/* Fused path only: where, inside a workspace of arc_linear_ex_workspace_size(M, qw, flags),
- * the fused kernel leaves the quantized activation (codes [M][Kp/2] at *code_off, scales in
- * the 128x4 tile layout at *sf_off; byte offsets from ws) -- for inspection and tests. */
-ARC_API arc_status_t arc_linear_fused_operand_offsets(int64_t M, const arc_qweight_t* qw, size_t* code_off,
-                                                      size_t* sf_off);
 /* arc_linear on HOST buffers: copies x_host (bf16 [M][K], pinned or pageable) to
  * the device, runs arc_linear, copies y back to y_host ([M][N] of y_dtype) and
  * synchronizes `stream`.  ws must hold arc_linear_hostio_workspace_size bytes. */

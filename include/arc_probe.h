@@ -24,11 +24,6 @@ ARC_API arc_status_t arc_probe_e4m3_ceil(const float* in, int64_t n, uint8_t* ou
 /* out[i] = the bf16 pattern of bf16(SiLU(g[i])) as the fused SiLU-mul quantize kernel computes
  * it (per-CTA table + closed-form tails, reading Q24), for bf16 patterns g[i]. */
 ARC_API arc_status_t arc_probe_silu(const uint16_t* g, int64_t n, uint16_t* out, void* stream);
-/* Timing experiments only: with env ARC_FUSED_TRACE set, the fused linear kernel records 8
- * globaltimer stamps per CTA of its last launch (entry, prologue, griddepcontrol.wait,
- * quantize phase, grid barrier, first full stage, last MMA, exit); copies up to max_ctas rows
- * of 8 uint64 to host memory (synchronous) and returns the row count (0 when tracing is off). */
-ARC_API int arc_debug_fused_trace(unsigned long long* host, int max_ctas);
 #ifdef __cplusplus
 }
 #endif

@@ -75,8 +75,6 @@ _sig("arc_linear", [_P, _i64, _i64, ctypes.POINTER(ArcProfile), ctypes.POINTER(A
 _sig("arc_linear_ex", [_P, _i64, _i64, ctypes.POINTER(ArcProfile), ctypes.POINTER(ArcQWeight), _P, ctypes.c_int,
                        _i64, _P, ctypes.c_size_t, ctypes.c_int, _P])
 _sig("arc_linear_ex_workspace_size", [_i64, ctypes.POINTER(ArcQWeight), ctypes.c_int, ctypes.POINTER(ctypes.c_size_t)])
-_sig("arc_linear_fused_operand_offsets", [_i64, ctypes.POINTER(ArcQWeight), ctypes.POINTER(ctypes.c_size_t),
-                                          ctypes.POINTER(ctypes.c_size_t)])
 _sig("arc_rmsnorm", [_P, _i64, _i64, _i64, _P, _f32, _P, _i64, _P])
 _sig("arc_rmsnorm_quantize_activation", [_P, _i64, _i64, _P, _f32, ctypes.POINTER(ArcProfile), _P, _P, _P])
 _sig("arc_linear_rmsnorm", [_P, _i64, _i64, _P, _f32, ctypes.POINTER(ArcProfile), ctypes.POINTER(ArcQWeight), _P,
@@ -107,11 +105,11 @@ EXPORTED = [
     "arc_linear_workspace_size",
     "arc_calib_absmax", "arc_select_outliers", "arc_gather_order", "arc_tensor_scale", "arc_quantize_weight",
     "arc_quantize_activation", "arc_gemm", "arc_linear", "arc_linear_ex", "arc_linear_ex_workspace_size",
-    "arc_linear_fused_operand_offsets", "arc_linear_hostio_workspace_size", "arc_rmsnorm",
+    "arc_linear_hostio_workspace_size", "arc_rmsnorm",
     "arc_rmsnorm_quantize_activation", "arc_linear_rmsnorm", "arc_linear_hostio",
     "arc_silu_mul", "arc_silu_mul_quantize_activation", "arc_linear_silu_mul", "arc_gemm_swiglu",
     "arc_mx_tensor_scale", "arc_mx_tensor_scale_device", "arc_quantize_activation_mx", "arc_quantize_weight_mx", "arc_gather_order_ex",
-    "arc_probe_e2m1", "arc_probe_e2m1_bits", "arc_probe_e2m1_raw_bits", "arc_probe_e4m3_ceil", "arc_debug_fused_trace", "arc_probe_silu",
+    "arc_probe_e2m1", "arc_probe_e2m1_bits", "arc_probe_e2m1_raw_bits", "arc_probe_e4m3_ceil", "arc_probe_silu",
 ]
 
 
@@ -312,8 +310,8 @@ def _dtype_code(dt) -> int:
 
 class Workspace:
     """Grow-only device workspace for arc_gemm / arc_linear (256-byte aligned by the
-    allocator, zero-filled on allocation: the sync words of the fused kernel (grid barrier,
-    per-tile counters) must start at 0, and every call leaves them at 0).  A Workspace belongs to
+    allocator, zero-filled on allocation: the decode-size GEMM's per-tile arrival counters must start
+    at 0, and every call leaves them at 0).  A Workspace belongs to
     one stream: calls that share one must be ordered on that stream (the defaults are per stream)."""
 
     def __init__(self, device="cuda"):
@@ -398,19 +396,11 @@ def linear_workspace_size_ex(M: int, qw, mode: str = "auto") -> int:
     return b.value
 
 
-def fused_operand_offsets(M: int, qw):
-    """Byte offsets (codes, scales) of the quantized activation the fused kernel leaves in its workspace."""
-    c, f = ctypes.c_size_t(), ctypes.c_size_t()
-    _check(_lib.arc_linear_fused_operand_offsets(M, ctypes.byref(qw.c()), ctypes.byref(c), ctypes.byref(f)),
-           "arc_linear_fused_operand_offsets")
-    return c.value, f.value
-
-
 def linear(x: torch.Tensor, prof: Profile, qw: QWeight, out_dtype=torch.bfloat16, out=None, ws: Workspace = None,
            stream=None, mode: str = "auto"):
-    """The ARC linear layer (Eq.2): activation quantize + augmented NVFP4 GEMM.  mode "unfused" = two
-    launches (quantize kernel, GEMM kernel); "fused" (M <= 128) = one kernel that quantizes, multiplies
-    and reduces (slower on B200, see decode.cu); "auto" = unfused."""
+    """The ARC linear layer (Eq.2): activation quantize + augmented NVFP4 GEMM (two PDL-chained kernels;
+    at M <= 64 the GEMM streams the weights while the quantize runs).  mode is kept for the C ABI's
+    flags; every mode runs the same path."""
     assert x.dtype == torch.bfloat16 and x.is_cuda
     M = x.shape[0]
     if out is None:

@@ -136,19 +136,11 @@ arc_status_t arc_gemm_workspace_size(int64_t M, const arc_qweight_t* qw, size_t*
   return ARC_OK;
 }
 
-// arc_linear workspace: [sync words | quantized A + arc_gemm workspace] (unfused) or
-// [sync words | fused-kernel workspace] (fused, M <= 128); the sync words sit at offset 0
-// in both so a workspace shared by both paths keeps them zero.
-static size_t linear_rest_bytes(int64_t M, const arc_qweight_t* qw, int flags) {
-  size_t rest = 0;
-  if (flags != ARC_LINEAR_FUSED) {
-    rest = act_ws_bytes(M, qw->K, qw->S) + (size_t)round_up((int64_t)plan_gemm(M, qw->N, qw->Kp).ws_bytes, 256);
-  }
-  if (flags != ARC_LINEAR_UNFUSED) {
-    const FusedPlan fp = plan_fused(M, qw->N, qw->Kp);
-    if (fp.ok) rest = std::max(rest, (size_t)round_up((int64_t)fp.ws_bytes, 256));
-  }
-  return rest;
+// arc_linear workspace: [GEMM tile counters (kGemmCounterBytes, fixed at offset 0 so calls of any
+// shape can share the workspace) | quantized A | GEMM fp32 partials].
+static size_t linear_rest_bytes(int64_t M, const arc_qweight_t* qw, int /*flags*/) {
+  const size_t g = plan_gemm(M, qw->N, qw->Kp).ws_bytes;
+  return act_ws_bytes(M, qw->K, qw->S) + (g ? (size_t)round_up((int64_t)(g - kGemmCounterBytes), 256) : 0);
 }
 
 arc_status_t arc_linear_workspace_size(int64_t M, const arc_qweight_t* qw, size_t* bytes) {
@@ -446,21 +438,34 @@ arc_status_t arc_silu_mul_quantize_activation(const void* gu, int64_t M, int64_t
 }
 
 static arc_status_t gemm_impl(const uint8_t* a_codes, const uint8_t* a_sf, const float* gs_x, int64_t M,
-                              const arc_qweight_t* qw, void* y, arc_dtype_t y_dtype, int64_t ldy, void* ws,
-                              size_t ws_bytes, void* stream, int weights_ready);
+                              const arc_qweight_t* qw, void* y, arc_dtype_t y_dtype, int64_t ldy, void* cnt,
+                              void* part, size_t part_bytes, void* stream, int weights_ready);
+
+// A public GEMM workspace is [kGemmCounterBytes of tile counters | fp32 partials].
+static void split_gemm_ws(void* ws, size_t ws_bytes, void** cnt, void** part, size_t* part_bytes) {
+  *cnt = ws;
+  *part = ws && ws_bytes >= kGemmCounterBytes ? static_cast<uint8_t*>(ws) + kGemmCounterBytes : nullptr;
+  *part_bytes = ws_bytes >= kGemmCounterBytes ? ws_bytes - kGemmCounterBytes : 0;
+}
 
 arc_status_t arc_gemm(const uint8_t* a_codes, const uint8_t* a_sf, const float* gs_x, int64_t M,
                       const arc_qweight_t* qw, void* y, arc_dtype_t y_dtype, int64_t ldy, void* ws, size_t ws_bytes,
                       void* stream) {
-  return gemm_impl(a_codes, a_sf, gs_x, M, qw, y, y_dtype, ldy, ws, ws_bytes, stream, 0);
+  const GemmPlan pl = M > 0 && check_qweight(qw) == ARC_OK ? plan_gemm(M, qw->N, qw->Kp) : GemmPlan{};
+  if (M > 0 && pl.ws_bytes > 0 && (!ws || ws_bytes < pl.ws_bytes))
+    return fail(ARC_ERR_WORKSPACE, "split-K workspace too small");
+  void *cnt, *part;
+  size_t part_bytes;
+  split_gemm_ws(ws, ws_bytes, &cnt, &part, &part_bytes);
+  return gemm_impl(a_codes, a_sf, gs_x, M, qw, y, y_dtype, ldy, cnt, part, part_bytes, stream, 0);
 }
 
 // weights_ready: the caller knows the weights were complete before the kernel preceding this GEMM
 // started (arc_linear*: that kernel is its own activation quantize), so the decode-size kernel may
 // stream them before griddepcontrol.wait.
 static arc_status_t gemm_impl(const uint8_t* a_codes, const uint8_t* a_sf, const float* gs_x, int64_t M,
-                              const arc_qweight_t* qw, void* y, arc_dtype_t y_dtype, int64_t ldy, void* ws,
-                              size_t ws_bytes, void* stream, int weights_ready) {
+                              const arc_qweight_t* qw, void* y, arc_dtype_t y_dtype, int64_t ldy, void* cnt,
+                              void* part, size_t part_bytes, void* stream, int weights_ready) {
   arc_status_t s = check_qweight(qw);
   if (s != ARC_OK) return s;
   if (M < 0 || M > (1 << 30)) return fail(ARC_ERR_SHAPE, "bad M");
@@ -471,11 +476,11 @@ static arc_status_t gemm_impl(const uint8_t* a_codes, const uint8_t* a_sf, const
     return fail(ARC_ERR_SHAPE, "ldy must be >= N and a multiple of 16 bytes");
   if (!aligned16(a_codes) || !aligned16(a_sf) || !aligned16(y)) return fail(ARC_ERR_ALIGN, "buffer not 16B aligned");
   const GemmPlan pl = plan_gemm(M, qw->N, qw->Kp);
-  if (pl.ws_bytes > 0 && (!ws || ws_bytes < pl.ws_bytes)) return fail(ARC_ERR_WORKSPACE, "split-K workspace too small");
-  if (ws && !aligned16(ws)) return fail(ARC_ERR_ALIGN, "ws not 16B aligned");
+  if (pl.ws_bytes > 0 && (!cnt || !part || part_bytes + kGemmCounterBytes < pl.ws_bytes))
+    return fail(ARC_ERR_WORKSPACE, "split-K workspace too small");
+  if ((cnt && !aligned16(cnt)) || (part && !aligned16(part))) return fail(ARC_ERR_ALIGN, "ws not 16B aligned");
   s = check_device();
   if (s != ARC_OK) return s;
-  if (M == 0) return ARC_OK;
   GemmProblem p;
   p.M = M;
   p.N = qw->N;
@@ -489,8 +494,9 @@ static arc_status_t gemm_impl(const uint8_t* a_codes, const uint8_t* a_sf, const
   p.y = y;
   p.ldy = ldy;
   p.y_fp32 = y_dtype == ARC_FP32;
-  p.ws = ws;
-  p.ws_bytes = ws_bytes;
+  p.cnt = static_cast<unsigned*>(cnt);
+  p.ws = part;
+  p.ws_bytes = part_bytes;
   p.weights_ready = weights_ready;
   const char* detail = nullptr;
   cudaError_t e = launch_gemm(p, (cudaStream_t)stream, &detail);
@@ -512,6 +518,9 @@ arc_status_t arc_gemm_swiglu(const uint8_t* a_codes, const uint8_t* a_sf, const 
   if (ws && !aligned16(ws)) return fail(ARC_ERR_ALIGN, "ws not 16B aligned");
   s = check_device();
   if (s != ARC_OK) return s;
+  void *cnt, *part;
+  size_t part_bytes;
+  split_gemm_ws(ws, ws_bytes, &cnt, &part, &part_bytes);
   GemmProblem p;
   p.M = M;
   p.N = qw->N;
@@ -526,8 +535,9 @@ arc_status_t arc_gemm_swiglu(const uint8_t* a_codes, const uint8_t* a_sf, const 
   p.ldy = ldh;
   p.y_fp32 = 0;
   p.swiglu = 1;
-  p.ws = ws;
-  p.ws_bytes = ws_bytes;
+  p.cnt = static_cast<unsigned*>(cnt);
+  p.ws = part;
+  p.ws_bytes = part_bytes;
   const char* detail = nullptr;
   cudaError_t e = launch_gemm(p, (cudaStream_t)stream, &detail);
   return e == cudaSuccess ? ARC_OK : cuda_fail(e, "arc_gemm_swiglu", detail);
@@ -545,7 +555,6 @@ arc_status_t arc_linear_ex(const void* x, int64_t M, int64_t ldx, const arc_prof
   if (flags != ARC_LINEAR_AUTO && flags != ARC_LINEAR_FUSED && flags != ARC_LINEAR_UNFUSED)
     return fail(ARC_ERR_SHAPE, "bad flags");
   if (M < 0 || M > (1 << 30)) return fail(ARC_ERR_SHAPE, "bad M");
-  if (flags == ARC_LINEAR_FUSED && M > 128) return fail(ARC_ERR_SHAPE, "ARC_LINEAR_FUSED needs M <= 128");
   if (M == 0) return ARC_OK;
   if (!ws || !x || !y) return fail(ARC_ERR_NULL, "null x / y / workspace");
   if (ldx < prof->K || ldx % 8) return fail(ARC_ERR_SHAPE, "bad ldx");
@@ -558,41 +567,12 @@ arc_status_t arc_linear_ex(const void* x, int64_t M, int64_t ldx, const arc_prof
   if (!aligned16(x) || !aligned16(y)) return fail(ARC_ERR_ALIGN, "x / y not 16B aligned");
   uint8_t* rest = static_cast<uint8_t*>(ws) + sync;
   const size_t rest_bytes = ws_bytes - sync;
-  // AUTO = unfused: the one-kernel fused path measured slower on B200 at every M (decode.cu)
-  const bool fused = flags == ARC_LINEAR_FUSED;
-  if (fused) {
-    s = check_device();
-    if (s != ARC_OK) return s;
-    FusedProblem p;
-    p.x = x;
-    p.ldx = ldx;
-    p.perm = prof->perm;
-    p.gs_x = prof->gs;
-    p.M = M;
-    p.N = qw->N;
-    p.K = qw->K;
-    p.S = qw->S;
-    p.Kp = qw->Kp;
-    p.layout = (int)qw->layout;
-    p.b_codes = qw->codes;
-    p.b_sf = qw->sf;
-    p.gs_w = qw->gs;
-    p.y = y;
-    p.ldy = ldy;
-    p.y_fp32 = y_dtype == ARC_FP32;
-    p.sync = reinterpret_cast<unsigned*>(ws);
-    p.ws = rest;
-    p.ws_bytes = rest_bytes;
-    const char* detail = nullptr;
-    cudaError_t e = launch_linear_fused(p, (cudaStream_t)stream, &detail);
-    return e == cudaSuccess ? ARC_OK : cuda_fail(e, "arc_linear (fused)", detail);
-  }
   uint8_t* codes = rest;
   uint8_t* sf = codes + round_up(M * (qw->Kp / 2), 256);
   const size_t act = act_ws_bytes(M, qw->K, qw->S);
   s = arc_quantize_activation(x, M, ldx, prof, codes, sf, stream);
   if (s != ARC_OK) return s;
-  return gemm_impl(codes, sf, prof->gs, M, qw, y, y_dtype, ldy, rest + act, rest_bytes - act, stream, 1);
+  return gemm_impl(codes, sf, prof->gs, M, qw, y, y_dtype, ldy, ws, rest + act, rest_bytes - act, stream, 1);
 }
 
 arc_status_t arc_linear_rmsnorm(const void* x, int64_t M, int64_t ldx, const void* gamma, float eps,
@@ -615,7 +595,7 @@ arc_status_t arc_linear_rmsnorm(const void* x, int64_t M, int64_t ldx, const voi
   const size_t act = act_ws_bytes(M, qw->K, qw->S);
   s = arc_rmsnorm_quantize_activation(x, M, ldx, gamma, eps, prof, codes, sf, stream);
   if (s != ARC_OK) return s;
-  return gemm_impl(codes, sf, prof->gs, M, qw, y, y_dtype, ldy, codes + act, ws_bytes - sync - act, stream, 1);
+  return gemm_impl(codes, sf, prof->gs, M, qw, y, y_dtype, ldy, ws, codes + act, ws_bytes - sync - act, stream, 1);
 }
 
 arc_status_t arc_linear_silu_mul(const void* gu, int64_t M, int64_t ld, int64_t up_off, const arc_profile_t* prof,
@@ -638,7 +618,7 @@ arc_status_t arc_linear_silu_mul(const void* gu, int64_t M, int64_t ld, int64_t 
   const size_t act = act_ws_bytes(M, qw->K, qw->S);
   s = arc_silu_mul_quantize_activation(gu, M, ld, up_off, prof, codes, sf, stream);
   if (s != ARC_OK) return s;
-  return gemm_impl(codes, sf, prof->gs, M, qw, y, y_dtype, ldy, codes + act, ws_bytes - sync - act, stream, 1);
+  return gemm_impl(codes, sf, prof->gs, M, qw, y, y_dtype, ldy, ws, codes + act, ws_bytes - sync - act, stream, 1);
 }
 
 arc_status_t arc_linear(const void* x, int64_t M, int64_t ldx, const arc_profile_t* prof, const arc_qweight_t* qw,
@@ -653,22 +633,10 @@ arc_status_t arc_linear_ex_workspace_size(int64_t M, const arc_qweight_t* qw, in
   if (M < 0) return fail(ARC_ERR_SHAPE, "M < 0");
   if (flags != ARC_LINEAR_AUTO && flags != ARC_LINEAR_FUSED && flags != ARC_LINEAR_UNFUSED)
     return fail(ARC_ERR_SHAPE, "bad flags");
-  if (flags == ARC_LINEAR_FUSED && M > 128) return fail(ARC_ERR_SHAPE, "ARC_LINEAR_FUSED needs M <= 128");
   *bytes = sync_bytes_of(qw->N) + (M == 0 ? 0 : linear_rest_bytes(M, qw, flags));
   return ARC_OK;
 }
 
-arc_status_t arc_linear_fused_operand_offsets(int64_t M, const arc_qweight_t* qw, size_t* code_off,
-                                              size_t* sf_off) {
-  arc_status_t s = check_qweight(qw);
-  if (s != ARC_OK) return s;
-  if (!code_off || !sf_off) return fail(ARC_ERR_NULL, "null offset");
-  const FusedPlan fp = plan_fused(M, qw->N, qw->Kp);
-  if (!fp.ok) return fail(ARC_ERR_SHAPE, "fused path needs 1 <= M <= 128");
-  *code_off = sync_bytes_of(qw->N);
-  *sf_off = *code_off + fp.a_code_bytes;
-  return ARC_OK;
-}
 
 arc_status_t arc_linear_hostio_workspace_size(int64_t M, const arc_qweight_t* qw, arc_dtype_t y_dtype,
                                               size_t* bytes) {

@@ -61,8 +61,9 @@ struct GemmProblem {
   int64_t ldy;
   int y_fp32;
   int swiglu = 0;    // SwiGLU epilogue (gate/up rows interleaved in groups of 16): y = h [M][N/2] bf16
-  void* ws;          // split-K partials (decode-size M), may be null when plan.ws_bytes == 0
-  size_t ws_bytes;
+  unsigned* cnt = nullptr;  // kGemmCounterBytes of per-tile arrival counters (zero; left zero), decode-size M
+  void* ws;                 // fp32 partials of the decode-size split paths (may be null when not split)
+  size_t ws_bytes;          // bytes at ws
   // The weights were complete before the kernel preceding this GEMM started (arc_linear: that
   // kernel is the activation quantize, which lets dependents launch only after its own
   // griddepcontrol.wait): the decode-size kernel may then stream them before its own wait.
@@ -88,40 +89,16 @@ GemmPlan plan_gemm(int64_t M, int64_t N, int64_t Kp);
 // Returns a CUresult-style error through cudaError_t (cudaErrorUnknown + text) on encode failure.
 cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t stream, const char** detail);
 
-// sync words at offset 0 of every arc_linear workspace (fused linear's grid-barrier count and
-// generation; a fixed size so workspaces shared across layers keep them in place): zero before
-// the first use, the count is left zero by every call.
-inline size_t sync_bytes_of(int64_t /*N*/) { return 256; }
+// Bytes at offset 0 of every arc_linear workspace: the GEMM's per-tile counters (kGemmCounterBytes).
+inline size_t sync_bytes_of(int64_t /*N*/);
 
 // 2-D K-major operand tensor map (uint8 [rows][row_bytes], 128B swizzle, box box_bytes x box_rows).
 bool make_operand_map(CUtensorMap* m, const void* base, int64_t rows, int64_t row_bytes, int box_rows, int box_bytes);
 
-// Fused decode linear (decode.cu): quantize + augmented GEMM + split reduction in one kernel, M <= 128.
-struct FusedProblem {
-  const void* x;
-  int64_t ldx;
-  const int32_t* perm;
-  const float* gs_x;
-  int64_t M, N, K, S, Kp;
-  int layout;
-  const uint8_t* b_codes;
-  const uint8_t* b_sf;
-  const float* gs_w;
-  void* y;
-  int64_t ldy;
-  int y_fp32;
-  unsigned* sync;    // sync_bytes_of(N) bytes, zero before first use
-  void* ws;          // FusedPlan::ws_bytes: A codes, A scales, partials
-  size_t ws_bytes;
-};
-struct FusedPlan {
-  bool ok;           // 1 <= M <= 128
-  int grid;          // CTAs (<= SM count, all co-resident)
-  int64_t units;     // stream-K units: N tiles x K blocks
-  int maxseg;        // most CTAs sharing one N tile
-  size_t a_code_bytes, a_sf_bytes, part_bytes, cnt_bytes, ws_bytes;
-};
-FusedPlan plan_fused(int64_t M, int64_t N, int64_t Kp);
-cudaError_t launch_linear_fused(const FusedProblem& p, cudaStream_t stream, const char** detail);
+// Every arc_gemm workspace starts with this many bytes of per-tile arrival counters (the
+// decode-size stream-K kernel's), zero before the first use and left zero by every call; the
+// fp32 partials of either split path follow them, so calls of any shape can share one workspace.
+constexpr size_t kGemmCounterBytes = 16384;
+inline size_t sync_bytes_of(int64_t /*N*/) { return kGemmCounterBytes; }
 
 }  // namespace arc

@@ -785,7 +785,8 @@ GemmPlan plan_gemm(int64_t M, int64_t N, int64_t Kp) {
       }
     }
   }
-  pl.ws_bytes = pl.nsplit > 1 ? (size_t)pl.nsplit * (size_t)M * (size_t)round_up(N, 4) * sizeof(float) : 0;
+  pl.ws_bytes = pl.nsplit > 1 ? kGemmCounterBytes + (size_t)pl.nsplit * (size_t)M * (size_t)round_up(N, 4) * sizeof(float)
+                              : 0;
   // decode-size M: the stream-K kernel (stream_gemm.cu); the split-K path stays for the SwiGLU epilogue
   const StreamPlan sp = plan_stream(M, N, Kp);
   if (sp.ok) pl.ws_bytes = std::max(pl.ws_bytes, sp.ws_bytes);
@@ -804,7 +805,7 @@ cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t stream, const char** 
   static const int env_swp = getenv("ARC_GEMM_SWIGLU_PAIR") ? atoi(getenv("ARC_GEMM_SWIGLU_PAIR")) : 1;
   if (p.swiglu && env_swp && pl.CL == 2 && pl.nsplit == 1) pl.pair = 1;
   const int CL = pl.CL;
-  if (pl.nsplit > 1 && (p.ws == nullptr || p.ws_bytes < pl.ws_bytes)) {
+  if (pl.nsplit > 1 && (p.ws == nullptr || p.ws_bytes + kGemmCounterBytes < pl.ws_bytes)) {
     if (detail) *detail = "split-K workspace too small";
     return cudaErrorInvalidValue;
   }
@@ -903,7 +904,7 @@ cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t stream, const char** 
     ra[0].val.programmaticStreamSerializationAllowed = 1;
     rc.attrs = ra;
     rc.numAttrs = 1;
-    e = cudaLaunchKernelEx(&rc, arc_splitk_reduce_kernel, static_cast<const float*>(p.ws), (int)pl.nsplit, (int)p.M,
+    e = cudaLaunchKernelEx(&rc, arc_splitk_reduce_kernel, static_cast<const float*>(a.ws), (int)pl.nsplit, (int)p.M,
                            (int)p.N, p.y, p.ldy, p.y_fp32, p.swiglu);
     if (e != cudaSuccess) return e;
   }

@@ -256,17 +256,20 @@ __global__ void __launch_bounds__(S_THREADS, 1)
       } else {
         // split tile: publish this segment's fp32 partial, the last arriver reduces in segment order
         float* slot = args.part + (((int64_t)tile * args.maxseg + si) * args.a_rows) * SBN;
-        if (has_rows && m < args.a_rows) {
+        // (tcgen05.ld is warp-collective: the loads run warp-uniformly, only the stores are per row)
+        if (has_rows) {
 #pragma unroll 1
           for (int c = 0; c < SBN / 32; ++c) {
             uint32_t r[32];
             tmem_ld_32x32b_x32(tacc + c * 32, r);
             tmem_ld_wait();
-            float* dst = slot + (int64_t)m * SBN + c * 32;
+            if (m < args.M) {
+              float* dst = slot + (int64_t)m * SBN + c * 32;
 #pragma unroll
-            for (int j = 0; j < 32; j += 4)
-              __stcg(reinterpret_cast<float4*>(dst + j), make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
-                                                                    __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3])));
+              for (int j = 0; j < 32; j += 4)
+                __stcg(reinterpret_cast<float4*>(dst + j), make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
+                                                                      __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3])));
+            }
           }
         }
         __threadfence();
@@ -281,7 +284,7 @@ __global__ void __launch_bounds__(S_THREADS, 1)
           *last_flag = is_last;
         }
         named_bar_sync(1, 128);
-        if (*last_flag && has_rows && m < args.M) {
+        if (*last_flag && has_rows) {  // warp-uniform (tcgen05.ld); rows >= M compute but never store
           const float* base = args.part + ((int64_t)tile * args.maxseg * args.a_rows + m) * SBN;
 #pragma unroll 1
           for (int c = 0; c < SBN / 32; ++c) {
@@ -289,12 +292,13 @@ __global__ void __launch_bounds__(S_THREADS, 1)
             tmem_ld_32x32b_x32(tacc + c * 32, r);
             tmem_ld_wait();
             float acc[32];
+            const int mr = min(m, args.M - 1);  // rows >= M read a valid row's partials (result unused)
             for (int s = 0; s < nseg; ++s) {
               if (s == si) {
 #pragma unroll
                 for (int j = 0; j < 32; ++j) acc[j] = s == 0 ? __uint_as_float(r[j]) : __fadd_rn(acc[j], __uint_as_float(r[j]));
               } else {
-                const float* src = base + (int64_t)s * args.a_rows * SBN + c * 32;
+                const float* src = base + ((int64_t)s * args.a_rows + (mr - m)) * SBN + c * 32;
 #pragma unroll
                 for (int j = 0; j < 32; j += 4) {
                   const float4 p = __ldcg(reinterpret_cast<const float4*>(src + j));
@@ -311,7 +315,7 @@ __global__ void __launch_bounds__(S_THREADS, 1)
             }
 #pragma unroll
             for (int j = 0; j < 32; ++j) acc[j] = __fmul_rn(acc[j], alpha);
-            if (n_base + c * 32 < args.N) store_row_chunk(args, m, n_base + c * 32, acc);
+            if (m < args.M && n_base + c * 32 < args.N) store_row_chunk(args, m, n_base + c * 32, acc);
           }
         }
       }
@@ -348,14 +352,18 @@ StreamPlan plan_stream(int64_t M, int64_t N, int64_t Kp) {
     const int64_t cf = ((f + 1) * pl.grid - 1) / pl.units, cl = ((l + 1) * pl.grid - 1) / pl.units;
     pl.maxseg = std::max<int64_t>(pl.maxseg, cl - cf + 1);
   }
+  if (pl.n_tiles * 4 > (int64_t)kGemmCounterBytes) {  // N > 524288: no counter room
+    pl.ok = false;
+    return pl;
+  }
   pl.part_bytes = (size_t)round_up((int64_t)pl.n_tiles * pl.maxseg * pl.a_rows * SBN * 4, 256);
-  pl.cnt_bytes = (size_t)round_up(pl.n_tiles * 4, 256);
-  pl.ws_bytes = pl.part_bytes + pl.cnt_bytes;
+  pl.cnt_bytes = kGemmCounterBytes;
+  pl.ws_bytes = pl.cnt_bytes + pl.part_bytes;  // [counters | partials]
   return pl;
 }
 
 cudaError_t launch_stream_gemm(const GemmProblem& p, const StreamPlan& pl, cudaStream_t stream, const char** detail) {
-  if (!pl.ok || p.ws == nullptr || p.ws_bytes < pl.ws_bytes) {
+  if (!pl.ok || p.ws == nullptr || p.cnt == nullptr || p.ws_bytes < pl.part_bytes) {
     if (detail) *detail = "stream-K workspace too small";
     return cudaErrorInvalidValue;
   }
@@ -386,8 +394,8 @@ cudaError_t launch_stream_gemm(const GemmProblem& p, const StreamPlan& pl, cudaS
   a.y = p.y;
   a.ldy = p.ldy;
   a.y_fp32 = p.y_fp32;
+  a.cnt = p.cnt;
   a.part = static_cast<float*>(p.ws);
-  a.cnt = reinterpret_cast<unsigned*>(static_cast<uint8_t*>(p.ws) + pl.part_bytes);
   a.maxseg = (int)pl.maxseg;
   a.w_early = p.weights_ready;
   static const int dbg = getenv("ARC_STREAM_DEBUG") ? atoi(getenv("ARC_STREAM_DEBUG")) : 0;

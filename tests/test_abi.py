@@ -83,7 +83,7 @@ def test_no_fallback_without_sm100(arc):
     assert lib.arc_device_supported() == 0
     assert lib.arc_quantize_activation(fake, 4, 256, ctypes.byref(prof), fake, fake, None) == 4
     qw = arc.ArcQWeight(64, 256, 320, 16, 0, 0x10000, 0x10000, 0x10000)
-    assert lib.arc_gemm(fake, fake, fake, 4, ctypes.byref(qw), fake, 0, 64, None, 0, None) == 4
+    assert lib.arc_gemm(fake, fake, fake, 4, ctypes.byref(qw), fake, 0, 64, fake, 1 << 20, None) == 4
 
 
 def test_select_outliers_matches_oracle(arc):
