@@ -337,7 +337,8 @@ def time_graph(fn, reps=50, warm=3):
 def decode_sweep(A, sites, device, peaks, Ms=(1, 4, 16, 32, 64)):
     """BASELINE configs[1] decode token counts: the same 4 sites at M tokens, CUDA-graph replay.  The
     weights of the 4 sites (~128 MB at LLaMA-3-8B, > L2) stream from HBM every step.  Bound = weight
-    + activation bytes / HBM."""
+    + activation bytes / HBM.  Default arc_linear (quantize kernel + split-K GEMM + reduce kernel per
+    site) and, beside it, ARC_LINEAR_FUSED (one in-kernel-quantize stream-K kernel per site)."""
     out = []
     wbytes = sum(s.N * s.Kp * 9 // 16 for s in sites)
     for Md in Ms:
@@ -349,10 +350,17 @@ def decode_sweep(A, sites, device, peaks, Ms=(1, 4, 16, 32, 64)):
             for s, x_, y_, w_ in zip(sites, xd, yd, wsd):
                 A.linear(x_, s.prof, s.qw, out=y_, ws=w_)
         ms = time_graph(step)
+
+        def step_fused():
+            for s, x_, y_, w_ in zip(sites, xd, yd, wsd):
+                A.linear(x_, s.prof, s.qw, out=y_, ws=w_, mode="fused")
+        ms_f = time_graph(step_fused)
         dbytes = wbytes + sum(Md * s.K * 2 + Md * s.N * 2 for s in sites)
         out.append({"M_tokens": Md, "us_per_layer_step": ms * 1e3, "bytes_per_step": dbytes,
                     "achieved_gbs": dbytes / (ms * 1e-3) / 1e9, "hbm_frac": dbytes / (ms * 1e-3) / 1e9 / peaks["hbm"],
-                    "tflops": sum(2.0 * Md * s.N * (s.K + s.S) for s in sites) / (ms * 1e-3) / 1e12})
+                    "tflops": sum(2.0 * Md * s.N * (s.K + s.S) for s in sites) / (ms * 1e-3) / 1e12,
+                    "fused_us_per_layer_step": ms_f * 1e3,
+                    "fused_hbm_frac": dbytes / (ms_f * 1e-3) / 1e9 / peaks["hbm"]})
     return out
 
 

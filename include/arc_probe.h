@@ -24,6 +24,12 @@ ARC_API arc_status_t arc_probe_e4m3_ceil(const float* in, int64_t n, uint8_t* ou
 /* out[i] = the bf16 pattern of bf16(SiLU(g[i])) as the fused SiLU-mul quantize kernel computes
  * it (per-CTA table + closed-form tails, reading Q24), for bf16 patterns g[i]. */
 ARC_API arc_status_t arc_probe_silu(const uint16_t* g, int64_t n, uint16_t* out, void* stream);
+/* Timing experiments only: with env ARC_STREAM_TRACE set, the decode-size stream-K GEMM records 8
+ * globaltimer stamps per CTA of its last launch (entry, early weight loads issued,
+ * griddepcontrol.wait passed, first stage ready, last MMA issued, last segment's accumulator
+ * ready, split-tile arrival counted, epilogue done); copies max_ctas rows of 8 uint64 to host
+ * memory (synchronous) and returns the row count (0 when tracing is off). */
+ARC_API int arc_debug_stream_trace(unsigned long long* host, int max_ctas);
 #ifdef __cplusplus
 }
 #endif

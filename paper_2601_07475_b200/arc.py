@@ -110,6 +110,7 @@ EXPORTED = [
     "arc_silu_mul", "arc_silu_mul_quantize_activation", "arc_linear_silu_mul", "arc_gemm_swiglu",
     "arc_mx_tensor_scale", "arc_mx_tensor_scale_device", "arc_quantize_activation_mx", "arc_quantize_weight_mx", "arc_gather_order_ex",
     "arc_probe_e2m1", "arc_probe_e2m1_bits", "arc_probe_e2m1_raw_bits", "arc_probe_e4m3_ceil", "arc_probe_silu",
+    "arc_debug_stream_trace",
 ]
 
 
@@ -398,9 +399,9 @@ def linear_workspace_size_ex(M: int, qw, mode: str = "auto") -> int:
 
 def linear(x: torch.Tensor, prof: Profile, qw: QWeight, out_dtype=torch.bfloat16, out=None, ws: Workspace = None,
            stream=None, mode: str = "auto"):
-    """The ARC linear layer (Eq.2): activation quantize + augmented NVFP4 GEMM (two PDL-chained kernels;
-    at M <= 64 the GEMM streams the weights while the quantize runs).  mode is kept for the C ABI's
-    flags; every mode runs the same path."""
+    """The ARC linear layer (Eq.2): activation quantize + augmented NVFP4 GEMM.  mode "auto" / "unfused" =
+    two PDL-chained kernels; "fused" (M <= 64) = one kernel that quantizes the activation and runs the
+    weight-streaming stream-K GEMM (arc.h ARC_LINEAR_FUSED; measured slower on B200)."""
     assert x.dtype == torch.bfloat16 and x.is_cuda
     M = x.shape[0]
     if out is None:

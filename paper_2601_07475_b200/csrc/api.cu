@@ -570,6 +570,37 @@ arc_status_t arc_linear_ex(const void* x, int64_t M, int64_t ldx, const arc_prof
   uint8_t* codes = rest;
   uint8_t* sf = codes + round_up(M * (qw->Kp / 2), 256);
   const size_t act = act_ws_bytes(M, qw->K, qw->S);
+  // ARC_LINEAR_FUSED at decode-size M: one kernel quantizes the activation into the workspace and runs
+  // the stream-K GEMM (measured slower than the two-kernel path on B200, so AUTO takes
+  // the two-kernel path)
+  const StreamPlan sp = plan_stream(M, qw->N, qw->Kp);
+  if (flags == ARC_LINEAR_FUSED && sp.ok) {
+    // decode-size M: one kernel quantizes the activation into the workspace and runs the stream-K GEMM
+    s = check_device();
+    if (s != ARC_OK) return s;
+    if (!aligned16(prof->perm)) return fail(ARC_ERR_ALIGN, "perm not 16B aligned");
+    GemmProblem p;
+    p.M = M;
+    p.N = qw->N;
+    p.Kp = qw->Kp;
+    p.a_codes = codes;
+    p.a_sf = sf;
+    p.b_codes = qw->codes;
+    p.b_sf = qw->sf;
+    p.gs_x = prof->gs;
+    p.gs_w = qw->gs;
+    p.y = y;
+    p.ldy = ldy;
+    p.y_fp32 = y_dtype == ARC_FP32;
+    p.cnt = static_cast<unsigned*>(ws);
+    p.ws = rest + act;
+    p.ws_bytes = rest_bytes - act;
+    p.weights_ready = 1;
+    StreamQuant fq{x, ldx, prof->perm, (int)prof->K, (int)prof->S, (int)prof->layout};
+    const char* detail = nullptr;
+    cudaError_t e = launch_stream_gemm(p, sp, (cudaStream_t)stream, &detail, &fq);
+    return e == cudaSuccess ? ARC_OK : cuda_fail(e, "arc_linear (fused decode)", detail);
+  }
   s = arc_quantize_activation(x, M, ldx, prof, codes, sf, stream);
   if (s != ARC_OK) return s;
   return gemm_impl(codes, sf, prof->gs, M, qw, y, y_dtype, ldy, ws, rest + act, rest_bytes - act, stream, 1);

@@ -78,7 +78,16 @@ struct StreamPlan {
   size_t part_bytes = 0, cnt_bytes = 0, ws_bytes = 0;   // workspace: partials + counters (zero before use)
 };
 StreamPlan plan_stream(int64_t M, int64_t N, int64_t Kp);
-cudaError_t launch_stream_gemm(const GemmProblem& p, const StreamPlan& pl, cudaStream_t stream, const char** detail);
+// The activation the decode-size kernel quantizes itself (fused arc_linear): bf16 x [M][ldx], the
+// profile's perm / S / layout; the codes and scales go to GemmProblem::a_codes / a_sf.
+struct StreamQuant {
+  const void* x;
+  int64_t ldx;
+  const int32_t* perm;
+  int K, S, layout;
+};
+cudaError_t launch_stream_gemm(const GemmProblem& p, const StreamPlan& pl, cudaStream_t stream, const char** detail,
+                               const StreamQuant* fq = nullptr);
 struct GemmPlan {
   int CL;            // CTAs per cluster along M
   int pair;          // CL == 2: 1 = 2-SM tcgen05 MMA (cta_group::2), 0 = two 1-SM CTAs sharing B by multicast

@@ -794,7 +794,9 @@ GemmPlan plan_gemm(int64_t M, int64_t N, int64_t Kp) {
 }
 
 cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t stream, const char** detail) {
-  static const int env_stream = getenv("ARC_GEMM_STREAM") ? atoi(getenv("ARC_GEMM_STREAM")) : 1;
+  // decode-size M: the split-K kernel + fixed-order reduce kernel by default; the weight-streaming
+  // stream-K kernel (stream_gemm.cu) measured slower on the LLaMA-3-8B decode step
+  static const int env_stream = getenv("ARC_GEMM_STREAM") ? atoi(getenv("ARC_GEMM_STREAM")) : 0;
   if (env_stream && !p.swiglu) {
     const StreamPlan sp = plan_stream(p.M, p.N, p.Kp);
     if (sp.ok) return launch_stream_gemm(p, sp, stream, detail);

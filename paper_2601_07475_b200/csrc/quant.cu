@@ -264,9 +264,11 @@ __global__ void __launch_bounds__(1024) arc_quant_kernel(QuantArgs p) {
   const int sf_rb_stride = (p.Kp >> 6) * 512;
   const int code_row = p.Kp >> 1;
   // (PDL) wait first, then let the next kernel launch: a dependent launched from here on knows every
-  // kernel before this one has completed (the decode GEMM streams weights before its own wait)
+  // kernel before this one has completed (the decode GEMM streams weights before its own wait).
+  // Weight preparation never lets dependents launch early: a kernel that follows it may then
+  // assume the weights are complete (the invariant the decode GEMM's early weight stream uses).
   pdl_wait();  // the previous kernel's writes are visible from here on
-  pdl_launch_dependents();
+  if (!p.weight_mode) pdl_launch_dependents();
   const float gs = __ldg(p.gs);
 
   if (tid == 0) {
