@@ -353,12 +353,22 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               bulk_load(sSFB + rb * 2048, args.sfb + ((int64_t)(2 * nbk + rb) * kc_total + kb * 4) * 512, nk * 512,
                         &full[stage]);
           } else {
-            // this CTA's half of B (128 rows) and its scale chunk, to both CTAs
-            tma_load_2d_mc(sB + rank * (B_BYTES / 2), &tmB, &full[stage], kb * BKB, nbk * BN + rank * (BN / 2),
+            // this CTA's 1/CL of B (BN/CL rows) and its share of the scale chunks, to every CTA of the cluster
+            tma_load_2d_mc(sB + rank * (B_BYTES / CL), &tmB, &full[stage], kb * BKB, nbk * BN + rank * (BN / CL),
                            mc_mask, pol);
-            if (rank < nrb)
-              bulk_load_mc(sSFB + rank * 2048, args.sfb + ((int64_t)(2 * nbk + rank) * kc_total + kb * 4) * 512,
-                           nk * 512, &full[stage], mc_mask);
+            if (CL == 2) {
+              if (rank < nrb)
+                bulk_load_mc(sSFB + rank * 2048, args.sfb + ((int64_t)(2 * nbk + rank) * kc_total + kb * 4) * 512,
+                             nk * 512, &full[stage], mc_mask);
+            } else {
+              for (int j = rank; j < 8; j += CL) {  // chunk j = (row block j/4, K chunk j%4)
+                const int rb = j >> 2, kk = j & 3;
+                if (rb < nrb && kk < nk)
+                  bulk_load_mc(sSFB + rb * 2048 + kk * 512,
+                               args.sfb + ((int64_t)(2 * nbk + rb) * kc_total + kb * 4 + kk) * 512, 512, &full[stage],
+                               mc_mask);
+              }
+            }
           }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
@@ -739,7 +749,9 @@ int64_t max_clusters(int CL, bool pair) {
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     int n = 0;
-    cudaError_t e = !pair ? cudaOccupancyMaxActiveClusters(&n, arc_gemm_kernel<2>, &cfg)
+    cudaError_t e = !pair ? (CL == 2 ? cudaOccupancyMaxActiveClusters(&n, arc_gemm_kernel<2>, &cfg)
+                             : CL == 4 ? cudaOccupancyMaxActiveClusters(&n, arc_gemm_kernel<4>, &cfg)
+                                       : cudaOccupancyMaxActiveClusters(&n, arc_gemm_kernel<8>, &cfg))
                     : CL == 2 ? cudaOccupancyMaxActiveClusters(&n, arc_gemm_pair_kernel<2, 5>, &cfg)
                               : cudaOccupancyMaxActiveClusters(&n, arc_gemm_pair_kernel<4, 5>, &cfg);
     if (e != cudaSuccess || n <= 0) {
@@ -760,7 +772,10 @@ GemmPlan plan_gemm(int64_t M, int64_t N, int64_t Kp) {
   static const int env_clp = getenv("ARC_GEMM_CLP") ? atoi(getenv("ARC_GEMM_CLP")) : 2;
   GemmPlan pl;
   const int64_t num_m = (M + BM - 1) / BM, num_n = (N + BN - 1) / BN, nkb = (Kp + BK - 1) / BK;
-  pl.CL = (env_cl == 1 || num_m < 2) ? 1 : 2;
+  // CTAs per cluster along M sharing the B tile by TMA multicast (ARC_GEMM_CL: 1, 2, 4 or 8)
+  pl.CL = 1;
+  for (int c = 2; c <= 8; c *= 2)
+    if (env_cl >= c && num_m >= c) pl.CL = c;
   pl.pair = pl.CL == 2 && env_pair != 0;
   if (pl.pair && env_clp == 4 && num_m >= 4) pl.CL = 4;
   const int64_t items = ((num_m + pl.CL - 1) / pl.CL) * num_n;  // cluster work items without split
@@ -836,6 +851,10 @@ cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t stream, const char** 
     if (attr_err == cudaSuccess)
       attr_err = cudaFuncSetAttribute(arc_gemm_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     if (attr_err == cudaSuccess)
+      attr_err = cudaFuncSetAttribute(arc_gemm_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    if (attr_err == cudaSuccess)
+      attr_err = cudaFuncSetAttribute(arc_gemm_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    if (attr_err == cudaSuccess)
       attr_err = cudaFuncSetAttribute(arc_gemm_pair_kernel<2, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       p_smem_bytes(5) + P_SILU_TAB_BYTES);
     if (attr_err == cudaSuccess)
@@ -891,7 +910,9 @@ cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t stream, const char** 
                                                 : cudaLaunchKernelEx(&cfg, arc_gemm_pair_kernel<2, 5>, tmA, tmB, tmSFA, tmSFB, tmY, a))
                                      : cudaLaunchKernelEx(&cfg, arc_gemm_pair_kernel<4, 5>, tmA, tmB, tmSFA, tmSFB, tmY, a))
                   : CL == 1 ? cudaLaunchKernelEx(&cfg, arc_gemm_kernel<1>, tmA, tmB, tmY, a)
-                            : cudaLaunchKernelEx(&cfg, arc_gemm_kernel<2>, tmA, tmB, tmY, a);
+                  : CL == 2 ? cudaLaunchKernelEx(&cfg, arc_gemm_kernel<2>, tmA, tmB, tmY, a)
+                  : CL == 4 ? cudaLaunchKernelEx(&cfg, arc_gemm_kernel<4>, tmA, tmB, tmY, a)
+                            : cudaLaunchKernelEx(&cfg, arc_gemm_kernel<8>, tmA, tmB, tmY, a);
   if (e != cudaSuccess) return e;
   if (pl.nsplit > 1) {
     const int64_t total = p.M * p.N;
