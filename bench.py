@@ -155,6 +155,7 @@ class Site:
         else:
             S_r = max(16, (S // world + 15) // 16 * 16)
             lin = tp.RowParallelLinear(w, cal, rank, world, s_override=S_r, backend=B)
+            self.lin = lin
             self.prof, self.qw = lin.profile, lin.qweight
             self.x = x[:, lin.shard.lo:lin.shard.hi].contiguous()
             self.w_local = w[:, lin.shard.lo:lin.shard.hi]
@@ -197,13 +198,24 @@ def build_sites(B, M, rank, world, device, layout="mp", workload="llama3-8b", ou
     return out
 
 
-def run_step(B, sites, ev=None, pg=None):
+def run_step(B, sites, ev=None, pg=None, tp_reduce="nccl"):
     """One pass of the layer's linears on this rank.  ev[i] = 4 CUDA events per site: before quantize,
-    after quantize, after GEMM, after the collective."""
+    after quantize, after GEMM, after the collective.  tp_reduce "fused": row-parallel sites add their
+    partials into every rank's symmetric-memory output from the GEMM epilogue (arc_gemm_reduce, NVLS
+    multicast or P2P) instead of an NCCL all-reduce; their quantize + GEMM + reduction is timed as
+    "gemm"."""
     from paper_2601_07475_b200 import tp
     for i, s in enumerate(sites):
         if ev is not None:
             ev[i][0].record()
+        if tp_reduce == "fused" and s.mode == "row" and pg is not None and not s.sp:
+            if ev is not None:
+                ev[i][1].record()
+            s.y_out = s.lin.forward(s.x, reduce="fused")
+            if ev is not None:
+                ev[i][2].record()
+                ev[i][3].record()
+            continue
         if s.sp and s.mode == "col":
             # sequence parallel: quantize this rank's token rows, all-gather the packed codes + scales
             c_loc, sf_loc = B.quantize_activation(s.x, s.prof)
@@ -447,6 +459,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-decode", action="store_true")
     ap.add_argument("--no-streaming", action="store_true")
+    ap.add_argument("--tp-reduce", default="nccl", choices=["nccl", "fused"],
+                    help="N>1 row-parallel sites: NCCL all-reduce after the GEMM, or the reduction fused into the GEMM "
+                         "epilogue over symmetric memory (NVLS multimem / P2P)")
     ap.add_argument("--tp-layout", default="mp", choices=["mp", "sp"],
                     help="N>1: sequence-parallel (quantize M/P rows + all-gather packed codes, reduce-scatter) "
                          "or plain Megatron (replicated quantize, all-reduce)")
@@ -475,7 +490,7 @@ def main():
     metric = "ARC NVFP4 linear TFLOPS"
     config = {"workload": WORKLOADS[workload][1], "M_tokens": args.M, "S": S_AUG,
               "sites": [f"{n}:K{k}xN{nn}" for n, k, nn in workload_sites(workload)],
-              "parallelism": "single" if args.gpus == 1 else f"tp{args.gpus}-{args.tp_layout}",
+              "parallelism": "single" if args.gpus == 1 else f"tp{args.gpus}-{args.tp_layout}-{args.tp_reduce}",
               "l2": "per-step footprint > 4x L2 (no flush needed)", "_workload": workload}
 
     if args.impl == "reference":
@@ -507,7 +522,7 @@ def main():
     torch.cuda.synchronize()
 
     for _ in range(args.warmup):
-        run_step(A, sites, pg=pg)
+        run_step(A, sites, pg=pg, tp_reduce=args.tp_reduce)
     torch.cuda.synchronize()
 
     nS = len(sites)
@@ -519,7 +534,7 @@ def main():
     with Clocks(local) as clk:
         start.record()
         for k in range(args.steps):
-            run_step(A, sites, ev=evs[k], pg=pg)
+            run_step(A, sites, ev=evs[k], pg=pg, tp_reduce=args.tp_reduce)
         stop.record()
         torch.cuda.synchronize()
     if pg is not None:
@@ -628,9 +643,9 @@ def main():
             def e2e_step():
                 for s, xh in zip(sites, xs):
                     s.x.copy_(xh, non_blocking=True)
-                run_step(A, sites, pg=pg)
+                run_step(A, sites, pg=pg, tp_reduce=args.tp_reduce)
                 for s, yh in zip(sites, ys):
-                    yh.copy_(s.y_out if (s.sp and s.mode == "row") else s.y, non_blocking=True)
+                    yh.copy_(s.y_out if (s.mode == "row" and hasattr(s, "y_out")) else s.y, non_blocking=True)
         for _ in range(2):
             e2e_step()
         if pg is not None:

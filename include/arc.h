@@ -267,6 +267,30 @@ ARC_API arc_status_t arc_linear_silu_mul(const void* gu, int64_t M, int64_t ld, 
 ARC_API arc_status_t arc_gemm(const uint8_t* a_codes, const uint8_t* a_sf, const float* gs_x, int64_t M,
                               const arc_qweight_t* qw, void* y, arc_dtype_t y_dtype, int64_t ldy, void* ws,
                               size_t ws_bytes, void* stream);
+/* Row-parallel tensor parallelism with the all-reduce fused into the GEMM epilogue (SURVEY.md §8(f)
+ * f2; BASELINE north_star "row-parallel over the extended K with an all-reduce over NVLink"): every
+ * output y_r[m][n] of THIS rank's partial GEMM (the arc_gemm result, fp32) is ADDED into every rank's
+ * fp32 output buffer instead of being stored --
+ *   ARC_REDUCE_MULTIMEM: one multimem.red.add.f32 per element into red->mc (the NVLS multicast address
+ *     of the symmetric [M][ldy] fp32 buffers of all ranks, e.g. torch symmetric memory's multicast_ptr):
+ *     the NVSwitch performs the sum, each rank sends its partial once;
+ *   ARC_REDUCE_PEERS: one red.add.f32 per element into each of red->peers[0 .. npeers) (every rank's
+ *     buffer mapped into this process: NVLink P2P, npeers <= 8).
+ * Contract: every rank's buffer is ZERO before any rank's call starts and nobody reads it before every
+ * rank's call has finished (e.g. symmetric-memory barriers on both sides); the sum over ranks is then
+ * in every rank's buffer.  The fp32 additions of different ranks land in arrival order (the result
+ * is within the GEMM tolerance of the exact sum, not bit-reproducible across runs at world > 1).
+ * The 16-byte vector reductions need ldy % 4 == 0 and 16-byte aligned buffers.  Workspace as arc_gemm. */
+typedef enum { ARC_REDUCE_MULTIMEM = 1, ARC_REDUCE_PEERS = 2 } arc_reduce_mode_t;
+typedef struct {
+  int32_t mode;        /* arc_reduce_mode_t */
+  int32_t npeers;      /* ARC_REDUCE_PEERS: 1..8 */
+  float* mc;           /* ARC_REDUCE_MULTIMEM: multicast address of the [M][ldy] fp32 buffers */
+  float* peers[8];     /* ARC_REDUCE_PEERS: each rank's [M][ldy] fp32 buffer (device addresses) */
+} arc_reduce_t;
+ARC_API arc_status_t arc_gemm_reduce(const uint8_t* a_codes, const uint8_t* a_sf, const float* gs_x, int64_t M,
+                                     const arc_qweight_t* qw, const arc_reduce_t* red, int64_t ldy, void* ws,
+                                     size_t ws_bytes, void* stream);
 /* arc_gemm with the SwiGLU activation in its epilogue (the MLP gate_up site, Fig.5):
  * qw is the fused gate_up weight with its rows interleaved in groups of 16 -- rows 32j..32j+15
  * are gate rows 16j..16j+15 and rows 32j+16..32j+31 the matching up rows (qw->N = 2I, I % 16

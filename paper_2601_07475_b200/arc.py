@@ -46,6 +46,14 @@ class ArcQWeight(ctypes.Structure):
                 ("codes", _P), ("sf", _P), ("gs", _P)]
 
 
+class ArcReduce(ctypes.Structure):
+    _fields_ = [("mode", _i32), ("npeers", _i32), ("mc", _P), ("peers", _P * 8)]
+
+
+REDUCE_MULTIMEM = 1  # arc.h ARC_REDUCE_MULTIMEM
+REDUCE_PEERS = 2     # arc.h ARC_REDUCE_PEERS
+
+
 def _sig(name, args, res=ctypes.c_int):
     f = getattr(_lib, name)
     f.argtypes = args
@@ -84,6 +92,8 @@ _sig("arc_mx_tensor_scale", [_f32, ctypes.POINTER(_f32)])
 _sig("arc_mx_tensor_scale_device", [_P, _i64, _i64, _i64, _P, _P])
 _sig("arc_quantize_activation_mx", [_P, _i64, _i64, ctypes.POINTER(ArcProfile), _P, _P, _P])
 _sig("arc_quantize_weight_mx", [_P, _i64, _i64, _i64, _P, _i32, _P, ctypes.c_int, _P, _P, _P])
+_sig("arc_gemm_reduce", [_P, _P, _P, _i64, ctypes.POINTER(ArcQWeight), ctypes.POINTER(ArcReduce), _i64, _P,
+                         ctypes.c_size_t, _P])
 _sig("arc_gemm_swiglu", [_P, _P, _P, _i64, ctypes.POINTER(ArcQWeight), _P, _i64, _P, ctypes.c_size_t, _P])
 _sig("arc_silu_mul", [_P, _i64, _i64, _i64, _i64, _P, _i64, _P])
 _sig("arc_silu_mul_quantize_activation", [_P, _i64, _i64, _i64, ctypes.POINTER(ArcProfile), _P, _P, _P])
@@ -107,7 +117,7 @@ EXPORTED = [
     "arc_quantize_activation", "arc_gemm", "arc_linear", "arc_linear_ex", "arc_linear_ex_workspace_size",
     "arc_linear_hostio_workspace_size", "arc_rmsnorm",
     "arc_rmsnorm_quantize_activation", "arc_linear_rmsnorm", "arc_linear_hostio",
-    "arc_silu_mul", "arc_silu_mul_quantize_activation", "arc_linear_silu_mul", "arc_gemm_swiglu",
+    "arc_silu_mul", "arc_silu_mul_quantize_activation", "arc_linear_silu_mul", "arc_gemm_swiglu", "arc_gemm_reduce",
     "arc_mx_tensor_scale", "arc_mx_tensor_scale_device", "arc_quantize_activation_mx", "arc_quantize_weight_mx", "arc_gather_order_ex",
     "arc_probe_e2m1", "arc_probe_e2m1_bits", "arc_probe_e2m1_raw_bits", "arc_probe_e4m3_ceil", "arc_probe_silu",
     "arc_debug_stream_trace",
@@ -368,6 +378,30 @@ def gemm_swiglu(a_codes, a_sf, gs_x: torch.Tensor, qw: QWeight, out=None, ws: Wo
                                 out.stride(0), _ptr(buf), 0 if buf is None else buf.numel(), _stream(stream)),
            "arc_gemm_swiglu")
     return out
+
+
+def gemm_reduce(a_codes, a_sf, gs_x: torch.Tensor, qw: QWeight, ldy: int, mc_ptr: int = 0, peer_ptrs=(),
+                ws: Workspace = None, stream=None):
+    """arc_gemm_reduce: this rank's partial GEMM ADDED into every rank's fp32 [M][ldy] output buffer --
+    through the NVLS multicast address mc_ptr (multimem.red) when given, else into each device address of
+    peer_ptrs (P2P red.add).  The buffers must be zero before any rank starts (see arc.h)."""
+    M = a_codes.shape[0]
+    red = ArcReduce()
+    if mc_ptr:
+        red.mode, red.mc = REDUCE_MULTIMEM, int(mc_ptr)
+    else:
+        red.mode, red.npeers = REDUCE_PEERS, len(peer_ptrs)
+        for i, p in enumerate(peer_ptrs):
+            red.peers[i] = int(p)
+    need = gemm_workspace_size(M, qw)
+    buf = None
+    if need:
+        if ws is None:
+            ws = _default_workspace("gemm", a_codes.device, stream)
+        buf = ws.get(need)
+    _check(_lib.arc_gemm_reduce(_ptr(a_codes), _ptr(a_sf), _ptr(gs_x), M, ctypes.byref(qw.c()), ctypes.byref(red),
+                                ldy, _ptr(buf), 0 if buf is None else buf.numel(), _stream(stream)),
+           "arc_gemm_reduce")
 
 
 def interleave_gate_up(w_gate: torch.Tensor, w_up: torch.Tensor, group: int = 16) -> torch.Tensor:

@@ -503,6 +503,62 @@ static arc_status_t gemm_impl(const uint8_t* a_codes, const uint8_t* a_sf, const
   return e == cudaSuccess ? ARC_OK : cuda_fail(e, "arc_gemm", detail);
 }
 
+arc_status_t arc_gemm_reduce(const uint8_t* a_codes, const uint8_t* a_sf, const float* gs_x, int64_t M,
+                             const arc_qweight_t* qw, const arc_reduce_t* red, int64_t ldy, void* ws, size_t ws_bytes,
+                             void* stream) {
+  arc_status_t s = check_qweight(qw);
+  if (s != ARC_OK) return s;
+  if (!red) return fail(ARC_ERR_NULL, "null red");
+  if (M < 0 || M > (1 << 30)) return fail(ARC_ERR_SHAPE, "bad M");
+  if (M == 0) return ARC_OK;
+  if (!a_codes || !a_sf || !gs_x) return fail(ARC_ERR_NULL, "null a_codes / a_sf / gs_x");
+  if (ldy < qw->N || ldy % 4) return fail(ARC_ERR_SHAPE, "ldy must be >= N and a multiple of 4");
+  if (red->mode == ARC_REDUCE_MULTIMEM) {
+    if (!red->mc) return fail(ARC_ERR_NULL, "null multicast address");
+    if (!aligned16(red->mc)) return fail(ARC_ERR_ALIGN, "multicast address not 16B aligned");
+  } else if (red->mode == ARC_REDUCE_PEERS) {
+    if (red->npeers < 1 || red->npeers > 8) return fail(ARC_ERR_SHAPE, "npeers must be 1..8");
+    for (int i = 0; i < red->npeers; ++i) {
+      if (!red->peers[i]) return fail(ARC_ERR_NULL, "null peer buffer");
+      if (!aligned16(red->peers[i])) return fail(ARC_ERR_ALIGN, "peer buffer not 16B aligned");
+    }
+  } else {
+    return fail(ARC_ERR_SHAPE, "bad reduce mode");
+  }
+  if (!aligned16(a_codes) || !aligned16(a_sf)) return fail(ARC_ERR_ALIGN, "buffer not 16B aligned");
+  const GemmPlan pl = plan_gemm(M, qw->N, qw->Kp);
+  if (pl.ws_bytes > 0 && (!ws || ws_bytes < pl.ws_bytes)) return fail(ARC_ERR_WORKSPACE, "split-K workspace too small");
+  if (ws && !aligned16(ws)) return fail(ARC_ERR_ALIGN, "ws not 16B aligned");
+  s = check_device();
+  if (s != ARC_OK) return s;
+  void *cnt, *part;
+  size_t part_bytes;
+  split_gemm_ws(ws, ws_bytes, &cnt, &part, &part_bytes);
+  GemmProblem p;
+  p.M = M;
+  p.N = qw->N;
+  p.Kp = qw->Kp;
+  p.a_codes = a_codes;
+  p.a_sf = a_sf;
+  p.b_codes = qw->codes;
+  p.b_sf = qw->sf;
+  p.gs_x = gs_x;
+  p.gs_w = qw->gs;
+  p.y = red->mode == ARC_REDUCE_MULTIMEM ? (void*)red->mc : (void*)red->peers[0];
+  p.ldy = ldy;
+  p.y_fp32 = 1;
+  p.cnt = static_cast<unsigned*>(cnt);
+  p.ws = part;
+  p.ws_bytes = part_bytes;
+  p.red_mode = red->mode;
+  p.red_np = red->mode == ARC_REDUCE_PEERS ? red->npeers : 0;
+  p.red_mc = red->mc;
+  for (int i = 0; i < p.red_np; ++i) p.red_peer[i] = red->peers[i];
+  const char* detail = nullptr;
+  cudaError_t e = launch_gemm(p, (cudaStream_t)stream, &detail);
+  return e == cudaSuccess ? ARC_OK : cuda_fail(e, "arc_gemm_reduce", detail);
+}
+
 arc_status_t arc_gemm_swiglu(const uint8_t* a_codes, const uint8_t* a_sf, const float* gs_x, int64_t M,
                              const arc_qweight_t* qw, void* h, int64_t ldh, void* ws, size_t ws_bytes, void* stream) {
   arc_status_t s = check_qweight(qw);

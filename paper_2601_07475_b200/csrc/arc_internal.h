@@ -68,6 +68,12 @@ struct GemmProblem {
   // kernel is the activation quantize, which lets dependents launch only after its own
   // griddepcontrol.wait): the decode-size kernel may then stream them before its own wait.
   int weights_ready = 0;
+  // fused row-parallel reduction (arc_gemm_reduce): 1 = NVLS multimem.red into red_mc, 2 = red.add into the
+  // red_np peer buffers; fp32 output only, the 1-SM kernel and the split-K reduce kernel
+  int red_mode = 0;
+  int red_np = 0;
+  float* red_mc = nullptr;
+  float* red_peer[8] = {};
 };
 // Decode-size M (<= 64): weight-streaming stream-K GEMM (stream_gemm.cu).
 struct StreamPlan {

@@ -77,6 +77,13 @@ struct Args {
                 // only on its own A row, and rows >= M are never stored)
   int swiglu;   // SwiGLU epilogue: y = h [M][N/2] bf16 from 16-row-interleaved gate/up weight rows
   int raster;   // tile order: 0 = M-tile groups fastest (the A panel stays in L2), 1 = N tiles fastest (B stays)
+  // Row-parallel reduction fused into the epilogue: 1 = multimem.red.add into the NVLS
+  // multicast view red_mc of every rank's fp32 Y (NVSwitch reduces), 2 = red.add into each of the red_np
+  // peer-mapped fp32 Y buffers red_peer[] (NVLink P2P); the Y buffers start at zero on every rank
+  int red_mode;
+  int red_np;
+  float* red_mc;
+  float* red_peer[8];
   int debug;  // perf experiments only (env ARC_GEMM_DEBUG): 1 = no epilogue work, 2 = no scale copies, 3 = no stores, 4 = no TMEM loads,
               // 5 = STG stores, 6 = no TMA store, 7 = MMA ignores the accumulator-free barriers,
               // 8 = MMAs issued twice, 9 = one MMA per stage, 10 = 9 without scale copies (pair kernel; timing only)
@@ -85,6 +92,35 @@ struct Args {
 // instruction descriptor: E2M1 x E2M1 (format 1), UE4M3 scales, K-major A/B,
 // N>>3 at [17,23), M>>4 at [24,29).
 constexpr uint32_t kIdesc = (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+
+// fp32 reductions of 4 consecutive outputs into other ranks' Y (sys scope: the other GPUs observe them)
+__device__ __forceinline__ void red_add_v4_mc(float* mc, float a, float b, float c, float d) {
+  asm volatile("multimem.red.relaxed.sys.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(mc), "f"(a), "f"(b), "f"(c),
+               "f"(d)
+               : "memory");
+}
+__device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, float d) {
+  asm volatile("red.relaxed.sys.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d)
+               : "memory");
+}
+__device__ __forceinline__ void red_add_1(float* p, float a) {
+  asm volatile("red.relaxed.sys.global.add.f32 [%0], %1;" ::"l"(p), "f"(a) : "memory");
+}
+// out[off .. off+3] += v (every rank's Y) through the configured reduction
+__device__ __forceinline__ void reduce_out4(const Args& args, int64_t off, float a, float b, float c, float d) {
+  if (args.red_mode == 1) {
+    red_add_v4_mc(args.red_mc + off, a, b, c, d);
+  } else {
+    for (int p = 0; p < args.red_np; ++p) red_add_v4(args.red_peer[p] + off, a, b, c, d);
+  }
+}
+__device__ __forceinline__ void reduce_out1(const Args& args, int64_t off, float a) {
+  if (args.red_mode == 1) {
+    asm volatile("multimem.red.relaxed.sys.global.add.f32 [%0], %1;" ::"l"(args.red_mc + off), "f"(a) : "memory");
+  } else {
+    for (int p = 0; p < args.red_np; ++p) red_add_1(args.red_peer[p] + off, a);
+  }
+}
 
 // Epilogue of one output tile, run by the 4 epilogue warps: warp q drains TMEM lanes
 // [32q, 32q+32) (= 32 output rows of this CTA's 128) x BN columns of accumulator buffer b,
@@ -138,7 +174,19 @@ __device__ __forceinline__ void epilogue_tile(const Args& args, const CUtensorMa
     }
     if (cc == BN / 32 - 1) release(buf_free);
     const int n0 = nbk * BN + c * 32;
-    if ((args.y_fp32 || nsplit > 1) && m < M && n0 < N) {
+    if (args.red_mode && nsplit == 1 && m < M && n0 < N) {
+      // row-parallel output: add this rank's partial into every rank's Y (NVLS multicast or P2P)
+      const int64_t off = (int64_t)m * args.ldy + n0;
+      if (n0 + 32 <= N) {
+#pragma unroll
+        for (int j = 0; j < 32; j += 4)
+          reduce_out4(args, off + j, __fmul_rn(__uint_as_float(r[j]), alpha), __fmul_rn(__uint_as_float(r[j + 1]), alpha),
+                      __fmul_rn(__uint_as_float(r[j + 2]), alpha), __fmul_rn(__uint_as_float(r[j + 3]), alpha));
+      } else {
+        for (int j = 0; j < 32; ++j)
+          if (n0 + j < N) reduce_out1(args, off + j, __fmul_rn(__uint_as_float(r[j]), alpha));
+      }
+    } else if ((args.y_fp32 || nsplit > 1) && m < M && n0 < N) {
       // split-K partial rows use the stride round_up(N, 4) so the float4 stores stay 16-byte
       // aligned for any N (plan_gemm sizes the workspace with the same stride)
       float* yr = nsplit > 1 ? args.ws + ((int64_t)ks * M + m) * ((N + 3) & ~3) + n0
@@ -630,7 +678,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
 // Deterministic split-K reduction: y[m][n] = sum_ks ws[ks][m][n] in ks order.
 __global__ void arc_splitk_reduce_kernel(const float* __restrict__ ws, int nsplit, int M, int N, void* y,
-                                         int64_t ldy, int y_fp32, int swiglu) {
+                                         int64_t ldy, int y_fp32, int swiglu, Args red) {
   pdl_launch_dependents();
   pdl_wait();
   const int ldp = (N + 3) & ~3;  // partial row stride (see epilogue_tile)
@@ -657,6 +705,10 @@ __global__ void arc_splitk_reduce_kernel(const float* __restrict__ ws, int nspli
     const int64_t m = i / N, n = i - m * N, ip = m * ldp + n;
     float acc = ws[ip];
     for (int k = 1; k < nsplit; ++k) acc = __fadd_rn(acc, ws[(int64_t)k * total + ip]);
+    if (red.red_mode) {  // row-parallel output: add the rank's partial into every rank's Y
+      reduce_out1(red, m * ldy + n, acc);
+      continue;
+    }
     if (y_fp32) static_cast<float*>(y)[m * ldy + n] = acc;
     else static_cast<__nv_bfloat16*>(y)[m * ldy + n] = __float2bfloat16_rn(acc);
   }
@@ -812,7 +864,7 @@ cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t stream, const char** 
   // decode-size M: the split-K kernel + fixed-order reduce kernel by default; the weight-streaming
   // stream-K kernel (stream_gemm.cu) measured slower on the LLaMA-3-8B decode step
   static const int env_stream = getenv("ARC_GEMM_STREAM") ? atoi(getenv("ARC_GEMM_STREAM")) : 0;
-  if (env_stream && !p.swiglu) {
+  if (env_stream && !p.swiglu && !p.red_mode) {
     const StreamPlan sp = plan_stream(p.M, p.N, p.Kp);
     if (sp.ok) return launch_stream_gemm(p, sp, stream, detail);
   }
@@ -886,6 +938,10 @@ cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t stream, const char** 
   a.nsplit = pl.nsplit;
   a.kbs = pl.kbs;
   a.ws = static_cast<float*>(p.ws);
+  a.red_mode = p.red_mode;
+  a.red_np = p.red_np;
+  a.red_mc = p.red_mc;
+  for (int i = 0; i < 8; ++i) a.red_peer[i] = i < p.red_np ? p.red_peer[i] : nullptr;
   const int64_t num_m = (p.M + BM - 1) / BM, num_n = (p.N + BN - 1) / BN;
   const int64_t work = ((num_m + CL - 1) / CL) * num_n * pl.nsplit;  // cluster work items
   const int64_t grid = std::min<int64_t>(work, max_clusters(CL, pl.pair)) * CL;
@@ -928,7 +984,7 @@ cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t stream, const char** 
     rc.attrs = ra;
     rc.numAttrs = 1;
     e = cudaLaunchKernelEx(&rc, arc_splitk_reduce_kernel, static_cast<const float*>(a.ws), (int)pl.nsplit, (int)p.M,
-                           (int)p.N, p.y, p.ldy, p.y_fp32, p.swiglu);
+                           (int)p.N, p.y, p.ldy, p.y_fp32, p.swiglu, a);
     if (e != cudaSuccess) return e;
   }
   return cudaGetLastError();

@@ -27,6 +27,13 @@ ARC linear:
   gathered codes are bit-identical to quantizing the full activation (quantization is
   per row), so the outputs equal the column-parallel layer's.
 
+* RowParallelLinear(reduce="fused") (second half): the all-reduce is fused into the
+  GEMM epilogue (arc_gemm_reduce): the fp32 output is a torch symmetric-memory buffer mapped on every
+  rank; each rank's GEMM adds its partial into every rank's buffer as its tiles finish -- one
+  multimem.red per element into the NVLS multicast address when the NVSwitch supports it (the switch
+  sums; each rank sends its partial once), else red.add into each peer's buffer over NVLink P2P.
+  Symmetric-memory barriers zero-fence the buffers before and publish the sum after.
+
 The compute backend is the ctypes binding of libarc.so by default; tests inject a
 CPU backend to exercise this host logic with the gloo backend on CPU.
 """
@@ -118,10 +125,40 @@ class RowParallelLinear:
                                               layout=layout)
         self.qweight = self.backend.quantize_weight(weight_full[:, lo:hi].contiguous(), self.profile)
 
+    def symmetric_output(self, M: int, device):
+        """fp32 [M][N] output buffer shared by every rank (torch symmetric memory) and its handle, cached per M."""
+        key = (M, str(device))
+        cache = self.__dict__.setdefault("_symm", {})
+        if key not in cache:
+            if hasattr(self.backend, "symmetric_buffer"):
+                cache[key] = self.backend.symmetric_buffer((M, self.qweight_N()), self.group)
+            else:
+                import torch.distributed._symmetric_memory as symm_mem
+                buf = symm_mem.empty((M, self.qweight_N()), dtype=torch.float32, device=device)
+                group = self.group if self.group is not None else dist.group.WORLD
+                cache[key] = (buf, symm_mem.rendezvous(buf, group))
+        return cache[key]
+
+    def qweight_N(self) -> int:
+        return int(self.qweight.codes.shape[0])
+
     def forward(self, x_shard: torch.Tensor, out_dtype=torch.float32, reduce="all") -> torch.Tensor:
         """x_shard: this rank's [M, K/P] slice of the activation.  reduce: "all" (all-reduce, every rank
-        gets Y), "scatter" (reduce-scatter over tokens, rank r gets rows [r M/P, (r+1) M/P): the
-        sequence-parallel layout) or None (the partial Y_r)."""
+        gets Y), "fused" (the all-reduce fused into the GEMM epilogue through symmetric memory: NVLS
+        multicast or P2P; the returned tensor is the shared buffer, valid until the next fused call),
+        "scatter" (reduce-scatter over tokens, rank r gets rows [r M/P, (r+1) M/P): the sequence-parallel
+        layout) or None (the partial Y_r)."""
+        if reduce == "fused":
+            M = x_shard.shape[0]
+            buf, h = self.symmetric_output(M, x_shard.device)
+            buf.zero_()
+            h.barrier()  # every rank's buffer is zero before any rank adds into it
+            codes, sf = self.backend.quantize_activation(x_shard, self.profile)
+            mc = int(h.multicast_ptr) if getattr(h, "has_multicast_support", False) and h.multicast_ptr else 0
+            self.backend.gemm_reduce(codes, sf, self.profile.gs, self.qweight, ldy=self.qweight_N(), mc_ptr=mc,
+                                     peer_ptrs=list(h.buffer_ptrs))
+            h.barrier()  # every rank's contribution has landed
+            return buf if out_dtype == torch.float32 else buf.to(out_dtype)
         y = self.backend.linear(x_shard, self.profile, self.qweight, out_dtype=out_dtype)
         if reduce is True or reduce == "all":
             if self.shard.world > 1 or self.group is not None:

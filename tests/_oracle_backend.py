@@ -93,3 +93,39 @@ class BenchOracleBackend(OracleBackend):
         if out is None:
             return super().gemm(codes, sf, gs, qw, out_dtype)
         return self.gemm_into(codes, sf, gs, qw, out)
+
+
+# --- fused row-parallel reduction (tp.RowParallelLinear(reduce="fused")): a CPU emulation of the
+# symmetric output buffer and of arc_gemm_reduce, whose every-rank-adds-into-every-buffer semantics
+# equals adding the all-reduced partials into each rank's (zeroed) buffer ---
+_SYMM_BUFS = {}
+
+
+class _SymmHandle:
+    def __init__(self, buf, group):
+        self.group = group
+        self.has_multicast_support = False
+        self.multicast_ptr = 0
+        self.buffer_ptrs = [id(buf)]
+
+    def barrier(self):
+        import torch.distributed as dist
+        dist.barrier(group=self.group)
+
+
+def _symmetric_buffer(self, shape, group):
+    buf = torch.zeros(shape, dtype=torch.float64)
+    _SYMM_BUFS[id(buf)] = buf
+    return buf, _SymmHandle(buf, group)
+
+
+def _gemm_reduce(self, codes, sf, gs, qw, ldy, mc_ptr=0, peer_ptrs=()):
+    import torch.distributed as dist
+    y, _ = oracle.gemm_reference(codes.numpy(), sf.numpy(), qw.codes, qw.sf, gs, qw.gs)
+    t = torch.from_numpy(y)
+    dist.all_reduce(t)
+    _SYMM_BUFS[peer_ptrs[0]] += t
+
+
+OracleBackend.symmetric_buffer = _symmetric_buffer
+OracleBackend.gemm_reduce = _gemm_reduce

@@ -36,6 +36,11 @@ def _worker(rank, world, port, outdir):
     bench.run_step(B, sites, pg=dist.group.WORLD)
     for s in sites:
         np.save(os.path.join(outdir, f"{s.name}{rank}.npy"), s.y.numpy())
+    # the row-parallel reduction fused into the GEMM epilogue (symmetric output) gives the same sums
+    bench.run_step(B, sites, pg=dist.group.WORLD, tp_reduce="fused")
+    for s in sites:
+        if s.mode == "row":
+            np.save(os.path.join(outdir, f"{s.name}_fused{rank}.npy"), s.y_out.numpy())
         np.save(os.path.join(outdir, f"{s.name}_S{rank}.npy"), np.array([s.S, s.K, s.N]))
     dist.barrier()
     dist.destroy_process_group()
@@ -90,6 +95,7 @@ def test_bench_tp_step_world2_gloo():
             for r in range(world):
                 got = np.load(os.path.join(d, f"{name}{r}.npy"))
                 assert np.all(np.abs(got - ref) <= bound + 1e-12), name
+                assert np.array_equal(np.load(os.path.join(d, f"{name}_fused{r}.npy")), got), name
 
 
 def test_bench_gpus_n_fails_loudly_without_n_gpus():

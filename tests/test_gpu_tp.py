@@ -81,3 +81,52 @@ def test_sequence_parallel_world1_nccl(pg):
     assert torch.equal(codes, c0) and torch.equal(sf, s0)
     assert torch.equal(y, y0) and torch.equal(yn, yn0)
     assert torch.equal(y_sc, y_all)
+
+
+@pytest.mark.parametrize("M,K,N", [(256, 2048, 512), (16, 4096, 1024), (300, 1024, 130)])
+def test_gemm_reduce_peers_equals_gemm(M, K, N):
+    """arc_gemm_reduce in P2P mode with this GPU as the only peer: zero + partial == the plain fp32 GEMM
+    (prefill epilogue and split-K reduce-kernel paths; ragged N uses the scalar reductions)."""
+    from paper_2601_07475_b200 import arc
+    st = synth.Structure(K, 32, seed=M)
+    x = synth.activation(M, K, st, seed=M + 1, device="cuda")
+    w = synth.weight(N, K, seed=N, device="cuda")
+    prof = arc.calibrate([synth.activation(256, K, st, seed=5, device="cuda")], s_override=32)
+    qw = arc.quantize_weight(w, prof)
+    codes, sf = arc.quantize_activation(x, prof)
+    y = arc.gemm(codes, sf, prof.gs, qw, out_dtype=torch.float32)
+    ldy = (N + 3) // 4 * 4
+    out = torch.zeros(M, ldy, dtype=torch.float32, device="cuda")
+    arc.gemm_reduce(codes, sf, prof.gs, qw, ldy=ldy, peer_ptrs=[out.data_ptr()])
+    torch.cuda.synchronize()
+    assert torch.equal(out[:, :N], y)
+    arc.gemm_reduce(codes, sf, prof.gs, qw, ldy=ldy, peer_ptrs=[out.data_ptr(), out.data_ptr()])
+    torch.cuda.synchronize()
+    assert torch.allclose(out[:, :N], 3 * y, rtol=1e-6, atol=0)  # every peer receives each partial
+
+
+def test_row_parallel_fused_reduce_world1_nccl(pg):
+    """tp.RowParallelLinear(reduce="fused") over torch symmetric memory (NVLS multicast when the box has
+    it, else P2P) equals the NCCL all-reduce path at world size 1, and the multicast mode itself (when
+    available) adds exactly once."""
+    from paper_2601_07475_b200 import arc, tp
+    import torch.distributed._symmetric_memory as symm_mem
+    M, K, N = 256, 2048, 512
+    st = synth.Structure(K, 32, seed=3)
+    x = synth.activation(M, K, st, seed=4, device="cuda")
+    cal = synth.activation(256, K, st, seed=5, device="cuda")
+    w = synth.weight(N, K, seed=6, device="cuda")
+    row = tp.RowParallelLinear(w, cal, 0, 1, backend=arc)
+    y_ar = row.forward(x, out_dtype=torch.float32, reduce="all").clone()
+    y_f1 = row.forward(x, reduce="fused").clone()
+    y_f2 = row.forward(x, reduce="fused").clone()
+    torch.cuda.synchronize()
+    assert torch.equal(y_f1, y_ar) and torch.equal(y_f2, y_ar)
+    buf, h = row.symmetric_output(M, x.device)
+    print("multicast support:", bool(getattr(h, "has_multicast_support", False)), "multicast_ptr:", h.multicast_ptr)
+    if getattr(h, "has_multicast_support", False) and h.multicast_ptr:
+        codes, sf = arc.quantize_activation(x, row.profile)
+        buf.zero_()
+        arc.gemm_reduce(codes, sf, row.profile.gs, row.qweight, ldy=N, mc_ptr=int(h.multicast_ptr))
+        torch.cuda.synchronize()
+        assert torch.equal(buf, y_ar)

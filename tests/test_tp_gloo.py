@@ -48,6 +48,10 @@ def _worker(rank, world, port, outdir):
     row = tp.RowParallelLinear(w, cal, rank, world, backend=be)
     lo, hi = row.shard.lo, row.shard.hi
     y_row = row.forward(x[:, lo:hi].contiguous(), out_dtype=torch.float64)
+    # the all-reduce fused into the GEMM epilogue (symmetric output buffer): the same sum
+    y_fused = row.forward(x[:, lo:hi].contiguous(), reduce="fused").clone()
+    y_fused2 = row.forward(x[:, lo:hi].contiguous(), reduce="fused").clone()  # buffer re-zeroed per call
+    np.save(os.path.join(outdir, f"fused{rank}.npy"), np.stack([y_fused.numpy(), y_fused2.numpy()]))
     np.save(os.path.join(outdir, f"col{rank}.npy"), y_col.numpy())
     np.save(os.path.join(outdir, f"row{rank}.npy"), y_row.numpy())
     np.save(os.path.join(outdir, f"S{rank}.npy"), np.array([row.profile.S]))
@@ -93,6 +97,8 @@ def test_tp_world2_gloo():
         for r in range(world):
             got = np.load(os.path.join(d, f"row{r}.npy"))
             assert np.all(np.abs(got - ref) <= bound + 1e-12)
+            fused = np.load(os.path.join(d, f"fused{r}.npy"))
+            assert np.array_equal(fused[0], got) and np.array_equal(fused[1], got)
 
 
 def test_shard_range():
