@@ -70,6 +70,7 @@ struct SArgs {
   unsigned* cnt;     // the counter region
   int maxseg;
   int w_early;       // stream the first stages' weights before griddepcontrol.wait
+  int hold_w;        // fused: start the weight stream only once the CTA's first K block is quantized
   // fused quantize (x != nullptr): x bf16 [M][ldx], perm[K], S, layout -> a_codes / a_sf (= sfa)
   const uint16_t* x;
   int64_t ldx;
@@ -269,14 +270,31 @@ __global__ void __launch_bounds__(S_THREADS, 2)
         tma_load_2d(st, &tmA, &full[i], kb * SBKB, 0, pol_a);
         bulk_load_hint(st + a_bytes + SB_BYTES, args.sfa + (int64_t)kb * 4 * 512, nk * 512, &full[i], pol_a);
       };
-      // weights of the first stages: independent of the previous kernel (see the file comment)
-      if (!args.w_early) pdl_wait();
-      for (int i = 0; i < n_pre; ++i) load_w(i, u0 + i);
-      STRACE(1);
-      if (args.w_early) pdl_wait();
-      if (fused) epoch = ld_acquire_u32(args.cnt + CNT_EPOCH);
-      STRACE(2);
-      for (int i = 0; i < n_pre; ++i) load_a(i, u0 + i);
+      if (fused && args.hold_w) {
+        // hold the weight stream until the first K block this CTA needs is quantized: a full-rate weight
+        // stream floods the memory queues and multiplies the latency of the quantize phase's gathers,
+        // stores and ready words, which sit on every CTA's critical path
+        pdl_wait();
+        epoch = ld_acquire_u32(args.cnt + CNT_EPOCH);
+        STRACE(1);
+        const int kb0 = u0 % nkb;
+        while (ld_acquire_u32(args.cnt + CNT_QRDY0 + kb0) != epoch + 1u) {
+        }
+        STRACE(2);
+        for (int i = 0; i < n_pre; ++i) {
+          load_w(i, u0 + i);
+          load_a(i, u0 + i);
+        }
+      } else {
+        // weights of the first stages: independent of the previous kernel (see the file comment)
+        if (!args.w_early) pdl_wait();
+        for (int i = 0; i < n_pre; ++i) load_w(i, u0 + i);
+        STRACE(1);
+        if (args.w_early) pdl_wait();
+        if (fused) epoch = ld_acquire_u32(args.cnt + CNT_EPOCH);
+        STRACE(2);
+        for (int i = 0; i < n_pre; ++i) load_a(i, u0 + i);
+      }
       int stage = n_pre % nst;
       uint32_t phase = n_pre == nst ? 1u : 0u;
       for (int i = n_pre; i < n_units; ++i) {
@@ -592,6 +610,8 @@ cudaError_t launch_stream_gemm(const GemmProblem& p, const StreamPlan& pl, cudaS
     a.a_codes = const_cast<uint8_t*>(p.a_codes);
     a.a_sf = const_cast<uint8_t*>(p.a_sf);
   }
+  static const int env_hold = getenv("ARC_STREAM_HOLD") ? atoi(getenv("ARC_STREAM_HOLD")) : 0;
+  a.hold_w = env_hold;
   a.trace = stream_trace_buffer();
   static const int dbg = getenv("ARC_STREAM_DEBUG") ? atoi(getenv("ARC_STREAM_DEBUG")) : 0;
   a.debug = dbg;

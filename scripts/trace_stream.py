@@ -25,7 +25,7 @@ for site, K, N in synth.LLAMA3_8B_SITES:
     ws = A.Workspace("cuda")
     for _ in range(3):
         flush.zero_()
-        y = A.linear(x, prof, qw, ws=ws)
+        y = A.linear(x, prof, qw, ws=ws, mode="fused")
     torch.cuda.synchronize()
     buf = np.zeros((4096, 8), np.uint64)
     n = lib.arc_debug_stream_trace(buf.ctypes.data, 4096)
