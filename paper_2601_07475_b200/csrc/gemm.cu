@@ -111,14 +111,18 @@ __device__ __forceinline__ void reduce_out4(const Args& args, int64_t off, float
   if (args.red_mode == 1) {
     red_add_v4_mc(args.red_mc + off, a, b, c, d);
   } else {
-    for (int p = 0; p < args.red_np; ++p) red_add_v4(args.red_peer[p] + off, a, b, c, d);
+#pragma unroll
+    for (int p = 0; p < 8; ++p)  // compile-time indices: no local-memory copy of the parameter array
+      if (p < args.red_np) red_add_v4(args.red_peer[p] + off, a, b, c, d);
   }
 }
 __device__ __forceinline__ void reduce_out1(const Args& args, int64_t off, float a) {
   if (args.red_mode == 1) {
     asm volatile("multimem.red.relaxed.sys.global.add.f32 [%0], %1;" ::"l"(args.red_mc + off), "f"(a) : "memory");
   } else {
-    for (int p = 0; p < args.red_np; ++p) red_add_1(args.red_peer[p] + off, a);
+#pragma unroll
+    for (int p = 0; p < 8; ++p)
+      if (p < args.red_np) red_add_1(args.red_peer[p] + off, a);
   }
 }
 
@@ -183,7 +187,8 @@ __device__ __forceinline__ void epilogue_tile(const Args& args, const CUtensorMa
           reduce_out4(args, off + j, __fmul_rn(__uint_as_float(r[j]), alpha), __fmul_rn(__uint_as_float(r[j + 1]), alpha),
                       __fmul_rn(__uint_as_float(r[j + 2]), alpha), __fmul_rn(__uint_as_float(r[j + 3]), alpha));
       } else {
-        for (int j = 0; j < 32; ++j)
+#pragma unroll
+        for (int j = 0; j < 32; ++j)  // unrolled: r[] stays in registers
           if (n0 + j < N) reduce_out1(args, off + j, __fmul_rn(__uint_as_float(r[j]), alpha));
       }
     } else if ((args.y_fp32 || nsplit > 1) && m < M && n0 < N) {
