@@ -59,6 +59,8 @@ constexpr int SFB_COL = 448 + 16;
 constexpr int NUM_THREADS = 192;
 constexpr int EPI_STAGE_BYTES = 32 * 64;   // per epilogue warp: 32 rows x 32 bf16 (64B-swizzled)
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 4 * EPI_STAGE_BYTES + 1024 /*align slack*/ + 256 /*barriers*/;
+// the 1-SM kernel with ST ring stages and EW chunks (2 KB each) of epilogue staging per warp
+constexpr int gemm_smem_bytes(int st, int ew) { return st * STAGE_BYTES + 4 * EPI_STAGE_BYTES * ew + 1024 + 256; }
 
 struct Args {
   int M, N, Kp;
@@ -131,7 +133,7 @@ __device__ __forceinline__ void reduce_out1(const Args& args, int64_t off, float
 // scales by alpha and stores.  The two chunks buffer b shares with the other buffer are read
 // first and released through ovl_free; the whole buffer is released through buf_free.  In the
 // 2-SM kernel (PAIR) both barriers live in the pair's leader CTA (cluster-scope remote arrivals).
-template <bool PAIR>
+template <bool PAIR, int EW = 1>
 __device__ __forceinline__ void epilogue_tile(const Args& args, const CUtensorMap* tmY, uint32_t tmem, int b, int mb,
                                               int nbk, int ks, float alpha, uint64_t y_policy, uint8_t* st,
                                               uint64_t* ovl_free, uint64_t* buf_free, int warp, int lane,
@@ -278,6 +280,38 @@ __device__ __forceinline__ void epilogue_tile(const Args& args, const CUtensorMa
       }
       continue;
     }
+    if (EW == 2 && !args.y_fp32 && nsplit == 1 && mb * BM + q * 32 < M && args.debug != 3) {
+      // bf16, wide stores: two column-adjacent 32x32 chunks are staged as one 32-row x 64-col tile
+      // (128-byte rows, 128B swizzle: 16-byte unit U of row r at U ^ (r & 7)) and written by ONE TMA
+      // store -- half the TMA store operations of the 2 KB path, which share the TMA unit with the
+      // operand loads.  The drain order pairs adjacent chunks: (6,7),(0,1),(2,3),(4,5) / (0,1),...
+      const int half = cc & 1;
+      if (half == 0) {
+        if (lane == 0) bulk_wait_read0();  // the previous pair's store finished reading the buffer
+        __syncwarp();
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        uint4 v;
+        uint32_t* pv = reinterpret_cast<uint32_t*>(&v);
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          __nv_bfloat162 b2 = __floats2bfloat162_rn(__fmul_rn(__uint_as_float(r[8 * u + 2 * h]), alpha),
+                                                    __fmul_rn(__uint_as_float(r[8 * u + 2 * h + 1]), alpha));
+          pv[h] = *reinterpret_cast<uint32_t*>(&b2);
+        }
+        *reinterpret_cast<uint4*>(st + lane * 128 + (((half * 4 + u) ^ (lane & 7)) << 4)) = v;
+      }
+      if (half == 1) {
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0 && n0 - 32 < N) {
+          tma_store_2d_hint(tmY, st, n0 - 32, mb * BM + q * 32, y_policy);
+          bulk_commit();
+        }
+      }
+      continue;
+    }
     if (!args.y_fp32 && nsplit == 1 && mb * BM + q * 32 < M && n0 < N && args.debug != 3) {
       // bf16: stage the 32x32 sub-tile in smem (64B swizzle: 16-byte unit u of row
       // r lives at unit u ^ ((r >> 1) & 3), bank-conflict-free) and TMA-store it
@@ -326,16 +360,16 @@ __device__ __forceinline__ void epilogue_tile(const Args& args, const CUtensorMa
 // tiles (m, n) and (m+1, n): each TMA-loads HALF of the shared B tile (and its
 // scale chunk) multicast into both CTAs' smem, halving L2->SM traffic for B --
 // at 128x256 tiles the kernel is otherwise bound by L2 bandwidth (~6 KB/clk).
-template <int CL>
+template <int CL, int ST = STAGES, int EW = 1>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     arc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const __grid_constant__ CUtensorMap tmY, Args args) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* epi_stage = smem + STAGES * STAGE_BYTES;  // [4 warps][2 KB]
-  uint64_t* full = reinterpret_cast<uint64_t*>(epi_stage + 4 * EPI_STAGE_BYTES);
-  uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;
+  uint8_t* epi_stage = smem + ST * STAGE_BYTES;  // [4 warps][EW x 2 KB]
+  uint64_t* full = reinterpret_cast<uint64_t*>(epi_stage + 4 * EPI_STAGE_BYTES * EW);
+  uint64_t* empty = full + ST;
+  uint64_t* tfull = empty + ST;
   uint64_t* ovl_free = tfull + 1;
   uint64_t* buf_free = ovl_free + 1;  // [2]
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(buf_free + 2);
@@ -356,7 +390,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const int n_rb = (N + 127) / 128;        // 128-row blocks of the B scale buffer
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) {
+    for (int s = 0; s < ST; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], CL);  // one MMA commit from every CTA of the cluster
     }
@@ -423,7 +457,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               }
             }
           }
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          if (++stage == ST) { stage = 0; phase ^= 1; }
         }
       }
     }
@@ -462,7 +496,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
           if (CL == 1) tc_commit(&empty[stage]);
           else tc_commit_mc(&empty[stage], mc_mask);  // frees the slot in both CTAs
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          if (++stage == ST) { stage = 0; phase ^= 1; }
         }
         tc_commit(tfull);
       }
@@ -478,8 +512,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const int nbk = args.raster ? rest % num_n : rest / num_mp;
       mbar_wait(tfull, t & 1);
       tc_fence_after();
-      epilogue_tile<false>(args, &tmY, tmem, t & 1, mb, nbk, ks, alpha, y_policy,
-                           epi_stage + (warp - 2) * EPI_STAGE_BYTES, ovl_free, &buf_free[t & 1], warp, lane);
+      epilogue_tile<false, EW>(args, &tmY, tmem, t & 1, mb, nbk, ks, alpha, y_policy,
+                               epi_stage + (warp - 2) * EPI_STAGE_BYTES * EW, ovl_free, &buf_free[t & 1], warp, lane);
     }
     if (lane == 0) bulk_wait_all();
   }
@@ -766,7 +800,9 @@ bool make_y_map(CUtensorMap* m, void* y, int64_t rows, int64_t cols, int64_t ldy
   cuuint32_t box[2] = {(cuuint32_t)box_cols, 32};
   cuuint32_t estr[2] = {1, 1};
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, y, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-             box_cols == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+             box_cols == 64 ? CU_TENSOR_MAP_SWIZZLE_128B
+                            : (box_cols == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_NONE),
+             CU_TENSOR_MAP_L2_PROMOTION_NONE,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -885,7 +921,11 @@ cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t stream, const char** 
   }
   CUtensorMap tmA, tmB, tmY;
   memset(&tmY, 0, sizeof(tmY));
-  if (p.swiglu ? !make_y_map(&tmY, p.y, p.M, p.N / 2, p.ldy, 16) : (!p.y_fp32 && !make_y_map(&tmY, p.y, p.M, p.N, p.ldy, 32))) {
+  // wide epilogue stores (two 32-column chunks per TMA store, 3-stage ring): ARC_GEMM_EPI=2
+  static const int env_epi = getenv("ARC_GEMM_EPI") ? atoi(getenv("ARC_GEMM_EPI")) : 1;
+  const bool wide = env_epi == 2 && !pl.pair && CL == 2 && !p.swiglu && !p.y_fp32 && pl.nsplit == 1;
+  if (p.swiglu ? !make_y_map(&tmY, p.y, p.M, p.N / 2, p.ldy, 16)
+               : (!p.y_fp32 && !make_y_map(&tmY, p.y, p.M, p.N, p.ldy, wide ? 64 : 32))) {
     if (detail) *detail = "cuTensorMapEncodeTiled (Y) failed";
     return cudaErrorInvalidValue;
   }
@@ -907,6 +947,9 @@ cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t stream, const char** 
     cudaError_t attr_err = cudaFuncSetAttribute(arc_gemm_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     if (attr_err == cudaSuccess)
       attr_err = cudaFuncSetAttribute(arc_gemm_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    if (attr_err == cudaSuccess)
+      attr_err = cudaFuncSetAttribute(arc_gemm_kernel<2, 3, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      gemm_smem_bytes(3, 2));
     if (attr_err == cudaSuccess)
       attr_err = cudaFuncSetAttribute(arc_gemm_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     if (attr_err == cudaSuccess)
@@ -956,7 +999,8 @@ cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t stream, const char** 
   cfg.blockDim = dim3(NUM_THREADS);
   static const int env_st = getenv("ARC_GEMM_STAGES") ? atoi(getenv("ARC_GEMM_STAGES")) : 5;
   const bool st4 = pl.pair && CL == 2 && env_st == 4;  // experiment only
-  cfg.dynamicSmemBytes = pl.pair ? p_smem_bytes(st4 ? 4 : 5) + (p.swiglu ? P_SILU_TAB_BYTES : 0) : SMEM_BYTES;
+  cfg.dynamicSmemBytes = pl.pair ? p_smem_bytes(st4 ? 4 : 5) + (p.swiglu ? P_SILU_TAB_BYTES : 0)
+                                  : (wide ? gemm_smem_bytes(3, 2) : SMEM_BYTES);
   cfg.stream = stream;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -971,6 +1015,7 @@ cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t stream, const char** 
                                                 : cudaLaunchKernelEx(&cfg, arc_gemm_pair_kernel<2, 5>, tmA, tmB, tmSFA, tmSFB, tmY, a))
                                      : cudaLaunchKernelEx(&cfg, arc_gemm_pair_kernel<4, 5>, tmA, tmB, tmSFA, tmSFB, tmY, a))
                   : CL == 1 ? cudaLaunchKernelEx(&cfg, arc_gemm_kernel<1>, tmA, tmB, tmY, a)
+                  : (CL == 2 && wide) ? cudaLaunchKernelEx(&cfg, arc_gemm_kernel<2, 3, 2>, tmA, tmB, tmY, a)
                   : CL == 2 ? cudaLaunchKernelEx(&cfg, arc_gemm_kernel<2>, tmA, tmB, tmY, a)
                   : CL == 4 ? cudaLaunchKernelEx(&cfg, arc_gemm_kernel<4>, tmA, tmB, tmY, a)
                             : cudaLaunchKernelEx(&cfg, arc_gemm_kernel<8>, tmA, tmB, tmY, a);

@@ -164,8 +164,9 @@ def test_decode_splitk_parity(A, M, N, K, S):
 
 @pytest.mark.parametrize("env", [{"ARC_GEMM_PAIR": "1", "ARC_GEMM_CLP": "2"}, {"ARC_GEMM_PAIR": "1", "ARC_GEMM_CLP": "4"},
                                  {"ARC_GEMM_CL": "1"}, {"ARC_GEMM_CL": "4"}, {"ARC_GEMM_CL": "8"},
-                                 {"ARC_GEMM_RASTER": "1"}, {"ARC_GEMM_RASTER": "0"}, {"ARC_GEMM_STREAM": "1"}],
-                         ids=["pair2", "pair4", "cl1", "cl4", "cl8", "raster1", "raster0", "stream"])
+                                 {"ARC_GEMM_RASTER": "1"}, {"ARC_GEMM_RASTER": "0"}, {"ARC_GEMM_STREAM": "1"},
+                                 {"ARC_GEMM_EPI": "2"}],
+                         ids=["pair2", "pair4", "cl1", "cl4", "cl8", "raster1", "raster0", "stream", "epi2"])
 def test_kernel_variants(env):
     """The non-default GEMM kernels/schedules (2-SM cta_group::2 pairs, 4-CTA clusters with
     multicast B, single-CTA, both tile orders) through the same parity tests, in a fresh
