@@ -90,9 +90,34 @@ def test_full_size_sampled_rows(A):
     y = A.linear(x, prof, qw, out_dtype=torch.bfloat16)
     codes, sf = A.quantize_activation(x, prof)
     torch.cuda.synchronize()
-    rows = np.array([0, 1, 127, 128, 1000, 4097, 8000, 8191], np.int64)
-    yref, bound = oracle.gemm_reference(codes.cpu().numpy(), sf.cpu().numpy(), qw.codes.cpu().numpy(),
-                                        qw.sf.cpu().numpy(), float(prof.gs.item()), float(qw.gs.item()), rows=rows)
+    # 64 rows: both ends of every 1024-row band, 128-row tile edges and seeded random rows
+    rng = np.random.default_rng(1)
+    rows = np.unique(np.concatenate([[0, 1, 127, 128, 255, 256, 4095, 4096, 8063, 8064, 8190, 8191],
+                                     rng.choice(M, 52, replace=False)])).astype(np.int64)
+    with oracle.openmp():
+        yref, bound = oracle.gemm_reference(codes.cpu().numpy(), sf.cpu().numpy(), qw.codes.cpu().numpy(),
+                                            qw.sf.cpu().numpy(), float(prof.gs.item()), float(qw.gs.item()), rows=rows)
+    _check(y[torch.from_numpy(rows).cuda()].float().cpu().numpy().astype(np.float64), yref, bound, True)
+
+
+@pytest.mark.parametrize("site", ["qkv", "o", "gate_up", "down"])
+def test_bench_sites_full_size(A, site):
+    """Every site of bench.py's step at its full size (M = 8192, S = 128) in the bench's launch
+    configuration: the whole quantized activation bit-exact against the oracle, the GEMM on 24 sampled
+    rows (all N columns) within the north_star bound."""
+    K, N = {n: (k, nn) for n, k, nn in synth.LLAMA3_8B_SITES}[site]
+    M, S = 8192, 128
+    x, w, prof, qw = _problem(A, M, N, K, S, seed=K + N)
+    codes, sf = A.quantize_activation(x, prof)
+    y = A.gemm(codes, sf, prof.gs, qw)
+    torch.cuda.synchronize()
+    with oracle.openmp():
+        oc, osf = oracle.quantize_activation(dev_bits(x), prof.perm.cpu().numpy(), S, float(prof.gs.item()))
+    assert np.array_equal(codes.cpu().numpy(), oc)
+    rows = np.unique(np.concatenate([[0, 127, 128, M - 1], np.random.default_rng(K).choice(M, 20, replace=False)]))
+    with oracle.openmp():
+        yref, bound = oracle.gemm_reference(oc, osf, qw.codes.cpu().numpy(), qw.sf.cpu().numpy(),
+                                            float(prof.gs.item()), float(qw.gs.item()), rows=rows.astype(np.int64))
     _check(y[torch.from_numpy(rows).cuda()].float().cpu().numpy().astype(np.float64), yref, bound, True)
 
 

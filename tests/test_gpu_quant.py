@@ -107,12 +107,11 @@ def test_full_size_sampled_rows(A):
     perm = prof.perm.cpu().numpy()
     gs = float(prof.gs.item())
     Kp = oracle.kp(K, S)
-    rows = [0, 1, 31, 32, 127, 128, 4095, 5000, 8064, 8191]
-    for r in rows:
-        oc, osf = oracle.quantize_activation(dev_bits(x[r:r + 1]), perm, S, gs, 0)
-        assert np.array_equal(gc[r], oc[0]), r
-        for c in range(Kp // 16):
-            assert gsf[oracle.sf_offset(r, c, Kp)] == osf[oracle.sf_offset(0, c, Kp)], (r, c)
+    # every row: the oracle (OpenMP build, identical per-element arithmetic) quantizes the whole tensor
+    with oracle.openmp():
+        oc, osf = oracle.quantize_activation(dev_bits(x), perm, S, gs, 0)
+    assert np.array_equal(gc, oc)
+    assert np.array_equal(gsf[valid_sf_mask(M, Kp)], osf[valid_sf_mask(M, Kp)])
 
 
 def test_calib_absmax_and_tensor_scale(A):
