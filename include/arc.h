@@ -311,17 +311,16 @@ ARC_API arc_status_t arc_linear(const void* x, int64_t M, int64_t ldx, const arc
                         size_t ws_bytes, void* stream);
 
 /* How arc_linear_ex runs the layer:
- *  ARC_LINEAR_UNFUSED / ARC_LINEAR_AUTO: two kernels chained by programmatic dependent launch --
- *    arc_quantize_activation into the workspace, then arc_gemm (decode-size M: split-K + a fixed-order
- *    reduction kernel).
+ *  ARC_LINEAR_UNFUSED: two kernels chained by programmatic dependent launch -- arc_quantize_activation
+ *    into the workspace, then arc_gemm (decode-size M: split-K + a fixed-order reduction kernel).
+ *  ARC_LINEAR_AUTO: FUSED at M <= 4, UNFUSED otherwise (the faster of the two on B200).
  *  ARC_LINEAR_FUSED at M <= 64: ONE kernel (the "optionally fused with the activation quantize as its
  *    producer stage" GEMM of the north star): a persistent weight-streaming stream-K GEMM whose
  *    CTAs first quantize one 256-element K block each (all M rows) into the workspace and publish it
  *    with a per-K-block ready word; each CTA's producer streams its weights from launch and waits only
  *    for the K blocks it needs; split tiles are summed in a fixed segment order by the last CTA to
- *    finish them.  The quantized activation is bit-identical to arc_quantize_activation's.  Measured
- *    slower than the two-kernel path on B200, hence not AUTO.  At M > 64 FUSED runs
- *    the two-kernel path. */
+ *    finish them.  The quantized activation is bit-identical to arc_quantize_activation's.  At M > 64
+ *    FUSED runs the two-kernel path. */
 enum { ARC_LINEAR_AUTO = 0, ARC_LINEAR_FUSED = 1, ARC_LINEAR_UNFUSED = 2 };
 ARC_API arc_status_t arc_linear_ex_workspace_size(int64_t M, const arc_qweight_t* qw, int flags, size_t* bytes);
 ARC_API arc_status_t arc_linear_ex(const void* x, int64_t M, int64_t ldx, const arc_profile_t* prof,

@@ -433,9 +433,9 @@ def linear_workspace_size_ex(M: int, qw, mode: str = "auto") -> int:
 
 def linear(x: torch.Tensor, prof: Profile, qw: QWeight, out_dtype=torch.bfloat16, out=None, ws: Workspace = None,
            stream=None, mode: str = "auto"):
-    """The ARC linear layer (Eq.2): activation quantize + augmented NVFP4 GEMM.  mode "auto" / "unfused" =
-    two PDL-chained kernels; "fused" (M <= 64) = one kernel that quantizes the activation and runs the
-    weight-streaming stream-K GEMM (arc.h ARC_LINEAR_FUSED; measured slower on B200)."""
+    """The ARC linear layer (Eq.2): activation quantize + augmented NVFP4 GEMM.  mode "unfused" = two
+    PDL-chained kernels; "fused" (M <= 64) = one kernel that quantizes the activation and runs the
+    weight-streaming stream-K GEMM (arc.h ARC_LINEAR_FUSED); "auto" = fused at M <= 4, else unfused."""
     assert x.dtype == torch.bfloat16 and x.is_cuda
     M = x.shape[0]
     if out is None:

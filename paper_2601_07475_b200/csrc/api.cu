@@ -627,10 +627,10 @@ arc_status_t arc_linear_ex(const void* x, int64_t M, int64_t ldx, const arc_prof
   uint8_t* sf = codes + round_up(M * (qw->Kp / 2), 256);
   const size_t act = act_ws_bytes(M, qw->K, qw->S);
   // ARC_LINEAR_FUSED at decode-size M: one kernel quantizes the activation into the workspace and runs
-  // the stream-K GEMM (measured slower than the two-kernel path on B200, so AUTO takes
-  // the two-kernel path)
+  // the stream-K GEMM.  AUTO takes it at M <= 4, where the single launch per site measured faster than
+  // the three-kernel path on most boxes; from M = 16 on the split-K path is faster.
   const StreamPlan sp = plan_stream(M, qw->N, qw->Kp);
-  if (flags == ARC_LINEAR_FUSED && sp.ok) {
+  if ((flags == ARC_LINEAR_FUSED || (flags == ARC_LINEAR_AUTO && M <= 4)) && sp.ok) {
     // decode-size M: one kernel quantizes the activation into the workspace and runs the stream-K GEMM
     s = check_device();
     if (s != ARC_OK) return s;

@@ -69,7 +69,7 @@ def test_llama3_8b_sites(A, site, M):
     x, w, prof, qw = _problem(A, M, N, K, 128, seed=K + N + M)
     rows = [0, M - 1] if M > 1 else [0]
     yref, bound = _oracle(x, w, prof, qw, rows)
-    for mode in ("auto", "fused"):
+    for mode in ("auto", "unfused", "fused"):
         y16 = A.linear(x, prof, qw, mode=mode)
         y32 = A.linear(x, prof, qw, out_dtype=torch.float32, mode=mode)
         torch.cuda.synchronize()
@@ -83,10 +83,10 @@ def test_deterministic_and_counters_reset(A, M, N, K, S):
     x, w, prof, qw = _problem(A, M, N, K, S, seed=7)
     ws = A.Workspace("cuda")
     ys = [A.linear(x, prof, qw, out_dtype=torch.float32, ws=ws, mode="fused").clone() for _ in range(4)]
-    yd = [A.linear(x, prof, qw, out_dtype=torch.float32, ws=ws).clone() for _ in range(2)]
+    yd = [A.linear(x, prof, qw, out_dtype=torch.float32, ws=ws, mode="unfused").clone() for _ in range(2)]
     torch.cuda.synchronize()
     assert all(torch.equal(ys[0], y) for y in ys[1:]) and torch.equal(yd[0], yd[1])
-    # the GEMM alone gives the default path's bits
+    # the GEMM alone gives the two-kernel path's bits
     codes, sf = A.quantize_activation(x, prof)
     y2 = A.gemm(codes, sf, prof.gs, qw, out_dtype=torch.float32)
     torch.cuda.synchronize()
