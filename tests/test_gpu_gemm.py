@@ -204,3 +204,24 @@ def test_kernel_variants(env):
                         "-k", "parity_fp32 or multi_tile or same_sign"],
                        env={**os.environ, **env}, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("site", ["qkv", "o", "gate_up", "down"])
+def test_llama3_70b_sites(A, site):
+    """BASELINE configs[3] shapes (LLaMA-3-70B: K = 8192 / 28672, N up to 57344) at M = 2048 through
+    arc_linear: the whole quantized activation bit-exact against the oracle, Y on 16 sampled rows within
+    the north_star bound (+ one bf16 ulp)."""
+    K, N = {n: (k, nn) for n, k, nn in synth.LLAMA3_70B_SITES}[site]
+    M, S = 2048, 128
+    x, w, prof, qw = _problem(A, M, N, K, S, seed=N + 1)
+    y = A.linear(x, prof, qw)
+    codes, sf = A.quantize_activation(x, prof)
+    torch.cuda.synchronize()
+    with oracle.openmp():
+        oc, osf = oracle.quantize_activation(dev_bits(x), prof.perm.cpu().numpy(), S, float(prof.gs.item()))
+    assert np.array_equal(codes.cpu().numpy(), oc)
+    rows = np.unique(np.concatenate([[0, 127, 128, M - 1], np.random.default_rng(N).choice(M, 12, replace=False)]))
+    with oracle.openmp():
+        yref, bound = oracle.gemm_reference(oc, osf, qw.codes.cpu().numpy(), qw.sf.cpu().numpy(),
+                                            float(prof.gs.item()), float(qw.gs.item()), rows=rows.astype(np.int64))
+    _check(y[torch.from_numpy(rows).cuda()].float().cpu().numpy().astype(np.float64), yref, bound, True)
