@@ -121,6 +121,12 @@ def lib():
         for n in ("or_e2m1_encode_n", "or_e4m3_ceil_n", "or_e4m3_rn_n"):
             getattr(L, n).restype = None
             getattr(L, n).argtypes = [P, i64, P]
+        L.or_kp8.restype = i64
+        L.or_kp8.argtypes = [i32]
+        L.or_quantize_mxfp8.restype = i32
+        L.or_quantize_mxfp8.argtypes = [P, i64, i32, i64, P, P]
+        L.or_gemm_mxfp8_exact.restype = None
+        L.or_gemm_mxfp8_exact.argtypes = [P, P, P, P, i64, i64, P, i64, P, P]
         L.or_num_threads.restype = i32
         L.or_num_threads.argtypes = []
         _libs[_variant] = L
@@ -394,3 +400,35 @@ def mxfp8_block(x32):
     xh = np.zeros(32, np.float32)
     lib().or_mxfp8_block(_p(x), _p(s), _p(xh))
     return float(s[0]), xh
+
+
+# ----------------------------------------------------------------------------- Fig.8a MXFP8 comparator
+def kp8(K: int) -> int:
+    return int(lib().or_kp8(K))
+
+
+def quantize_mxfp8(x_bits):
+    """Plain MXFP8 (Eq.3 per 32-block, no reordering / residual; the Fig.8a comparison format):
+    E4M3 codes [rows][Kp8] and E8M0 scale bytes in the 128x4 tile layout (Kp8/32 columns)."""
+    x = as_bf16_bits(x_bits)
+    M, K = x.shape
+    K8 = kp8(K)
+    codes = np.zeros((M, K8), np.uint8)
+    sf = np.zeros(sf_rows_padded(M) * K8 // 32, np.uint8)
+    _check(lib().or_quantize_mxfp8(_p(x), M, K, K, _p(codes), _p(sf)))
+    return codes, sf
+
+
+def gemm_mxfp8_reference(a_codes, a_sf, b_codes, b_sf, rows=None):
+    """Exact MXFP8 x MXFP8 GEMM (float64 of exact per-block int64 sums) and the 1e-5 * sum|ab| bound."""
+    a_codes = np.ascontiguousarray(a_codes, np.uint8)
+    b_codes = np.ascontiguousarray(b_codes, np.uint8)
+    a_sf = np.ascontiguousarray(a_sf, np.uint8)
+    b_sf = np.ascontiguousarray(b_sf, np.uint8)
+    M, K8 = a_codes.shape
+    N = b_codes.shape[0]
+    rows = np.arange(M, dtype=np.int64) if rows is None else np.ascontiguousarray(rows, np.int64)
+    Y = np.zeros((rows.size, N))
+    Yabs = np.zeros((rows.size, N))
+    lib().or_gemm_mxfp8_exact(_p(a_codes), _p(a_sf), _p(b_codes), _p(b_sf), N, K8, _p(rows), rows.size, _p(Y), _p(Yabs))
+    return Y, 1e-5 * Yabs

@@ -396,6 +396,69 @@ void or_gemm_exact(const uint8_t* a_codes, const uint8_t* a_sf, const uint8_t* b
     free(Va);
 }
 
+/* ------------------------------------------------------------------------- */
+/* Fig.8a comparator: plain MXFP8 -- Eq.3's single stage per   */
+/* 32-block (E8M0 scale = smallest power of two >= amax/448, E4M3  */
+/* elements round-to-nearest-even), no reordering, no residual, K padded to a */
+/* multiple of 128 with zero blocks (scale 1).  codes: E4M3 bytes [rows][Kp8];*/
+/* sf: E8M0 bytes (2^(b-127)) in the 128x4 tile layout with Kp8/32 columns.   */
+/* ------------------------------------------------------------------------- */
+int64_t or_kp8(int K) { return ((int64_t)K + 127) / 128 * 128; }
+void or_mxfp8_block(const float x[32], float* scale, float xhat[32]);  /* Eq.3, below */
+
+int or_quantize_mxfp8(const uint16_t* x, int64_t rows, int K, int64_t ldx, uint8_t* codes, uint8_t* sf) {
+    if (K <= 0 || K % 32 || rows < 0 || ldx < K) return OR_ERR_SHAPE;
+    const int64_t Kp8 = or_kp8(K);
+    for (int64_t m = 0; m < rows; ++m)
+        for (int j = 0; j < K; ++j)
+            if (!isfinite(bf16_to_f32(x[m * ldx + j]))) return OR_ERR_NONFINITE;
+    #pragma omp parallel for schedule(static)
+    for (int64_t m = 0; m < rows; ++m) {
+        for (int64_t b = 0; b < Kp8 / 32; ++b) {
+            float z[32], xh[32], s = 1.0f;
+            uint8_t* c = codes + m * Kp8 + b * 32;
+            if (b * 32 < K) {
+                for (int i = 0; i < 32; ++i) z[i] = bf16_to_f32(x[m * ldx + b * 32 + i]);
+                or_mxfp8_block(z, &s, xh);                      /* Eq.3: the scale */
+                for (int i = 0; i < 32; ++i) c[i] = or_e4m3_rn(z[i] / s);
+            } else {
+                memset(c, 0, 32);
+            }
+            int e;
+            frexpf(s, &e);                                      /* s = 2^(e-1) */
+            sf[or_sf_offset(m, b, Kp8 / 2)] = (uint8_t)(e - 1 + 127);
+        }
+    }
+    return OR_OK;
+}
+
+/* Exact MXFP8 GEMM: per 32-block the int64 sum of V_a V_b with V = 512 e4m3 (an integer), scaled by
+ * 2^(ea + eb - 18) in double; |.| sums likewise for the bound.  Y, Yabs: [nrows][N]. */
+void or_gemm_mxfp8_exact(const uint8_t* a_codes, const uint8_t* a_sf, const uint8_t* b_codes, const uint8_t* b_sf,
+                         int64_t N, int64_t Kp8, const int64_t* rows, int64_t nrows, double* Y, double* Yabs) {
+    #pragma omp parallel for schedule(static)
+    for (int64_t n = 0; n < N; ++n) {
+        for (int64_t ri = 0; ri < nrows; ++ri) {
+            const int64_t r = rows[ri];
+            double acc = 0.0, aabs = 0.0;
+            for (int64_t b = 0; b < Kp8 / 32; ++b) {
+                int64_t s = 0, sa = 0;
+                for (int i = 0; i < 32; ++i) {
+                    const int64_t va = (int64_t)(512.0f * or_e4m3_value(a_codes[r * Kp8 + b * 32 + i]));
+                    const int64_t vb = (int64_t)(512.0f * or_e4m3_value(b_codes[n * Kp8 + b * 32 + i]));
+                    s += va * vb;
+                    sa += va * vb < 0 ? -va * vb : va * vb;
+                }
+                const int e = (int)a_sf[or_sf_offset(r, b, Kp8 / 2)] + (int)b_sf[or_sf_offset(n, b, Kp8 / 2)] - 254 - 18;
+                acc += ldexp((double)s, e);
+                aabs += ldexp((double)sa, e);
+            }
+            Y[ri * N + n] = acc;
+            Yabs[ri * N + n] = aabs;
+        }
+    }
+}
+
 /* Threads the OpenMP build uses (1 in the plain build). */
 #ifdef _OPENMP
 #include <omp.h>
