@@ -224,6 +224,26 @@ ARC_API arc_status_t arc_quantize_weight_mx(const void* w, int64_t N, int64_t K,
                                             int32_t S, const float* gs_w, arc_layout_t layout, uint8_t* codes,
                                             uint8_t* sf, void* stream);
 
+/* ---------------------------------------------------------------- Fig.8a comparator: plain MXFP8 */
+/* The MXFP8 format the paper compares ARC's kernel against (Eq.3's single stage,
+ * P:181-184): per 32-element block of a row, scale 2^e = the smallest power of two >= RN(amax/448)
+ * (UE8M0 byte e + 127), codes = E4M3 round-to-nearest-even of x / 2^e; no reordering, no residual.
+ * K % 32 == 0; rows are padded to Kp8 = roundup(K, 128) with zero blocks (scale byte 127).
+ * codes: [rows][Kp8] bytes; sf: roundup(rows, 128) * Kp8 / 32 bytes in the 128x4 tile layout
+ * (one byte per 32-block).  Sizes: */
+ARC_API arc_status_t arc_mxfp8_buffer_sizes(int64_t rows, int64_t K, int64_t* Kp8, size_t* code_bytes,
+                                            size_t* sf_bytes);
+ARC_API arc_status_t arc_quantize_mxfp8(const void* x, int64_t rows, int64_t K, int64_t ldx, uint8_t* codes,
+                                        uint8_t* sf, void* stream);
+/* y[M][N] = A B^T of two MXFP8 operands (activations a: [M][Kp8], weights b: [N][Kp8], both from
+ * arc_quantize_mxfp8 with the same K), FP32 accumulation in TMEM (tcgen05.mma kind::mxf8f6f4.block_scale,
+ * K = 32 per MMA, UE8M0 scales), stored as y_dtype (ldy as arc_gemm).  ws: arc_gemm_mxfp8_workspace_size
+ * bytes (decode-size M splits K), zero before first use. */
+ARC_API arc_status_t arc_gemm_mxfp8_workspace_size(int64_t M, int64_t N, int64_t K, size_t* bytes);
+ARC_API arc_status_t arc_gemm_mxfp8(const uint8_t* a_codes, const uint8_t* a_sf, int64_t M, const uint8_t* b_codes,
+                                    const uint8_t* b_sf, int64_t N, int64_t K, void* y, arc_dtype_t y_dtype,
+                                    int64_t ldy, void* ws, size_t ws_bytes, void* stream);
+
 /* ---------------------------------------------------------------- SiLU-mul (fused producer, Fig.5) */
 /* The down-projection input of a LLaMA/Qwen decoder layer (Fig.5 P:157 quantizes every linear
  * input): h = SiLU(gate) * up of the bf16 gate/up projections, with the roundings of a bf16

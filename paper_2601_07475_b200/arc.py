@@ -94,6 +94,11 @@ _sig("arc_quantize_activation_mx", [_P, _i64, _i64, ctypes.POINTER(ArcProfile), 
 _sig("arc_quantize_weight_mx", [_P, _i64, _i64, _i64, _P, _i32, _P, ctypes.c_int, _P, _P, _P])
 _sig("arc_gemm_reduce", [_P, _P, _P, _i64, ctypes.POINTER(ArcQWeight), ctypes.POINTER(ArcReduce), _i64, _P,
                          ctypes.c_size_t, _P])
+_sig("arc_mxfp8_buffer_sizes", [_i64, _i64, ctypes.POINTER(_i64), ctypes.POINTER(ctypes.c_size_t),
+                                ctypes.POINTER(ctypes.c_size_t)])
+_sig("arc_quantize_mxfp8", [_P, _i64, _i64, _i64, _P, _P, _P])
+_sig("arc_gemm_mxfp8_workspace_size", [_i64, _i64, _i64, ctypes.POINTER(ctypes.c_size_t)])
+_sig("arc_gemm_mxfp8", [_P, _P, _i64, _P, _P, _i64, _i64, _P, ctypes.c_int, _i64, _P, ctypes.c_size_t, _P])
 _sig("arc_gemm_swiglu", [_P, _P, _P, _i64, ctypes.POINTER(ArcQWeight), _P, _i64, _P, ctypes.c_size_t, _P])
 _sig("arc_silu_mul", [_P, _i64, _i64, _i64, _i64, _P, _i64, _P])
 _sig("arc_silu_mul_quantize_activation", [_P, _i64, _i64, _i64, ctypes.POINTER(ArcProfile), _P, _P, _P])
@@ -118,6 +123,7 @@ EXPORTED = [
     "arc_linear_hostio_workspace_size", "arc_rmsnorm",
     "arc_rmsnorm_quantize_activation", "arc_linear_rmsnorm", "arc_linear_hostio",
     "arc_silu_mul", "arc_silu_mul_quantize_activation", "arc_linear_silu_mul", "arc_gemm_swiglu", "arc_gemm_reduce",
+    "arc_mxfp8_buffer_sizes", "arc_quantize_mxfp8", "arc_gemm_mxfp8_workspace_size", "arc_gemm_mxfp8",
     "arc_mx_tensor_scale", "arc_mx_tensor_scale_device", "arc_quantize_activation_mx", "arc_quantize_weight_mx", "arc_gather_order_ex",
     "arc_probe_e2m1", "arc_probe_e2m1_bits", "arc_probe_e2m1_raw_bits", "arc_probe_e4m3_ceil", "arc_probe_silu",
     "arc_debug_stream_trace",
@@ -643,4 +649,38 @@ def probe_silu(g_bits: torch.Tensor) -> torch.Tensor:
     (g_bits: int16/uint16-viewed bf16 patterns on the device)."""
     out = torch.empty(g_bits.numel(), dtype=torch.int16, device=g_bits.device)
     _check(_lib.arc_probe_silu(_ptr(g_bits), g_bits.numel(), _ptr(out), _stream()), "arc_probe_silu")
+    return out
+
+
+# ----------------------------------------------------------------------------- Fig.8a comparator: MXFP8
+def quantize_mxfp8(x: torch.Tensor, stream=None):
+    """Plain MXFP8 (arc.h arc_quantize_mxfp8): E4M3 codes [rows][Kp8] and E8M0 scales (128x4 tile layout)."""
+    assert x.dtype == torch.bfloat16 and x.is_cuda and x.dim() == 2
+    rows, K = x.shape
+    k8, cb, sb = _i64(), ctypes.c_size_t(), ctypes.c_size_t()
+    _check(_lib.arc_mxfp8_buffer_sizes(rows, K, ctypes.byref(k8), ctypes.byref(cb), ctypes.byref(sb)),
+           "arc_mxfp8_buffer_sizes")
+    codes = torch.empty(rows, k8.value, dtype=torch.uint8, device=x.device)
+    sf = torch.empty(sb.value, dtype=torch.uint8, device=x.device)
+    _check(_lib.arc_quantize_mxfp8(_ptr(x), rows, K, x.stride(0), _ptr(codes), _ptr(sf), _stream(stream)),
+           "arc_quantize_mxfp8")
+    return codes, sf
+
+
+def gemm_mxfp8(a_codes, a_sf, b_codes, b_sf, K: int, out_dtype=torch.bfloat16, out=None, ws: Workspace = None,
+               stream=None):
+    """arc_gemm_mxfp8: y = A B^T of two plain-MXFP8 operands (the Fig.8a comparison GEMM)."""
+    M, N = a_codes.shape[0], b_codes.shape[0]
+    if out is None:
+        out = _alloc_out(M, N, out_dtype, a_codes.device)
+    b = ctypes.c_size_t()
+    _check(_lib.arc_gemm_mxfp8_workspace_size(M, N, K, ctypes.byref(b)), "arc_gemm_mxfp8_workspace_size")
+    buf = None
+    if b.value:
+        if ws is None:
+            ws = _default_workspace("gemm", a_codes.device, stream)
+        buf = ws.get(b.value)
+    _check(_lib.arc_gemm_mxfp8(_ptr(a_codes), _ptr(a_sf), M, _ptr(b_codes), _ptr(b_sf), N, K, _ptr(out),
+                               _dtype_code(out.dtype), out.stride(0), _ptr(buf), 0 if buf is None else buf.numel(),
+                               _stream(stream)), "arc_gemm_mxfp8")
     return out

@@ -94,6 +94,19 @@ struct Args {
 // instruction descriptor: E2M1 x E2M1 (format 1), UE4M3 scales, K-major A/B,
 // N>>3 at [17,23), M>>4 at [24,29).
 constexpr uint32_t kIdesc = (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+// MXFP8 (Fig.8a comparator): E4M3 x E4M3 (format 0), UE8M0 scales (bit 23), K = 32 per MMA; the SF byte ids
+// (bits 29-30 for A, 4-5 for B) are or-ed in per MMA
+constexpr uint32_t kIdescF8 = (1u << 23) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+__device__ __forceinline__ void mma_mxf8(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate, uint32_t sfa_tmem, uint32_t sfb_tmem) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::mxf8f6f4.block_scale [%0], %1, %2, %3, [%5], [%6], p;\n\t"
+      "}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(sfa_tmem), "r"(sfb_tmem)
+      : "memory");
+}
 
 // fp32 reductions of 4 consecutive outputs into other ranks' Y (sys scope: the other GPUs observe them)
 __device__ __forceinline__ void red_add_v4_mc(float* mc, float a, float b, float c, float d) {
@@ -360,7 +373,7 @@ __device__ __forceinline__ void epilogue_tile(const Args& args, const CUtensorMa
 // tiles (m, n) and (m+1, n): each TMA-loads HALF of the shared B tile (and its
 // scale chunk) multicast into both CTAs' smem, halving L2->SM traffic for B --
 // at 128x256 tiles the kernel is otherwise bound by L2 bandwidth (~6 KB/clk).
-template <int CL, int ST = STAGES, int EW = 1>
+template <int CL, int ST = STAGES, int EW = 1, int FMT = 0>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     arc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const __grid_constant__ CUtensorMap tmY, Args args) {
@@ -385,8 +398,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const int rank = CL == 1 ? 0 : (int)cluster_ctarank();
   const int cid = blockIdx.x / CL, ncl = gridDim.x / CL;
   const uint16_t mc_mask = (uint16_t)((1u << CL) - 1u);
-  const int nkb = (Kp + BK - 1) / BK;
-  const int kc_total = Kp / 64;            // 64-element scale chunks per row block
+  // FMT 0: NVFP4 (256 K per stage, 4 scale chunks of 64 K, UE4M3 per 16); FMT 1: MXFP8 (the Fig.8a
+  // comparison format: 128 E4M3 K per stage, 1 scale chunk of 128 K, UE8M0 per 32).  Both move 128 B per
+  // operand row per stage.
+  constexpr int KST = FMT == 0 ? BK : 128;          // K elements per stage
+  constexpr int CPS = FMT == 0 ? 4 : 1;             // scale chunks per stage
+  const int nkb = (Kp + KST - 1) / KST;
+  const int kc_total = Kp / (FMT == 0 ? 64 : 128);  // scale chunks per row block
   const int n_rb = (N + 127) / 128;        // 128-row blocks of the B scale buffer
 
   if (threadIdx.x == 0) {
@@ -426,18 +444,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const int kb0 = ks * args.kbs, kb1 = min(nkb, kb0 + args.kbs);
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);     // the slot is free in EVERY CTA of the cluster
-          const int nk = min(4, kc_total - kb * 4);
+          const int nk = min(CPS, kc_total - kb * CPS);
           uint8_t* sA = smem + stage * STAGE_BYTES;
           uint8_t* sB = sA + A_BYTES;
           uint8_t* sSFA = sB + B_BYTES;
           uint8_t* sSFB = sSFA + SFA_BYTES;
           mbar_expect_tx(&full[stage], (uint32_t)(args.a_rows * BKB + B_BYTES + nk * 512 * ((a_ok ? 1 : 0) + nrb)));
           tma_load_2d(sA, &tmA, &full[stage], kb * BKB, mb * BM, pol);
-          if (a_ok) bulk_load(sSFA, args.sfa + ((int64_t)mb * kc_total + kb * 4) * 512, nk * 512, &full[stage]);
+          if (a_ok) bulk_load(sSFA, args.sfa + ((int64_t)mb * kc_total + kb * CPS) * 512, nk * 512, &full[stage]);
           if (CL == 1) {
             tma_load_2d(sB, &tmB, &full[stage], kb * BKB, nbk * BN, pol);
             for (int rb = 0; rb < nrb; ++rb)
-              bulk_load(sSFB + rb * 2048, args.sfb + ((int64_t)(2 * nbk + rb) * kc_total + kb * 4) * 512, nk * 512,
+              bulk_load(sSFB + rb * 2048, args.sfb + ((int64_t)(2 * nbk + rb) * kc_total + kb * CPS) * 512, nk * 512,
                         &full[stage]);
           } else {
             // this CTA's 1/CL of B (BN/CL rows) and its share of the scale chunks, to every CTA of the cluster
@@ -445,7 +463,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                            mc_mask, pol);
             if (CL == 2) {
               if (rank < nrb)
-                bulk_load_mc(sSFB + rank * 2048, args.sfb + ((int64_t)(2 * nbk + rank) * kc_total + kb * 4) * 512,
+                bulk_load_mc(sSFB + rank * 2048, args.sfb + ((int64_t)(2 * nbk + rank) * kc_total + kb * CPS) * 512,
                              nk * 512, &full[stage], mc_mask);
             } else {
               for (int j = rank; j < 8; j += CL) {  // chunk j = (row block j/4, K chunk j%4)
@@ -478,11 +496,30 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          const int nk = min(4, kc_total - kb * 4);
+          const int nk = min(CPS, kc_total - kb * CPS);
           const uint32_t sA = smem_u32(smem + stage * STAGE_BYTES);
           const uint32_t sB = sA + A_BYTES;
           const uint32_t sSFA = sB + B_BYTES;
           const uint32_t sSFB = sSFA + SFA_BYTES;
+          if (FMT == 1) {
+            // one 128-K scale chunk per 128 rows; MMA j (K = 32) reads byte j of each row's 32-bit TMEM scale
+            // word: the byte index rides in bits 30-31 of the scale address and in the descriptor's SF ids
+            utccp_32x128b_warpx4(tmem + SFA_COL, smem_desc(sSFA, 0, 128, kLayoutSwizzleNone));
+            utccp_32x128b_warpx4(tmem + SFB_COL, smem_desc(sSFB, 0, 128, kLayoutSwizzleNone));
+            utccp_32x128b_warpx4(tmem + SFB_COL + 4, smem_desc(sSFB + 2048, 0, 128, kLayoutSwizzleNone));
+            const int nmma = min(4, (Kp - kb * KST) / 32);
+            for (int j = 0; j < nmma; ++j) {
+              const uint64_t ad = smem_desc(sA + j * 32, 16, 1024, kLayoutSwizzle128B);
+              const uint64_t bd = smem_desc(sB + j * 32, 16, 1024, kLayoutSwizzle128B);
+              const uint32_t idesc = kIdescF8 | ((uint32_t)j << 29) | ((uint32_t)j << 4);
+              mma_mxf8(acc, ad, bd, idesc, (kb != kb0) || (j != 0), (tmem + SFA_COL) | ((uint32_t)j << 30),
+                       (tmem + SFB_COL) | ((uint32_t)j << 30));
+            }
+            if (CL == 1) tc_commit(&empty[stage]);
+            else tc_commit_mc(&empty[stage], mc_mask);
+            if (++stage == ST) { stage = 0; phase ^= 1; }
+            continue;
+          }
           for (int kk = 0; kk < nk && args.debug != 2; ++kk) {
             utccp_32x128b_warpx4(tmem + SFA_COL + 4 * kk, smem_desc(sSFA + kk * 512, 0, 128, kLayoutSwizzleNone));
             utccp_32x128b_warpx4(tmem + SFB_COL + 8 * kk, smem_desc(sSFB + kk * 512, 0, 128, kLayoutSwizzleNone));
@@ -503,7 +540,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
   } else {
     // ---------------------------------------------------------------- epilogue (warps 2..5)
-    const float alpha = __fdiv_rn(1.0f, __fmul_rn(__ldg(args.gs_x), __ldg(args.gs_w)));
+    const float alpha = args.gs_x ? __fdiv_rn(1.0f, __fmul_rn(__ldg(args.gs_x), __ldg(args.gs_w))) : 1.0f;
     const uint64_t y_policy = policy_evict_first();
     int t = 0;
     for (int tile = cid; tile < num_tiles; tile += ncl, ++t) {
@@ -905,11 +942,16 @@ cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t stream, const char** 
   // decode-size M: the split-K kernel + fixed-order reduce kernel by default; the weight-streaming
   // stream-K kernel (stream_gemm.cu) measured slower on the LLaMA-3-8B decode step
   static const int env_stream = getenv("ARC_GEMM_STREAM") ? atoi(getenv("ARC_GEMM_STREAM")) : 0;
-  if (env_stream && !p.swiglu && !p.red_mode) {
+  if (env_stream && !p.swiglu && !p.red_mode && !p.fmt) {
     const StreamPlan sp = plan_stream(p.M, p.N, p.Kp);
     if (sp.ok) return launch_stream_gemm(p, sp, stream, detail);
   }
-  GemmPlan pl = plan_gemm(p.M, p.N, p.Kp);
+  // MXFP8 (p.fmt == 1): 128 K per 128-byte stage -> plan as an NVFP4 problem with twice the K
+  GemmPlan pl = plan_gemm(p.M, p.N, p.fmt ? 2 * p.Kp : p.Kp);
+  if (p.fmt) {
+    pl.pair = 0;
+    if (pl.CL > 2) pl.CL = 2;
+  }
   // SwiGLU epilogue: the 2-SM kernel leaves shared memory for the SiLU table (the 1-SM kernel's
   // 4 x 54 KB ring does not), so prefill-size SwiGLU GEMMs run as CTA pairs
   static const int env_swp = getenv("ARC_GEMM_SWIGLU_PAIR") ? atoi(getenv("ARC_GEMM_SWIGLU_PAIR")) : 1;
@@ -923,7 +965,7 @@ cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t stream, const char** 
   memset(&tmY, 0, sizeof(tmY));
   // wide epilogue stores (two 32-column chunks per TMA store, 3-stage ring): ARC_GEMM_EPI=2
   static const int env_epi = getenv("ARC_GEMM_EPI") ? atoi(getenv("ARC_GEMM_EPI")) : 1;
-  const bool wide = env_epi == 2 && !pl.pair && CL == 2 && !p.swiglu && !p.y_fp32 && pl.nsplit == 1;
+  const bool wide = env_epi == 2 && !pl.pair && CL == 2 && !p.swiglu && !p.y_fp32 && pl.nsplit == 1 && !p.fmt;
   if (p.swiglu ? !make_y_map(&tmY, p.y, p.M, p.N / 2, p.ldy, 16)
                : (!p.y_fp32 && !make_y_map(&tmY, p.y, p.M, p.N, p.ldy, wide ? 64 : 32))) {
     if (detail) *detail = "cuTensorMapEncodeTiled (Y) failed";
@@ -936,7 +978,8 @@ cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t stream, const char** 
   // decode-size M on the 1-SM kernel: a 16/32/64-row A box instead of 128 rows of TMA zero fill
   static const int env_abox = getenv("ARC_GEMM_ABOX") ? atoi(getenv("ARC_GEMM_ABOX")) : 1;
   const int a_rows = (!pl.pair && CL == 1 && env_abox && p.M <= 64) ? (p.M <= 16 ? 16 : p.M <= 32 ? 32 : 64) : BM;
-  if (!make_map(&tmA, p.a_codes, p.M, p.Kp / 2, a_rows) || !make_map(&tmB, p.b_codes, p.N, p.Kp / 2, b_rows) ||
+  const int64_t row_bytes = p.fmt ? p.Kp : p.Kp / 2;
+  if (!make_map(&tmA, p.a_codes, p.M, row_bytes, a_rows) || !make_map(&tmB, p.b_codes, p.N, row_bytes, b_rows) ||
       (pl.pair && (!make_sf_map(&tmSFA, p.a_sf, (p.M + 127) / 128, p.Kp / 64, 4, 1) ||
                    !make_sf_map(&tmSFB, p.b_sf, (p.N + 127) / 128, p.Kp / 64, CL == 2 ? 4 : 2, 1)))) {
     if (detail) *detail = "cuTensorMapEncodeTiled failed";
@@ -950,6 +993,12 @@ cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t stream, const char** 
     if (attr_err == cudaSuccess)
       attr_err = cudaFuncSetAttribute(arc_gemm_kernel<2, 3, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       gemm_smem_bytes(3, 2));
+    if (attr_err == cudaSuccess)
+      attr_err = cudaFuncSetAttribute(arc_gemm_kernel<1, STAGES, 1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      SMEM_BYTES);
+    if (attr_err == cudaSuccess)
+      attr_err = cudaFuncSetAttribute(arc_gemm_kernel<2, STAGES, 1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      SMEM_BYTES);
     if (attr_err == cudaSuccess)
       attr_err = cudaFuncSetAttribute(arc_gemm_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     if (attr_err == cudaSuccess)
@@ -1014,6 +1063,8 @@ cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t stream, const char** 
   cudaError_t e = pl.pair ? (CL == 2 ? (st4 ? cudaLaunchKernelEx(&cfg, arc_gemm_pair_kernel<2, 4>, tmA, tmB, tmSFA, tmSFB, tmY, a)
                                                 : cudaLaunchKernelEx(&cfg, arc_gemm_pair_kernel<2, 5>, tmA, tmB, tmSFA, tmSFB, tmY, a))
                                      : cudaLaunchKernelEx(&cfg, arc_gemm_pair_kernel<4, 5>, tmA, tmB, tmSFA, tmSFB, tmY, a))
+                  : (p.fmt && CL == 1) ? cudaLaunchKernelEx(&cfg, arc_gemm_kernel<1, STAGES, 1, 1>, tmA, tmB, tmY, a)
+                  : (p.fmt && CL == 2) ? cudaLaunchKernelEx(&cfg, arc_gemm_kernel<2, STAGES, 1, 1>, tmA, tmB, tmY, a)
                   : CL == 1 ? cudaLaunchKernelEx(&cfg, arc_gemm_kernel<1>, tmA, tmB, tmY, a)
                   : (CL == 2 && wide) ? cudaLaunchKernelEx(&cfg, arc_gemm_kernel<2, 3, 2>, tmA, tmB, tmY, a)
                   : CL == 2 ? cudaLaunchKernelEx(&cfg, arc_gemm_kernel<2>, tmA, tmB, tmY, a)

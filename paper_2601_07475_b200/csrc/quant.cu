@@ -725,6 +725,60 @@ __global__ void arc_finalize_mx_scale_kernel(float* gs) {
   *gs = ldexpf(1.0f, -c);
 }
 
+// Fig.8a comparator: plain MXFP8 of a bf16 matrix -- Eq.3's single stage per 32-block
+// (E8M0 scale = smallest power of two >= RN(amax/448), E4M3 codes RN-even of x / scale), no reordering, no
+// residual; K padded to Kp8 = roundup(K, 128) with zero blocks of scale 1.  One thread per (row, 32-block):
+// 64 B of x in, 32 code bytes + 1 scale byte (128x4 tile layout, Kp8/32 columns) out.
+__global__ void arc_mxfp8_quant_kernel(const uint16_t* __restrict__ x, int64_t rows, int K, int Kp8, int64_t ldx,
+                                       uint8_t* __restrict__ codes, uint8_t* __restrict__ sf) {
+  pdl_wait();
+  pdl_launch_dependents();
+  const int nb = Kp8 >> 5;
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= rows * nb) return;
+  const int64_t m = idx / nb;
+  const int b = (int)(idx - m * nb);
+  uint4 out[2] = {make_uint4(0u, 0u, 0u, 0u), make_uint4(0u, 0u, 0u, 0u)};
+  int e = 0;
+  if (b * 32 < K) {
+    float z[32];
+    const uint4* src = reinterpret_cast<const uint4*>(x + m * ldx + b * 32);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint4 v = __ldg(src + q);
+      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        z[8 * q + 2 * h] = __uint_as_float(w[h] << 16);
+        z[8 * q + 2 * h + 1] = __uint_as_float(w[h] & 0xFFFF0000u);
+      }
+    }
+    float a = 0.0f;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) a = fmaxf(a, fabsf(z[i]));
+    if (a > 0.0f) {
+      int ex;
+      const float f = frexpf(__fdiv_rn(a, 448.0f), &ex);  // RN(a/448) = f 2^ex, f in [0.5, 1)
+      e = f == 0.5f ? ex - 1 : ex;                        // smallest 2^e >= RN(a/448)
+    }
+    const float inv = ldexpf(1.0f, -e);                   // x / 2^e is exact
+    uint32_t* o = reinterpret_cast<uint32_t*>(out);
+#pragma unroll
+    for (int i = 0; i < 32; i += 4) {
+      uint16_t lo, hi;
+      asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(lo) : "f"(__fmul_rn(z[i + 1], inv)), "f"(__fmul_rn(z[i], inv)));
+      asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(hi) : "f"(__fmul_rn(z[i + 3], inv)), "f"(__fmul_rn(z[i + 2], inv)));
+      o[i >> 2] = (uint32_t)lo | ((uint32_t)hi << 16);
+    }
+  }
+  uint4* dst = reinterpret_cast<uint4*>(codes + m * Kp8 + b * 32);
+  dst[0] = out[0];
+  dst[1] = out[1];
+  const int64_t rb = m >> 7;
+  sf[rb * (int64_t)(nb >> 2) * 512 + (b >> 2) * 512 + (m & 31) * 16 + ((m >> 5) & 3) * 4 + (b & 3)] =
+      (uint8_t)(e + 127);
+}
+
 // ------------------------------------------------------------------ launchers
 
 // Per-(kernel, threads, smem) launch configuration, computed once per process:
@@ -998,6 +1052,27 @@ __global__ void __launch_bounds__(128) probe_silu_block_kernel(const uint16_t* g
     for (int q = 0; q < 16; ++q)
       if (b + q < n) out[b + q] = (uint16_t)(__float_as_uint(z[q]) >> 16);
   }
+}
+
+cudaError_t launch_mxfp8_quant(const void* x, int64_t rows, int K, int64_t ld, uint8_t* codes, uint8_t* sf,
+                               cudaStream_t stream) {
+  const int Kp8 = (K + 127) / 128 * 128;
+  const int64_t n = rows * (Kp8 / 32);
+  if (n == 0) return cudaSuccess;
+  cudaLaunchConfig_t cfg;
+  memset(&cfg, 0, sizeof(cfg));
+  cfg.gridDim = dim3((unsigned)((n + 255) / 256));
+  cfg.blockDim = dim3(256);
+  cfg.stream = stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, arc_mxfp8_quant_kernel, static_cast<const uint16_t*>(x), rows, K, Kp8, ld,
+                                     codes, sf);
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
 }
 
 }  // namespace arc
