@@ -121,6 +121,12 @@ def lib():
         for n in ("or_e2m1_encode_n", "or_e4m3_ceil_n", "or_e4m3_rn_n"):
             getattr(L, n).restype = None
             getattr(L, n).argtypes = [P, i64, P]
+        L.or_kpm.restype = i64
+        L.or_kpm.argtypes = [i32, i32]
+        L.or_quantize_mx_native.restype = i32
+        L.or_quantize_mx_native.argtypes = [P, i64, i32, i64, P, i32, i32, i32, P, P]
+        L.or_gemm_mx_native_exact.restype = None
+        L.or_gemm_mx_native_exact.argtypes = [P, P, P, P, i64, i64, P, i64, P, P]
         L.or_kp8.restype = i64
         L.or_kp8.argtypes = [i32]
         L.or_quantize_mxfp8.restype = i32
@@ -431,4 +437,38 @@ def gemm_mxfp8_reference(a_codes, a_sf, b_codes, b_sf, rows=None):
     Y = np.zeros((rows.size, N))
     Yabs = np.zeros((rows.size, N))
     lib().or_gemm_mxfp8_exact(_p(a_codes), _p(a_sf), _p(b_codes), _p(b_sf), N, K8, _p(rows), rows.size, _p(Y), _p(Yabs))
+    return Y, 1e-5 * Yabs
+
+
+# ----------------------------------------------------------------------------- native MXFP4-ARC (f3)
+def kpm(K: int, S: int) -> int:
+    return int(lib().or_kpm(K, S))
+
+
+def quantize_mx_native(x_bits, perm, S: int, weight: bool = False, layout: int = INTERLEAVED):
+    """Native MXFP4-ARC (UE8M0 byte per 32-block, 32-granular block map, Kpm = roundup(K+S, 128)):
+    packed E2M1 codes [rows][Kpm/2] and scale bytes in the 128x4 tile layout (Kpm/32 columns)."""
+    x = as_bf16_bits(x_bits)
+    M, K = x.shape
+    Km = kpm(K, S)
+    codes = np.zeros((M, Km // 2), np.uint8)
+    sf = np.zeros(sf_rows_padded(M) * Km // 32, np.uint8)
+    perm = np.ascontiguousarray(perm, np.int32)
+    _check(lib().or_quantize_mx_native(_p(x), M, K, K, _p(perm), S, int(bool(weight)), layout, _p(codes), _p(sf)))
+    return codes, sf
+
+
+def gemm_mx_native_reference(a_codes, a_sf, b_codes, b_sf, rows=None):
+    """Exact native-MXFP4 GEMM (float64 of exact per-block int64 sums) and the 1e-5 * sum|ab| bound."""
+    a_codes = np.ascontiguousarray(a_codes, np.uint8)
+    b_codes = np.ascontiguousarray(b_codes, np.uint8)
+    a_sf = np.ascontiguousarray(a_sf, np.uint8)
+    b_sf = np.ascontiguousarray(b_sf, np.uint8)
+    M, half = a_codes.shape
+    N = b_codes.shape[0]
+    rows = np.arange(M, dtype=np.int64) if rows is None else np.ascontiguousarray(rows, np.int64)
+    Y = np.zeros((rows.size, N))
+    Yabs = np.zeros((rows.size, N))
+    lib().or_gemm_mx_native_exact(_p(a_codes), _p(a_sf), _p(b_codes), _p(b_sf), N, 2 * half, _p(rows), rows.size,
+                                  _p(Y), _p(Yabs))
     return Y, 1e-5 * Yabs

@@ -726,6 +726,89 @@ int or_quantize_mx(const uint16_t* x, int64_t M, int K, int64_t ldx, const int32
     return rc;
 }
 
+/* ------------------------------------------------------------------------- */
+/* Native MXFP4-ARC (reading Q25 without the NVFP4-format offset): */
+/* the same 32-block stages as above with the exponent range of UE8M0        */
+/* itself ([-127, 127]: no offset, nothing clamped in practice), stored as   */
+/* the MX physical format of tcgen05 kind::mxf4 -- packed E2M1 codes and one */
+/* UE8M0 byte (e + 127; an all-zero block 0) per 32-block, the App.D block    */
+/* map at 32-element granularity (interleaved: outlier 32-block j -> 2j, its */
+/* residual -> 2j+1), K+S padded to Kpm = roundup(K+S, 128), scales in the    */
+/* 128x4 tile layout with Kpm/32 columns.                                     */
+/* ------------------------------------------------------------------------- */
+int64_t or_kpm(int K, int S) { return ((int64_t)K + S + 127) / 128 * 128; }
+
+int or_quantize_mx_native(const uint16_t* x, int64_t M, int K, int64_t ldx, const int32_t* perm, int S, int weight,
+                          int layout, uint8_t* codes, uint8_t* sf) {
+    if (K <= 0 || K % 32 || S < 0 || S % 32 || S > K || M < 0 || ldx < K) return OR_ERR_SHAPE;
+    const int64_t Kpm = or_kpm(K, S);
+    const int nb = K / 32, ns = S / 32, nphys = (int)(Kpm / 32);
+    for (int64_t m = 0; m < M; ++m)
+        for (int j = 0; j < K; ++j)
+            if (!isfinite(bf16_to_f32(x[m * ldx + j]))) return OR_ERR_NONFINITE;
+    #pragma omp parallel for schedule(static)
+    for (int64_t m = 0; m < M; ++m) {
+        uint8_t* crow = codes + m * (Kpm / 2);
+        memset(crow, 0, (size_t)(Kpm / 2));
+        for (int pb = 0; pb < nphys; ++pb) sf[or_sf_offset(m, pb, Kpm / 2)] = 0;
+        for (int b = 0; b < nb; ++b) {
+            float z[32], t[32], r[32], u[32];
+            uint8_t q[32], q2[32];
+            int e, e2;
+            for (int i = 0; i < 32; ++i) z[i] = bf16_to_f32(x[m * ldx + perm[32 * b + i]]);
+            mx_stage(z, -127, 127, t, q, &e);
+            const int pp = layout == 1 ? b : (b < ns ? 2 * b : b + ns);   /* physical primary block */
+            for (int i = 0; i < 32; i += 2) crow[pp * 16 + i / 2] = (uint8_t)(q[i] | (q[i + 1] << 4));
+            sf[or_sf_offset(m, pp, Kpm / 2)] = e == INT32_MIN ? 0 : (uint8_t)(e + 127);
+            if (b < ns) {
+                const int pr = layout == 1 ? nb + b : 2 * b + 1;               /* physical residual block */
+                uint8_t s2 = 0;
+                if (weight) {                                                  /* duplicate */
+                    memcpy(q2, q, 32);
+                    s2 = e == INT32_MIN ? 0 : (uint8_t)(e + 127);
+                } else {
+                    for (int i = 0; i < 32; ++i) r[i] = t[i] - or_e2m1_value(q[i]);   /* exact */
+                    if (e == INT32_MIN) mx_stage(r, 0, 0, u, q2, &e2);
+                    else mx_stage(r, -127 - e, 127 - e, u, q2, &e2);
+                    s2 = (e != INT32_MIN && e2 != INT32_MIN) ? (uint8_t)(e + e2 + 127) : 0;
+                }
+                for (int i = 0; i < 32; i += 2) crow[pr * 16 + i / 2] = (uint8_t)(q2[i] | (q2[i + 1] << 4));
+                sf[or_sf_offset(m, pr, Kpm / 2)] = s2;
+            }
+        }
+    }
+    return OR_OK;
+}
+
+/* Exact native-MX GEMM: per 32-block the int64 sum of V_a V_b (V = 2 e2m1, an integer) scaled by
+ * 2^(ea + eb - 254 - 2) in double; |.| sums for the bound.  Y, Yabs: [nrows][N]. */
+void or_gemm_mx_native_exact(const uint8_t* a_codes, const uint8_t* a_sf, const uint8_t* b_codes, const uint8_t* b_sf,
+                             int64_t N, int64_t Kpm, const int64_t* rows, int64_t nrows, double* Y, double* Yabs) {
+    #pragma omp parallel for schedule(static)
+    for (int64_t n = 0; n < N; ++n) {
+        for (int64_t ri = 0; ri < nrows; ++ri) {
+            const int64_t r = rows[ri];
+            double acc = 0.0, aabs = 0.0;
+            for (int64_t b = 0; b < Kpm / 32; ++b) {
+                int64_t s = 0, sa = 0;
+                for (int i = 0; i < 32; ++i) {
+                    const int64_t p = b * 32 + i;
+                    const uint8_t ab = a_codes[r * (Kpm / 2) + p / 2], bb = b_codes[n * (Kpm / 2) + p / 2];
+                    const int64_t va = (int64_t)(2.0f * or_e2m1_value((p & 1) ? (ab >> 4) : (ab & 15)));
+                    const int64_t vb = (int64_t)(2.0f * or_e2m1_value((p & 1) ? (bb >> 4) : (bb & 15)));
+                    s += va * vb;
+                    sa += va * vb < 0 ? -va * vb : va * vb;
+                }
+                const int e = (int)a_sf[or_sf_offset(r, b, Kpm / 2)] + (int)b_sf[or_sf_offset(n, b, Kpm / 2)] - 254 - 2;
+                acc += ldexp((double)s, e);
+                aabs += ldexp((double)sa, e);
+            }
+            Y[ri * N + n] = acc;
+            Yabs[ri * N + n] = aabs;
+        }
+    }
+}
+
 /* tensor offset c for a tensor whose largest |value| is amax: the largest block scale
  * E8M0_up(amax/6) = 2^E maps to 2^8 (E4M3's largest power of two): c = E - 8; amax = 0 -> 0 */
 int or_mx_offset(float amax) { return amax > 0.0f ? mx_ceil_log2(amax / 6.0f) - 8 : 0; }

@@ -169,3 +169,78 @@ def test_out_of_range_residual_clamped():
     # in-range block 1: primary + residual within half a residual quantum of x (Q25's definition)
     rec = vals[0, 32:64] + vals[0, 96:128]
     assert np.all(np.abs(rec - xf[32:]) <= scales[0, 96:128] * 0.5 + 1e-9 * np.abs(xf[32:]))
+
+
+# ----------------------------------------------------------------------------- native MX format (f3)
+def _decode_native(codes, sf, rows, K, S, layout=0):
+    """Logical values (K+S per row) of the native MX physical format, from the documented map: 32-block
+    l -> physical 2l / l+ns / 2(l-nb)+1 (interleaved) or l (contiguous), UE8M0 byte b -> 2^(b-127)."""
+    Km = oracle.kpm(K, S)
+    nb, ns = K // 32, S // 32
+    vals = np.zeros((rows, K + S))
+    for m in range(rows):
+        for lb in range((K + S) // 32):
+            if layout == 1:
+                pb = lb
+            else:
+                pb = 2 * lb if lb < ns else (lb + ns if lb < nb else 2 * (lb - nb) + 1)
+            d = 2.0 ** (int(sf[oracle.sf_offset(m, pb, Km // 2)]) - 127)
+            for i in range(32):
+                byte = codes[m, (32 * pb + i) // 2]
+                q = (byte >> (4 * ((32 * pb + i) % 2))) & 15
+                vals[m, 32 * lb + i] = E2M1[q & 7] * (-1 if q & 8 else 1) * d
+    return vals
+
+
+@pytest.mark.parametrize("layout", [0, 1])
+@pytest.mark.parametrize("weight", [False, True])
+def test_native_equals_nvfp4_format_in_range(layout, weight):
+    """Within the offset's 18 binades the native MX format (UE8M0 per 32-block) and the NVFP4-format MX
+    representation (E4M3 codes of 2^(e-c)) decode to the same values, element by element."""
+    x, perm = _inputs(6, 256, seed=21 + layout)
+    S = 64
+    c = oracle.mx_offset(float(x.float().abs().max()))
+    a, asf = oracle.quantize_mx(x, perm, S, c, weight=weight, layout=layout)
+    v_nv, _ = _decode(a, asf, 6, 256, S, c, layout)
+    n, nsf = oracle.quantize_mx_native(x, perm, S, weight=weight, layout=layout)
+    v_na = _decode_native(n, nsf, 6, 256, S, layout)
+    assert np.array_equal(v_na, v_nv)
+
+
+def test_native_wide_range_is_the_unclamped_definition():
+    """Beyond E4M3's range for any one offset (blocks 2^60 apart) the native format still holds the
+    definition exactly: scale = smallest power of two >= RN(amax/6), codes = nearest E2M1 of x / scale,
+    residual = the same stage on x/scale - v(q)."""
+    x = torch.zeros(2, 128)
+    g = torch.Generator().manual_seed(3)
+    x[:, :32] = torch.randn(2, 32, generator=g) * 2.0 ** 30
+    x[:, 32:64] = torch.randn(2, 32, generator=g) * 2.0 ** -30
+    x[:, 64:] = torch.randn(2, 64, generator=g)
+    xb = x.to(torch.bfloat16)
+    perm = np.arange(128, dtype=np.int32)
+    codes, sf = oracle.quantize_mx_native(xb, perm, 32)
+    vals = _decode_native(codes, sf, 2, 128, 32)
+    xf = xb.float().numpy().astype(np.float64)
+    for m in range(2):
+        for b in range(4):
+            z = xf[m, 32 * b:32 * b + 32]
+            s = 2.0 ** np.ceil(np.log2(np.float32(np.abs(z).max() / np.float32(6.0))))
+            want = _nearest_e2m1(z / s) * s
+            assert np.array_equal(vals[m, 32 * b:32 * b + 32], want), (m, b)
+        # residual of outlier block 0
+        z = xf[m, :32]
+        s = 2.0 ** np.ceil(np.log2(np.float32(np.abs(z).max() / np.float32(6.0))))
+        r = z / s - _nearest_e2m1(z / s)
+        s2 = 2.0 ** np.ceil(np.log2(np.float32(np.abs(r).max() / np.float32(6.0))))
+        assert np.array_equal(vals[m, 128:160], _nearest_e2m1(r / s2) * s2 * s)
+
+
+def test_native_gemm_equals_float64_of_decoded():
+    x, perm = _inputs(5, 256, seed=31)
+    w, _ = _inputs(7, 256, seed=32)
+    a, asf = oracle.quantize_mx_native(x, perm, 64)
+    b, bsf = oracle.quantize_mx_native(w, perm, 64, weight=True)
+    y, bound = oracle.gemm_mx_native_reference(a, asf, b, bsf)
+    va = _decode_native(a, asf, 5, 256, 64)
+    vb = _decode_native(b, bsf, 7, 256, 64)
+    assert np.allclose(y, va @ vb.T, rtol=1e-12, atol=1e-300)
