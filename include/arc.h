@@ -224,6 +224,29 @@ ARC_API arc_status_t arc_quantize_weight_mx(const void* w, int64_t N, int64_t K,
                                             int32_t S, const float* gs_w, arc_layout_t layout, uint8_t* codes,
                                             uint8_t* sf, void* stream);
 
+/* ---------------------------------------------------------------- native MXFP4-ARC */
+/* MXFP4-ARC (reading Q25: 32-element blocks, 2^e = E8M0_up(RN(amax/6)), codes rne_e2m1_sat(x 2^-e), the
+ * outlier blocks' exact residual through the same stage, weights duplicate their outlier blocks) in the
+ * native MX physical format of tcgen05 kind::mxf4: one UE8M0 scale byte (e + 127; an all-zero block 0)
+ * per 32-element block -- the full E8M0 exponent range, no tensor offset (contrast arc_quantize_*_mx,
+ * which stores MX in the NVFP4 format within an offset's 18 binades, reading Q25b).  Block map: App.D
+ * at 32-element granularity (interleaved: outlier 32-block j -> physical 2j, its residual 2j+1); K+S is
+ * padded to Kpm = roundup(K+S, 128) with zero blocks.  codes: [rows][Kpm/2] (element 2i in the low
+ * nibble of byte i); sf: roundup(rows, 128) * Kpm / 32 bytes in the 128x4 tile layout.  K and S must be
+ * multiples of 32; perm as arc_quantize_activation. */
+ARC_API arc_status_t arc_mx_native_buffer_sizes(int64_t rows, int64_t K, int32_t S, int64_t* Kpm, size_t* code_bytes,
+                                                size_t* sf_bytes);
+ARC_API arc_status_t arc_quantize_mx_native(const void* x, int64_t rows, int64_t K, int64_t ldx, const int32_t* perm,
+                                            int32_t S, int32_t weight, arc_layout_t layout, uint8_t* codes,
+                                            uint8_t* sf, void* stream);
+/* y[M][N] = A B^T of two native MXFP4 operands with the same K, S and layout (tcgen05 kind::mxf4
+ * block_scale scale_vec::2X, UE8M0, FP32 accumulation; no tensor scale).  ws as arc_gemm_mxfp8
+ * (arc_gemm_mx_native_workspace_size). */
+ARC_API arc_status_t arc_gemm_mx_native_workspace_size(int64_t M, int64_t N, int64_t Kpm, size_t* bytes);
+ARC_API arc_status_t arc_gemm_mx_native(const uint8_t* a_codes, const uint8_t* a_sf, int64_t M, const uint8_t* b_codes,
+                                        const uint8_t* b_sf, int64_t N, int64_t Kpm, void* y, arc_dtype_t y_dtype,
+                                        int64_t ldy, void* ws, size_t ws_bytes, void* stream);
+
 /* ---------------------------------------------------------------- Fig.8a comparator: plain MXFP8 */
 /* The MXFP8 format the paper compares ARC's kernel against (Eq.3's single stage,
  * P:181-184): per 32-element block of a row, scale 2^e = the smallest power of two >= RN(amax/448)

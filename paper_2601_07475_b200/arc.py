@@ -94,6 +94,11 @@ _sig("arc_quantize_activation_mx", [_P, _i64, _i64, ctypes.POINTER(ArcProfile), 
 _sig("arc_quantize_weight_mx", [_P, _i64, _i64, _i64, _P, _i32, _P, ctypes.c_int, _P, _P, _P])
 _sig("arc_gemm_reduce", [_P, _P, _P, _i64, ctypes.POINTER(ArcQWeight), ctypes.POINTER(ArcReduce), _i64, _P,
                          ctypes.c_size_t, _P])
+_sig("arc_mx_native_buffer_sizes", [_i64, _i64, _i32, ctypes.POINTER(_i64), ctypes.POINTER(ctypes.c_size_t),
+                                    ctypes.POINTER(ctypes.c_size_t)])
+_sig("arc_quantize_mx_native", [_P, _i64, _i64, _i64, _P, _i32, _i32, ctypes.c_int, _P, _P, _P])
+_sig("arc_gemm_mx_native_workspace_size", [_i64, _i64, _i64, ctypes.POINTER(ctypes.c_size_t)])
+_sig("arc_gemm_mx_native", [_P, _P, _i64, _P, _P, _i64, _i64, _P, ctypes.c_int, _i64, _P, ctypes.c_size_t, _P])
 _sig("arc_mxfp8_buffer_sizes", [_i64, _i64, ctypes.POINTER(_i64), ctypes.POINTER(ctypes.c_size_t),
                                 ctypes.POINTER(ctypes.c_size_t)])
 _sig("arc_quantize_mxfp8", [_P, _i64, _i64, _i64, _P, _P, _P])
@@ -123,6 +128,7 @@ EXPORTED = [
     "arc_linear_hostio_workspace_size", "arc_rmsnorm",
     "arc_rmsnorm_quantize_activation", "arc_linear_rmsnorm", "arc_linear_hostio",
     "arc_silu_mul", "arc_silu_mul_quantize_activation", "arc_linear_silu_mul", "arc_gemm_swiglu", "arc_gemm_reduce",
+    "arc_mx_native_buffer_sizes", "arc_quantize_mx_native", "arc_gemm_mx_native_workspace_size", "arc_gemm_mx_native",
     "arc_mxfp8_buffer_sizes", "arc_quantize_mxfp8", "arc_gemm_mxfp8_workspace_size", "arc_gemm_mxfp8",
     "arc_mx_tensor_scale", "arc_mx_tensor_scale_device", "arc_quantize_activation_mx", "arc_quantize_weight_mx", "arc_gather_order_ex",
     "arc_probe_e2m1", "arc_probe_e2m1_bits", "arc_probe_e2m1_raw_bits", "arc_probe_e4m3_ceil", "arc_probe_silu",
@@ -683,4 +689,38 @@ def gemm_mxfp8(a_codes, a_sf, b_codes, b_sf, K: int, out_dtype=torch.bfloat16, o
     _check(_lib.arc_gemm_mxfp8(_ptr(a_codes), _ptr(a_sf), M, _ptr(b_codes), _ptr(b_sf), N, K, _ptr(out),
                                _dtype_code(out.dtype), out.stride(0), _ptr(buf), 0 if buf is None else buf.numel(),
                                _stream(stream)), "arc_gemm_mxfp8")
+    return out
+
+
+# ----------------------------------------------------------------------------- native MXFP4-ARC (f3)
+def quantize_mx_native(x: torch.Tensor, prof: "Profile", weight: bool = False, stream=None):
+    """Native MXFP4-ARC (arc.h arc_quantize_mx_native): codes [rows][Kpm/2], UE8M0 scales (128x4 tile layout)."""
+    assert x.dtype == torch.bfloat16 and x.is_cuda and x.dim() == 2 and x.shape[1] == prof.K
+    rows, K = x.shape
+    km, cb, sb = _i64(), ctypes.c_size_t(), ctypes.c_size_t()
+    _check(_lib.arc_mx_native_buffer_sizes(rows, K, prof.S, ctypes.byref(km), ctypes.byref(cb), ctypes.byref(sb)),
+           "arc_mx_native_buffer_sizes")
+    codes = torch.empty(rows, km.value // 2, dtype=torch.uint8, device=x.device)
+    sf = torch.empty(sb.value, dtype=torch.uint8, device=x.device)
+    _check(_lib.arc_quantize_mx_native(_ptr(x), rows, K, x.stride(0), _ptr(prof.perm), prof.S, int(bool(weight)),
+                                       prof.layout, _ptr(codes), _ptr(sf), _stream(stream)), "arc_quantize_mx_native")
+    return codes, sf
+
+
+def gemm_mx_native(a_codes, a_sf, b_codes, b_sf, out_dtype=torch.bfloat16, out=None, ws: Workspace = None,
+                   stream=None):
+    """arc_gemm_mx_native: y = A B^T of two native MXFP4-ARC operands (tcgen05 kind::mxf4 scale_vec::2X)."""
+    M, N, Kpm = a_codes.shape[0], b_codes.shape[0], 2 * a_codes.shape[1]
+    if out is None:
+        out = _alloc_out(M, N, out_dtype, a_codes.device)
+    b = ctypes.c_size_t()
+    _check(_lib.arc_gemm_mx_native_workspace_size(M, N, Kpm, ctypes.byref(b)), "arc_gemm_mx_native_workspace_size")
+    buf = None
+    if b.value:
+        if ws is None:
+            ws = _default_workspace("gemm", a_codes.device, stream)
+        buf = ws.get(b.value)
+    _check(_lib.arc_gemm_mx_native(_ptr(a_codes), _ptr(a_sf), M, _ptr(b_codes), _ptr(b_sf), N, Kpm, _ptr(out),
+                                   _dtype_code(out.dtype), out.stride(0), _ptr(buf), 0 if buf is None else buf.numel(),
+                                   _stream(stream)), "arc_gemm_mx_native")
     return out

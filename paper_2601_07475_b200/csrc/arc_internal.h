@@ -44,6 +44,9 @@ cudaError_t launch_silu_mul(const void* gu, int64_t rows, int K, int64_t ld, int
                             cudaStream_t s);
 cudaError_t launch_rmsnorm(const void* x, int64_t rows, int K, int64_t ldx, const void* gamma, float eps, void* y,
                            int64_t ldy, cudaStream_t s);
+// Native MXFP4-ARC (UE8M0 per 32-block, 32-granular block map, Kpm = roundup(K+S, 128)).
+cudaError_t launch_mx_native_quant(const void* x, int64_t rows, int K, int S, int64_t ld, const int32_t* perm,
+                                   int weight, int layout, uint8_t* codes, uint8_t* sf, cudaStream_t stream);
 // Fig.8a comparator: plain MXFP8 (E4M3 codes [rows][roundup(K,128)], E8M0 scales per 32-block).
 cudaError_t launch_mxfp8_quant(const void* x, int64_t rows, int K, int64_t ld, uint8_t* codes, uint8_t* sf,
                                cudaStream_t stream);
@@ -73,7 +76,8 @@ struct GemmProblem {
   int weights_ready = 0;
   // fused row-parallel reduction (arc_gemm_reduce): 1 = NVLS multimem.red into red_mc, 2 = red.add into the
   // red_np peer buffers; fp32 output only, the 1-SM kernel and the split-K reduce kernel
-  int fmt = 0;       // 0: NVFP4 ARC operands (Kp = K+S padded to 64); 1: plain MXFP8 (Fig.8a comparator, Kp % 128 == 0)
+  int fmt = 0;       // 0: NVFP4 ARC operands (Kp = K+S padded to 64); 1: plain MXFP8 (Fig.8a comparator, Kp % 128 == 0);
+                     // 2: native MXFP4 (UE8M0 per 32, Kp % 128 == 0)
   int red_mode = 0;
   int red_np = 0;
   float* red_mc = nullptr;

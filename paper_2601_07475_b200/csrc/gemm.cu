@@ -97,6 +97,19 @@ constexpr uint32_t kIdesc = (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17)
 // MXFP8 (Fig.8a comparator): E4M3 x E4M3 (format 0), UE8M0 scales (bit 23), K = 32 per MMA; the SF byte ids
 // (bits 29-30 for A, 4-5 for B) are or-ed in per MMA
 constexpr uint32_t kIdescF8 = (1u << 23) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+// native MXFP4: E2M1 x E2M1 (MXF4 format 1), UE8M0 scales (bit 23), scale_vec::2X (32 elements per scale)
+constexpr uint32_t kIdescMX = (1u << 7) | (1u << 10) | (1u << 23) | ((uint32_t)(BN >> 3) << 17) |
+                              ((uint32_t)(BM >> 4) << 24);
+__device__ __forceinline__ void mma_mxf4_2x(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t accumulate, uint32_t sfa_tmem, uint32_t sfb_tmem) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.scale_vec::2X [%0], %1, %2, %3, [%5], [%6], p;\n\t"
+      "}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(sfa_tmem), "r"(sfb_tmem)
+      : "memory");
+}
 __device__ __forceinline__ void mma_mxf8(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                          uint32_t accumulate, uint32_t sfa_tmem, uint32_t sfb_tmem) {
   asm volatile(
@@ -401,8 +414,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   // FMT 0: NVFP4 (256 K per stage, 4 scale chunks of 64 K, UE4M3 per 16); FMT 1: MXFP8 (the Fig.8a
   // comparison format: 128 E4M3 K per stage, 1 scale chunk of 128 K, UE8M0 per 32).  Both move 128 B per
   // operand row per stage.
-  constexpr int KST = FMT == 0 ? BK : 128;          // K elements per stage
-  constexpr int CPS = FMT == 0 ? 4 : 1;             // scale chunks per stage
+  // FMT 2: native MXFP4 (256 K per stage, 2 scale chunks of 128 K, UE8M0 per 32).
+  constexpr int KST = FMT == 1 ? 128 : BK;          // K elements per stage
+  constexpr int CPS = FMT == 0 ? 4 : (FMT == 1 ? 1 : 2);  // scale chunks per stage
   const int nkb = (Kp + KST - 1) / KST;
   const int kc_total = Kp / (FMT == 0 ? 64 : 128);  // scale chunks per row block
   const int n_rb = (N + 127) / 128;        // 128-row blocks of the B scale buffer
@@ -501,6 +515,28 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const uint32_t sB = sA + A_BYTES;
           const uint32_t sSFA = sB + B_BYTES;
           const uint32_t sSFB = sSFA + SFA_BYTES;
+          if (FMT == 2) {
+            // native MXFP4: two 128-K scale chunks per stage; MMA kk (K = 64) reads bytes 2(kk%2), 2(kk%2)+1 of
+            // chunk kk/2's 32-bit TMEM scale words (byte id in bits 30-31 of the address and in the SF ids)
+            for (int c = 0; c < nk; ++c) {
+              utccp_32x128b_warpx4(tmem + SFA_COL + 4 * c, smem_desc(sSFA + c * 512, 0, 128, kLayoutSwizzleNone));
+              utccp_32x128b_warpx4(tmem + SFB_COL + 8 * c, smem_desc(sSFB + c * 512, 0, 128, kLayoutSwizzleNone));
+              utccp_32x128b_warpx4(tmem + SFB_COL + 8 * c + 4,
+                                   smem_desc(sSFB + 2048 + c * 512, 0, 128, kLayoutSwizzleNone));
+            }
+            const int nmma = min(4, (Kp - kb * KST) / 64);
+            for (int kk = 0; kk < nmma; ++kk) {
+              const uint32_t id = 2u * (uint32_t)(kk & 1);
+              const uint64_t ad = smem_desc(sA + kk * 32, 16, 1024, kLayoutSwizzle128B);
+              const uint64_t bd = smem_desc(sB + kk * 32, 16, 1024, kLayoutSwizzle128B);
+              mma_mxf4_2x(acc, ad, bd, kIdescMX | (id << 29) | (id << 4), (kb != kb0) || (kk != 0),
+                          (tmem + SFA_COL + 4 * (kk >> 1)) | (id << 30), (tmem + SFB_COL + 8 * (kk >> 1)) | (id << 30));
+            }
+            if (CL == 1) tc_commit(&empty[stage]);
+            else tc_commit_mc(&empty[stage], mc_mask);
+            if (++stage == ST) { stage = 0; phase ^= 1; }
+            continue;
+          }
           if (FMT == 1) {
             // one 128-K scale chunk per 128 rows; MMA j (K = 32) reads byte j of each row's 32-bit TMEM scale
             // word: the byte index rides in bits 30-31 of the scale address and in the descriptor's SF ids
@@ -947,7 +983,7 @@ cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t stream, const char** 
     if (sp.ok) return launch_stream_gemm(p, sp, stream, detail);
   }
   // MXFP8 (p.fmt == 1): 128 K per 128-byte stage -> plan as an NVFP4 problem with twice the K
-  GemmPlan pl = plan_gemm(p.M, p.N, p.fmt ? 2 * p.Kp : p.Kp);
+  GemmPlan pl = plan_gemm(p.M, p.N, p.fmt == 1 ? 2 * p.Kp : p.Kp);
   if (p.fmt) {
     pl.pair = 0;
     if (pl.CL > 2) pl.CL = 2;
@@ -978,7 +1014,7 @@ cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t stream, const char** 
   // decode-size M on the 1-SM kernel: a 16/32/64-row A box instead of 128 rows of TMA zero fill
   static const int env_abox = getenv("ARC_GEMM_ABOX") ? atoi(getenv("ARC_GEMM_ABOX")) : 1;
   const int a_rows = (!pl.pair && CL == 1 && env_abox && p.M <= 64) ? (p.M <= 16 ? 16 : p.M <= 32 ? 32 : 64) : BM;
-  const int64_t row_bytes = p.fmt ? p.Kp : p.Kp / 2;
+  const int64_t row_bytes = p.fmt == 1 ? p.Kp : p.Kp / 2;
   if (!make_map(&tmA, p.a_codes, p.M, row_bytes, a_rows) || !make_map(&tmB, p.b_codes, p.N, row_bytes, b_rows) ||
       (pl.pair && (!make_sf_map(&tmSFA, p.a_sf, (p.M + 127) / 128, p.Kp / 64, 4, 1) ||
                    !make_sf_map(&tmSFB, p.b_sf, (p.N + 127) / 128, p.Kp / 64, CL == 2 ? 4 : 2, 1)))) {
@@ -998,6 +1034,12 @@ cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t stream, const char** 
                                       SMEM_BYTES);
     if (attr_err == cudaSuccess)
       attr_err = cudaFuncSetAttribute(arc_gemm_kernel<2, STAGES, 1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      SMEM_BYTES);
+    if (attr_err == cudaSuccess)
+      attr_err = cudaFuncSetAttribute(arc_gemm_kernel<1, STAGES, 1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      SMEM_BYTES);
+    if (attr_err == cudaSuccess)
+      attr_err = cudaFuncSetAttribute(arc_gemm_kernel<2, STAGES, 1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       SMEM_BYTES);
     if (attr_err == cudaSuccess)
       attr_err = cudaFuncSetAttribute(arc_gemm_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
@@ -1063,8 +1105,10 @@ cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t stream, const char** 
   cudaError_t e = pl.pair ? (CL == 2 ? (st4 ? cudaLaunchKernelEx(&cfg, arc_gemm_pair_kernel<2, 4>, tmA, tmB, tmSFA, tmSFB, tmY, a)
                                                 : cudaLaunchKernelEx(&cfg, arc_gemm_pair_kernel<2, 5>, tmA, tmB, tmSFA, tmSFB, tmY, a))
                                      : cudaLaunchKernelEx(&cfg, arc_gemm_pair_kernel<4, 5>, tmA, tmB, tmSFA, tmSFB, tmY, a))
-                  : (p.fmt && CL == 1) ? cudaLaunchKernelEx(&cfg, arc_gemm_kernel<1, STAGES, 1, 1>, tmA, tmB, tmY, a)
-                  : (p.fmt && CL == 2) ? cudaLaunchKernelEx(&cfg, arc_gemm_kernel<2, STAGES, 1, 1>, tmA, tmB, tmY, a)
+                  : (p.fmt == 1 && CL == 1) ? cudaLaunchKernelEx(&cfg, arc_gemm_kernel<1, STAGES, 1, 1>, tmA, tmB, tmY, a)
+                  : (p.fmt == 1 && CL == 2) ? cudaLaunchKernelEx(&cfg, arc_gemm_kernel<2, STAGES, 1, 1>, tmA, tmB, tmY, a)
+                  : (p.fmt == 2 && CL == 1) ? cudaLaunchKernelEx(&cfg, arc_gemm_kernel<1, STAGES, 1, 2>, tmA, tmB, tmY, a)
+                  : (p.fmt == 2 && CL == 2) ? cudaLaunchKernelEx(&cfg, arc_gemm_kernel<2, STAGES, 1, 2>, tmA, tmB, tmY, a)
                   : CL == 1 ? cudaLaunchKernelEx(&cfg, arc_gemm_kernel<1>, tmA, tmB, tmY, a)
                   : (CL == 2 && wide) ? cudaLaunchKernelEx(&cfg, arc_gemm_kernel<2, 3, 2>, tmA, tmB, tmY, a)
                   : CL == 2 ? cudaLaunchKernelEx(&cfg, arc_gemm_kernel<2>, tmA, tmB, tmY, a)

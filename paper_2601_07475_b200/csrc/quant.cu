@@ -725,6 +725,74 @@ __global__ void arc_finalize_mx_scale_kernel(float* gs) {
   *gs = ldexpf(1.0f, -c);
 }
 
+// Native MXFP4-ARC (reading Q25 with UE8M0's own exponent range): one thread per (row,
+// physical 32-block) of the native MX format -- the App.D block map at 32-element granularity, packed E2M1
+// codes and one UE8M0 byte (e + 127; an all-zero block 0) per block, Kpm = roundup(K+S, 128).  The
+// thread gathers its 32 calibrated channels straight from x (L2), runs the primary stage, and for a
+// residual block the exact residual stage (activations) or the bitwise duplicate (weights).
+__global__ void arc_mx_native_quant_kernel(const uint16_t* __restrict__ x, int64_t rows, int K, int S, int Kpm,
+                                           int64_t ldx, const int32_t* __restrict__ perm, int weight, int layout,
+                                           uint8_t* __restrict__ codes, uint8_t* __restrict__ sf) {
+  pdl_wait();
+  if (!weight) pdl_launch_dependents();
+  const int np = Kpm >> 5, nb = K >> 5, ns = S >> 5;
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= rows * np) return;
+  const int64_t m = idx / np;
+  const int pb = (int)(idx - m * np);
+  int l = -1;
+  bool res = false;
+  if (layout == 0) {
+    if (pb < 2 * ns) { l = pb >> 1; res = (pb & 1) != 0; }
+    else if (pb < nb + ns) l = pb - ns;
+  } else {
+    if (pb < nb) l = pb;
+    else if (pb < nb + ns) { l = pb - nb; res = true; }
+  }
+  uint2 pk[2] = {make_uint2(0u, 0u), make_uint2(0u, 0u)};
+  uint32_t byte = 0;
+  if (l >= 0) {
+    float z[2][16];
+    const int4* pp = reinterpret_cast<const int4*>(perm + 32 * l);
+    const unsigned short* xr = x + m * ldx;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int4 c = __ldg(pp + q);
+      z[q >> 2][4 * (q & 3) + 0] = bf16_bits_to_f32(__ldg(xr + c.x));
+      z[q >> 2][4 * (q & 3) + 1] = bf16_bits_to_f32(__ldg(xr + c.y));
+      z[q >> 2][4 * (q & 3) + 2] = bf16_bits_to_f32(__ldg(xr + c.z));
+      z[q >> 2][4 * (q & 3) + 3] = bf16_bits_to_f32(__ldg(xr + c.w));
+    }
+    const float a = fmaxf(absmax16(z[0]), absmax16(z[1]));
+    int e = 0;
+    if (a != 0.0f) e = min(max(mx_ceil_exp(a), -127), 127);
+    const float k = ldexpf(1.0f, -e);
+    float t[2][16];
+    pk[0] = encode16(z[0], k, t[0]);
+    pk[1] = encode16(z[1], k, t[1]);
+    byte = a != 0.0f ? (uint32_t)(e + 127) : 0u;
+    if (res && !weight) {
+      float ee[2][16];
+      residual16(t[0], pk[0], ee[0]);
+      residual16(t[1], pk[1], ee[1]);
+      const float a2 = fmaxf(absmax16(ee[0]), absmax16(ee[1]));
+      float k2 = 1.0f;
+      byte = 0u;
+      if (a != 0.0f && a2 != 0.0f) {
+        const int ea = min(max(e + mx_ceil_exp(a2), -127), 127);
+        k2 = ldexpf(1.0f, e - ea);
+        byte = (uint32_t)(ea + 127);
+      }
+      pk[0] = encode16(ee[0], k2);
+      pk[1] = encode16(ee[1], k2);
+    }  // weights: the residual block is the bitwise duplicate of the primary
+  }
+  uint4* dst = reinterpret_cast<uint4*>(codes + m * (Kpm >> 1) + pb * 16);
+  *dst = make_uint4(pk[0].x, pk[0].y, pk[1].x, pk[1].y);
+  const int64_t rb = m >> 7;
+  sf[rb * (int64_t)(np >> 2) * 512 + (pb >> 2) * 512 + (m & 31) * 16 + ((m >> 5) & 3) * 4 + (pb & 3)] = (uint8_t)byte;
+}
+
 // Fig.8a comparator: plain MXFP8 of a bf16 matrix -- Eq.3's single stage per 32-block
 // (E8M0 scale = smallest power of two >= RN(amax/448), E4M3 codes RN-even of x / scale), no reordering, no
 // residual; K padded to Kp8 = roundup(K, 128) with zero blocks of scale 1.  One thread per (row, 32-block):
@@ -1052,6 +1120,27 @@ __global__ void __launch_bounds__(128) probe_silu_block_kernel(const uint16_t* g
     for (int q = 0; q < 16; ++q)
       if (b + q < n) out[b + q] = (uint16_t)(__float_as_uint(z[q]) >> 16);
   }
+}
+
+cudaError_t launch_mx_native_quant(const void* x, int64_t rows, int K, int S, int64_t ld, const int32_t* perm,
+                                   int weight, int layout, uint8_t* codes, uint8_t* sf, cudaStream_t stream) {
+  const int Kpm = (K + S + 127) / 128 * 128;
+  const int64_t n = rows * (Kpm / 32);
+  if (n == 0) return cudaSuccess;
+  cudaLaunchConfig_t cfg;
+  memset(&cfg, 0, sizeof(cfg));
+  cfg.gridDim = dim3((unsigned)((n + 127) / 128));
+  cfg.blockDim = dim3(128);
+  cfg.stream = stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, arc_mx_native_quant_kernel, static_cast<const uint16_t*>(x), rows, K, S,
+                                     Kpm, ld, perm, weight, layout, codes, sf);
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
 }
 
 cudaError_t launch_mxfp8_quant(const void* x, int64_t rows, int K, int64_t ld, uint8_t* codes, uint8_t* sf,
