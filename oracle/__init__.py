@@ -127,6 +127,8 @@ def lib():
         L.or_quantize_mx_native.argtypes = [P, i64, i32, i64, P, i32, i32, i32, P, P]
         L.or_gemm_mx_native_exact.restype = None
         L.or_gemm_mx_native_exact.argtypes = [P, P, P, P, i64, i64, P, i64, P, P]
+        L.or_gemm_w4a8_exact.restype = None
+        L.or_gemm_w4a8_exact.argtypes = [P, P, P, P, i64, i64, P, i64, P, P]
         L.or_kp8.restype = i64
         L.or_kp8.argtypes = [i32]
         L.or_quantize_mxfp8.restype = i32
@@ -471,4 +473,20 @@ def gemm_mx_native_reference(a_codes, a_sf, b_codes, b_sf, rows=None):
     Yabs = np.zeros((rows.size, N))
     lib().or_gemm_mx_native_exact(_p(a_codes), _p(a_sf), _p(b_codes), _p(b_sf), N, 2 * half, _p(rows), rows.size,
                                   _p(Y), _p(Yabs))
+    return Y, 1e-5 * Yabs
+
+
+def gemm_w4a8_reference(a_codes, a_sf, b_codes, b_sf, rows=None):
+    """Exact W4A8 GEMM (MXFP8 activations x plain MXFP4 weights) and the 1e-5 * sum|ab| bound."""
+    a_codes = np.ascontiguousarray(a_codes, np.uint8)
+    b_codes = np.ascontiguousarray(b_codes, np.uint8)
+    a_sf = np.ascontiguousarray(a_sf, np.uint8)
+    b_sf = np.ascontiguousarray(b_sf, np.uint8)
+    M, K8 = a_codes.shape
+    N = b_codes.shape[0]
+    assert b_codes.shape[1] * 2 == K8
+    rows = np.arange(M, dtype=np.int64) if rows is None else np.ascontiguousarray(rows, np.int64)
+    Y = np.zeros((rows.size, N))
+    Yabs = np.zeros((rows.size, N))
+    lib().or_gemm_w4a8_exact(_p(a_codes), _p(a_sf), _p(b_codes), _p(b_sf), N, K8, _p(rows), rows.size, _p(Y), _p(Yabs))
     return Y, 1e-5 * Yabs

@@ -459,6 +459,37 @@ void or_gemm_mxfp8_exact(const uint8_t* a_codes, const uint8_t* a_sf, const uint
     }
 }
 
+/* Fig.8a W4A8 comparator (MXFP4 weights, MXFP8 activations): exact GEMM of an MXFP8 A
+ * (or_quantize_mxfp8: E4M3 bytes [M][Kp8]) and a plain MXFP4 B (or_quantize_mx_native with S = 0 and
+ * the identity permutation: packed E2M1 [N][Kp8/2]); both UE8M0 scale layouts have Kp8/32 columns.
+ * Per 32-block: int64 sum of (512 e4m3)(2 e2m1) scaled by 2^(ea + eb - 254 - 10). */
+void or_gemm_w4a8_exact(const uint8_t* a_codes, const uint8_t* a_sf, const uint8_t* b_codes, const uint8_t* b_sf,
+                        int64_t N, int64_t Kp8, const int64_t* rows, int64_t nrows, double* Y, double* Yabs) {
+    #pragma omp parallel for schedule(static)
+    for (int64_t n = 0; n < N; ++n) {
+        for (int64_t ri = 0; ri < nrows; ++ri) {
+            const int64_t r = rows[ri];
+            double acc = 0.0, aabs = 0.0;
+            for (int64_t b = 0; b < Kp8 / 32; ++b) {
+                int64_t s = 0, sa = 0;
+                for (int i = 0; i < 32; ++i) {
+                    const int64_t p = b * 32 + i;
+                    const int64_t va = (int64_t)(512.0f * or_e4m3_value(a_codes[r * Kp8 + p]));
+                    const uint8_t bb = b_codes[n * (Kp8 / 2) + p / 2];
+                    const int64_t vb = (int64_t)(2.0f * or_e2m1_value((p & 1) ? (bb >> 4) : (bb & 15)));
+                    s += va * vb;
+                    sa += va * vb < 0 ? -va * vb : va * vb;
+                }
+                const int e = (int)a_sf[or_sf_offset(r, b, Kp8 / 2)] + (int)b_sf[or_sf_offset(n, b, Kp8 / 2)] - 254 - 10;
+                acc += ldexp((double)s, e);
+                aabs += ldexp((double)sa, e);
+            }
+            Y[ri * N + n] = acc;
+            Yabs[ri * N + n] = aabs;
+        }
+    }
+}
+
 /* Threads the OpenMP build uses (1 in the plain build). */
 #ifdef _OPENMP
 #include <omp.h>

@@ -72,3 +72,23 @@ def test_gemm_exact_equals_float64_of_decoded():
         y2, _ = oracle.gemm_mxfp8_reference(a, asf, b, bsf)
         a2, asf2 = oracle.quantize_mxfp8(_x(M, K, seed=1))
     assert np.array_equal(y, y2) and np.array_equal(a, a2) and np.array_equal(asf, asf2)
+
+
+def test_w4a8_gemm_exact_equals_float64_of_decoded():
+    """Fig.8a W4A8 comparator: MXFP8 activations x plain MXFP4 weights (native MX format, S = 0,
+    identity order); the exact GEMM equals float64 dot products of the independently decoded operands."""
+    M, N, K = 5, 7, 288
+    a, asf = oracle.quantize_mxfp8(_x(M, K, seed=3))
+    w = _x(N, K, seed=4)
+    b, bsf = oracle.quantize_mx_native(w, np.arange(K, dtype=np.int32), 0, weight=True)
+    K8 = oracle.kp8(K)
+    assert oracle.kpm(K, 0) == K8
+    y, bound = oracle.gemm_w4a8_reference(a, asf, b, bsf)
+    va, _ = _decode(a, asf, M, K8)
+    E2M1 = np.array([0.0, 0.5, 1.0, 1.5, 2.0, 3.0, 4.0, 6.0])
+    vb = np.zeros((N, K8))
+    for n in range(N):
+        for p in range(K8):
+            q = (b[n, p // 2] >> (4 * (p % 2))) & 15
+            vb[n, p] = E2M1[q & 7] * (-1 if q & 8 else 1) * 2.0 ** (int(bsf[oracle.sf_offset(n, p // 32, K8 // 2)]) - 127)
+    assert np.allclose(y, va @ vb.T, rtol=1e-12, atol=1e-300)
