@@ -263,6 +263,13 @@ ARC_API arc_status_t arc_quantize_mxfp8(const void* x, int64_t rows, int64_t K, 
  * K = 32 per MMA, UE8M0 scales), stored as y_dtype (ldy as arc_gemm).  ws: arc_gemm_mxfp8_workspace_size
  * bytes (decode-size M splits K), zero before first use. */
 ARC_API arc_status_t arc_gemm_mxfp8_workspace_size(int64_t M, int64_t N, int64_t K, size_t* bytes);
+/* The Fig.8a W4A8 comparator (MXFP4 weights, MXFP8 activations): a from arc_quantize_mxfp8
+ * ([M][Kp8]), b a plain MXFP4 weight from arc_quantize_mx_native with S = 0 and the identity permutation
+ * ([N][Kp8/2] packed E2M1, UE8M0 per 32; Kpm == Kp8); y = A B^T on tcgen05 kind::mxf8f6f4 (E4M3 x E2M1,
+ * the weight landing as one byte per element in shared memory).  Workspace as arc_gemm_mxfp8. */
+ARC_API arc_status_t arc_gemm_w4a8(const uint8_t* a_codes, const uint8_t* a_sf, int64_t M, const uint8_t* b_codes,
+                                   const uint8_t* b_sf, int64_t N, int64_t K, void* y, arc_dtype_t y_dtype, int64_t ldy,
+                                   void* ws, size_t ws_bytes, void* stream);
 ARC_API arc_status_t arc_gemm_mxfp8(const uint8_t* a_codes, const uint8_t* a_sf, int64_t M, const uint8_t* b_codes,
                                     const uint8_t* b_sf, int64_t N, int64_t K, void* y, arc_dtype_t y_dtype,
                                     int64_t ldy, void* ws, size_t ws_bytes, void* stream);

@@ -24,6 +24,12 @@ ARC_API arc_status_t arc_probe_e4m3_ceil(const float* in, int64_t n, uint8_t* ou
 /* out[i] = the bf16 pattern of bf16(SiLU(g[i])) as the fused SiLU-mul quantize kernel computes
  * it (per-CTA table + closed-form tails, reading Q24), for bf16 patterns g[i]. */
 ARC_API arc_status_t arc_probe_silu(const uint16_t* g, int64_t n, uint16_t* out, void* stream);
+/* TMA layout probe for the W4A8 comparator (tests only): loads a rows x 128-element box of packed
+ * E2M1 codes `src` (device, rows*64 bytes, row-major) through a CU_TENSOR_MAP_DATA_TYPE_16U4_ALIGN16B
+ * map into two shared-memory buffers whose mbarriers expect rows*64 and rows*128 transaction bytes;
+ * status[0..1] (device int32) = whether each barrier completed within a bounded wait; out (device,
+ * 16384 bytes) = both 8 KB buffers (0xEE = untouched). Synchronous; rows in [1, 64]. */
+ARC_API arc_status_t arc_probe_u4_unpack(const uint8_t* src, int64_t rows, uint8_t* out, int32_t* status);
 /* Timing experiments only: with env ARC_STREAM_TRACE set, the decode-size stream-K GEMM records 8
  * globaltimer stamps per CTA of its last launch (entry, early weight loads issued,
  * griddepcontrol.wait passed, first stage ready, last MMA issued, last segment's accumulator

@@ -103,6 +103,7 @@ _sig("arc_mxfp8_buffer_sizes", [_i64, _i64, ctypes.POINTER(_i64), ctypes.POINTER
                                 ctypes.POINTER(ctypes.c_size_t)])
 _sig("arc_quantize_mxfp8", [_P, _i64, _i64, _i64, _P, _P, _P])
 _sig("arc_gemm_mxfp8_workspace_size", [_i64, _i64, _i64, ctypes.POINTER(ctypes.c_size_t)])
+_sig("arc_gemm_w4a8", [_P, _P, _i64, _P, _P, _i64, _i64, _P, ctypes.c_int, _i64, _P, ctypes.c_size_t, _P])
 _sig("arc_gemm_mxfp8", [_P, _P, _i64, _P, _P, _i64, _i64, _P, ctypes.c_int, _i64, _P, ctypes.c_size_t, _P])
 _sig("arc_gemm_swiglu", [_P, _P, _P, _i64, ctypes.POINTER(ArcQWeight), _P, _i64, _P, ctypes.c_size_t, _P])
 _sig("arc_silu_mul", [_P, _i64, _i64, _i64, _i64, _P, _i64, _P])
@@ -118,6 +119,7 @@ _sig("arc_probe_e2m1_bits", [ctypes.c_uint32, _i64, _P, _P])
 _sig("arc_probe_e2m1_raw_bits", [ctypes.c_uint32, _i64, _P, _P])
 _sig("arc_probe_e4m3_ceil", [_P, _i64, _P, _P])
 _sig("arc_probe_silu", [_P, _i64, _P, _P])
+_sig("arc_probe_u4_unpack", [_P, _i64, _P, _P])
 
 # every symbol include/arc.h and include/arc_probe.h declare (checked by tests)
 EXPORTED = [
@@ -129,9 +131,10 @@ EXPORTED = [
     "arc_rmsnorm_quantize_activation", "arc_linear_rmsnorm", "arc_linear_hostio",
     "arc_silu_mul", "arc_silu_mul_quantize_activation", "arc_linear_silu_mul", "arc_gemm_swiglu", "arc_gemm_reduce",
     "arc_mx_native_buffer_sizes", "arc_quantize_mx_native", "arc_gemm_mx_native_workspace_size", "arc_gemm_mx_native",
-    "arc_mxfp8_buffer_sizes", "arc_quantize_mxfp8", "arc_gemm_mxfp8_workspace_size", "arc_gemm_mxfp8",
+    "arc_mxfp8_buffer_sizes", "arc_quantize_mxfp8", "arc_gemm_mxfp8_workspace_size", "arc_gemm_mxfp8", "arc_gemm_w4a8",
     "arc_mx_tensor_scale", "arc_mx_tensor_scale_device", "arc_quantize_activation_mx", "arc_quantize_weight_mx", "arc_gather_order_ex",
     "arc_probe_e2m1", "arc_probe_e2m1_bits", "arc_probe_e2m1_raw_bits", "arc_probe_e4m3_ceil", "arc_probe_silu",
+    "arc_probe_u4_unpack",
     "arc_debug_stream_trace",
 ]
 
@@ -650,6 +653,15 @@ def probe_e4m3_ceil(x: torch.Tensor) -> torch.Tensor:
     return out
 
 
+def probe_u4_unpack(packed: torch.Tensor):
+    """(status[2], smem bytes[2, 8192]) of the 16U4_ALIGN16B TMA layout probe (arc_probe.h)."""
+    rows = packed.shape[0]
+    out = torch.empty(16384, dtype=torch.uint8, device=packed.device)
+    st = torch.zeros(2, dtype=torch.int32, device=packed.device)
+    _check(_lib.arc_probe_u4_unpack(_ptr(packed), rows, _ptr(out), _ptr(st)), "arc_probe_u4_unpack")
+    return st.cpu(), out.view(2, 8192).cpu()
+
+
 def probe_silu(g_bits: torch.Tensor) -> torch.Tensor:
     """bf16 patterns of bf16(SiLU(g)) as the fused SiLU-mul quantize kernel computes them
     (g_bits: int16/uint16-viewed bf16 patterns on the device)."""
@@ -723,4 +735,24 @@ def gemm_mx_native(a_codes, a_sf, b_codes, b_sf, out_dtype=torch.bfloat16, out=N
     _check(_lib.arc_gemm_mx_native(_ptr(a_codes), _ptr(a_sf), M, _ptr(b_codes), _ptr(b_sf), N, Kpm, _ptr(out),
                                    _dtype_code(out.dtype), out.stride(0), _ptr(buf), 0 if buf is None else buf.numel(),
                                    _stream(stream)), "arc_gemm_mx_native")
+    return out
+
+
+def gemm_w4a8(a_codes, a_sf, b_codes, b_sf, K: int, out_dtype=torch.bfloat16, out=None, ws: Workspace = None,
+              stream=None):
+    """arc_gemm_w4a8: MXFP8 activations (quantize_mxfp8) x plain MXFP4 weights (quantize_mx_native with S = 0,
+    identity order) -- the Fig.8a W4A8 comparison GEMM."""
+    M, N = a_codes.shape[0], b_codes.shape[0]
+    if out is None:
+        out = _alloc_out(M, N, out_dtype, a_codes.device)
+    b = ctypes.c_size_t()
+    _check(_lib.arc_gemm_mxfp8_workspace_size(M, N, K, ctypes.byref(b)), "arc_gemm_mxfp8_workspace_size")
+    buf = None
+    if b.value:
+        if ws is None:
+            ws = _default_workspace("gemm", a_codes.device, stream)
+        buf = ws.get(b.value)
+    _check(_lib.arc_gemm_w4a8(_ptr(a_codes), _ptr(a_sf), M, _ptr(b_codes), _ptr(b_sf), N, K, _ptr(out),
+                              _dtype_code(out.dtype), out.stride(0), _ptr(buf), 0 if buf is None else buf.numel(),
+                              _stream(stream)), "arc_gemm_w4a8")
     return out

@@ -476,6 +476,46 @@ arc_status_t arc_gemm_mx_native(const uint8_t* a_codes, const uint8_t* a_sf, int
   return e == cudaSuccess ? ARC_OK : cuda_fail(e, "arc_gemm_mx_native", detail);
 }
 
+arc_status_t arc_gemm_w4a8(const uint8_t* a_codes, const uint8_t* a_sf, int64_t M, const uint8_t* b_codes,
+                           const uint8_t* b_sf, int64_t N, int64_t K, void* y, arc_dtype_t y_dtype, int64_t ldy, void* ws,
+                           size_t ws_bytes, void* stream) {
+  if (M < 0 || M > (1 << 30) || N <= 0 || N > (1 << 30) || K <= 0 || K % 32) return fail(ARC_ERR_SHAPE, "bad M/N/K");
+  if (M == 0) return ARC_OK;
+  if (!a_codes || !a_sf || !b_codes || !b_sf || !y) return fail(ARC_ERR_NULL, "null operand / y");
+  if (y_dtype != ARC_BF16 && y_dtype != ARC_FP32) return fail(ARC_ERR_SHAPE, "y_dtype must be ARC_BF16 or ARC_FP32");
+  if (ldy < N || ldy % (y_dtype == ARC_FP32 ? 4 : 8)) return fail(ARC_ERR_SHAPE, "ldy must be >= N and a multiple of 16 bytes");
+  if (!aligned16(a_codes) || !aligned16(a_sf) || !aligned16(b_codes) || !aligned16(b_sf) || !aligned16(y))
+    return fail(ARC_ERR_ALIGN, "buffer not 16B aligned");
+  const int64_t k8 = round_up(K, 128);
+  const GemmPlan pl = plan_gemm(M, N, 2 * k8);
+  if (pl.ws_bytes > 0 && (!ws || ws_bytes < pl.ws_bytes)) return fail(ARC_ERR_WORKSPACE, "split-K workspace too small");
+  arc_status_t s = check_device();
+  if (s != ARC_OK) return s;
+  void *cnt, *part;
+  size_t part_bytes;
+  split_gemm_ws(ws, ws_bytes, &cnt, &part, &part_bytes);
+  GemmProblem p;
+  p.M = M;
+  p.N = N;
+  p.Kp = k8;
+  p.a_codes = a_codes;
+  p.a_sf = a_sf;
+  p.b_codes = b_codes;
+  p.b_sf = b_sf;
+  p.gs_x = nullptr;
+  p.gs_w = nullptr;
+  p.y = y;
+  p.ldy = ldy;
+  p.y_fp32 = y_dtype == ARC_FP32;
+  p.cnt = static_cast<unsigned*>(cnt);
+  p.ws = part;
+  p.ws_bytes = part_bytes;
+  p.fmt = 3;
+  const char* detail = nullptr;
+  cudaError_t e = launch_gemm(p, (cudaStream_t)stream, &detail);
+  return e == cudaSuccess ? ARC_OK : cuda_fail(e, "arc_gemm_w4a8", detail);
+}
+
 arc_status_t arc_mxfp8_buffer_sizes(int64_t rows, int64_t K, int64_t* Kp8, size_t* code_bytes, size_t* sf_bytes) {
   if (rows < 0 || K <= 0 || K % 32) return fail(ARC_ERR_SHAPE, "rows >= 0, K > 0, K % 32 == 0 required");
   const int64_t k8 = round_up(K, 128);

@@ -77,7 +77,7 @@ struct GemmProblem {
   // fused row-parallel reduction (arc_gemm_reduce): 1 = NVLS multimem.red into red_mc, 2 = red.add into the
   // red_np peer buffers; fp32 output only, the 1-SM kernel and the split-K reduce kernel
   int fmt = 0;       // 0: NVFP4 ARC operands (Kp = K+S padded to 64); 1: plain MXFP8 (Fig.8a comparator, Kp % 128 == 0);
-                     // 2: native MXFP4 (UE8M0 per 32, Kp % 128 == 0)
+                     // 2: native MXFP4 (UE8M0 per 32, Kp % 128 == 0); 3: W4A8 (MXFP8 A x packed MXFP4 B, Kp % 128 == 0)
   int red_mode = 0;
   int red_np = 0;
   float* red_mc = nullptr;
@@ -124,4 +124,5 @@ bool make_operand_map(CUtensorMap* m, const void* base, int64_t rows, int64_t ro
 constexpr size_t kGemmCounterBytes = 16384;
 inline size_t sync_bytes_of(int64_t /*N*/) { return kGemmCounterBytes; }
 
+bool make_u4_unpack_map_probe(CUtensorMap* m, const uint8_t* base, int64_t rows, int64_t k_elems, int box_rows);
 }  // namespace arc

@@ -97,6 +97,8 @@ constexpr uint32_t kIdesc = (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17)
 // MXFP8 (Fig.8a comparator): E4M3 x E4M3 (format 0), UE8M0 scales (bit 23), K = 32 per MMA; the SF byte ids
 // (bits 29-30 for A, 4-5 for B) are or-ed in per MMA
 constexpr uint32_t kIdescF8 = (1u << 23) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+// W4A8: E4M3 A (format 0) x E2M1 B (MXF8F6F4 format 5, unpacked in shared memory), UE8M0 scales
+constexpr uint32_t kIdescW4A8 = kIdescF8 | (5u << 10);
 // native MXFP4: E2M1 x E2M1 (MXF4 format 1), UE8M0 scales (bit 23), scale_vec::2X (32 elements per scale)
 constexpr uint32_t kIdescMX = (1u << 7) | (1u << 10) | (1u << 23) | ((uint32_t)(BN >> 3) << 17) |
                               ((uint32_t)(BM >> 4) << 24);
@@ -415,8 +417,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   // comparison format: 128 E4M3 K per stage, 1 scale chunk of 128 K, UE8M0 per 32).  Both move 128 B per
   // operand row per stage.
   // FMT 2: native MXFP4 (256 K per stage, 2 scale chunks of 128 K, UE8M0 per 32).
-  constexpr int KST = FMT == 1 ? 128 : BK;          // K elements per stage
-  constexpr int CPS = FMT == 0 ? 4 : (FMT == 1 ? 1 : 2);  // scale chunks per stage
+  // FMT 3: W4A8 (Fig.8a comparator): MXFP8 A x MXFP4 B on the MXFP8 instruction, B landing in
+  // shared memory as one byte per E2M1 element (TMA 16U4_ALIGN16B), so the stage geometry is FMT 1's.
+  constexpr bool F8 = FMT == 1 || FMT == 3;
+  constexpr int KST = F8 ? 128 : BK;                // K elements per stage
+  constexpr int CPS = FMT == 0 ? 4 : (F8 ? 1 : 2);  // scale chunks per stage
   const int nkb = (Kp + KST - 1) / KST;
   const int kc_total = Kp / (FMT == 0 ? 64 : 128);  // scale chunks per row block
   const int n_rb = (N + 127) / 128;        // 128-row blocks of the B scale buffer
@@ -463,7 +468,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           uint8_t* sB = sA + A_BYTES;
           uint8_t* sSFA = sB + B_BYTES;
           uint8_t* sSFB = sSFA + SFA_BYTES;
-          mbar_expect_tx(&full[stage], (uint32_t)(args.a_rows * BKB + B_BYTES + nk * 512 * ((a_ok ? 1 : 0) + nrb)));
+          // FMT 3: a 16U4_ALIGN16B load counts the packed bytes (half of what lands in shared memory:
+          // 8 code bytes + 8 untouched pad bytes per 16 elements; measured by arc_probe_u4_unpack)
+          constexpr uint32_t B_TX = FMT == 3 ? B_BYTES / 2 : B_BYTES;
+          mbar_expect_tx(&full[stage], (uint32_t)(args.a_rows * BKB + B_TX + nk * 512 * ((a_ok ? 1 : 0) + nrb)));
           tma_load_2d(sA, &tmA, &full[stage], kb * BKB, mb * BM, pol);
           if (a_ok) bulk_load(sSFA, args.sfa + ((int64_t)mb * kc_total + kb * CPS) * 512, nk * 512, &full[stage]);
           if (CL == 1) {
@@ -537,7 +545,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             if (++stage == ST) { stage = 0; phase ^= 1; }
             continue;
           }
-          if (FMT == 1) {
+          if (F8) {
             // one 128-K scale chunk per 128 rows; MMA j (K = 32) reads byte j of each row's 32-bit TMEM scale
             // word: the byte index rides in bits 30-31 of the scale address and in the descriptor's SF ids
             utccp_32x128b_warpx4(tmem + SFA_COL, smem_desc(sSFA, 0, 128, kLayoutSwizzleNone));
@@ -547,7 +555,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             for (int j = 0; j < nmma; ++j) {
               const uint64_t ad = smem_desc(sA + j * 32, 16, 1024, kLayoutSwizzle128B);
               const uint64_t bd = smem_desc(sB + j * 32, 16, 1024, kLayoutSwizzle128B);
-              const uint32_t idesc = kIdescF8 | ((uint32_t)j << 29) | ((uint32_t)j << 4);
+              const uint32_t idesc = (FMT == 3 ? kIdescW4A8 : kIdescF8) | ((uint32_t)j << 29) | ((uint32_t)j << 4);
               mma_mxf8(acc, ad, bd, idesc, (kb != kb0) || (j != 0), (tmem + SFA_COL) | ((uint32_t)j << 30),
                        (tmem + SFB_COL) | ((uint32_t)j << 30));
             }
@@ -844,6 +852,21 @@ EncodeTiledFn get_encode_fn() {
   return fn;
 }
 
+// Packed E2M1 rows [rows][k_elems/2] loaded as one byte per element in shared memory (16 elements per
+// 16-byte group, CU_TENSOR_MAP_DATA_TYPE_16U4_ALIGN16B): the W4A8 B operand of kind::mxf8f6f4.  Box 128
+// elements (128 bytes in shared memory) x box_rows, 128B swizzle.
+bool make_u4_unpack_map(CUtensorMap* m, const uint8_t* base, int64_t rows, int64_t k_elems, int box_rows) {
+  EncodeTiledFn enc = get_encode_fn();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)k_elems, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(k_elems / 2)};
+  cuuint32_t box[2] = {128, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_16U4_ALIGN16B, 2, const_cast<uint8_t*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 bool make_map(CUtensorMap* m, const uint8_t* base, int64_t rows, int64_t row_bytes, int box_rows) {
   return make_operand_map(m, base, rows, row_bytes, box_rows, BKB);
 }
@@ -880,6 +903,19 @@ bool make_y_map(CUtensorMap* m, void* y, int64_t rows, int64_t cols, int64_t ldy
 }
 
 }  // namespace
+
+bool make_u4_unpack_map_probe(CUtensorMap* m, const uint8_t* base, int64_t rows, int64_t k_elems, int box_rows) {
+  EncodeTiledFn enc = get_encode_fn();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)k_elems, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(k_elems / 2)};
+  cuuint32_t box[2] = {128, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_16U4_ALIGN16B, 2, const_cast<uint8_t*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 
 bool make_operand_map(CUtensorMap* m, const void* base, int64_t rows, int64_t row_bytes, int box_rows, int box_bytes) {
   EncodeTiledFn enc = get_encode_fn();
@@ -983,7 +1019,7 @@ cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t stream, const char** 
     if (sp.ok) return launch_stream_gemm(p, sp, stream, detail);
   }
   // MXFP8 (p.fmt == 1): 128 K per 128-byte stage -> plan as an NVFP4 problem with twice the K
-  GemmPlan pl = plan_gemm(p.M, p.N, p.fmt == 1 ? 2 * p.Kp : p.Kp);
+  GemmPlan pl = plan_gemm(p.M, p.N, (p.fmt == 1 || p.fmt == 3) ? 2 * p.Kp : p.Kp);
   if (p.fmt) {
     pl.pair = 0;
     if (pl.CL > 2) pl.CL = 2;
@@ -1014,8 +1050,10 @@ cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t stream, const char** 
   // decode-size M on the 1-SM kernel: a 16/32/64-row A box instead of 128 rows of TMA zero fill
   static const int env_abox = getenv("ARC_GEMM_ABOX") ? atoi(getenv("ARC_GEMM_ABOX")) : 1;
   const int a_rows = (!pl.pair && CL == 1 && env_abox && p.M <= 64) ? (p.M <= 16 ? 16 : p.M <= 32 ? 32 : 64) : BM;
-  const int64_t row_bytes = p.fmt == 1 ? p.Kp : p.Kp / 2;
-  if (!make_map(&tmA, p.a_codes, p.M, row_bytes, a_rows) || !make_map(&tmB, p.b_codes, p.N, row_bytes, b_rows) ||
+  const int64_t row_bytes = (p.fmt == 1 || p.fmt == 3) ? p.Kp : p.Kp / 2;
+  const bool b_ok = p.fmt == 3 ? make_u4_unpack_map(&tmB, p.b_codes, p.N, p.Kp, b_rows)
+                               : make_map(&tmB, p.b_codes, p.N, row_bytes, b_rows);
+  if (!make_map(&tmA, p.a_codes, p.M, row_bytes, a_rows) || !b_ok ||
       (pl.pair && (!make_sf_map(&tmSFA, p.a_sf, (p.M + 127) / 128, p.Kp / 64, 4, 1) ||
                    !make_sf_map(&tmSFB, p.b_sf, (p.N + 127) / 128, p.Kp / 64, CL == 2 ? 4 : 2, 1)))) {
     if (detail) *detail = "cuTensorMapEncodeTiled failed";
@@ -1037,6 +1075,12 @@ cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t stream, const char** 
                                       SMEM_BYTES);
     if (attr_err == cudaSuccess)
       attr_err = cudaFuncSetAttribute(arc_gemm_kernel<1, STAGES, 1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      SMEM_BYTES);
+    if (attr_err == cudaSuccess)
+      attr_err = cudaFuncSetAttribute(arc_gemm_kernel<1, STAGES, 1, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      SMEM_BYTES);
+    if (attr_err == cudaSuccess)
+      attr_err = cudaFuncSetAttribute(arc_gemm_kernel<2, STAGES, 1, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       SMEM_BYTES);
     if (attr_err == cudaSuccess)
       attr_err = cudaFuncSetAttribute(arc_gemm_kernel<2, STAGES, 1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1107,6 +1151,8 @@ cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t stream, const char** 
                                      : cudaLaunchKernelEx(&cfg, arc_gemm_pair_kernel<4, 5>, tmA, tmB, tmSFA, tmSFB, tmY, a))
                   : (p.fmt == 1 && CL == 1) ? cudaLaunchKernelEx(&cfg, arc_gemm_kernel<1, STAGES, 1, 1>, tmA, tmB, tmY, a)
                   : (p.fmt == 1 && CL == 2) ? cudaLaunchKernelEx(&cfg, arc_gemm_kernel<2, STAGES, 1, 1>, tmA, tmB, tmY, a)
+                  : (p.fmt == 3 && CL == 1) ? cudaLaunchKernelEx(&cfg, arc_gemm_kernel<1, STAGES, 1, 3>, tmA, tmB, tmY, a)
+                  : (p.fmt == 3 && CL == 2) ? cudaLaunchKernelEx(&cfg, arc_gemm_kernel<2, STAGES, 1, 3>, tmA, tmB, tmY, a)
                   : (p.fmt == 2 && CL == 1) ? cudaLaunchKernelEx(&cfg, arc_gemm_kernel<1, STAGES, 1, 2>, tmA, tmB, tmY, a)
                   : (p.fmt == 2 && CL == 2) ? cudaLaunchKernelEx(&cfg, arc_gemm_kernel<2, STAGES, 1, 2>, tmA, tmB, tmY, a)
                   : CL == 1 ? cudaLaunchKernelEx(&cfg, arc_gemm_kernel<1>, tmA, tmB, tmY, a)

@@ -60,3 +60,40 @@ def test_gemm_mxfp8_vs_oracle(A, M, N, K):
     err = np.abs(got - yref)
     assert (err <= bound).all(), f"{(err > bound).sum()} out of tolerance; worst {np.max(err / np.maximum(bound, 1e-300))}"
     assert torch.equal(y16, y.to(torch.bfloat16))
+
+
+@pytest.mark.parametrize("M,N,K", [(128, 256, 128), (256, 512, 4096), (200, 300, 1056), (16, 4096, 4096),
+                                   (1000, 768, 2048)])
+def test_gemm_w4a8_vs_oracle(A, M, N, K):
+    """The Fig.8a W4A8 comparator (P:312): MXFP8 activations x plain MXFP4 weights on kind::mxf8f6f4 with the
+    weight unpacked to one byte per element by the TMA, within the north_star bound of the oracle's exact
+    W4A8 GEMM; the weights come from arc_quantize_mx_native (S = 0, identity order), bit-exact vs the oracle."""
+    st = synth.Structure(K, 16, seed=N + 7)
+    x = synth.activation(M, K, st, seed=M + 3, device="cuda")
+    w = synth.weight(N, K, seed=N + 5, device="cuda")
+    ac, asf = A.quantize_mxfp8(x)
+    prof = A.profile_from(np.arange(K, dtype=np.int32), 0, 1.0)
+    bc, bsf = A.quantize_mx_native(w, prof, weight=True)
+    obc, obsf = oracle.quantize_mx_native(dev_bits(w), np.arange(K, dtype=np.int32), 0, weight=True)
+    assert np.array_equal(bc.cpu().numpy(), obc)
+    y = A.gemm_w4a8(ac, asf, bc, bsf, K, out_dtype=torch.float32)
+    torch.cuda.synchronize()
+    rows = np.unique(np.concatenate([[0, M - 1], np.arange(0, M, max(1, M // 24))])).astype(np.int64)
+    with oracle.openmp():
+        yref, bound = oracle.gemm_w4a8_reference(ac.cpu().numpy(), asf.cpu().numpy(), obc, obsf, rows=rows)
+    err = np.abs(y.cpu().numpy().astype(np.float64)[rows] - yref)
+    assert (err <= bound).all(), f"{(err > bound).sum()} out of tolerance; worst {np.max(err / np.maximum(bound, 1e-300))}"
+
+
+@pytest.mark.gpu
+def test_u4_unpack_tma_layout(A):
+    """The W4A8 B operand's TMA form (16U4_ALIGN16B): the load completes `rows * 64` (packed) transaction
+    bytes, not the 128 bytes per row it places in shared memory, and each 16-element group lands as its 8
+    packed code bytes at a 16-byte-aligned offset (the kernel's expect_tx and stage geometry rely on both)."""
+    rows = 8
+    g = torch.Generator().manual_seed(5)
+    packed = torch.randint(0, 256, (rows, 64), generator=g, dtype=torch.uint8)
+    st, buf = A.probe_u4_unpack(packed.cuda())
+    assert st.tolist() == [1, 0]
+    sm = buf[0, : rows * 128].view(rows, 8, 16)
+    assert torch.equal(sm[:, :, :8].reshape(rows, 64), packed)
