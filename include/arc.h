@@ -376,12 +376,6 @@ ARC_API arc_status_t arc_linear_ex_workspace_size(int64_t M, const arc_qweight_t
 ARC_API arc_status_t arc_linear_ex(const void* x, int64_t M, int64_t ldx, const arc_profile_t* prof,
                                    const arc_qweight_t* qw, void* y, arc_dtype_t y_dtype, int64_t ldy, void* ws,
                                    size_t ws_bytes, int flags, void* stream);
-/* Decode-size layers: enqueue L2 prefetches of a read-only device buffer -- typically the
- * next linear's weight codes and scales -- so its HBM stream overlaps the current linear's dependent
- * kernels (the 126 MB L2 holds a LLaMA-3-8B layer's largest weight).  A hint: no result, no completion
- * signal; the call keeps stream order (the following kernel still waits for everything before it).
- * ptr and bytes 16-byte aligned (ARC_ERR_ALIGN); bytes = 0 is a no-op. */
-ARC_API arc_status_t arc_prefetch_l2(const void* ptr, size_t bytes, void* stream);
 /* arc_linear on HOST buffers: copies x_host (bf16 [M][K], pinned or pageable) to
  * the device, runs arc_linear, copies y back to y_host ([M][N] of y_dtype) and
  * synchronizes `stream`.  ws must hold arc_linear_hostio_workspace_size bytes. */

@@ -120,7 +120,6 @@ _sig("arc_probe_e2m1_raw_bits", [ctypes.c_uint32, _i64, _P, _P])
 _sig("arc_probe_e4m3_ceil", [_P, _i64, _P, _P])
 _sig("arc_probe_silu", [_P, _i64, _P, _P])
 _sig("arc_probe_u4_unpack", [_P, _i64, _P, _P])
-_sig("arc_prefetch_l2", [_P, ctypes.c_size_t, _P])
 
 # every symbol include/arc.h and include/arc_probe.h declare (checked by tests)
 EXPORTED = [
@@ -135,7 +134,7 @@ EXPORTED = [
     "arc_mxfp8_buffer_sizes", "arc_quantize_mxfp8", "arc_gemm_mxfp8_workspace_size", "arc_gemm_mxfp8", "arc_gemm_w4a8",
     "arc_mx_tensor_scale", "arc_mx_tensor_scale_device", "arc_quantize_activation_mx", "arc_quantize_weight_mx", "arc_gather_order_ex",
     "arc_probe_e2m1", "arc_probe_e2m1_bits", "arc_probe_e2m1_raw_bits", "arc_probe_e4m3_ceil", "arc_probe_silu",
-    "arc_probe_u4_unpack", "arc_prefetch_l2",
+    "arc_probe_u4_unpack",
     "arc_debug_stream_trace",
 ]
 
@@ -610,17 +609,6 @@ def linear_silu_mul(gu: torch.Tensor, prof: Profile, qw: QWeight, up_off: int | 
                                     _ptr(out), _dtype_code(out.dtype), out.stride(0), _ptr(buf), buf.numel(),
                                     _stream(stream)), "arc_linear_silu_mul")
     return out
-
-
-def prefetch_l2(t: torch.Tensor, stream=None):
-    """arc_prefetch_l2 over a contiguous device tensor's bytes."""
-    _check(_lib.arc_prefetch_l2(_ptr(t), t.numel() * t.element_size(), _stream(stream)), "arc_prefetch_l2")
-
-
-def prefetch_weights(qw: "QWeight", stream=None):
-    """L2 prefetch of a quantized weight (codes + scales): issue one linear ahead at decode sizes."""
-    prefetch_l2(qw.codes, stream)
-    prefetch_l2(qw.sf, stream)
 
 
 def linear_hostio_workspace_size(M: int, qw, out_dtype=torch.bfloat16) -> int:

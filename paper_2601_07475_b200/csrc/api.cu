@@ -263,16 +263,6 @@ arc_status_t arc_gather_order_ex(const int32_t* perm_host, int64_t K, int elem_b
   return ARC_OK;
 }
 
-arc_status_t arc_prefetch_l2(const void* ptr, size_t bytes, void* stream) {
-  if (bytes == 0) return ARC_OK;
-  if (!ptr) return fail(ARC_ERR_NULL, "null ptr");
-  if (!aligned16(ptr) || bytes % 16) return fail(ARC_ERR_ALIGN, "ptr / bytes not 16-byte aligned");
-  arc_status_t s = check_device();
-  if (s != ARC_OK) return s;
-  cudaError_t e = launch_prefetch_l2(ptr, bytes, (cudaStream_t)stream);
-  return e == cudaSuccess ? ARC_OK : cuda_fail(e, "arc_prefetch_l2");
-}
-
 arc_status_t arc_tensor_scale(const void* x, int64_t rows, int64_t K, int64_t ldx, float* gs_out, void* stream) {
   if (!x || !gs_out) return fail(ARC_ERR_NULL, "null x / gs_out");
   if (K <= 0 || K % 16 || rows < 0 || ldx < K || ldx % 8) return fail(ARC_ERR_SHAPE, "bad rows/K/ldx");

@@ -124,6 +124,5 @@ bool make_operand_map(CUtensorMap* m, const void* base, int64_t rows, int64_t ro
 constexpr size_t kGemmCounterBytes = 16384;
 inline size_t sync_bytes_of(int64_t /*N*/) { return kGemmCounterBytes; }
 
-cudaError_t launch_prefetch_l2(const void* ptr, size_t bytes, cudaStream_t stream);
 bool make_u4_unpack_map_probe(CUtensorMap* m, const uint8_t* base, int64_t rows, int64_t k_elems, int box_rows);
 }  // namespace arc
