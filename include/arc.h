@@ -362,8 +362,12 @@ ARC_API arc_status_t arc_linear(const void* x, int64_t M, int64_t ldx, const arc
 
 /* How arc_linear_ex runs the layer:
  *  ARC_LINEAR_UNFUSED: two kernels chained by programmatic dependent launch -- arc_quantize_activation
- *    into the workspace, then arc_gemm (decode-size M: split-K + a fixed-order reduction kernel).
- *  ARC_LINEAR_AUTO: FUSED at M <= 4, UNFUSED otherwise (the faster of the two on B200).
+ *    into the workspace, then arc_gemm.  At decode-size M (<= 64) the quantize is a direct-gather kernel
+ *    and the GEMM a cluster split-K kernel whose K partials are summed in distributed shared memory in a
+ *    fixed rank order (no fp32 partials in HBM, no second kernel); both read the calibration constants
+ *    (perm) and the prepared weights before griddepcontrol.wait, so these -- like every library-prepared
+ *    weight -- must not be written by the kernel that immediately precedes the arc_linear call.
+ *  ARC_LINEAR_AUTO: UNFUSED (the faster path on B200 at every M).
  *  ARC_LINEAR_FUSED at M <= 64: ONE kernel (the "optionally fused with the activation quantize as its
  *    producer stage" GEMM of the north star): a persistent weight-streaming stream-K GEMM whose
  *    CTAs first quantize one 256-element K block each (all M rows) into the workspace and publish it

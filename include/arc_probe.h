@@ -36,6 +36,13 @@ ARC_API arc_status_t arc_probe_u4_unpack(const uint8_t* src, int64_t rows, uint8
  * ready, split-tile arrival counted, epilogue done); copies max_ctas rows of 8 uint64 to host
  * memory (synchronous) and returns the row count (0 when tracing is off). */
 ARC_API int arc_debug_stream_trace(unsigned long long* host, int max_ctas);
+/* Timing experiments only: with env ARC_TRACE set, every quantize and decode-size GEMM launch takes the
+ * next of 64 slots of [1024 CTAs][8] uint64 globaltimer stamps (quantize: entry, griddepcontrol.wait
+ * passed, producer done, first primary warp done; decode GEMM: entry, griddepcontrol.wait passed,
+ * accumulator ready, partials sent, arrivals done, partials received, exit).  Copies the 64 slots to host (synchronous; host holds 64*1024*8 uint64),
+ * clears them and restarts at slot 0; returns the number of slots used since the last call (0 when
+ * tracing is off). */
+ARC_API int arc_debug_trace(unsigned long long* host);
 #ifdef __cplusplus
 }
 #endif

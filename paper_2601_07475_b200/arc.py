@@ -135,7 +135,7 @@ EXPORTED = [
     "arc_mx_tensor_scale", "arc_mx_tensor_scale_device", "arc_quantize_activation_mx", "arc_quantize_weight_mx", "arc_gather_order_ex",
     "arc_probe_e2m1", "arc_probe_e2m1_bits", "arc_probe_e2m1_raw_bits", "arc_probe_e4m3_ceil", "arc_probe_silu",
     "arc_probe_u4_unpack",
-    "arc_debug_stream_trace",
+    "arc_debug_stream_trace", "arc_debug_trace",
 ]
 
 
@@ -450,7 +450,7 @@ def linear(x: torch.Tensor, prof: Profile, qw: QWeight, out_dtype=torch.bfloat16
            stream=None, mode: str = "auto"):
     """The ARC linear layer (Eq.2): activation quantize + augmented NVFP4 GEMM.  mode "unfused" = two
     PDL-chained kernels; "fused" (M <= 64) = one kernel that quantizes the activation and runs the
-    weight-streaming stream-K GEMM (arc.h ARC_LINEAR_FUSED); "auto" = fused at M <= 4, else unfused."""
+    weight-streaming stream-K GEMM (arc.h ARC_LINEAR_FUSED); "auto" = unfused (faster at every M)."""
     assert x.dtype == torch.bfloat16 and x.is_cuda
     M = x.shape[0]
     if out is None:

@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -26,6 +27,39 @@ static arc_status_t cuda_fail(cudaError_t e, const char* where, const char* deta
   return ARC_ERR_CUDA;
 }
 
+namespace {
+constexpr int kTraceSlots = 64, kTraceCtas = 1024;
+unsigned long long* g_trace = nullptr;
+int g_trace_next = 0;
+std::once_flag g_trace_once;
+}  // namespace
+
+unsigned long long* trace_slot() {
+  std::call_once(g_trace_once, [] {
+    if (getenv("ARC_TRACE") &&
+        cudaMalloc(&g_trace, (size_t)kTraceSlots * kTraceCtas * 8 * sizeof(unsigned long long)) != cudaSuccess)
+      g_trace = nullptr;
+    if (g_trace) cudaMemset(g_trace, 0, (size_t)kTraceSlots * kTraceCtas * 8 * sizeof(unsigned long long));
+  });
+  if (!g_trace) return nullptr;
+  return g_trace + (size_t)(g_trace_next++ % kTraceSlots) * kTraceCtas * 8;
+}
+
+}  // namespace arc
+
+extern "C" ARC_API int arc_debug_trace(unsigned long long* host) {
+  using namespace arc;
+  if (!g_trace || !host) return 0;
+  const size_t bytes = (size_t)kTraceSlots * kTraceCtas * 8 * sizeof(unsigned long long);
+  if (cudaDeviceSynchronize() != cudaSuccess) return 0;
+  if (cudaMemcpy(host, g_trace, bytes, cudaMemcpyDeviceToHost) != cudaSuccess) return 0;
+  cudaMemset(g_trace, 0, bytes);
+  const int n = g_trace_next;
+  g_trace_next = 0;
+  return n;
+}
+
+namespace arc {
 int num_sms() {
   static int cache[64] = {0};
   int dev = 0;
@@ -288,8 +322,15 @@ arc_status_t arc_quantize_weight(const void* w, int64_t N, int64_t K, int64_t ld
   return e == cudaSuccess ? ARC_OK : cuda_fail(e, "arc_quantize_weight");
 }
 
+static arc_status_t quantize_activation_impl(const void* x, int64_t M, int64_t ldx, const arc_profile_t* prof,
+                                            uint8_t* codes, uint8_t* sf, void* stream, int consts_ready);
 arc_status_t arc_quantize_activation(const void* x, int64_t M, int64_t ldx, const arc_profile_t* prof,
                                      uint8_t* codes, uint8_t* sf, void* stream) {
+  return quantize_activation_impl(x, M, ldx, prof, codes, sf, stream, 0);
+}
+// consts_ready: arc_linear's promise that perm (like the weights) was complete before the preceding kernel
+static arc_status_t quantize_activation_impl(const void* x, int64_t M, int64_t ldx, const arc_profile_t* prof,
+                                            uint8_t* codes, uint8_t* sf, void* stream, int consts_ready) {
   arc_status_t s = check_profile(prof);
   if (s != ARC_OK) return s;
   if (M < 0 || ldx < prof->K || ldx % 8) return fail(ARC_ERR_SHAPE, "bad M/ldx");
@@ -300,7 +341,7 @@ arc_status_t arc_quantize_activation(const void* x, int64_t M, int64_t ldx, cons
   if (s != ARC_OK) return s;
   if (M == 0) return ARC_OK;
   cudaError_t e = launch_quant(x, M, (int)prof->K, ldx, prof->perm, prof->S, prof->gs, (int)prof->layout, 0, codes,
-                               sf, (cudaStream_t)stream);
+                               sf, (cudaStream_t)stream, nullptr, 0.0f, -1, 0, consts_ready);
   return e == cudaSuccess ? ARC_OK : cuda_fail(e, "arc_quantize_activation");
 }
 
@@ -808,10 +849,10 @@ arc_status_t arc_linear_ex(const void* x, int64_t M, int64_t ldx, const arc_prof
   uint8_t* sf = codes + round_up(M * (qw->Kp / 2), 256);
   const size_t act = act_ws_bytes(M, qw->K, qw->S);
   // ARC_LINEAR_FUSED at decode-size M: one kernel quantizes the activation into the workspace and runs
-  // the stream-K GEMM.  AUTO takes it at M <= 4, where the single launch per site measured faster than
-  // the three-kernel path on most boxes; from M = 16 on the split-K path is faster.
+  // the stream-K GEMM.  AUTO runs the two-kernel path at every M: the direct-gather quantize + the
+  // cluster split-K GEMM (decode_gemm.cu) measured faster than the fused kernel from M = 1.
   const StreamPlan sp = plan_stream(M, qw->N, qw->Kp);
-  if ((flags == ARC_LINEAR_FUSED || (flags == ARC_LINEAR_AUTO && M <= 4)) && sp.ok) {
+  if (flags == ARC_LINEAR_FUSED && sp.ok) {
     // decode-size M: one kernel quantizes the activation into the workspace and runs the stream-K GEMM
     s = check_device();
     if (s != ARC_OK) return s;
@@ -838,7 +879,7 @@ arc_status_t arc_linear_ex(const void* x, int64_t M, int64_t ldx, const arc_prof
     cudaError_t e = launch_stream_gemm(p, sp, (cudaStream_t)stream, &detail, &fq);
     return e == cudaSuccess ? ARC_OK : cuda_fail(e, "arc_linear (fused decode)", detail);
   }
-  s = arc_quantize_activation(x, M, ldx, prof, codes, sf, stream);
+  s = quantize_activation_impl(x, M, ldx, prof, codes, sf, stream, 1);
   if (s != ARC_OK) return s;
   return gemm_impl(codes, sf, prof->gs, M, qw, y, y_dtype, ldy, ws, rest + act, rest_bytes - act, stream, 1);
 }

@@ -35,11 +35,18 @@ inline int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
 
 int num_sms();  // SM count of the current device (cached per device)
 
+// Timing experiments only (env ARC_TRACE): per-launch slots of [1024 CTAs][4] globaltimer stamps that the
+// quantize and decode-GEMM kernels fill; nullptr when tracing is off (the normal case).
+unsigned long long* trace_slot();
+
 // gamma != nullptr: RMSNorm (reading Q23) each row in place before quantizing it.
 // up_off >= 0: SiLU-mul mode (reading Q24): quantize bf16(bf16(SiLU(x)) * x[up_off..]) per row.
 cudaError_t launch_quant(const void* x, int64_t rows, int K, int64_t ld, const int32_t* perm, int S, const float* gs,
                          int layout, int weight_mode, uint8_t* codes, uint8_t* sf, cudaStream_t stream,
-                         const void* gamma = nullptr, float eps = 0.0f, int64_t up_off = -1, int mx = 0);
+                         const void* gamma = nullptr, float eps = 0.0f, int64_t up_off = -1, int mx = 0,
+                         int consts_ready = 0);
+// consts_ready (arc_linear): perm was complete before the preceding kernel started (calibration constants,
+// like the prepared weights), so the decode-size quantize may load it before griddepcontrol.wait.
 cudaError_t launch_silu_mul(const void* gu, int64_t rows, int K, int64_t ld, int64_t up_off, void* h, int64_t ldh,
                             cudaStream_t s);
 cudaError_t launch_rmsnorm(const void* x, int64_t rows, int K, int64_t ldx, const void* gamma, float eps, void* y,
@@ -102,6 +109,18 @@ struct StreamQuant {
 };
 cudaError_t launch_stream_gemm(const GemmProblem& p, const StreamPlan& pl, cudaStream_t stream, const char** detail,
                                const StreamQuant* fq = nullptr);
+// Decode-size M (<= 64): cluster split-K GEMM with the K reduction in distributed shared memory
+// (decode_gemm.cu): n_tiles x ks CTAs, clusters of ks, no workspace.
+struct DecodePlan {
+  bool ok = false;
+  int a_rows = 0;                  // tokens rounded up to the MMA N: 16 / 32 / 64
+  int64_t n_tiles = 0, nkb = 0;    // 128-row weight tiles, 256-K blocks
+  int ks = 1;                      // CTAs per cluster (K ranges per tile)
+  int64_t grid = 0;
+  int nst = 2, stage_bytes = 0;
+};
+DecodePlan plan_decode(int64_t M, int64_t N, int64_t Kp);
+cudaError_t launch_decode_gemm(const GemmProblem& p, const DecodePlan& pl, cudaStream_t stream, const char** detail);
 struct GemmPlan {
   int CL;            // CTAs per cluster along M
   int pair;          // CL == 2: 1 = 2-SM tcgen05 MMA (cta_group::2), 0 = two 1-SM CTAs sharing B by multicast

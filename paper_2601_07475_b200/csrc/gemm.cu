@@ -1018,6 +1018,11 @@ cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t stream, const char** 
     const StreamPlan sp = plan_stream(p.M, p.N, p.Kp);
     if (sp.ok) return launch_stream_gemm(p, sp, stream, detail);
   }
+  // decode-size M: cluster split-K with the reduction in distributed shared memory (decode_gemm.cu)
+  if (!p.swiglu && !p.red_mode && !p.fmt) {
+    const DecodePlan dp = plan_decode(p.M, p.N, p.Kp);
+    if (dp.ok) return launch_decode_gemm(p, dp, stream, detail);
+  }
   // MXFP8 (p.fmt == 1): 128 K per 128-byte stage -> plan as an NVFP4 problem with twice the K
   GemmPlan pl = plan_gemm(p.M, p.N, (p.fmt == 1 || p.fmt == 3) ? 2 * p.Kp : p.Kp);
   if (p.fmt) {

@@ -61,7 +61,17 @@ struct QuantArgs {
   float eps;
   int32_t norm;    // 1: RMSNorm the staged rows in place before quantizing (R norm warps)
   int64_t up_off;  // SiLU-mul mode (Fig.5, reading Q24): x holds gate, x + up_off holds up
+  unsigned long long* trace;  // timing experiments only (ARC_TRACE): [cta][8] globaltimer stamps
+  int32_t consts_ready;       // perm may be read before griddepcontrol.wait (arc_linear)
 };
+
+ARC_DEV void qtrace(const QuantArgs& a, int i) {
+  if (a.trace && blockIdx.x < 1024) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.trace[(size_t)blockIdx.x * 8 + i] = t;
+  }
+}
 
 ARC_DEV void cp_async16(uint32_t dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
@@ -267,8 +277,10 @@ __global__ void __launch_bounds__(1024) arc_quant_kernel(QuantArgs p) {
   // kernel before this one has completed (the decode GEMM streams weights before its own wait).
   // Weight preparation never lets dependents launch early: a kernel that follows it may then
   // assume the weights are complete (the invariant the decode GEMM's early weight stream uses).
+  if (threadIdx.x == 0) qtrace(p, 0);
   pdl_wait();  // the previous kernel's writes are visible from here on
   if (!p.weight_mode) pdl_launch_dependents();
+  if (threadIdx.x == 0) qtrace(p, 1);
   const float gs = __ldg(p.gs);
 
   if (tid == 0) {
@@ -308,7 +320,9 @@ __global__ void __launch_bounds__(1024) arc_quant_kernel(QuantArgs p) {
     const uint32_t ring = smem_u32(smem) + (uint32_t)lane * 16u;
     const int kc = K >> 3;  // 16-byte chunks per row
     const uint32_t rowbytes = (uint32_t)K * (SILU ? 4u : 2u);
-    const uint64_t x_policy = policy_evict_first();
+    // X is read once: evict-first at streaming sizes; a decode-size activation (<= 64 rows) keeps the
+    // normal priority so it stays in L2 while the next GEMM streams its weights with evict-first
+    const uint64_t x_policy = p.rows <= 64 ? policy_evict_normal() : policy_evict_first();
     // scales staged for tile jt (slot s) -> global, one UB-byte word per unit
     auto flush_sf = [&](int s, int jt) {
       const int base = tile_base<R>((int)blockIdx.x + jt * (int)gridDim.x);
@@ -368,6 +382,7 @@ __global__ void __launch_bounds__(1024) arc_quant_kernel(QuantArgs p) {
       flush_sf(s, jt);
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
+    if (lane == 0) qtrace(p, 2);
     return;
   }
 
@@ -501,6 +516,7 @@ __global__ void __launch_bounds__(1024) arc_quant_kernel(QuantArgs p) {
         }
       }
     }
+    if (warp == 0 && lane == 0) qtrace(p, 3);
     return;
   }
 
@@ -908,11 +924,81 @@ static cudaError_t launch_silu_cfg(QuantArgs a, int th, int ipt, int64_t rb, cud
   return launch_quant_cfg<2, 1, 65536, 3, false, SILU>(a, th, stream);
 }
 
+// Decode-size activations (<= 64 rows): one thread per (row m, physical block pb), gathering the
+// block's 16 calibrated channels straight from x (L2) -- no staging ring, no mbarriers, one memory
+// round trip between griddepcontrol.wait and the stores.  The STAGE arithmetic of arc_quant_kernel
+// (Q7 op order: primary stage, residual stage of P:138 for residual blocks), bit-identical.
+__global__ void __launch_bounds__(256) arc_quant_small_kernel(QuantArgs p) {
+  if (threadIdx.x == 0) qtrace(p, 0);
+  const int NB = p.Kp >> 4, nb = p.K >> 4, ns = p.S >> 4;
+  const int it = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool live = it < p.rows * NB;
+  const int m = live ? it / NB : 0, pb = live ? it - m * NB : 0;
+  int l = -1;
+  bool res = false;
+  if (p.layout == 0) {  // interleaved P0 R0 P1 R1 ... (App.D)
+    if (pb < 2 * ns) { l = pb >> 1; res = (pb & 1) != 0; }
+    else if (pb < nb + ns) l = pb - ns;
+  } else {              // contiguous [Q_X | Q_Ro]
+    if (pb < nb) l = pb;
+    else if (pb < nb + ns) { l = pb - nb; res = true; }
+  }
+  // the block's 16 channel indices: a calibration constant -- loaded before the wait when the caller
+  // guarantees it was complete before the preceding kernel started (arc_linear), so only the x gathers
+  // sit between griddepcontrol.wait and the stores
+  int4 c[4];
+  if (p.consts_ready && live && l >= 0) {
+    const int4* pp = reinterpret_cast<const int4*>(p.perm + 16 * l);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) c[q] = __ldg(pp + q);
+  }
+  pdl_wait();
+  pdl_launch_dependents();  // (after the wait: see arc_quant_kernel)
+  if (threadIdx.x == 0) qtrace(p, 1);
+  if (!live) return;
+  if (!p.consts_ready && l >= 0) {
+    const int4* pp = reinterpret_cast<const int4*>(p.perm + 16 * l);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) c[q] = __ldg(pp + q);
+  }
+  uint2 packed = make_uint2(0u, 0u);
+  uint32_t sfb = 0;
+  if (l >= 0) {
+    const float gs = __ldg(p.gs);
+    const unsigned short* xr = reinterpret_cast<const unsigned short*>(p.x) + (int64_t)m * p.ld;
+    float z[16];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      z[4 * q + 0] = bf16_bits_to_f32(__ldg(xr + c[q].x));
+      z[4 * q + 1] = bf16_bits_to_f32(__ldg(xr + c[q].y));
+      z[4 * q + 2] = bf16_bits_to_f32(__ldg(xr + c[q].z));
+      z[4 * q + 3] = bf16_bits_to_f32(__ldg(xr + c[q].w));
+    }
+    const uint32_t sf1 = e4m3_ceil_nb(__fmul_rn(absmax16(z), __fdiv_rn(gs, 6.0f)));
+    const float d1 = e4m3_value(sf1);
+    float t[16];
+    packed = encode16(z, sf1 == 0u ? 0.0f : __fdiv_rn(gs, d1), t);
+    sfb = sf1;
+    if (res) {
+      float e[16];
+      residual16(t, packed, e);
+      const uint32_t sf2 = e4m3_ceil_nb(__fmul_rn(absmax16(e), __fdiv_rn(d1, 6.0f)));
+      packed = encode16(e, sf2 == 0u ? 0.0f : __fdiv_rn(d1, e4m3_value(sf2)));
+      sfb = sf2;
+    }
+  }
+  *reinterpret_cast<uint2*>(p.codes + (int64_t)m * (p.Kp >> 1) + pb * 8) = packed;
+  p.sf[(pb >> 2) * 512 + (m & 31) * 16 + ((m >> 5) & 3) * 4 + (pb & 3)] = (uint8_t)sfb;
+  if (it == 0) qtrace(p, 3);
+}
+
 cudaError_t launch_quant(const void* x, int64_t rows, int K, int64_t ld, const int32_t* perm, int S, const float* gs,
                          int layout, int weight_mode, uint8_t* codes, uint8_t* sf, cudaStream_t stream,
-                         const void* gamma, float eps, int64_t up_off, int mx) {
+                         const void* gamma, float eps, int64_t up_off, int mx, int consts_ready) {
   QuantArgs a;
+  a.consts_ready = consts_ready;
   a.up_off = up_off;
+  a.trace = trace_slot();
   a.gamma = static_cast<const uint16_t*>(gamma);
   a.eps = eps;
   a.norm = gamma != nullptr ? 1 : 0;
@@ -936,6 +1022,22 @@ cudaError_t launch_quant(const void* x, int64_t rows, int K, int64_t ld, const i
   const int NB = a.Kp / 16, ns = S / 16;
   const int nprim = NB - ns;                 // primary + pad blocks per row
   const int64_t rowb = (int64_t)K * 2;
+  // decode-size activations: the direct-gather kernel (ARC_QUANT_SMALL=0 keeps the ring kernel)
+  static const int env_small = getenv("ARC_QUANT_SMALL") ? atoi(getenv("ARC_QUANT_SMALL")) : 1;
+  if (env_small && rows <= 64 && !weight_mode && !a.norm && up_off == -1 && !mx) {
+    cudaLaunchConfig_t cfg;
+    memset(&cfg, 0, sizeof(cfg));
+    cfg.gridDim = dim3((unsigned)((rows * NB + 255) / 256));
+    cfg.blockDim = dim3(256);
+    cfg.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, arc_quant_small_kernel, a);
+    return e != cudaSuccess ? e : cudaGetLastError();
+  }
   if (up_off >= 0 || up_off == -2) {
     // SiLU-mul mode: a staged row is gate + up (4K bytes); always whole-row bulk copies.
     // up_off == -2: (g, u) pairs (SILU = 2); else up at x + up_off (SILU = 1).

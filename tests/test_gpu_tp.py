@@ -99,10 +99,17 @@ def test_gemm_reduce_peers_equals_gemm(M, K, N):
     out = torch.zeros(M, ldy, dtype=torch.float32, device="cuda")
     arc.gemm_reduce(codes, sf, prof.gs, qw, ldy=ldy, peer_ptrs=[out.data_ptr()])
     torch.cuda.synchronize()
-    assert torch.equal(out[:, :N], y)
+    if M > 64:
+        assert torch.equal(out[:, :N], y)
+    else:
+        # decode-size M: arc_gemm runs the cluster split-K kernel (partials summed in DSMEM, then scaled),
+        # arc_gemm_reduce the split-K kernel + reduce kernel (scaled partials summed): same math, another
+        # fp32 summation order -- both within 1e-5 * sum|ab| of the exact GEMM (test_gpu_decode_cluster)
+        assert torch.allclose(out[:, :N], y, rtol=1e-5, atol=1e-6 * float(y.abs().max()))
+    p1 = out[:, :N].clone()
     arc.gemm_reduce(codes, sf, prof.gs, qw, ldy=ldy, peer_ptrs=[out.data_ptr(), out.data_ptr()])
     torch.cuda.synchronize()
-    assert torch.allclose(out[:, :N], 3 * y, rtol=1e-6, atol=0)  # every peer receives each partial
+    assert torch.allclose(out[:, :N], 3 * p1, rtol=1e-6, atol=0)  # every peer receives each partial
 
 
 def test_row_parallel_fused_reduce_world1_nccl(pg):
