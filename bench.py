@@ -349,8 +349,9 @@ def time_graph(fn, reps=50, warm=3):
 def decode_sweep(A, sites, device, peaks, Ms=(1, 4, 16, 32, 64)):
     """BASELINE configs[1] decode token counts: the same 4 sites at M tokens, CUDA-graph replay.  The
     weights of the 4 sites (~128 MB at LLaMA-3-8B, > L2) stream from HBM every step.  Bound = weight
-    + activation bytes / HBM.  Default arc_linear (quantize kernel + split-K GEMM + reduce kernel per
-    site) and, beside it, ARC_LINEAR_FUSED (one in-kernel-quantize stream-K kernel per site)."""
+    + activation bytes / HBM.  Default arc_linear (per site: the direct-gather quantize kernel + the
+    cluster split-K GEMM whose K partials are reduced in distributed shared memory, decode_gemm.cu) and,
+    beside it, ARC_LINEAR_FUSED (one in-kernel-quantize stream-K kernel per site)."""
     out = []
     wbytes = sum(s.N * s.Kp * 9 // 16 for s in sites)
     for Md in Ms:
@@ -637,8 +638,11 @@ def main():
                    for s in sites]
 
             def e2e_step():
+                # arc_linear_hostio_async per site (H2D / linear / D2H pipelined over row chunks, the copies
+                # of consecutive sites overlapping), then one arc_linear_hostio_wait
                 for s, xh, yh, ws in zip(sites, xs, ys, wss):
-                    A.linear_hostio(xh, s.prof, s.qw, yh, ws)
+                    A.linear_hostio(xh, s.prof, s.qw, yh, ws, wait=False)
+                A.linear_hostio_wait()
         else:
             def e2e_step():
                 for s, xh in zip(sites, xs):
@@ -667,7 +671,7 @@ def main():
                       "h2d_bytes_per_step": sum(x.numel() * x.element_size() for x in xs),
                       "d2h_bytes_per_step": sum(y.numel() * y.element_size() for y in ys),
                       "ms_per_step": ems,
-                      "api": "arc_linear_hostio (C-ABI, pinned host buffers)" if world == 1 else
+                      "api": "arc_linear_hostio_async + arc_linear_hostio_wait (C-ABI, pinned host buffers)" if world == 1 else
                              "arc quantize+gemm per rank + NCCL collectives, pinned host copies in the step"}
 
     if keep:

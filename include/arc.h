@@ -382,12 +382,26 @@ ARC_API arc_status_t arc_linear_ex(const void* x, int64_t M, int64_t ldx, const 
                                    size_t ws_bytes, int flags, void* stream);
 /* arc_linear on HOST buffers: copies x_host (bf16 [M][K], pinned or pageable) to
  * the device, runs arc_linear, copies y back to y_host ([M][N] of y_dtype) and
- * synchronizes `stream`.  ws must hold arc_linear_hostio_workspace_size bytes. */
+ * waits for all of it (arc_linear_hostio_wait).  ws must hold arc_linear_hostio_workspace_size bytes.
+ * The rows are pipelined in chunks of 128-multiples (~8 per call): chunk i's host->device copy runs on a
+ * library-owned copy-in stream, its arc_linear on `stream`, its device->host copy on a library-owned
+ * copy-out stream (two non-blocking streams and an event ring per device, created on first use), so the
+ * copies overlap the compute and each other.  Y equals arc_linear applied to each chunk of rows (quantization is
+ * per row; a chunk's GEMM may choose a different K split than the whole batch's: same tolerance). */
 ARC_API arc_status_t arc_linear_hostio_workspace_size(int64_t M, const arc_qweight_t* qw, arc_dtype_t y_dtype,
                                                       size_t* bytes);
 ARC_API arc_status_t arc_linear_hostio(const void* x_host, int64_t M, const arc_profile_t* prof,
                                const arc_qweight_t* qw, void* y_host, arc_dtype_t y_dtype, void* ws,
                                size_t ws_bytes, void* stream);
+/* The same pipeline without the final wait: returns once everything is enqueued, so the copies of
+ * consecutive calls overlap (device->host of one layer with host->device of the next).  The host buffers
+ * and ws must stay untouched until arc_linear_hostio_wait(stream) returns; concurrent calls need distinct
+ * workspaces. */
+ARC_API arc_status_t arc_linear_hostio_async(const void* x_host, int64_t M, const arc_profile_t* prof,
+                                             const arc_qweight_t* qw, void* y_host, arc_dtype_t y_dtype, void* ws,
+                                             size_t ws_bytes, void* stream);
+/* Blocks until every arc_linear_hostio_async call on this device (and `stream`) has completed. */
+ARC_API arc_status_t arc_linear_hostio_wait(void* stream);
 
 #ifdef __cplusplus
 }

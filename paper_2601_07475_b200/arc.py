@@ -114,6 +114,9 @@ _sig("arc_linear_hostio_workspace_size", [_i64, ctypes.POINTER(ArcQWeight), ctyp
                                          ctypes.POINTER(ctypes.c_size_t)])
 _sig("arc_linear_hostio", [_P, _i64, ctypes.POINTER(ArcProfile), ctypes.POINTER(ArcQWeight), _P, ctypes.c_int, _P,
                            ctypes.c_size_t, _P])
+_sig("arc_linear_hostio_async", [_P, _i64, ctypes.POINTER(ArcProfile), ctypes.POINTER(ArcQWeight), _P, ctypes.c_int,
+                                 _P, ctypes.c_size_t, _P])
+_sig("arc_linear_hostio_wait", [_P])
 _sig("arc_probe_e2m1", [_P, _i64, _P, _P])
 _sig("arc_probe_e2m1_bits", [ctypes.c_uint32, _i64, _P, _P])
 _sig("arc_probe_e2m1_raw_bits", [ctypes.c_uint32, _i64, _P, _P])
@@ -135,7 +138,7 @@ EXPORTED = [
     "arc_mx_tensor_scale", "arc_mx_tensor_scale_device", "arc_quantize_activation_mx", "arc_quantize_weight_mx", "arc_gather_order_ex",
     "arc_probe_e2m1", "arc_probe_e2m1_bits", "arc_probe_e2m1_raw_bits", "arc_probe_e4m3_ceil", "arc_probe_silu",
     "arc_probe_u4_unpack",
-    "arc_debug_stream_trace", "arc_debug_trace",
+    "arc_debug_stream_trace", "arc_debug_trace", "arc_linear_hostio_async", "arc_linear_hostio_wait",
 ]
 
 
@@ -619,13 +622,21 @@ def linear_hostio_workspace_size(M: int, qw, out_dtype=torch.bfloat16) -> int:
 
 
 def linear_hostio(x_host: torch.Tensor, prof: Profile, qw: QWeight, y_host: torch.Tensor, ws: torch.Tensor,
-                  stream=None):
-    """arc_linear on host buffers (H2D of x, D2H of y inside the call; synchronizes the stream)."""
+                  stream=None, wait: bool = True):
+    """arc_linear on host buffers: H2D of x, the linear and D2H of y pipelined over row chunks (arc.h).
+    wait=False: arc_linear_hostio_async (returns once enqueued; call linear_hostio_wait before touching
+    x_host / y_host / ws)."""
     assert not x_host.is_cuda and not y_host.is_cuda
-    _check(_lib.arc_linear_hostio(_ptr(x_host), x_host.shape[0], ctypes.byref(prof.c()), ctypes.byref(qw.c()),
-                                  _ptr(y_host), _dtype_code(y_host.dtype), _ptr(ws), ws.numel(), _stream(stream)),
-           "arc_linear_hostio")
+    fn = _lib.arc_linear_hostio if wait else _lib.arc_linear_hostio_async
+    _check(fn(_ptr(x_host), x_host.shape[0], ctypes.byref(prof.c()), ctypes.byref(qw.c()),
+              _ptr(y_host), _dtype_code(y_host.dtype), _ptr(ws), ws.numel(), _stream(stream)),
+           "arc_linear_hostio" if wait else "arc_linear_hostio_async")
     return y_host
+
+
+def linear_hostio_wait(stream=None):
+    """Wait for every linear_hostio(wait=False) call on the current device."""
+    _check(_lib.arc_linear_hostio_wait(_stream(stream)), "arc_linear_hostio_wait")
 
 
 # --------------------------------------------------------------------------- probes (tests only)

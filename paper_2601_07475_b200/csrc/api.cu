@@ -947,18 +947,63 @@ arc_status_t arc_linear_ex_workspace_size(int64_t M, const arc_qweight_t* qw, in
 }
 
 
+// rows per pipelined chunk of arc_linear_hostio: a multiple of 128, ~8 chunks per call (one below 512 rows)
+static int64_t hostio_chunk_rows(int64_t M) { return M < 512 ? M : round_up((M + 7) / 8, 128); }
+
 arc_status_t arc_linear_hostio_workspace_size(int64_t M, const arc_qweight_t* qw, arc_dtype_t y_dtype,
                                               size_t* bytes) {
-  size_t w = 0;
+  // the chunks share one arc_linear workspace: the largest any chunk size needs
+  const int64_t mc = hostio_chunk_rows(M), tail = M > 0 ? M - (M - 1) / mc * mc : 0;
+  size_t w = 0, w1 = 0, w2 = 0;
   arc_status_t s = arc_linear_workspace_size(M, qw, &w);
   if (s != ARC_OK) return s;
+  if ((s = arc_linear_workspace_size(mc, qw, &w1)) != ARC_OK || (s = arc_linear_workspace_size(tail, qw, &w2)) != ARC_OK)
+    return s;
+  w = std::max(w, std::max(w1, w2));
   const int64_t yb = M * qw->N * (y_dtype == ARC_FP32 ? 4 : 2);
-  *bytes = w + (size_t)round_up(M * qw->K * 2, 256) + (size_t)round_up(yb, 256);
+  *bytes = round_up((int64_t)w, 256) + (size_t)round_up(M * qw->K * 2, 256) + (size_t)round_up(yb, 256);
   return ARC_OK;
 }
 
-arc_status_t arc_linear_hostio(const void* x_host, int64_t M, const arc_profile_t* prof, const arc_qweight_t* qw,
-                               void* y_host, arc_dtype_t y_dtype, void* ws, size_t ws_bytes, void* stream) {
+// Host-IO pipeline: per device, two library-owned non-blocking streams (host->device copies, device->host
+// copies) and a ring of events; created on first use.  A call splits its rows into chunks: chunk i's H2D
+// runs on the copy-in stream, its arc_linear on the caller's stream once the H2D event fired, its D2H on
+// the copy-out stream once the compute event fired -- copies of one chunk overlap the compute of the next
+// and, across consecutive async calls, device->host and host->device copies overlap (PCIe is full duplex).
+namespace {
+struct HostIo {
+  std::mutex mu;
+  bool init = false;
+  cudaError_t err = cudaSuccess;
+  cudaStream_t in = nullptr, out = nullptr;
+  static constexpr int kEv = 512;
+  cudaEvent_t ev[kEv];
+  int next = 0;
+  cudaEvent_t get() { cudaEvent_t e = ev[next]; next = (next + 1) % kEv; return e; }
+};
+HostIo g_hio[64];
+HostIo* hostio_for_device(cudaError_t* err) {
+  int dev = 0;
+  *err = cudaGetDevice(&dev);
+  if (*err != cudaSuccess) return nullptr;
+  if (dev < 0 || dev >= 64) { *err = cudaErrorInvalidDevice; return nullptr; }
+  HostIo* h = &g_hio[dev];
+  std::lock_guard<std::mutex> g(h->mu);
+  if (!h->init) {
+    h->init = true;
+    h->err = cudaStreamCreateWithFlags(&h->in, cudaStreamNonBlocking);
+    if (h->err == cudaSuccess) h->err = cudaStreamCreateWithFlags(&h->out, cudaStreamNonBlocking);
+    for (int i = 0; i < HostIo::kEv && h->err == cudaSuccess; ++i)
+      h->err = cudaEventCreateWithFlags(&h->ev[i], cudaEventDisableTiming);
+  }
+  *err = h->err;
+  return h->err == cudaSuccess ? h : nullptr;
+}
+}  // namespace
+
+static arc_status_t hostio_enqueue(const void* x_host, int64_t M, const arc_profile_t* prof, const arc_qweight_t* qw,
+                                   void* y_host, arc_dtype_t y_dtype, void* ws, size_t ws_bytes, void* stream,
+                                   HostIo** hio_out) {
   if (!x_host || !y_host || !ws) return fail(ARC_ERR_NULL, "null x_host / y_host / ws");
   arc_status_t s = check_profile(prof);
   if (s != ARC_OK) return s;
@@ -969,22 +1014,71 @@ arc_status_t arc_linear_hostio(const void* x_host, int64_t M, const arc_profile_
   if (s != ARC_OK) return s;
   if (ws_bytes < need) return fail(ARC_ERR_WORKSPACE, "workspace too small");
   if (M == 0) return ARC_OK;
-  size_t lin = 0;
-  arc_linear_workspace_size(M, qw, &lin);
-  uint8_t* base = static_cast<uint8_t*>(ws);
-  void* xd = base + lin;
-  void* yd = base + lin + round_up(M * prof->K * 2, 256);
-  const size_t xb = (size_t)(M * prof->K * 2);
-  const size_t yb = (size_t)(M * qw->N * (y_dtype == ARC_FP32 ? 4 : 2));
-  cudaStream_t st = (cudaStream_t)stream;
-  cudaError_t e = cudaMemcpyAsync(xd, x_host, xb, cudaMemcpyHostToDevice, st);
-  if (e != cudaSuccess) return cuda_fail(e, "arc_linear_hostio H2D");
-  s = arc_linear(xd, M, prof->K, prof, qw, yd, y_dtype, qw->N, base, lin, stream);
+  s = check_device();
   if (s != ARC_OK) return s;
-  e = cudaMemcpyAsync(y_host, yd, yb, cudaMemcpyDeviceToHost, st);
-  if (e != cudaSuccess) return cuda_fail(e, "arc_linear_hostio D2H");
-  e = cudaStreamSynchronize(st);
-  return e == cudaSuccess ? ARC_OK : cuda_fail(e, "arc_linear_hostio sync");
+  cudaError_t e = cudaSuccess;
+  HostIo* h = hostio_for_device(&e);
+  if (!h) return cuda_fail(e, "arc_linear_hostio streams");
+  *hio_out = h;
+  const int64_t mc = hostio_chunk_rows(M), tail = M - (M - 1) / mc * mc;
+  size_t lin = 0, l1 = 0, l2 = 0;
+  arc_linear_workspace_size(M, qw, &lin);
+  arc_linear_workspace_size(mc, qw, &l1);
+  arc_linear_workspace_size(tail, qw, &l2);
+  lin = (size_t)round_up((int64_t)std::max(lin, std::max(l1, l2)), 256);
+  uint8_t* base = static_cast<uint8_t*>(ws);
+  uint8_t* xd = base + lin;
+  uint8_t* yd = base + lin + round_up(M * prof->K * 2, 256);
+  const int64_t xrow = prof->K * 2, yrow = qw->N * (y_dtype == ARC_FP32 ? 4 : 2);
+  cudaStream_t st = (cudaStream_t)stream;
+  std::lock_guard<std::mutex> g(h->mu);
+  // the copies into this workspace start after the work already enqueued on the caller's stream
+  cudaEvent_t e0 = h->get();
+  if ((e = cudaEventRecord(e0, st)) != cudaSuccess || (e = cudaStreamWaitEvent(h->in, e0, 0)) != cudaSuccess)
+    return cuda_fail(e, "arc_linear_hostio order");
+  for (int64_t r0 = 0; r0 < M; r0 += mc) {
+    const int64_t rows = std::min<int64_t>(mc, M - r0);
+    cudaEvent_t ein = h->get(), ec = h->get();
+    e = cudaMemcpyAsync(xd + r0 * xrow, static_cast<const uint8_t*>(x_host) + r0 * xrow, (size_t)(rows * xrow),
+                        cudaMemcpyHostToDevice, h->in);
+    if (e == cudaSuccess) e = cudaEventRecord(ein, h->in);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, ein, 0);
+    if (e != cudaSuccess) return cuda_fail(e, "arc_linear_hostio H2D");
+    // chunks reuse the linear workspace in stream order (the compute of the chunks is serial on st)
+    s = arc_linear(xd + r0 * xrow, rows, prof->K, prof, qw, yd + r0 * yrow, y_dtype, qw->N, base, lin, stream);
+    if (s != ARC_OK) return s;
+    e = cudaEventRecord(ec, st);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(h->out, ec, 0);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(static_cast<uint8_t*>(y_host) + r0 * yrow, yd + r0 * yrow, (size_t)(rows * yrow),
+                          cudaMemcpyDeviceToHost, h->out);
+    if (e != cudaSuccess) return cuda_fail(e, "arc_linear_hostio D2H");
+  }
+  return ARC_OK;
+}
+
+arc_status_t arc_linear_hostio_async(const void* x_host, int64_t M, const arc_profile_t* prof, const arc_qweight_t* qw,
+                                     void* y_host, arc_dtype_t y_dtype, void* ws, size_t ws_bytes, void* stream) {
+  HostIo* h = nullptr;
+  return hostio_enqueue(x_host, M, prof, qw, y_host, y_dtype, ws, ws_bytes, stream, &h);
+}
+
+arc_status_t arc_linear_hostio_wait(void* stream) {
+  cudaError_t e = cudaSuccess;
+  HostIo* h = hostio_for_device(&e);
+  if (!h) return cuda_fail(e, "arc_linear_hostio streams");
+  if ((e = cudaStreamSynchronize(h->in)) != cudaSuccess || (e = cudaStreamSynchronize((cudaStream_t)stream)) != cudaSuccess ||
+      (e = cudaStreamSynchronize(h->out)) != cudaSuccess)
+    return cuda_fail(e, "arc_linear_hostio_wait");
+  return ARC_OK;
+}
+
+arc_status_t arc_linear_hostio(const void* x_host, int64_t M, const arc_profile_t* prof, const arc_qweight_t* qw,
+                               void* y_host, arc_dtype_t y_dtype, void* ws, size_t ws_bytes, void* stream) {
+  HostIo* h = nullptr;
+  arc_status_t s = hostio_enqueue(x_host, M, prof, qw, y_host, y_dtype, ws, ws_bytes, stream, &h);
+  if (s != ARC_OK || M == 0) return s;
+  return arc_linear_hostio_wait(stream);
 }
 
 }  // extern "C"

@@ -225,3 +225,30 @@ def test_llama3_70b_sites(A, site):
         yref, bound = oracle.gemm_reference(oc, osf, qw.codes.cpu().numpy(), qw.sf.cpu().numpy(),
                                             float(prof.gs.item()), float(qw.gs.item()), rows=rows.astype(np.int64))
     _check(y[torch.from_numpy(rows).cuda()].float().cpu().numpy().astype(np.float64), yref, bound, True)
+
+
+@pytest.mark.parametrize("pinned", [True, False])
+def test_hostio_pipelined_chunks_and_async(A, pinned):
+    """arc_linear_hostio pipelines its rows in 128-multiple chunks (H2D / linear / D2H on three streams):
+    Y equals arc_linear applied chunk by chunk (bit-exact) and the whole-batch linear within the GEMM
+    tolerance; three async calls with distinct workspaces then one wait give the same bits."""
+    M, N, K, S = 3000, 640, 1024, 64
+    x, w, prof, qw = _problem(A, M, N, K, S, seed=21)
+    mc = ((M + 7) // 8 + 127) // 128 * 128
+    y_chunks = torch.cat([A.linear(x[r:r + mc], prof, qw) for r in range(0, M, mc)])
+    y_whole = A.linear(x, prof, qw, out_dtype=torch.float32)
+    xh = x.cpu().pin_memory() if pinned else x.cpu()
+    yh = torch.empty(M, N, dtype=torch.bfloat16)
+    if pinned:
+        yh = yh.pin_memory()
+    ws = torch.zeros(A.linear_hostio_workspace_size(M, qw), dtype=torch.uint8, device="cuda")
+    A.linear_hostio(xh, prof, qw, yh, ws)
+    torch.cuda.synchronize()
+    assert torch.equal(yh, y_chunks.cpu())
+    assert torch.allclose(yh.float(), y_whole.cpu(), rtol=2 ** -7, atol=1e-3 * float(y_whole.abs().max()))
+    outs = [torch.zeros_like(yh) for _ in range(3)]
+    wss = [torch.zeros_like(ws) for _ in range(3)]
+    for o, wsi in zip(outs, wss):
+        A.linear_hostio(xh, prof, qw, o, wsi, wait=False)
+    A.linear_hostio_wait()
+    assert all(torch.equal(o, yh) for o in outs)
