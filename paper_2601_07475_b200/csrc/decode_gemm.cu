@@ -13,11 +13,13 @@
 //    griddepcontrol.wait when the caller guarantees the weights were complete before the preceding kernel
 //    started (arc_linear: the weights never depend on the activation quantize that precedes the GEMM),
 //    and the activation stages after it; ring of up to 8 stages;
-//  * epilogue: each thread (one weight row) reads its token columns from TMEM and pushes each fp32
-//    partial into the receive buffer of the CTA that owns the token (m % KS) with st.shared::cluster,
-//    then every warp arrives on the owner's mbarrier (release, cluster scope); the owner sums the KS
-//    partials in rank order (deterministic), scales by alpha = 1/(gs_x gs_w) and stores Y.  Nothing is
-//    read remotely, so the critical path after the MMAs is one DSMEM store burst and one barrier.
+//  * epilogue: each thread (one weight row) reads its token columns from TMEM into a [tokens][128] fp32
+//    slice of its CTA's shared memory; after one cluster barrier the owner of token m (CTA m % KS) reads the
+//    KS slices with ld.shared::cluster (all loads issued before the first add), sums them in rank order
+//    (deterministic), scales by alpha = 1/(gs_x gs_w) and stores Y; a final cluster barrier keeps every
+//    slice alive until its readers are done.  (ARC_DECODE_PULL=0: the push variant -- each CTA sends each
+//    owner its block with one bulk shared::cta -> shared::cluster copy completing on the owner's mbarrier;
+//    measured 2-9 % slower.)
 #include "arc_device.cuh"
 #include "arc_internal.h"
 
@@ -49,6 +51,7 @@ struct DArgs {
   int tpd;              // tokens per destination CTA: ceil(M / ks)
   int spin;             // mbarrier waits without a suspend-time hint
   int ybulk;            // Y rows written with bulk copies (else per-element stores)
+  int pull;             // split-K reduction: owners pull the slices with ld.shared::cluster after a cluster barrier
   const uint8_t* sfx;   // activation scales [roundup(M,128)][Kp/16] (tcgen05 128x4 layout)
   const uint8_t* sfw;   // weight scales [roundup(N,128)][Kp/16]
   const float* gs_x;
@@ -68,9 +71,6 @@ __device__ __forceinline__ void dtrace(const DArgs& a, int i) {
   }
 }
 
-__device__ __forceinline__ void dclk(const DArgs& a, int i, long long c0) {
-  if (a.trace && blockIdx.x < 1024) a.trace[(size_t)blockIdx.x * 8 + i] = (unsigned long long)(clock64() - c0);
-}
 // bulk copy of this CTA's shared memory into another CTA's (cluster addresses of the destination and
 // of its mbarrier, which receives the complete_tx)
 __device__ __forceinline__ void bulk_s2c(uint32_t dst_cluster, uint32_t src_cta, uint32_t bytes, uint32_t bar_cluster) {
@@ -119,6 +119,11 @@ __device__ __forceinline__ void dwait_cluster(uint64_t* bar, uint32_t parity, in
       : "memory");
 }
 __device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
+__device__ __forceinline__ float ld_dsmem_f32(uint32_t cluster_addr) {
+  float v;
+  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(cluster_addr) : "memory");
+  return v;
+}
 __device__ __forceinline__ uint32_t mapa_u32(uint32_t smem_addr, uint32_t rank) {
   uint32_t r;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_addr), "r"(rank));
@@ -170,6 +175,9 @@ __global__ void __launch_bounds__(D_THREADS, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_holder;
 
+  long long ck[4] = {0, 0, 0, 0};  // epilogue clock stamps (trace only; written once at the end)
+  long long clk2 = 0;
+  float alpha_pull = 0.0f;
   if (warp == 0) {
     if (elect_one()) {
       // ---------------------------------------------------------------- producer
@@ -253,7 +261,8 @@ __global__ void __launch_bounds__(D_THREADS, 1)
     dwait(acc_full, 0, args.spin);
     tc_fence_after();
     if (threadIdx.x == 64) dtrace(args, 2);
-    const long long clk2 = clock64();  // stamps 3..6: SM cycles since the accumulator was ready
+    clk2 = clock64();  // stamps 3..6: SM cycles since the accumulator was ready
+    alpha_pull = alpha;
     // Y rows of this CTA's tokens, staged as one [tpd][128] tile after the send staging and written with
     // one bulk copy per token row (no per-element global stores on the critical path)
     const int eb = args.y_fp32 ? 4 : 2;
@@ -274,7 +283,18 @@ __global__ void __launch_bounds__(D_THREADS, 1)
         for (int j = 0; j < 32; ++j)
           if (c + j < args.M) put(c + j, __uint_as_float(v[j]));
       }
-      if (threadIdx.x == 64) { dclk(args, 3, clk2); dclk(args, 4, clk2); dclk(args, 5, clk2); }
+      if (threadIdx.x == 64) ck[0] = ck[1] = ck[2] = clock64() - clk2;
+    } else if (args.pull) {
+      // pull variant: stage [m][n] locally; owners read the ks slices after one cluster barrier (below)
+      for (int c = 0; c < args.M; c += 32) {
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(tmem + ((uint32_t)(q * 32) << 16) + c, v);
+        tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (c + j < args.M) stg[(c + j) * DBW + n] = __uint_as_float(v[j]);
+      }
+      if (threadIdx.x == 64) ck[0] = ck[1] = clock64() - clk2;
     } else {
       int d = 0, slot = 0;
       for (int c = 0; c < args.M; c += 32) {
@@ -292,16 +312,16 @@ __global__ void __launch_bounds__(D_THREADS, 1)
       fence_proxy_async();                 // generic staging writes -> the async (bulk copy) proxy
       named_bar_sync(1, 128);              // all four epilogue warps staged
       if (threadIdx.x == 64) {
-        dclk(args, 3, clk2);
+        ck[0] = clock64() - clk2;
         const int nd = min(ks, args.M);
         for (int dd = 0; dd < nd; ++dd)
           bulk_s2c(mapa_u32(smem_u32(recv) + (uint32_t)r * blk, (uint32_t)dd), smem_u32(stg) + (uint32_t)dd * blk, blk,
                    mapa_u32(smem_u32(recv_bar), (uint32_t)dd));
-        dclk(args, 4, clk2);
+        ck[1] = clock64() - clk2;
       }
       if (r < args.M) {
         dwait(recv_bar, 0, args.spin);
-        if (threadIdx.x == 64) dclk(args, 5, clk2);
+        if (threadIdx.x == 64) ck[2] = clock64() - clk2;
         for (int sl = 0, m = r; m < args.M; ++sl, m += ks) {
           float p[8];
 #pragma unroll
@@ -314,7 +334,7 @@ __global__ void __launch_bounds__(D_THREADS, 1)
         }
       }
     }
-    if (r < args.M) {
+    if (r < args.M && !(args.pull && ks > 1)) {
       const int valid = min(DBW, args.N - tile * DBW);
       const bool bulk_ok = args.ybulk && ((valid * eb) & 15) == 0;
       if (bulk_ok) {
@@ -338,11 +358,48 @@ __global__ void __launch_bounds__(D_THREADS, 1)
       }
     }
     if (threadIdx.x == 64) {
-      dclk(args, 6, clk2);
-      if (args.trace && blockIdx.x < 1024) args.trace[(size_t)blockIdx.x * 8 + 7] = (unsigned long long)(clock64() - clk0);
+      ck[3] = clock64() - clk2;
+      if (args.trace && blockIdx.x < 1024) {
+        for (int i = 0; i < 4; ++i) args.trace[(size_t)blockIdx.x * 8 + 3 + i] = (unsigned long long)ck[i];
+        args.trace[(size_t)blockIdx.x * 8 + 7] = (unsigned long long)(clock64() - clk0);
+      }
     }
   }
   if (warp < 2) cluster_wait();  // (pairs with the arrive after initialisation)
+
+  if (args.pull && ks > 1) {
+    // every CTA's [m][n] slice is staged: one cluster barrier, then the owner of token m (CTA m % ks) reads
+    // the ks slices with ld.shared::cluster (all issued before the first add), sums them in rank order,
+    // scales and stores Y
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    if (warp >= 2 && r < args.M) {
+      const int n = (warp & 3) * 32 + lane;
+      const int gn = tile * DBW + n;
+      if (threadIdx.x == 64) ck[2] = clock64() - clk2;
+      for (int m = r; m < args.M; m += ks) {
+        const uint32_t off = smem_u32(smem) + (uint32_t)(m * DBW + n) * 4u;
+        float p[8];
+#pragma unroll
+        for (int src = 0; src < 8; ++src) p[src] = src < ks ? ld_dsmem_f32(mapa_u32(off, (uint32_t)src)) : 0.0f;
+        float acc = p[0];
+#pragma unroll
+        for (int src = 1; src < 8; ++src)
+          if (src < ks) acc = __fadd_rn(acc, p[src]);
+        const float out = __fmul_rn(acc, alpha_pull);
+        if (gn < args.N) {
+          if (args.y_fp32) static_cast<float*>(args.y)[(int64_t)m * args.ldy + gn] = out;
+          else static_cast<__nv_bfloat16*>(args.y)[(int64_t)m * args.ldy + gn] = __float2bfloat16_rn(out);
+        }
+      }
+      if (threadIdx.x == 64) {
+        ck[3] = clock64() - clk2;
+        if (args.trace && blockIdx.x < 1024) {
+          for (int i = 0; i < 4; ++i) args.trace[(size_t)blockIdx.x * 8 + 3 + i] = (unsigned long long)ck[i];
+          args.trace[(size_t)blockIdx.x * 8 + 7] = (unsigned long long)(clock64() - clk0);
+        }
+      }
+    }
+  }
 
   // every CTA's blocks have landed once every owner has passed its receive wait
   cluster_arrive_relaxed();
@@ -485,6 +542,8 @@ cudaError_t launch_decode_gemm(const GemmProblem& p, const DecodePlan& pl, cudaS
   a.spin = env_spin;
   static const int env_yb = getenv("ARC_DECODE_YBULK") ? atoi(getenv("ARC_DECODE_YBULK")) : 0;
   a.ybulk = env_yb;
+  static const int env_pull = getenv("ARC_DECODE_PULL") ? atoi(getenv("ARC_DECODE_PULL")) : 1;
+  a.pull = env_pull;
   a.trace = trace_slot();
   const size_t smem = decode_smem(pl, p.M);
   static PerDeviceOnce attr_once;
