@@ -242,12 +242,21 @@ ARC_DEV int tile_rows(int base, int64_t rows) {  // valid rows base + 32 i < row
 // MX mode (reading Q25): MXFP4-ARC -- 32-channel blocks (the 16-blocks of lanes 2j, 2j+1,
 // max combined with one shuffle), power-of-two scales 2^e = E8M0_up(amax/6), t = z * 2^-e, written in
 // the NVFP4 physical format with the E4M3 code of 2^(e - c) (gs = 2^-c), so arc_gemm consumes it.
+#ifndef ARC_QUANT_ROLL_ALL
+#define ARC_QUANT_ROLL_ALL 0
+#endif
+constexpr bool kRollAll = ARC_QUANT_ROLL_ALL != 0;  // experiment: roll the plain kernels' loops too
 template <int IPT, int R, int ROWB, int ST, bool NORM, int SILU, bool MX>
 __global__ void __launch_bounds__(1024) arc_quant_kernel(QuantArgs p) {
   extern __shared__ __align__(16) uint8_t smem[];
   constexpr int ROWP = ROWB + 16;
   constexpr int SLOT = R * ROWP;
   constexpr int UB = R * 4;  // staged scale bytes per 4-block unit per tile
+  // The fused producers' per-block bodies (RMSNorm / SiLU-mul + quantize) are large: unrolling them over
+  // the ring's stages and the tile's rows made 250-370 KB kernels that stall on instruction fetch, so those
+  // instantiations keep the stage and row loops rolled (the slot / row offsets become uniform registers).
+  constexpr int UNR_S = (NORM || SILU || kRollAll) ? 1 : ST;
+  constexpr int UNR_R = (NORM || SILU || kRollAll) ? 1 : R;
   const int K = p.K;
   const int npw = p.npw, nrw = p.nrw;
   constexpr uint32_t OSC = SILU == 2 ? 4u : 2u;  // staged bytes per channel index
@@ -393,14 +402,14 @@ __global__ void __launch_bounds__(1024) arc_quant_kernel(QuantArgs p) {
     // the 16 channels they gather (norm16)
     const int r = warp - (npw + nrw + 1);
     for (int j0 = 0; j0 < my_tiles; j0 += ST) {
-#pragma unroll
+#pragma unroll 1
       for (int s = 0; s < ST; ++s) {
         const int j = j0 + s;
         if (j < my_tiles) {
           mbar_wait(&full[s], (j / ST) & 1);
           const int base = tile_base<R>((int)blockIdx.x + j * (int)gridDim.x);
           if (r < tile_rows<R>(base, p.rows) && p.debug != 1 && p.debug != 4) {
-            const float sc = rms_scale_any(smem + s * SLOT + r * ROWP, K, p.eps, lane);
+            const float sc = rms_scale_any<ROWB / 32>(smem + s * SLOT + r * ROWP, K, p.eps, lane);
             if (lane == 0) rscale[s * R + r] = sc;
           }
           __syncwarp();
@@ -447,7 +456,7 @@ __global__ void __launch_bounds__(1024) arc_quant_kernel(QuantArgs p) {
       }
     }
     for (int j0 = 0; j0 < my_tiles; j0 += ST) {
-#pragma unroll
+#pragma unroll UNR_S
       for (int s = 0; s < ST; ++s) {
         const int j = j0 + s;
         if (j < my_tiles) {
@@ -487,7 +496,7 @@ __global__ void __launch_bounds__(1024) arc_quant_kernel(QuantArgs p) {
                 const int pb = pbs[i];
                 uint8_t* cptr = p.codes + (int64_t)base * code_row + pb * 8;
                 uint8_t* sst = st + (pb >> 2) * UB + (pb & 3);
-#pragma unroll
+#pragma unroll UNR_R
                 for (int r = 0; r < R; ++r) {
                   uint32_t sfb = 0;
                   if (r < nr) {
@@ -539,7 +548,7 @@ __global__ void __launch_bounds__(1024) arc_quant_kernel(QuantArgs p) {
       }
     }
     for (int j0 = 0; j0 < my_tiles; j0 += ST) {
-#pragma unroll
+#pragma unroll UNR_S
       for (int s = 0; s < ST; ++s) {
         const int j = j0 + s;
         if (j < my_tiles) {
@@ -1100,7 +1109,7 @@ __global__ void __launch_bounds__(128) arc_rmsnorm_kernel(const uint16_t* x, int
   const int lane = threadIdx.x & 31;
   for (int64_t m = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5); m < rows; m += (int64_t)gridDim.x * 4) {
     const uint8_t* row = reinterpret_cast<const uint8_t*>(x + m * ldx);
-    const float sc = rms_scale_any(row, K, eps, lane);
+    const float sc = rms_scale_any<>(row, K, eps, lane);
     for (int c0 = lane * 8; c0 < K; c0 += 256) {
       const uint4 g = __ldg(reinterpret_cast<const uint4*>(gamma + c0));
       *reinterpret_cast<uint4*>(y + m * ldy + c0) = rms_apply8(*reinterpret_cast<const uint4*>(row + c0 * 2), g, sc);

@@ -190,14 +190,17 @@ ARC_DEV float rms_scale_warp(const uint8_t* row, int K, float eps, int lane) {
   return __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(mean, eps)));
 }
 
+// MAXNB: an upper bound on K/16 known at compile time (the kernel's row-slot size), so only the tree
+// depths that can occur are instantiated (each deeper one is a fully unrolled loop of 2x the code)
+template <int MAXNB = 2048>
 ARC_DEV float rms_scale_any(const uint8_t* row, int K, float eps, int lane) {
   const int nb = K >> 4;
-  if (nb <= 32) return rms_scale_warp<1>(row, K, eps, lane);
-  if (nb <= 64) return rms_scale_warp<2>(row, K, eps, lane);
-  if (nb <= 128) return rms_scale_warp<4>(row, K, eps, lane);
-  if (nb <= 256) return rms_scale_warp<8>(row, K, eps, lane);
-  if (nb <= 512) return rms_scale_warp<16>(row, K, eps, lane);
-  if (nb <= 1024) return rms_scale_warp<32>(row, K, eps, lane);
+  if (MAXNB <= 32 || nb <= 32) return rms_scale_warp<1>(row, K, eps, lane);
+  if (MAXNB <= 64 || nb <= 64) return rms_scale_warp<2>(row, K, eps, lane);
+  if (MAXNB <= 128 || nb <= 128) return rms_scale_warp<4>(row, K, eps, lane);
+  if (MAXNB <= 256 || nb <= 256) return rms_scale_warp<8>(row, K, eps, lane);
+  if (MAXNB <= 512 || nb <= 512) return rms_scale_warp<16>(row, K, eps, lane);
+  if (MAXNB <= 1024 || nb <= 1024) return rms_scale_warp<32>(row, K, eps, lane);
   return rms_scale_warp<64>(row, K, eps, lane);
 }
 
