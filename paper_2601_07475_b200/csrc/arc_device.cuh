@@ -344,6 +344,7 @@ ARC_DEV uint64_t smem_desc(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_byte
   return d;
 }
 constexpr uint32_t kLayoutSwizzle128B = 2;
+constexpr uint32_t kLayoutSwizzle64B = 4;
 constexpr uint32_t kLayoutSwizzleNone = 0;
 
 // Programmatic dependent launch: let the next kernel in the stream start its prologue,

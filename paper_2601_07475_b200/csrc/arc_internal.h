@@ -136,6 +136,9 @@ inline size_t sync_bytes_of(int64_t /*N*/);
 
 // 2-D K-major operand tensor map (uint8 [rows][row_bytes], 128B swizzle, box box_bytes x box_rows).
 bool make_operand_map(CUtensorMap* m, const void* base, int64_t rows, int64_t row_bytes, int box_rows, int box_bytes);
+// the same with a 32 / 64 / 128-byte swizzle (0: none)
+bool make_operand_map_sw(CUtensorMap* m, const void* base, int64_t rows, int64_t row_bytes, int box_rows, int box_bytes,
+                         int swizzle_bytes);
 
 // Every arc_gemm workspace starts with this many bytes of per-tile arrival counters (the
 // decode-size stream-K kernel's), zero before the first use and left zero by every call; the

@@ -86,6 +86,8 @@ struct Args {
   int red_np;
   float* red_mc;
   float* red_peer[8];
+  int tail64;  // NVFP4 1-SM kernel: the last K block holds 64 or 128 K (Kp % 256): it is loaded with the 64-byte-box,
+              // 64B-swizzled tail maps instead of a 128-byte box that the TMA zero-fills past Kp
   int debug;  // perf experiments only (env ARC_GEMM_DEBUG): 1 = no epilogue work, 2 = no scale copies, 3 = no stores, 4 = no TMEM loads,
               // 5 = STG stores, 6 = no TMA store, 7 = MMA ignores the accumulator-free barriers,
               // 8 = MMAs issued twice, 9 = one MMA per stage, 10 = 9 without scale copies (pair kernel; timing only)
@@ -391,7 +393,8 @@ __device__ __forceinline__ void epilogue_tile(const Args& args, const CUtensorMa
 template <int CL, int ST = STAGES, int EW = 1, int FMT = 0>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     arc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                    const __grid_constant__ CUtensorMap tmY, Args args) {
+                    const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUtensorMap tmAt,
+                    const __grid_constant__ CUtensorMap tmBt, Args args) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* epi_stage = smem + ST * STAGE_BYTES;  // [4 warps][EW x 2 KB]
@@ -471,6 +474,36 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           // FMT 3: a 16U4_ALIGN16B load counts the packed bytes (half of what lands in shared memory:
           // 8 code bytes + 8 untouched pad bytes per 16 elements; measured by arc_probe_u4_unpack)
           constexpr uint32_t B_TX = FMT == 3 ? B_BYTES / 2 : B_BYTES;
+          if (FMT == 0 && args.tail64 && kb == nkb - 1) {
+            // last K block of 64 / 128 K: 64-byte boxes (64B swizzle), nothing zero-filled past Kp
+            mbar_expect_tx(&full[stage], (uint32_t)(args.a_rows * 64 + BN * 64 + nk * 512 * ((a_ok ? 1 : 0) + nrb)));
+            tma_load_2d(sA, &tmAt, &full[stage], kb * BKB, mb * BM, pol);
+            if (a_ok) bulk_load(sSFA, args.sfa + ((int64_t)mb * kc_total + kb * CPS) * 512, nk * 512, &full[stage]);
+            if (CL == 1) {
+              tma_load_2d(sB, &tmBt, &full[stage], kb * BKB, nbk * BN, pol);
+              for (int rb = 0; rb < nrb; ++rb)
+                bulk_load(sSFB + rb * 2048, args.sfb + ((int64_t)(2 * nbk + rb) * kc_total + kb * CPS) * 512, nk * 512,
+                          &full[stage]);
+            } else {
+              tma_load_2d_mc(sB + rank * (BN / CL) * 64, &tmBt, &full[stage], kb * BKB, nbk * BN + rank * (BN / CL),
+                             mc_mask, pol);
+              if (CL == 2) {
+                if (rank < nrb)
+                  bulk_load_mc(sSFB + rank * 2048, args.sfb + ((int64_t)(2 * nbk + rank) * kc_total + kb * CPS) * 512,
+                               nk * 512, &full[stage], mc_mask);
+              } else {
+                for (int j = rank; j < 8; j += CL) {
+                  const int rb = j >> 2, kk = j & 3;
+                  if (rb < nrb && kk < nk)
+                    bulk_load_mc(sSFB + rb * 2048 + kk * 512,
+                                 args.sfb + ((int64_t)(2 * nbk + rb) * kc_total + kb * 4 + kk) * 512, 512, &full[stage],
+                                 mc_mask);
+                }
+              }
+            }
+            if (++stage == ST) { stage = 0; phase ^= 1; }
+            continue;
+          }
           mbar_expect_tx(&full[stage], (uint32_t)(args.a_rows * BKB + B_TX + nk * 512 * ((a_ok ? 1 : 0) + nrb)));
           tma_load_2d(sA, &tmA, &full[stage], kb * BKB, mb * BM, pol);
           if (a_ok) bulk_load(sSFA, args.sfa + ((int64_t)mb * kc_total + kb * CPS) * 512, nk * 512, &full[stage]);
@@ -570,9 +603,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             utccp_32x128b_warpx4(tmem + SFB_COL + 8 * kk + 4,
                                  smem_desc(sSFB + 2048 + kk * 512, 0, 128, kLayoutSwizzleNone));
           }
+          const bool t64 = FMT == 0 && args.tail64 && kb == nkb - 1;  // 64-byte rows, 64B swizzle (see producer)
           for (int kk = 0; kk < nk; ++kk) {
-            const uint64_t ad = smem_desc(sA + kk * 32, 16, 1024, kLayoutSwizzle128B);
-            const uint64_t bd = smem_desc(sB + kk * 32, 16, 1024, kLayoutSwizzle128B);
+            const uint64_t ad = t64 ? smem_desc(sA + kk * 32, 16, 512, kLayoutSwizzle64B)
+                                    : smem_desc(sA + kk * 32, 16, 1024, kLayoutSwizzle128B);
+            const uint64_t bd = t64 ? smem_desc(sB + kk * 32, 16, 512, kLayoutSwizzle64B)
+                                    : smem_desc(sB + kk * 32, 16, 1024, kLayoutSwizzle128B);
             mma_nvf4(acc, ad, bd, kIdesc, (kb != kb0) || (kk != 0), tmem + SFA_COL + 4 * kk, tmem + SFB_COL + 8 * kk);
           }
           if (CL == 1) tc_commit(&empty[stage]);
@@ -917,6 +953,22 @@ bool make_u4_unpack_map_probe(CUtensorMap* m, const uint8_t* base, int64_t rows,
 }
 
 
+bool make_operand_map_sw(CUtensorMap* m, const void* base, int64_t rows, int64_t row_bytes, int box_rows, int box_bytes,
+                         int swizzle_bytes) {
+  EncodeTiledFn enc = get_encode_fn();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)row_bytes, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)row_bytes};
+  cuuint32_t box[2] = {(cuuint32_t)box_bytes, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  const CUtensorMapSwizzle sw = swizzle_bytes == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                : swizzle_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                : swizzle_bytes == 32 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_NONE;
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 bool make_operand_map(CUtensorMap* m, const void* base, int64_t rows, int64_t row_bytes, int box_rows, int box_bytes) {
   EncodeTiledFn enc = get_encode_fn();
   if (!enc) return false;
@@ -1058,6 +1110,18 @@ cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t stream, const char** 
   const int64_t row_bytes = (p.fmt == 1 || p.fmt == 3) ? p.Kp : p.Kp / 2;
   const bool b_ok = p.fmt == 3 ? make_u4_unpack_map(&tmB, p.b_codes, p.N, p.Kp, b_rows)
                                : make_map(&tmB, p.b_codes, p.N, row_bytes, b_rows);
+  // tail maps: 64-byte boxes with 64B swizzle for a last K block of 64 / 128 K (Kp % 256), so the TMA does not
+  // zero-fill the second half of a 128-byte box (measured: a half-empty last block cost more than a full one)
+  CUtensorMap tmAt, tmBt;
+  memset(&tmAt, 0, sizeof(tmAt));
+  memset(&tmBt, 0, sizeof(tmBt));
+  static const int env_tail = getenv("ARC_GEMM_TAIL64") ? atoi(getenv("ARC_GEMM_TAIL64")) : 1;
+  const int tail64 = env_tail && p.fmt == 0 && !pl.pair && (p.Kp % 256 == 64 || p.Kp % 256 == 128) ? 1 : 0;
+  if (tail64 && (!make_operand_map_sw(&tmAt, p.a_codes, p.M, row_bytes, a_rows, 64, 64) ||
+                 !make_operand_map_sw(&tmBt, p.b_codes, p.N, row_bytes, b_rows, 64, 64))) {
+    if (detail) *detail = "cuTensorMapEncodeTiled (tail) failed";
+    return cudaErrorInvalidValue;
+  }
   if (!make_map(&tmA, p.a_codes, p.M, row_bytes, a_rows) || !b_ok ||
       (pl.pair && (!make_sf_map(&tmSFA, p.a_sf, (p.M + 127) / 128, p.Kp / 64, 4, 1) ||
                    !make_sf_map(&tmSFB, p.b_sf, (p.N + 127) / 128, p.Kp / 64, CL == 2 ? 4 : 2, 1)))) {
@@ -1117,6 +1181,7 @@ cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t stream, const char** 
   a.y_fp32 = p.y_fp32;
   a.swiglu = p.swiglu;
   a.a_rows = a_rows;
+  a.tail64 = tail64;
   static const int dbg = getenv("ARC_GEMM_DEBUG") ? atoi(getenv("ARC_GEMM_DEBUG")) : 0;
   a.debug = dbg;
   // Keep the smaller operand L2-resident: sweep the tiles along it fastest so each wave of
@@ -1154,17 +1219,17 @@ cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t stream, const char** 
   cudaError_t e = pl.pair ? (CL == 2 ? (st4 ? cudaLaunchKernelEx(&cfg, arc_gemm_pair_kernel<2, 4>, tmA, tmB, tmSFA, tmSFB, tmY, a)
                                                 : cudaLaunchKernelEx(&cfg, arc_gemm_pair_kernel<2, 5>, tmA, tmB, tmSFA, tmSFB, tmY, a))
                                      : cudaLaunchKernelEx(&cfg, arc_gemm_pair_kernel<4, 5>, tmA, tmB, tmSFA, tmSFB, tmY, a))
-                  : (p.fmt == 1 && CL == 1) ? cudaLaunchKernelEx(&cfg, arc_gemm_kernel<1, STAGES, 1, 1>, tmA, tmB, tmY, a)
-                  : (p.fmt == 1 && CL == 2) ? cudaLaunchKernelEx(&cfg, arc_gemm_kernel<2, STAGES, 1, 1>, tmA, tmB, tmY, a)
-                  : (p.fmt == 3 && CL == 1) ? cudaLaunchKernelEx(&cfg, arc_gemm_kernel<1, STAGES, 1, 3>, tmA, tmB, tmY, a)
-                  : (p.fmt == 3 && CL == 2) ? cudaLaunchKernelEx(&cfg, arc_gemm_kernel<2, STAGES, 1, 3>, tmA, tmB, tmY, a)
-                  : (p.fmt == 2 && CL == 1) ? cudaLaunchKernelEx(&cfg, arc_gemm_kernel<1, STAGES, 1, 2>, tmA, tmB, tmY, a)
-                  : (p.fmt == 2 && CL == 2) ? cudaLaunchKernelEx(&cfg, arc_gemm_kernel<2, STAGES, 1, 2>, tmA, tmB, tmY, a)
-                  : CL == 1 ? cudaLaunchKernelEx(&cfg, arc_gemm_kernel<1>, tmA, tmB, tmY, a)
-                  : (CL == 2 && wide) ? cudaLaunchKernelEx(&cfg, arc_gemm_kernel<2, 3, 2>, tmA, tmB, tmY, a)
-                  : CL == 2 ? cudaLaunchKernelEx(&cfg, arc_gemm_kernel<2>, tmA, tmB, tmY, a)
-                  : CL == 4 ? cudaLaunchKernelEx(&cfg, arc_gemm_kernel<4>, tmA, tmB, tmY, a)
-                            : cudaLaunchKernelEx(&cfg, arc_gemm_kernel<8>, tmA, tmB, tmY, a);
+                  : (p.fmt == 1 && CL == 1) ? cudaLaunchKernelEx(&cfg, arc_gemm_kernel<1, STAGES, 1, 1>, tmA, tmB, tmY, tmAt, tmBt, a)
+                  : (p.fmt == 1 && CL == 2) ? cudaLaunchKernelEx(&cfg, arc_gemm_kernel<2, STAGES, 1, 1>, tmA, tmB, tmY, tmAt, tmBt, a)
+                  : (p.fmt == 3 && CL == 1) ? cudaLaunchKernelEx(&cfg, arc_gemm_kernel<1, STAGES, 1, 3>, tmA, tmB, tmY, tmAt, tmBt, a)
+                  : (p.fmt == 3 && CL == 2) ? cudaLaunchKernelEx(&cfg, arc_gemm_kernel<2, STAGES, 1, 3>, tmA, tmB, tmY, tmAt, tmBt, a)
+                  : (p.fmt == 2 && CL == 1) ? cudaLaunchKernelEx(&cfg, arc_gemm_kernel<1, STAGES, 1, 2>, tmA, tmB, tmY, tmAt, tmBt, a)
+                  : (p.fmt == 2 && CL == 2) ? cudaLaunchKernelEx(&cfg, arc_gemm_kernel<2, STAGES, 1, 2>, tmA, tmB, tmY, tmAt, tmBt, a)
+                  : CL == 1 ? cudaLaunchKernelEx(&cfg, arc_gemm_kernel<1>, tmA, tmB, tmY, tmAt, tmBt, a)
+                  : (CL == 2 && wide) ? cudaLaunchKernelEx(&cfg, arc_gemm_kernel<2, 3, 2>, tmA, tmB, tmY, tmAt, tmBt, a)
+                  : CL == 2 ? cudaLaunchKernelEx(&cfg, arc_gemm_kernel<2>, tmA, tmB, tmY, tmAt, tmBt, a)
+                  : CL == 4 ? cudaLaunchKernelEx(&cfg, arc_gemm_kernel<4>, tmA, tmB, tmY, tmAt, tmBt, a)
+                            : cudaLaunchKernelEx(&cfg, arc_gemm_kernel<8>, tmA, tmB, tmY, tmAt, tmBt, a);
   if (e != cudaSuccess) return e;
   if (pl.nsplit > 1) {
     const int64_t total = p.M * p.N;
