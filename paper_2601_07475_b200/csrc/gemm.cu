@@ -86,6 +86,11 @@ struct Args {
   int red_np;
   float* red_mc;
   float* red_peer[8];
+  int mode4;   // CL = 2 kernel launched with a preferred cluster of 4 (NVFP4): a CTA in a 4-CTA cluster shares operands
+              // across the cluster's two pairs -- 1: B multicast to all 4 (raster 0: the pairs hold M-tiles
+              // 2p..2p+3 of one N tile), 2: A halves multicast across the pairs + B within each pair (raster 1: the
+              // pairs hold N tiles n, n+1 of the same two M tiles); CTAs in fallback 2-CTA clusters run as pairs
+  unsigned long long* trace;  // timing experiments only (ARC_TRACE): [cta][8] = entry, exit, cluster size, tiles
   int tail64;  // NVFP4 1-SM kernel: the last K block holds 64 or 128 K (Kp % 256): it is loaded with the 64-byte-box,
               // 64B-swizzled tail maps instead of a 128-byte box that the TMA zero-fills past Kp
   int debug;  // perf experiments only (env ARC_GEMM_DEBUG): 1 = no epilogue work, 2 = no scale copies, 3 = no stores, 4 = no TMEM loads,
@@ -394,7 +399,8 @@ template <int CL, int ST = STAGES, int EW = 1, int FMT = 0>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     arc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUtensorMap tmAt,
-                    const __grid_constant__ CUtensorMap tmBt, Args args) {
+                    const __grid_constant__ CUtensorMap tmBt, const __grid_constant__ CUtensorMap tmA64,
+                    const __grid_constant__ CUtensorMap tmB64, Args args) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* epi_stage = smem + ST * STAGE_BYTES;  // [4 warps][EW x 2 KB]
@@ -405,6 +411,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* buf_free = ovl_free + 1;  // [2]
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(buf_free + 2);
 
+  unsigned long long t_entry = 0;
+  if (args.trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_entry));
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int M = args.M, N = args.N, Kp = args.Kp;
@@ -413,9 +421,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const int num_mp = (num_m + CL - 1) / CL;   // M-tile groups (one per cluster step)
   const int nsplit = args.nsplit;
   const int num_tiles = num_mp * num_n * nsplit;  // cluster work items (split-K innermost)
-  const int rank = CL == 1 ? 0 : (int)cluster_ctarank();
+  // CL = 2 kernel in a (preferred) 4-CTA cluster: crank 0..3, pair pp = crank / 2, rank = the CTA's row in
+  // its pair; tiles are still assigned per pair (cid = blockIdx / 2), so 2- and 4-CTA clusters coexist
+  const int crank = CL == 1 ? 0 : (int)cluster_ctarank();
+  const int nct = CL == 1 ? 1 : (int)cluster_nctarank();
+  const int rank = CL == 2 ? (crank & 1) : crank;
+  const int pp = CL == 2 ? (crank >> 1) : 0;
+  const int mode4 = (FMT == 0 && CL == 2 && nct == 4) ? args.mode4 : 0;
   const int cid = blockIdx.x / CL, ncl = gridDim.x / CL;
-  const uint16_t mc_mask = (uint16_t)((1u << CL) - 1u);
+  const uint16_t mc_mask = mode4 ? (uint16_t)0xF
+                                 : (uint16_t)(((1u << CL) - 1u) << (CL == 2 ? 2 * pp : 0));  // the pair / cluster
+  const uint16_t pair_mask = (uint16_t)(3u << (2 * pp));
+  const uint16_t amc_mask = (uint16_t)((1u << rank) | (1u << (rank + 2)));  // mode 2: the CTAs sharing this A tile
   // FMT 0: NVFP4 (256 K per stage, 4 scale chunks of 64 K, UE4M3 per 16); FMT 1: MXFP8 (the Fig.8a
   // comparison format: 128 E4M3 K per stage, 1 scale chunk of 128 K, UE8M0 per 32).  Both move 128 B per
   // operand row per stage.
@@ -432,7 +449,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < ST; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], CL);  // one MMA commit from every CTA of the cluster
+      mbar_init(&empty[s], mode4 ? 4 : CL);  // one MMA commit from every CTA the slot's data came from / went to
     }
     mbar_init(tfull, 1);
     mbar_init(ovl_free, 4);  // one arrival per epilogue warp
@@ -500,6 +517,39 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                                  mc_mask);
                 }
               }
+            }
+            if (++stage == ST) { stage = 0; phase ^= 1; }
+            continue;
+          }
+          if (FMT == 0 && CL == 2 && mode4) {
+            mbar_expect_tx(&full[stage], (uint32_t)(args.a_rows * BKB + B_TX + nk * 512 * ((a_ok ? 1 : 0) + nrb)));
+            if (mode4 == 1) {
+              // B shared by the 4 CTAs (M tiles 2p..2p+3 of N tile nbk): a quarter each, multicast to all
+              tma_load_2d(sA, &tmA, &full[stage], kb * BKB, mb * BM, pol);
+              if (a_ok) bulk_load(sSFA, args.sfa + ((int64_t)mb * kc_total + kb * CPS) * 512, nk * 512, &full[stage]);
+              tma_load_2d_mc(sB + crank * (B_BYTES / 4), &tmB64, &full[stage], kb * BKB, nbk * BN + crank * (BN / 4),
+                             (uint16_t)0xF, pol);
+              for (int j = crank; j < 8; j += 4) {  // chunk j = (row block j/4, K chunk j%4)
+                const int rb = j >> 2, kk = j & 3;
+                if (rb < nrb && kk < nk)
+                  bulk_load_mc(sSFB + rb * 2048 + kk * 512,
+                               args.sfb + ((int64_t)(2 * nbk + rb) * kc_total + kb * 4 + kk) * 512, 512, &full[stage],
+                               (uint16_t)0xF);
+              }
+            } else {
+              // pairs hold N tiles nbk, nbk+1 of the same two M tiles: the A tile (and its scales) is shared with
+              // the same-row CTA of the other pair (half each), B within the pair as usual
+              tma_load_2d_mc(sA + pp * (A_BYTES / 2), &tmA64, &full[stage], kb * BKB, mb * BM + pp * (BM / 2), amc_mask,
+                             pol);
+              if (a_ok)
+                for (int kk = pp; kk < nk; kk += 2)
+                  bulk_load_mc(sSFA + kk * 512, args.sfa + ((int64_t)mb * kc_total + kb * CPS + kk) * 512, 512,
+                               &full[stage], amc_mask);
+              tma_load_2d_mc(sB + rank * (B_BYTES / 2), &tmB, &full[stage], kb * BKB, nbk * BN + rank * (BN / 2),
+                             pair_mask, pol);
+              if (rank < nrb)
+                bulk_load_mc(sSFB + rank * 2048, args.sfb + ((int64_t)(2 * nbk + rank) * kc_total + kb * CPS) * 512,
+                             nk * 512, &full[stage], pair_mask);
             }
             if (++stage == ST) { stage = 0; phase ^= 1; }
             continue;
@@ -637,6 +687,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   tc_fence_before();
   __syncthreads();
+  if (args.trace && threadIdx.x == 0 && blockIdx.x < 1024) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    args.trace[(size_t)blockIdx.x * 8 + 0] = t_entry;
+    args.trace[(size_t)blockIdx.x * 8 + 1] = t;
+    args.trace[(size_t)blockIdx.x * 8 + 2] = (unsigned long long)nct;
+    args.trace[(size_t)blockIdx.x * 8 + 3] = (unsigned long long)cluster_ctarank();
+  }
   if (CL > 1) cluster_sync();  // no CTA leaves while its peer may still multicast into it
   if (warp == 1) {
     tc_fence_after();
@@ -1122,6 +1180,25 @@ cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t stream, const char** 
     if (detail) *detail = "cuTensorMapEncodeTiled (tail) failed";
     return cudaErrorInvalidValue;
   }
+  // preferred clusters of 4 over the CL = 2 kernel (NVFP4 prefill): operands shared across the two pairs of a
+  // 4-CTA cluster where the GPC packs one, plain pairs elsewhere (ARC_GEMM_PREF4=0 disables)
+  static const int env_pref4 = getenv("ARC_GEMM_PREF4") ? atoi(getenv("ARC_GEMM_PREF4")) : 1;
+  const int64_t num_m_ = (p.M + BM - 1) / BM, num_n_ = (p.N + BN - 1) / BN;
+  const int raster_ = getenv("ARC_GEMM_RASTER") ? atoi(getenv("ARC_GEMM_RASTER")) : (p.M > p.N ? 1 : 0);
+  const int64_t grid_pre = std::min<int64_t>(((num_m_ + CL - 1) / CL) * num_n_ * pl.nsplit, max_clusters(CL, pl.pair)) * CL;
+  // measured (profiles/r2_gemm_variants_same_box.txt): B shared 4 ways (raster 0) 2.6 % faster on gate_up; the
+  // A-sharing 2x2 mode (raster 1) made the 4-CTA clusters ~10 % slower per tile than plain pairs -> opt-in only
+  // (ARC_GEMM_PREF4=2)
+  const bool pref4 = env_pref4 && p.fmt == 0 && CL == 2 && !pl.pair && !wide && pl.nsplit == 1 && a_rows == BM &&
+                     grid_pre % 4 == 0 &&
+                     (raster_ == 0 ? ((num_m_ + 1) / 2) % 2 == 0 : (env_pref4 == 2 && num_n_ % 2 == 0));
+  CUtensorMap tmA64, tmB64;
+  memset(&tmA64, 0, sizeof(tmA64));
+  memset(&tmB64, 0, sizeof(tmB64));
+  if (pref4 && (!make_map(&tmA64, p.a_codes, p.M, row_bytes, BM / 2) || !make_map(&tmB64, p.b_codes, p.N, row_bytes, BN / 4))) {
+    if (detail) *detail = "cuTensorMapEncodeTiled (cluster-4 boxes) failed";
+    return cudaErrorInvalidValue;
+  }
   if (!make_map(&tmA, p.a_codes, p.M, row_bytes, a_rows) || !b_ok ||
       (pl.pair && (!make_sf_map(&tmSFA, p.a_sf, (p.M + 127) / 128, p.Kp / 64, 4, 1) ||
                    !make_sf_map(&tmSFB, p.b_sf, (p.N + 127) / 128, p.Kp / 64, CL == 2 ? 4 : 2, 1)))) {
@@ -1181,7 +1258,9 @@ cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t stream, const char** 
   a.y_fp32 = p.y_fp32;
   a.swiglu = p.swiglu;
   a.a_rows = a_rows;
-  a.tail64 = tail64;
+  a.tail64 = pref4 ? 0 : tail64;
+  a.mode4 = pref4 ? (raster_ == 0 ? 1 : 2) : 0;
+  a.trace = (pl.pair || pl.nsplit > 1) ? nullptr : trace_slot();
   static const int dbg = getenv("ARC_GEMM_DEBUG") ? atoi(getenv("ARC_GEMM_DEBUG")) : 0;
   a.debug = dbg;
   // Keep the smaller operand L2-resident: sweep the tiles along it fastest so each wave of
@@ -1207,29 +1286,33 @@ cudaError_t launch_gemm(const GemmProblem& p, cudaStream_t stream, const char** 
   cfg.dynamicSmemBytes = pl.pair ? p_smem_bytes(st4 ? 4 : 5) + (p.swiglu ? P_SILU_TAB_BYTES : 0)
                                   : (wide ? gemm_smem_bytes(3, 2) : SMEM_BYTES);
   cfg.stream = stream;
-  cudaLaunchAttribute attr[2];
+  cudaLaunchAttribute attr[3];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = CL;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[1].val.programmaticStreamSerializationAllowed = 1;
+  attr[2].id = cudaLaunchAttributePreferredClusterDimension;
+  attr[2].val.preferredClusterDim.x = 4;
+  attr[2].val.preferredClusterDim.y = 1;
+  attr[2].val.preferredClusterDim.z = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 2;
+  cfg.numAttrs = pref4 ? 3 : 2;
   cudaError_t e = pl.pair ? (CL == 2 ? (st4 ? cudaLaunchKernelEx(&cfg, arc_gemm_pair_kernel<2, 4>, tmA, tmB, tmSFA, tmSFB, tmY, a)
                                                 : cudaLaunchKernelEx(&cfg, arc_gemm_pair_kernel<2, 5>, tmA, tmB, tmSFA, tmSFB, tmY, a))
                                      : cudaLaunchKernelEx(&cfg, arc_gemm_pair_kernel<4, 5>, tmA, tmB, tmSFA, tmSFB, tmY, a))
-                  : (p.fmt == 1 && CL == 1) ? cudaLaunchKernelEx(&cfg, arc_gemm_kernel<1, STAGES, 1, 1>, tmA, tmB, tmY, tmAt, tmBt, a)
-                  : (p.fmt == 1 && CL == 2) ? cudaLaunchKernelEx(&cfg, arc_gemm_kernel<2, STAGES, 1, 1>, tmA, tmB, tmY, tmAt, tmBt, a)
-                  : (p.fmt == 3 && CL == 1) ? cudaLaunchKernelEx(&cfg, arc_gemm_kernel<1, STAGES, 1, 3>, tmA, tmB, tmY, tmAt, tmBt, a)
-                  : (p.fmt == 3 && CL == 2) ? cudaLaunchKernelEx(&cfg, arc_gemm_kernel<2, STAGES, 1, 3>, tmA, tmB, tmY, tmAt, tmBt, a)
-                  : (p.fmt == 2 && CL == 1) ? cudaLaunchKernelEx(&cfg, arc_gemm_kernel<1, STAGES, 1, 2>, tmA, tmB, tmY, tmAt, tmBt, a)
-                  : (p.fmt == 2 && CL == 2) ? cudaLaunchKernelEx(&cfg, arc_gemm_kernel<2, STAGES, 1, 2>, tmA, tmB, tmY, tmAt, tmBt, a)
-                  : CL == 1 ? cudaLaunchKernelEx(&cfg, arc_gemm_kernel<1>, tmA, tmB, tmY, tmAt, tmBt, a)
-                  : (CL == 2 && wide) ? cudaLaunchKernelEx(&cfg, arc_gemm_kernel<2, 3, 2>, tmA, tmB, tmY, tmAt, tmBt, a)
-                  : CL == 2 ? cudaLaunchKernelEx(&cfg, arc_gemm_kernel<2>, tmA, tmB, tmY, tmAt, tmBt, a)
-                  : CL == 4 ? cudaLaunchKernelEx(&cfg, arc_gemm_kernel<4>, tmA, tmB, tmY, tmAt, tmBt, a)
-                            : cudaLaunchKernelEx(&cfg, arc_gemm_kernel<8>, tmA, tmB, tmY, tmAt, tmBt, a);
+                  : (p.fmt == 1 && CL == 1) ? cudaLaunchKernelEx(&cfg, arc_gemm_kernel<1, STAGES, 1, 1>, tmA, tmB, tmY, tmAt, tmBt, tmA64, tmB64, a)
+                  : (p.fmt == 1 && CL == 2) ? cudaLaunchKernelEx(&cfg, arc_gemm_kernel<2, STAGES, 1, 1>, tmA, tmB, tmY, tmAt, tmBt, tmA64, tmB64, a)
+                  : (p.fmt == 3 && CL == 1) ? cudaLaunchKernelEx(&cfg, arc_gemm_kernel<1, STAGES, 1, 3>, tmA, tmB, tmY, tmAt, tmBt, tmA64, tmB64, a)
+                  : (p.fmt == 3 && CL == 2) ? cudaLaunchKernelEx(&cfg, arc_gemm_kernel<2, STAGES, 1, 3>, tmA, tmB, tmY, tmAt, tmBt, tmA64, tmB64, a)
+                  : (p.fmt == 2 && CL == 1) ? cudaLaunchKernelEx(&cfg, arc_gemm_kernel<1, STAGES, 1, 2>, tmA, tmB, tmY, tmAt, tmBt, tmA64, tmB64, a)
+                  : (p.fmt == 2 && CL == 2) ? cudaLaunchKernelEx(&cfg, arc_gemm_kernel<2, STAGES, 1, 2>, tmA, tmB, tmY, tmAt, tmBt, tmA64, tmB64, a)
+                  : CL == 1 ? cudaLaunchKernelEx(&cfg, arc_gemm_kernel<1>, tmA, tmB, tmY, tmAt, tmBt, tmA64, tmB64, a)
+                  : (CL == 2 && wide) ? cudaLaunchKernelEx(&cfg, arc_gemm_kernel<2, 3, 2>, tmA, tmB, tmY, tmAt, tmBt, tmA64, tmB64, a)
+                  : CL == 2 ? cudaLaunchKernelEx(&cfg, arc_gemm_kernel<2>, tmA, tmB, tmY, tmAt, tmBt, tmA64, tmB64, a)
+                  : CL == 4 ? cudaLaunchKernelEx(&cfg, arc_gemm_kernel<4>, tmA, tmB, tmY, tmAt, tmBt, tmA64, tmB64, a)
+                            : cudaLaunchKernelEx(&cfg, arc_gemm_kernel<8>, tmA, tmB, tmY, tmAt, tmBt, tmA64, tmB64, a);
   if (e != cudaSuccess) return e;
   if (pl.nsplit > 1) {
     const int64_t total = p.M * p.N;
