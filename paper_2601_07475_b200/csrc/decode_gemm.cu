@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(D_THREADS, 1)
   const int nst = args.nst, stage_bytes = args.stage_bytes;
   const int x_bytes = args.a_rows * DBKB;
   float* recv = reinterpret_cast<float*>(smem + nst * stage_bytes);  // [ks][tpd][128] fp32 partials pushed here
-  uint64_t* full = reinterpret_cast<uint64_t*>(recv + args.ks * args.tpd * DBW);
+  uint64_t* full = reinterpret_cast<uint64_t*>(recv + (args.ks == 1 ? 0 : args.ks * args.tpd * DBW));
   uint64_t* empty = full + D_MAX_STAGES;
   uint64_t* acc_full = empty + D_MAX_STAGES;
   uint64_t* recv_bar = acc_full + 1;
@@ -266,7 +266,7 @@ __global__ void __launch_bounds__(D_THREADS, 1)
     // Y rows of this CTA's tokens, staged as one [tpd][128] tile after the send staging and written with
     // one bulk copy per token row (no per-element global stores on the critical path)
     const int eb = args.y_fp32 ? 4 : 2;
-    uint8_t* ytile = smem + (size_t)ks * blk;
+    uint8_t* ytile = ks == 1 ? smem : smem + (size_t)ks * blk;  // (ks = 1: no send staging)
     const int gn = tile * DBW + n;
     auto put = [&](int sl, float acc) {
       const float out = __fmul_rn(acc, alpha);
@@ -376,19 +376,30 @@ __global__ void __launch_bounds__(D_THREADS, 1)
       const int n = (warp & 3) * 32 + lane;
       const int gn = tile * DBW + n;
       if (threadIdx.x == 64) ck[2] = clock64() - clk2;
-      for (int m = r; m < args.M; m += ks) {
-        const uint32_t off = smem_u32(smem) + (uint32_t)(m * DBW + n) * 4u;
-        float p[8];
+      // up to 4 of this CTA's tokens per round, all 4 x ks remote loads issued before the first add
+      for (int m0 = r; m0 < args.M; m0 += 4 * ks) {
+        float p[4][8];
 #pragma unroll
-        for (int src = 0; src < 8; ++src) p[src] = src < ks ? ld_dsmem_f32(mapa_u32(off, (uint32_t)src)) : 0.0f;
-        float acc = p[0];
+        for (int u = 0; u < 4; ++u) {
+          const int m = m0 + u * ks;
+          const uint32_t off = smem_u32(smem) + (uint32_t)(m * DBW + n) * 4u;
 #pragma unroll
-        for (int src = 1; src < 8; ++src)
-          if (src < ks) acc = __fadd_rn(acc, p[src]);
-        const float out = __fmul_rn(acc, alpha_pull);
-        if (gn < args.N) {
-          if (args.y_fp32) static_cast<float*>(args.y)[(int64_t)m * args.ldy + gn] = out;
-          else static_cast<__nv_bfloat16*>(args.y)[(int64_t)m * args.ldy + gn] = __float2bfloat16_rn(out);
+          for (int src = 0; src < 8; ++src)
+            p[u][src] = (src < ks && m < args.M) ? ld_dsmem_f32(mapa_u32(off, (uint32_t)src)) : 0.0f;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int m = m0 + u * ks;
+          if (m >= args.M) break;
+          float acc = p[u][0];
+#pragma unroll
+          for (int src = 1; src < 8; ++src)
+            if (src < ks) acc = __fadd_rn(acc, p[u][src]);
+          const float out = __fmul_rn(acc, alpha_pull);
+          if (gn < args.N) {
+            if (args.y_fp32) static_cast<float*>(args.y)[(int64_t)m * args.ldy + gn] = out;
+            else static_cast<__nv_bfloat16*>(args.y)[(int64_t)m * args.ldy + gn] = __float2bfloat16_rn(out);
+          }
         }
       }
       if (threadIdx.x == 64) {
@@ -449,7 +460,7 @@ static int decode_max_clusters(int ks, size_t smem) {
 
 static size_t decode_smem(const DecodePlan& pl, int64_t M) {
   const int64_t tpd = (M + pl.ks - 1) / pl.ks;
-  return (size_t)pl.nst * pl.stage_bytes + (size_t)pl.ks * tpd * DBW * 4 + 1024 + 256;
+  return (size_t)pl.nst * pl.stage_bytes + (pl.ks == 1 ? 0 : (size_t)pl.ks * tpd * DBW * 4) + 1024 + 256;
 }
 
 DecodePlan plan_decode(int64_t M, int64_t N, int64_t Kp) {
@@ -502,7 +513,9 @@ DecodePlan plan_decode(int64_t M, int64_t N, int64_t Kp) {
   if (best_grid < 0 || (ks_hi == 1 && env_nst == 0)) {  // one CTA per tile, two per SM
     pl.ks = 1;
     pl.grid = pl.n_tiles;
-    pl.nst = (int)std::max<int64_t>(2, std::min<int64_t>({pl.nkb, 4, (int64_t)D_MAX_STAGES}));
+    // as many stages as leave room for two CTAs per SM (the grid then runs in one wave up to 296 tiles)
+    const int64_t fit2 = (113 * 1024 - 1024 - 1280) / pl.stage_bytes;
+    pl.nst = (int)std::max<int64_t>(2, std::min<int64_t>({pl.nkb, 4, fit2}));
   }
   if (getenv("ARC_DECODE_VERBOSE"))
     fprintf(stderr, "arc_decode: M=%lld N=%lld Kp=%lld tiles=%lld nkb=%lld -> ks=%d grid=%lld nst=%d smem=%zu\n",
