@@ -1034,10 +1034,12 @@ cudaError_t launch_quant(const void* x, int64_t rows, int K, int64_t ld, const i
   // decode-size activations: the direct-gather kernel (ARC_QUANT_SMALL=0 keeps the ring kernel)
   static const int env_small = getenv("ARC_QUANT_SMALL") ? atoi(getenv("ARC_QUANT_SMALL")) : 1;
   if (env_small && rows <= 64 && !weight_mode && !a.norm && up_off == -1 && !mx) {
+    static const int env_tpb = getenv("ARC_QSMALL_TPB") ? atoi(getenv("ARC_QSMALL_TPB")) : 256;
+    const int tpb = (env_tpb == 64 || env_tpb == 128 || env_tpb == 256) ? env_tpb : 256;
     cudaLaunchConfig_t cfg;
     memset(&cfg, 0, sizeof(cfg));
-    cfg.gridDim = dim3((unsigned)((rows * NB + 255) / 256));
-    cfg.blockDim = dim3(256);
+    cfg.gridDim = dim3((unsigned)((rows * NB + tpb - 1) / tpb));
+    cfg.blockDim = dim3(tpb);
     cfg.stream = stream;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
