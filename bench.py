@@ -377,6 +377,53 @@ def decode_sweep(A, sites, device, peaks, Ms=(1, 4, 16, 32, 64)):
     return out
 
 
+QWEN_SITES = {  # (site, K, N): BASELINE configs[2] (Qwen2.5-7B / 32B linear shapes)
+    "qwen2.5-7b": [("qkv", 3584, 4608), ("down", 18944, 3584)],
+    "qwen2.5-32b": [("qkv", 5120, 7168), ("down", 27648, 5120)],
+}
+
+
+def s_sweep(A, device, M=2048, Ss=(0, 64, 128, 256)):
+    """BASELINE configs[2]: GEMM time vs the augmented channel count S on Qwen2.5-7B / 32B shapes (the
+    paper's Fig.8a question): arc_gemm of the quantized operands, CUDA graph of 5 launches."""
+    out = []
+    for model, sites in QWEN_SITES.items():
+        for site, K, N in sites:
+            st = synth.Structure(K, 128, seed=K)
+            x = synth.activation(M, K, st, seed=K + 1, device=device)
+            w = synth.weight(N, K, seed=N, device=device)
+            y = torch.empty(M, N, dtype=torch.bfloat16, device=device)
+            base = A.calibrate([x[:1024]], s_override=0)
+            perm = base.perm.cpu().numpy()
+            rec = {"model": model, "site": site, "M": M, "K": K, "N": N, "by_S": []}
+            for S in Ss:
+                prof = A.profile_from(perm, S, float(base.gs.item()))
+                qw = A.quantize_weight(w, prof)
+                codes, sf = A.quantize_activation(x, prof)
+                ms = time_graph(lambda: A.gemm(codes, sf, prof.gs, qw, out=y), reps=5)
+                rec["by_S"].append({"S": S, "gemm_us": ms * 1e3, "tflops_K_plus_S": 2.0 * M * N * (K + S) / (ms * 1e-3) / 1e12})
+                del qw, codes, sf
+            t0 = rec["by_S"][0]["gemm_us"]
+            for r in rec["by_S"]:
+                r["time_vs_S0"] = r["gemm_us"] / t0
+            out.append(rec)
+            del x, w, y
+            torch.cuda.empty_cache()
+    return out
+
+
+def layer_chain_config5():
+    """BASELINE configs[4]: scripts/layer_chain.py (one LLaMA-3-8B decoder layer's linear chain with fused
+    producers at 16 x 2048 tokens vs BF16 cuBLAS and plain NVFP4) in a subprocess; its JSON summary."""
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "scripts", "layer_chain.py")], capture_output=True, text=True,
+                       timeout=600)
+    if r.returncode != 0:
+        return {"error": (r.stderr or "")[-400:]}
+    d = json.loads(r.stdout.strip().splitlines()[-1])
+    return {"M_tokens": d["M_tokens"], "us": d["us"], "arc_speedup_vs_bf16": d["arc_speedup_vs_bf16"],
+            "arc_vs_nvfp4_overhead": d["arc_vs_nvfp4_overhead"], "fusion_saving_vs_unfused": d["fusion_saving_vs_unfused"]}
+
+
 def quantize_streaming(A, device, peaks, reps=5):
     """The quantize pass at streaming sizes (footprint >= 4x the 126 MB L2, so every launch reads its
     input from HBM): M=65536 x K=4096 and M=16384 x K=14336, S = 128."""
@@ -460,6 +507,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-decode", action="store_true")
     ap.add_argument("--no-streaming", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip the config-3 S sweep and the config-5 layer chain")
     ap.add_argument("--tp-reduce", default="nccl", choices=["nccl", "fused"],
                     help="N>1 row-parallel sites: NCCL all-reduce after the GEMM, or the reduction fused into the GEMM "
                          "epilogue over symmetric memory (NVLS multimem / P2P)")
@@ -626,6 +674,9 @@ def main():
         out["decode"] = decode_sweep(A, sites, device, peaks)
     if not args.no_streaming and world == 1:
         out["quantize_streaming"] = quantize_streaming(A, device, peaks)
+    if not args.no_extras and world == 1:
+        out["config3_s_sweep"] = s_sweep(A, device)
+        out["config5_layer_chain"] = layer_chain_config5()
 
     # e2e through the public API: every step copies the step's inputs from pinned host memory to the
     # device and the outputs back (world 1: the C-ABI host-buffer call arc_linear_hostio does both
