@@ -39,3 +39,27 @@ for (M, K, S) in [(16, 256, 32), (130, 1024, 64)]:
     A.gemm_swiglu(c1, s1, prof.gs, qgu)
     torch.cuda.synchronize()
     print("ok producers/mx/swiglu", M, K, S)
+
+# round 2: decode-size cluster split-K GEMM (pull reduction, ks = 1 and ks > 1), the direct-gather decode quantize,
+# the preferred-cluster-4 prefill GEMM (raster 0) and the pipelined host-IO linear
+for (M, K, N, S) in [(1, 1024, 384, 64), (13, 2048, 300, 32), (64, 4096, 1024, 128), (4, 512, 20000, 16)]:
+    st = synth.Structure(K, max(S, 16), seed=11)
+    prof = A.calibrate([synth.activation(256, K, st, seed=12, device="cuda")], s_override=S)
+    qw = A.quantize_weight(synth.weight(N, K, seed=13, device="cuda"), prof)
+    x = synth.activation(M, K, st, seed=14, device="cuda")
+    A.linear(x, prof, qw)
+    A.linear(x, prof, qw, out_dtype=torch.float32)
+    torch.cuda.synchronize()
+    print("ok decode", M, K, N, S)
+for (M, K, N, S) in [(512, 1024, 2048, 64), (1024, 2048, 4096, 128)]:
+    st = synth.Structure(K, max(S, 16), seed=15)
+    prof = A.calibrate([synth.activation(256, K, st, seed=16, device="cuda")], s_override=S)
+    qw = A.quantize_weight(synth.weight(N, K, seed=17, device="cuda"), prof)
+    x = synth.activation(M, K, st, seed=18, device="cuda")
+    A.linear(x, prof, qw)
+    xh = x.cpu().pin_memory()
+    yh = torch.empty(M, N, dtype=torch.bfloat16).pin_memory()
+    ws = torch.zeros(A.linear_hostio_workspace_size(M, qw), dtype=torch.uint8, device="cuda")
+    A.linear_hostio(xh, prof, qw, yh, ws)
+    torch.cuda.synchronize()
+    print("ok prefill pref4 / hostio", M, K, N, S)
