@@ -677,6 +677,13 @@ def main():
     if not args.no_extras and world == 1:
         out["config3_s_sweep"] = s_sweep(A, device)
         out["config5_layer_chain"] = layer_chain_config5()
+        if workload == "llama3-8b":
+            # the decode path on the LLaMA-3-70B layer's weights (488 MB per 4-site step, configs[3] shapes
+            # unsharded): the fixed per-launch latencies that bound the 8B step are amortized there
+            s70 = build_sites(A, 128, 0, 1, device, workload="llama3-70b", cal_rows=1024)
+            out["decode_llama3_70b_layer"] = decode_sweep(A, s70, device, peaks, Ms=(1, 16, 64))
+            del s70
+            torch.cuda.empty_cache()
 
     # e2e through the public API: every step copies the step's inputs from pinned host memory to the
     # device and the outputs back (world 1: the C-ABI host-buffer call arc_linear_hostio does both
