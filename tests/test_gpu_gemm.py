@@ -190,12 +190,16 @@ def test_decode_splitk_parity(A, M, N, K, S):
 @pytest.mark.parametrize("env", [{"ARC_GEMM_PAIR": "1", "ARC_GEMM_CLP": "2"}, {"ARC_GEMM_PAIR": "1", "ARC_GEMM_CLP": "4"},
                                  {"ARC_GEMM_CL": "1"}, {"ARC_GEMM_CL": "4"}, {"ARC_GEMM_CL": "8"},
                                  {"ARC_GEMM_RASTER": "1"}, {"ARC_GEMM_RASTER": "0"}, {"ARC_GEMM_STREAM": "1"},
-                                 {"ARC_GEMM_EPI": "2"}],
-                         ids=["pair2", "pair4", "cl1", "cl4", "cl8", "raster1", "raster0", "stream", "epi2"])
+                                 {"ARC_GEMM_EPI": "2"}, {"ARC_GEMM_PREF4": "0"}, {"ARC_GEMM_PREF4": "2"},
+                                 {"ARC_GEMM_TAIL64": "0"}, {"ARC_DECODE_PULL": "0"}, {"ARC_GEMM_DECODE": "0"},
+                                 {"ARC_DECODE_KSMAX": "8"}],
+                         ids=["pair2", "pair4", "cl1", "cl4", "cl8", "raster1", "raster0", "stream", "epi2", "pref4_off",
+                              "pref4_2x2", "tail64_off", "decode_push", "decode_splitk", "decode_ks8"])
 def test_kernel_variants(env):
     """The non-default GEMM kernels/schedules (2-SM cta_group::2 pairs, 4-CTA clusters with
-    multicast B, single-CTA, both tile orders) through the same parity tests, in a fresh
-    process (the selection is read once per process)."""
+    multicast B, single-CTA, both tile orders, the preferred-cluster modes, the full-box tail, and the
+    decode-size variants: bulk-copy push reduction, the split-K + reduce-kernel path, 8-CTA clusters)
+    through the same parity tests, in a fresh process (the selection is read once per process)."""
     import os
     import subprocess
     import sys
