@@ -100,6 +100,10 @@ def lib():
         L.or_quantize_weight.argtypes = [P, i64, i32, i64, P, i32, f32, i32, P, P]
         L.or_calib_absmax.restype = i32
         L.or_calib_absmax.argtypes = [P, i64, i32, i64, P]
+        L.or_f16_to_f32.restype = ctypes.c_float
+        L.or_f16_to_f32.argtypes = [ctypes.c_uint16]
+        L.or_set_input_fp16.restype = None
+        L.or_set_input_fp16.argtypes = [i32]
         L.or_select_outliers.restype = i32
         L.or_select_outliers.argtypes = [P, i32, i32, P, P, P, P, P]
         L.or_gemm_exact.restype = None
@@ -153,6 +157,36 @@ class OracleError(RuntimeError):
 def _check(rc: int):
     if rc != 0:
         raise OracleError({2: "shape", 7: "non-finite input"}.get(rc, f"rc={rc}"))
+
+
+def as_fp16_bits(x) -> np.ndarray:
+    """Accept a torch float16 tensor or a uint16 array of IEEE binary16 bits."""
+    if hasattr(x, "view") and hasattr(x, "dtype") and str(x.dtype) == "torch.float16":
+        import torch
+        return x.detach().cpu().contiguous().view(torch.int16).numpy().view(np.uint16)
+    a = np.ascontiguousarray(x)
+    assert a.dtype == np.uint16
+    return a
+
+
+def f16_to_f32(bits: int) -> float:
+    """The oracle's IEEE binary16 decode (arc_oracle.c or_f16_to_f32)."""
+    return float(lib().or_f16_to_f32(int(bits)))
+
+
+class _InputFp16:
+    """Within the block the C quantizers / calibration read their 16-bit rows as IEEE fp16 (arc_dtype_t
+    ARC_FP16) instead of bf16."""
+
+    def __enter__(self):
+        lib().or_set_input_fp16(1)
+
+    def __exit__(self, *a):
+        lib().or_set_input_fp16(0)
+
+
+def _bits16(x, fp16: bool):
+    return as_fp16_bits(x) if fp16 else as_bf16_bits(x)
 
 
 def as_bf16_bits(x) -> np.ndarray:
@@ -259,8 +293,12 @@ def sf_rows_padded(rows: int) -> int:
     return (rows + 127) // 128 * 128
 
 
-def quantize_activation(x_bits, perm, S: int, gs: float, layout: int = INTERLEAVED):
-    """C5+C8+C9: packed codes [M][Kp/2] and swizzled SF [roundup(M,128)*Kp/16]."""
+def quantize_activation(x_bits, perm, S: int, gs: float, layout: int = INTERLEAVED, fp16: bool = False):
+    """C5+C8+C9: packed codes [M][Kp/2] and swizzled SF [roundup(M,128)*Kp/16].  fp16: the rows are IEEE
+    binary16 (decoded exactly to fp32), else bf16."""
+    if fp16:
+        with _InputFp16():
+            return quantize_activation(as_fp16_bits(x_bits), perm, S, gs, layout)
     x = as_bf16_bits(x_bits)
     M, K = x.shape
     Kp = kp(K, S)
@@ -271,7 +309,10 @@ def quantize_activation(x_bits, perm, S: int, gs: float, layout: int = INTERLEAV
     return codes, sf
 
 
-def quantize_weight(w_bits, perm, S: int, gs: float, layout: int = INTERLEAVED):
+def quantize_weight(w_bits, perm, S: int, gs: float, layout: int = INTERLEAVED, fp16: bool = False):
+    if fp16:
+        with _InputFp16():
+            return quantize_weight(as_fp16_bits(w_bits), perm, S, gs, layout)
     w = as_bf16_bits(w_bits)
     N, K = w.shape
     Kp = kp(K, S)
@@ -346,7 +387,10 @@ def silu_mul(gu_bits, K: int | None = None, up_off: int | None = None) -> np.nda
 
 
 # ----------------------------------------------------------------------------- calibration
-def calib_absmax(x_bits, chan_max=None) -> np.ndarray:
+def calib_absmax(x_bits, chan_max=None, fp16: bool = False) -> np.ndarray:
+    if fp16:
+        with _InputFp16():
+            return calib_absmax(as_fp16_bits(x_bits), chan_max)
     x = as_bf16_bits(x_bits)
     rows, K = x.shape
     cm = np.zeros(K, np.float32) if chan_max is None else np.ascontiguousarray(chan_max, np.float32)

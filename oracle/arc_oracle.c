@@ -150,6 +150,22 @@ static float bf16_to_f32(uint16_t h) {
     return f;
 }
 
+/* IEEE binary16 -> fp32 (exact): 1 sign, 5 exponent (bias 15), 10 fraction bits; subnormals m * 2^-24. */
+float or_f16_to_f32(uint16_t h) {
+    const int s = (h >> 15) & 1, e = (h >> 10) & 31, m = h & 1023;
+    float v;
+    if (e == 0) v = ldexpf((float)m, -24);
+    else if (e == 31) v = m ? NAN : INFINITY;
+    else v = ldexpf((float)(m | 1024), e - 25);
+    return s ? -v : v;
+}
+
+/* Element format of the 16-bit activation / weight rows the quantizers read (SURVEY 8(b) arc_dtype_t):
+ * 0 = bf16 (default), 1 = fp16.  Set by the Python wrapper around a call (test infrastructure). */
+static int g_in_fp16 = 0;
+void or_set_input_fp16(int on) { g_in_fp16 = on ? 1 : 0; }
+static float in16_to_f32(uint16_t h) { return g_in_fp16 ? or_f16_to_f32(h) : bf16_to_f32(h); }
+
 /* ------------------------------------------------------------------------- */
 /* C5: ARC activation row, logical (unpacked) order -- P:138 §3.2 "Online     */
 /* Activation Quantization": (1) reorder + primary quantization of all K      */
@@ -167,7 +183,7 @@ int or_arc_row_logical(const uint16_t* x_row, const int32_t* perm, int K, int S,
         float z[16], t[16], e[16], t2[16], d1, d2;
         uint8_t q1[16], q2[16], s1, s2;
         for (int i = 0; i < 16; ++i) {
-            z[i] = bf16_to_f32(x_row[perm[16 * b + i]]);       /* (1) reorder */
+            z[i] = in16_to_f32(x_row[perm[16 * b + i]]);       /* (1) reorder */
             if (!isfinite(z[i])) return OR_ERR_NONFINITE;
         }
         or_stage(z, gs, &s1, &d1, t, q1);                      /* (1) primary */
@@ -195,7 +211,7 @@ int or_weight_row_logical(const uint16_t* w_row, const int32_t* perm, int K, int
         float z[16], t[16], d;
         uint8_t q[16], s;
         for (int i = 0; i < 16; ++i) {
-            z[i] = bf16_to_f32(w_row[perm[16 * b + i]]);
+            z[i] = in16_to_f32(w_row[perm[16 * b + i]]);
             if (!isfinite(z[i])) return OR_ERR_NONFINITE;
         }
         or_stage(z, gs, &s, &d, t, q);
@@ -311,7 +327,7 @@ int or_quantize_weight(const uint16_t* w, int64_t N, int K, int64_t ldw, const i
 int or_calib_absmax(const uint16_t* x, int64_t rows, int K, int64_t ldx, float* chan_max) {
     for (int64_t r = 0; r < rows; ++r)
         for (int j = 0; j < K; ++j) {
-            float v = bf16_to_f32(x[r * ldx + j]);
+            float v = in16_to_f32(x[r * ldx + j]);
             if (!isfinite(v)) return OR_ERR_NONFINITE;
             if (fabsf(v) > chan_max[j]) chan_max[j] = fabsf(v);
         }
