@@ -77,7 +77,11 @@ typedef enum {
   ARC_ERR_NONFINITE = 7
 } arc_status_t;
 
-typedef enum { ARC_BF16 = 0, ARC_FP32 = 2 } arc_dtype_t;
+/* Element types.  Inputs (activations, weights, calibration rows): ARC_BF16 everywhere, ARC_FP16 through the
+ * _ex entry points (arc_calib_absmax_ex, arc_tensor_scale_ex, arc_quantize_weight_ex, arc_quantize_activation_ex,
+ * arc_linear_ex with ARC_LINEAR_X_FP16); fp16 values are decoded exactly to fp32 before the same STAGE
+ * arithmetic.  Outputs: ARC_BF16 or ARC_FP32. */
+typedef enum { ARC_BF16 = 0, ARC_FP16 = 1, ARC_FP32 = 2 } arc_dtype_t;
 
 typedef enum { ARC_LAYOUT_INTERLEAVED = 0, ARC_LAYOUT_CONTIGUOUS = 1 } arc_layout_t;
 
@@ -129,6 +133,9 @@ ARC_API arc_status_t arc_linear_workspace_size(int64_t M, const arc_qweight_t* q
  * initialises (zeros) and may accumulate over several batches (exact). */
 ARC_API arc_status_t arc_calib_absmax(const void* x, int64_t rows, int64_t K, int64_t ldx, float* chan_max,
                               void* stream);
+/* As arc_calib_absmax for x_dtype ARC_BF16 or ARC_FP16 rows (other types: ARC_ERR_SHAPE). */
+ARC_API arc_status_t arc_calib_absmax_ex(const void* x, arc_dtype_t x_dtype, int64_t rows, int64_t K, int64_t ldx,
+                                         float* chan_max, void* stream);
 /* Host, synchronous.  perm_host = channels sorted by chan_max descending, ties to
  * the lower index (reading Q9); M = max chan_max; tau = 2^-3 M;
  * S_raw = #{j : chan_max[j] > tau} (strict, Q8); S = min(K, 16*ceil(S_raw/16))
@@ -154,6 +161,9 @@ ARC_API arc_status_t arc_gather_order_ex(const int32_t* perm_host, int64_t K, in
  * the NVFP4 encode tensor scale (reading Q3).  gs_out is a device float. */
 ARC_API arc_status_t arc_tensor_scale(const void* x, int64_t rows, int64_t K, int64_t ldx, float* gs_out,
                               void* stream);
+/* As arc_tensor_scale for x_dtype ARC_BF16 or ARC_FP16. */
+ARC_API arc_status_t arc_tensor_scale_ex(const void* x, arc_dtype_t x_dtype, int64_t rows, int64_t K, int64_t ldx,
+                                         float* gs_out, void* stream);
 
 /* ---------------------------------------------------------------- quantization */
 /* Offline weight preparation: reorder the N x K bf16 weight by perm,
@@ -163,6 +173,10 @@ ARC_API arc_status_t arc_tensor_scale(const void* x, int64_t rows, int64_t K, in
 ARC_API arc_status_t arc_quantize_weight(const void* w, int64_t N, int64_t K, int64_t ldw, const int32_t* perm,
                                  int32_t S, const float* gs_w, arc_layout_t layout, uint8_t* codes,
                                  uint8_t* sf, void* stream);
+/* As arc_quantize_weight for w_dtype ARC_BF16 or ARC_FP16 (fp16 decoded exactly to fp32). */
+ARC_API arc_status_t arc_quantize_weight_ex(const void* w, arc_dtype_t w_dtype, int64_t N, int64_t K, int64_t ldw,
+                                            const int32_t* perm, int32_t S, const float* gs_w, arc_layout_t layout,
+                                            uint8_t* codes, uint8_t* sf, void* stream);
 /* Online activation quantization: reorder, primary NVFP4 quantization of
  * all K channels, residual of the S outlier channels (against the encoded
  * primary, reading Q6) quantized again with fresh E4M3 block scales and the same
@@ -170,6 +184,10 @@ ARC_API arc_status_t arc_quantize_weight(const void* w, int64_t N, int64_t K, in
  * x: bf16 [M][ldx]; codes [M][Kp/2]; sf roundup(M,128)*Kp/16 bytes. */
 ARC_API arc_status_t arc_quantize_activation(const void* x, int64_t M, int64_t ldx, const arc_profile_t* prof,
                                      uint8_t* codes, uint8_t* sf, void* stream);
+/* As arc_quantize_activation for x_dtype ARC_BF16 or ARC_FP16 (fp16 decoded exactly to fp32, then the same
+ * STAGE arithmetic; the fused RMSNorm / SiLU producers and the MX variants take bf16 only). */
+ARC_API arc_status_t arc_quantize_activation_ex(const void* x, arc_dtype_t x_dtype, int64_t M, int64_t ldx,
+                                                const arc_profile_t* prof, uint8_t* codes, uint8_t* sf, void* stream);
 
 /* ---------------------------------------------------------------- RMSNorm (fused producer) */
 /* The RMSNorm stage of the paper's "Fused Quantization Kernel that integrates Channel
@@ -376,6 +394,8 @@ ARC_API arc_status_t arc_linear(const void* x, int64_t M, int64_t ldx, const arc
  *    finish them.  The quantized activation is bit-identical to arc_quantize_activation's.  At M > 64
  *    FUSED runs the two-kernel path. */
 enum { ARC_LINEAR_AUTO = 0, ARC_LINEAR_FUSED = 1, ARC_LINEAR_UNFUSED = 2 };
+/* Or-ed into arc_linear_ex's flags: x holds IEEE fp16 rows (ARC_FP16); the layer then runs UNFUSED. */
+enum { ARC_LINEAR_X_FP16 = 16 };
 ARC_API arc_status_t arc_linear_ex_workspace_size(int64_t M, const arc_qweight_t* qw, int flags, size_t* bytes);
 ARC_API arc_status_t arc_linear_ex(const void* x, int64_t M, int64_t ldx, const arc_profile_t* prof,
                                    const arc_qweight_t* qw, void* y, arc_dtype_t y_dtype, int64_t ldy, void* ws,

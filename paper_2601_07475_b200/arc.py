@@ -117,6 +117,10 @@ _sig("arc_linear_hostio", [_P, _i64, ctypes.POINTER(ArcProfile), ctypes.POINTER(
 _sig("arc_linear_hostio_async", [_P, _i64, ctypes.POINTER(ArcProfile), ctypes.POINTER(ArcQWeight), _P, ctypes.c_int,
                                  _P, ctypes.c_size_t, _P])
 _sig("arc_linear_hostio_wait", [_P])
+_sig("arc_calib_absmax_ex", [_P, ctypes.c_int, _i64, _i64, _i64, _P, _P])
+_sig("arc_tensor_scale_ex", [_P, ctypes.c_int, _i64, _i64, _i64, _P, _P])
+_sig("arc_quantize_weight_ex", [_P, ctypes.c_int, _i64, _i64, _i64, _P, ctypes.c_int32, _P, ctypes.c_int, _P, _P, _P])
+_sig("arc_quantize_activation_ex", [_P, ctypes.c_int, _i64, _i64, ctypes.POINTER(ArcProfile), _P, _P, _P])
 _sig("arc_probe_e2m1", [_P, _i64, _P, _P])
 _sig("arc_probe_e2m1_bits", [ctypes.c_uint32, _i64, _P, _P])
 _sig("arc_probe_e2m1_raw_bits", [ctypes.c_uint32, _i64, _P, _P])
@@ -139,6 +143,7 @@ EXPORTED = [
     "arc_probe_e2m1", "arc_probe_e2m1_bits", "arc_probe_e2m1_raw_bits", "arc_probe_e4m3_ceil", "arc_probe_silu",
     "arc_probe_u4_unpack",
     "arc_debug_stream_trace", "arc_debug_trace", "arc_linear_hostio_async", "arc_linear_hostio_wait",
+    "arc_calib_absmax_ex", "arc_tensor_scale_ex", "arc_quantize_weight_ex", "arc_quantize_activation_ex",
 ]
 
 
@@ -231,14 +236,24 @@ class QWeight:
         return self._c
 
 
+ARC_FP16 = 1  # arc.h arc_dtype_t
+LINEAR_X_FP16 = 16  # arc.h ARC_LINEAR_X_FP16
+
+
+def _in16(x: torch.Tensor) -> int:
+    """arc_dtype_t of a 16-bit input tensor: ARC_BF16 (0) or ARC_FP16 (1)."""
+    assert x.dtype in (torch.bfloat16, torch.float16), x.dtype
+    return ARC_FP16 if x.dtype == torch.float16 else 0
+
+
 def calib_absmax(x: torch.Tensor, chan_max: torch.Tensor | None = None, stream=None) -> torch.Tensor:
-    """Running per-channel abs-max over bf16 rows (device)."""
-    assert x.dtype == torch.bfloat16 and x.is_cuda and x.dim() == 2
+    """Running per-channel abs-max over bf16 / fp16 rows (device)."""
+    assert x.is_cuda and x.dim() == 2
     rows, K = x.shape
     if chan_max is None:
         chan_max = torch.zeros(K, dtype=torch.float32, device=x.device)
-    _check(_lib.arc_calib_absmax(_ptr(x), rows, K, x.stride(0), _ptr(chan_max), _stream(stream)),
-           "arc_calib_absmax")
+    _check(_lib.arc_calib_absmax_ex(_ptr(x), _in16(x), rows, K, x.stride(0), _ptr(chan_max), _stream(stream)),
+           "arc_calib_absmax_ex")
     return chan_max
 
 
@@ -291,34 +306,34 @@ def profile_from(perm, S: int, gs: float, layout: int = INTERLEAVED, device="cud
 def tensor_scale(x: torch.Tensor, stream=None) -> torch.Tensor:
     """Device gs = 2688/amax(x) (reading Q3)."""
     gs = torch.empty(1, dtype=torch.float32, device=x.device)
-    _check(_lib.arc_tensor_scale(_ptr(x), x.shape[0], x.shape[1], x.stride(0), _ptr(gs), _stream(stream)),
-           "arc_tensor_scale")
+    _check(_lib.arc_tensor_scale_ex(_ptr(x), _in16(x), x.shape[0], x.shape[1], x.stride(0), _ptr(gs), _stream(stream)),
+           "arc_tensor_scale_ex")
     return gs
 
 
 def quantize_weight(w: torch.Tensor, prof: Profile, gs: torch.Tensor | None = None, stream=None) -> QWeight:
-    assert w.dtype == torch.bfloat16 and w.is_cuda and w.dim() == 2 and w.shape[1] == prof.K
+    assert w.is_cuda and w.dim() == 2 and w.shape[1] == prof.K
     N, K = w.shape
     Kp, cb, sb = buffer_sizes(N, K, prof.S)
     if gs is None:
         gs = tensor_scale(w, stream)
     codes = torch.empty(N, Kp // 2, dtype=torch.uint8, device=w.device)
     sf = torch.empty(sb, dtype=torch.uint8, device=w.device)
-    _check(_lib.arc_quantize_weight(_ptr(w), N, K, w.stride(0), _ptr(prof.perm), prof.S, _ptr(gs), prof.layout,
-                                    _ptr(codes), _ptr(sf), _stream(stream)), "arc_quantize_weight")
+    _check(_lib.arc_quantize_weight_ex(_ptr(w), _in16(w), N, K, w.stride(0), _ptr(prof.perm), prof.S, _ptr(gs),
+                                       prof.layout, _ptr(codes), _ptr(sf), _stream(stream)), "arc_quantize_weight_ex")
     return QWeight(N=N, K=K, Kp=Kp, S=prof.S, layout=prof.layout, codes=codes, sf=sf, gs=gs)
 
 
 def quantize_activation(x: torch.Tensor, prof: Profile, codes=None, sf=None, stream=None):
-    assert x.dtype == torch.bfloat16 and x.is_cuda and x.dim() == 2 and x.shape[1] == prof.K
+    assert x.is_cuda and x.dim() == 2 and x.shape[1] == prof.K
     M = x.shape[0]
     Kp, cb, sb = buffer_sizes(M, prof.K, prof.S)
     if codes is None:
         codes = torch.empty(M, Kp // 2, dtype=torch.uint8, device=x.device)
     if sf is None:
         sf = torch.empty(sb, dtype=torch.uint8, device=x.device)
-    _check(_lib.arc_quantize_activation(_ptr(x), M, x.stride(0), ctypes.byref(prof.c()), _ptr(codes), _ptr(sf),
-                                        _stream(stream)), "arc_quantize_activation")
+    _check(_lib.arc_quantize_activation_ex(_ptr(x), _in16(x), M, x.stride(0), ctypes.byref(prof.c()), _ptr(codes),
+                                           _ptr(sf), _stream(stream)), "arc_quantize_activation_ex")
     return codes, sf
 
 
@@ -453,8 +468,10 @@ def linear(x: torch.Tensor, prof: Profile, qw: QWeight, out_dtype=torch.bfloat16
            stream=None, mode: str = "auto"):
     """The ARC linear layer (Eq.2): activation quantize + augmented NVFP4 GEMM.  mode "unfused" = two
     PDL-chained kernels; "fused" (M <= 64) = one kernel that quantizes the activation and runs the
-    weight-streaming stream-K GEMM (arc.h ARC_LINEAR_FUSED); "auto" = unfused (faster at every M)."""
-    assert x.dtype == torch.bfloat16 and x.is_cuda
+    weight-streaming stream-K GEMM (arc.h ARC_LINEAR_FUSED); "auto" = unfused (faster at every M).  x may be bf16
+    or fp16 (ARC_LINEAR_X_FP16: the two-kernel path)."""
+    assert x.is_cuda
+    xf = LINEAR_X_FP16 if _in16(x) == ARC_FP16 else 0
     M = x.shape[0]
     if out is None:
         out = _alloc_out(M, qw.N, out_dtype, x.device)
@@ -463,7 +480,7 @@ def linear(x: torch.Tensor, prof: Profile, qw: QWeight, out_dtype=torch.bfloat16
         ws = _default_workspace("linear", x.device, stream)
     buf = ws.get(need)
     _check(_lib.arc_linear_ex(_ptr(x), M, x.stride(0), ctypes.byref(prof.c()), ctypes.byref(qw.c()), _ptr(out),
-                              _dtype_code(out.dtype), out.stride(0), _ptr(buf), buf.numel(), LINEAR_MODES[mode],
+                              _dtype_code(out.dtype), out.stride(0), _ptr(buf), buf.numel(), LINEAR_MODES[mode] | xf,
                               _stream(stream)),
            "arc_linear_ex")
     return out

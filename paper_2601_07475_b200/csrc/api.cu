@@ -186,14 +186,22 @@ arc_status_t arc_linear_workspace_size(int64_t M, const arc_qweight_t* qw, size_
   return ARC_OK;
 }
 
+static int in16_dtype(arc_dtype_t t) { return t == ARC_FP16 ? 1 : (t == ARC_BF16 ? 0 : -1); }
+
 arc_status_t arc_calib_absmax(const void* x, int64_t rows, int64_t K, int64_t ldx, float* chan_max, void* stream) {
+  return arc_calib_absmax_ex(x, ARC_BF16, rows, K, ldx, chan_max, stream);
+}
+arc_status_t arc_calib_absmax_ex(const void* x, arc_dtype_t x_dtype, int64_t rows, int64_t K, int64_t ldx,
+                                 float* chan_max, void* stream) {
+  const int f16 = in16_dtype(x_dtype);
+  if (f16 < 0) return fail(ARC_ERR_SHAPE, "x_dtype must be ARC_BF16 or ARC_FP16");
   if (!x || !chan_max) return fail(ARC_ERR_NULL, "null x / chan_max");
   if (K <= 0 || K % 16 || rows < 0 || ldx < K || ldx % 8) return fail(ARC_ERR_SHAPE, "bad rows/K/ldx");
   if (!aligned16(x)) return fail(ARC_ERR_ALIGN, "x not 16B aligned");
   arc_status_t s = check_device();
   if (s != ARC_OK) return s;
   if (rows == 0) return ARC_OK;
-  cudaError_t e = launch_calib_absmax(x, rows, (int)K, ldx, chan_max, (cudaStream_t)stream);
+  cudaError_t e = launch_calib_absmax(x, rows, (int)K, ldx, chan_max, (cudaStream_t)stream, f16);
   return e == cudaSuccess ? ARC_OK : cuda_fail(e, "arc_calib_absmax");
 }
 
@@ -298,17 +306,30 @@ arc_status_t arc_gather_order_ex(const int32_t* perm_host, int64_t K, int elem_b
 }
 
 arc_status_t arc_tensor_scale(const void* x, int64_t rows, int64_t K, int64_t ldx, float* gs_out, void* stream) {
+  return arc_tensor_scale_ex(x, ARC_BF16, rows, K, ldx, gs_out, stream);
+}
+arc_status_t arc_tensor_scale_ex(const void* x, arc_dtype_t x_dtype, int64_t rows, int64_t K, int64_t ldx,
+                                 float* gs_out, void* stream) {
+  const int f16 = in16_dtype(x_dtype);
+  if (f16 < 0) return fail(ARC_ERR_SHAPE, "x_dtype must be ARC_BF16 or ARC_FP16");
   if (!x || !gs_out) return fail(ARC_ERR_NULL, "null x / gs_out");
   if (K <= 0 || K % 16 || rows < 0 || ldx < K || ldx % 8) return fail(ARC_ERR_SHAPE, "bad rows/K/ldx");
   if (!aligned16(x)) return fail(ARC_ERR_ALIGN, "x not 16B aligned");
   arc_status_t s = check_device();
   if (s != ARC_OK) return s;
-  cudaError_t e = launch_tensor_scale(x, rows, (int)K, ldx, gs_out, (cudaStream_t)stream);
+  cudaError_t e = launch_tensor_scale(x, rows, (int)K, ldx, gs_out, (cudaStream_t)stream, 0, f16);
   return e == cudaSuccess ? ARC_OK : cuda_fail(e, "arc_tensor_scale");
 }
 
 arc_status_t arc_quantize_weight(const void* w, int64_t N, int64_t K, int64_t ldw, const int32_t* perm, int32_t S,
                                  const float* gs_w, arc_layout_t layout, uint8_t* codes, uint8_t* sf, void* stream) {
+  return arc_quantize_weight_ex(w, ARC_BF16, N, K, ldw, perm, S, gs_w, layout, codes, sf, stream);
+}
+arc_status_t arc_quantize_weight_ex(const void* w, arc_dtype_t w_dtype, int64_t N, int64_t K, int64_t ldw,
+                                    const int32_t* perm, int32_t S, const float* gs_w, arc_layout_t layout,
+                                    uint8_t* codes, uint8_t* sf, void* stream) {
+  const int f16 = in16_dtype(w_dtype);
+  if (f16 < 0) return fail(ARC_ERR_SHAPE, "w_dtype must be ARC_BF16 or ARC_FP16");
   if (!w || !perm || !gs_w || !codes || !sf) return fail(ARC_ERR_NULL, "null argument");
   arc_status_t s = check_ks(K, S);
   if (s != ARC_OK) return s;
@@ -318,19 +339,26 @@ arc_status_t arc_quantize_weight(const void* w, int64_t N, int64_t K, int64_t ld
   s = check_device();
   if (s != ARC_OK) return s;
   if (N == 0) return ARC_OK;
-  cudaError_t e = launch_quant(w, N, (int)K, ldw, perm, S, gs_w, (int)layout, 1, codes, sf, (cudaStream_t)stream);
+  cudaError_t e = launch_quant(w, N, (int)K, ldw, perm, S, gs_w, (int)layout, 1, codes, sf, (cudaStream_t)stream,
+                               nullptr, 0.0f, -1, 0, 0, f16);
   return e == cudaSuccess ? ARC_OK : cuda_fail(e, "arc_quantize_weight");
 }
 
 static arc_status_t quantize_activation_impl(const void* x, int64_t M, int64_t ldx, const arc_profile_t* prof,
-                                            uint8_t* codes, uint8_t* sf, void* stream, int consts_ready);
+                                            uint8_t* codes, uint8_t* sf, void* stream, int consts_ready, int f16 = 0);
 arc_status_t arc_quantize_activation(const void* x, int64_t M, int64_t ldx, const arc_profile_t* prof,
                                      uint8_t* codes, uint8_t* sf, void* stream) {
   return quantize_activation_impl(x, M, ldx, prof, codes, sf, stream, 0);
 }
+arc_status_t arc_quantize_activation_ex(const void* x, arc_dtype_t x_dtype, int64_t M, int64_t ldx,
+                                        const arc_profile_t* prof, uint8_t* codes, uint8_t* sf, void* stream) {
+  const int f16 = in16_dtype(x_dtype);
+  if (f16 < 0) return fail(ARC_ERR_SHAPE, "x_dtype must be ARC_BF16 or ARC_FP16");
+  return quantize_activation_impl(x, M, ldx, prof, codes, sf, stream, 0, f16);
+}
 // consts_ready: arc_linear's promise that perm (like the weights) was complete before the preceding kernel
 static arc_status_t quantize_activation_impl(const void* x, int64_t M, int64_t ldx, const arc_profile_t* prof,
-                                            uint8_t* codes, uint8_t* sf, void* stream, int consts_ready) {
+                                            uint8_t* codes, uint8_t* sf, void* stream, int consts_ready, int f16) {
   arc_status_t s = check_profile(prof);
   if (s != ARC_OK) return s;
   if (M < 0 || ldx < prof->K || ldx % 8) return fail(ARC_ERR_SHAPE, "bad M/ldx");
@@ -341,7 +369,7 @@ static arc_status_t quantize_activation_impl(const void* x, int64_t M, int64_t l
   if (s != ARC_OK) return s;
   if (M == 0) return ARC_OK;
   cudaError_t e = launch_quant(x, M, (int)prof->K, ldx, prof->perm, prof->S, prof->gs, (int)prof->layout, 0, codes,
-                               sf, (cudaStream_t)stream, nullptr, 0.0f, -1, 0, consts_ready);
+                               sf, (cudaStream_t)stream, nullptr, 0.0f, -1, 0, consts_ready, f16);
   return e == cudaSuccess ? ARC_OK : cuda_fail(e, "arc_quantize_activation");
 }
 
@@ -830,8 +858,11 @@ arc_status_t arc_linear_ex(const void* x, int64_t M, int64_t ldx, const arc_prof
   if (s != ARC_OK) return s;
   if (qw->K != prof->K || qw->S != prof->S || qw->layout != prof->layout)
     return fail(ARC_ERR_SHAPE, "profile and qweight disagree on K / S / layout");
+  const int x_f16 = (flags & ARC_LINEAR_X_FP16) ? 1 : 0;
+  flags &= ~ARC_LINEAR_X_FP16;
   if (flags != ARC_LINEAR_AUTO && flags != ARC_LINEAR_FUSED && flags != ARC_LINEAR_UNFUSED)
     return fail(ARC_ERR_SHAPE, "bad flags");
+  if (x_f16) flags = ARC_LINEAR_UNFUSED;  // fp16 rows: the two-kernel path (its quantize takes ARC_FP16)
   if (M < 0 || M > (1 << 30)) return fail(ARC_ERR_SHAPE, "bad M");
   if (M == 0) return ARC_OK;
   if (!ws || !x || !y) return fail(ARC_ERR_NULL, "null x / y / workspace");
@@ -879,7 +910,7 @@ arc_status_t arc_linear_ex(const void* x, int64_t M, int64_t ldx, const arc_prof
     cudaError_t e = launch_stream_gemm(p, sp, (cudaStream_t)stream, &detail, &fq);
     return e == cudaSuccess ? ARC_OK : cuda_fail(e, "arc_linear (fused decode)", detail);
   }
-  s = quantize_activation_impl(x, M, ldx, prof, codes, sf, stream, 1);
+  s = quantize_activation_impl(x, M, ldx, prof, codes, sf, stream, 1, x_f16);
   if (s != ARC_OK) return s;
   return gemm_impl(codes, sf, prof->gs, M, qw, y, y_dtype, ldy, ws, rest + act, rest_bytes - act, stream, 1);
 }
@@ -940,6 +971,7 @@ arc_status_t arc_linear_ex_workspace_size(int64_t M, const arc_qweight_t* qw, in
   if (s != ARC_OK) return s;
   if (!bytes) return fail(ARC_ERR_NULL, "null bytes");
   if (M < 0) return fail(ARC_ERR_SHAPE, "M < 0");
+  flags &= ~ARC_LINEAR_X_FP16;
   if (flags != ARC_LINEAR_AUTO && flags != ARC_LINEAR_FUSED && flags != ARC_LINEAR_UNFUSED)
     return fail(ARC_ERR_SHAPE, "bad flags");
   *bytes = sync_bytes_of(qw->N) + (M == 0 ? 0 : linear_rest_bytes(M, qw, flags));

@@ -44,7 +44,7 @@ unsigned long long* trace_slot();
 cudaError_t launch_quant(const void* x, int64_t rows, int K, int64_t ld, const int32_t* perm, int S, const float* gs,
                          int layout, int weight_mode, uint8_t* codes, uint8_t* sf, cudaStream_t stream,
                          const void* gamma = nullptr, float eps = 0.0f, int64_t up_off = -1, int mx = 0,
-                         int consts_ready = 0);
+                         int consts_ready = 0, int f16 = 0);
 // consts_ready (arc_linear): perm was complete before the preceding kernel started (calibration constants,
 // like the prepared weights), so the decode-size quantize may load it before griddepcontrol.wait.
 cudaError_t launch_silu_mul(const void* gu, int64_t rows, int K, int64_t ld, int64_t up_off, void* h, int64_t ldh,
@@ -57,10 +57,11 @@ cudaError_t launch_mx_native_quant(const void* x, int64_t rows, int K, int S, in
 // Fig.8a comparator: plain MXFP8 (E4M3 codes [rows][roundup(K,128)], E8M0 scales per 32-block).
 cudaError_t launch_mxfp8_quant(const void* x, int64_t rows, int K, int64_t ld, uint8_t* codes, uint8_t* sf,
                                cudaStream_t stream);
-cudaError_t launch_calib_absmax(const void* x, int64_t rows, int K, int64_t ld, float* chan_max, cudaStream_t s);
+cudaError_t launch_calib_absmax(const void* x, int64_t rows, int K, int64_t ld, float* chan_max, cudaStream_t s,
+                                int f16 = 0);
 // mx = 0: gs = 2688/amax (reading Q3); mx = 1: the MXFP4-ARC offset gs = 2^-c (reading Q25).
 cudaError_t launch_tensor_scale(const void* x, int64_t rows, int K, int64_t ld, float* gs_out, cudaStream_t s,
-                                int mx = 0);
+                                int mx = 0, int f16 = 0);
 
 struct GemmProblem {
   int64_t M, N, Kp;

@@ -63,6 +63,7 @@ struct QuantArgs {
   int64_t up_off;  // SiLU-mul mode (Fig.5, reading Q24): x holds gate, x + up_off holds up
   unsigned long long* trace;  // timing experiments only (ARC_TRACE): [cta][8] globaltimer stamps
   int32_t consts_ready;       // perm may be read before griddepcontrol.wait (arc_linear)
+  int32_t f16;                // the 16-bit rows are IEEE fp16 (ARC_FP16), else bf16
 };
 
 ARC_DEV void qtrace(const QuantArgs& a, int i) {
@@ -81,10 +82,17 @@ ARC_DEV void cp_async_arrive(uint64_t* bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
+// a 16-bit input element (bf16, or IEEE fp16 for F16 = true: arc_dtype_t ARC_FP16) as fp32 (exact)
+template <bool F16>
+ARC_DEV float in16_to_f32(uint32_t h) {
+  if (F16) return __half2float(__ushort_as_half((unsigned short)h));
+  return bf16_bits_to_f32(h);
+}
 // gather 16 channels of one staged row (byte offsets into smem) as fp32 (exact)
+template <bool F16 = false>
 ARC_DEV void gather16(const uint8_t* base, const uint32_t (&off)[16], float (&z)[16]) {
 #pragma unroll
-  for (int q = 0; q < 16; ++q) z[q] = bf16_bits_to_f32(*reinterpret_cast<const uint16_t*>(base + off[q]));
+  for (int q = 0; q < 16; ++q) z[q] = in16_to_f32<F16>(*reinterpret_cast<const uint16_t*>(base + off[q]));
 }
 
 // RMSNorm of the 16 gathered channels of logical block l (reading Q23): z = bf16(g * bf16(z * r)).
@@ -246,7 +254,7 @@ ARC_DEV int tile_rows(int base, int64_t rows) {  // valid rows base + 32 i < row
 #define ARC_QUANT_ROLL_ALL 0
 #endif
 constexpr bool kRollAll = ARC_QUANT_ROLL_ALL != 0;  // experiment: roll the plain kernels' loops too
-template <int IPT, int R, int ROWB, int ST, bool NORM, int SILU, bool MX>
+template <int IPT, int R, int ROWB, int ST, bool NORM, int SILU, bool MX, bool F16 = false>
 __global__ void __launch_bounds__(1024) arc_quant_kernel(QuantArgs p) {
   extern __shared__ __align__(16) uint8_t smem[];
   constexpr int ROWP = ROWB + 16;
@@ -477,7 +485,7 @@ __global__ void __launch_bounds__(1024) arc_quant_kernel(QuantArgs p) {
                   uint32_t sfb = 0;
                   if (r < nr) {
                     float z[16];
-                    if (kind[i] == 1) gather16(smem + s * SLOT + r * ROWP, off[i], z);
+                    if (kind[i] == 1) gather16<F16>(smem + s * SLOT + r * ROWP, off[i], z);
                     else
 #pragma unroll
                       for (int q = 0; q < 16; ++q) z[q] = 0.0f;
@@ -506,7 +514,7 @@ __global__ void __launch_bounds__(1024) arc_quant_kernel(QuantArgs p) {
                       if (SILU) {
                         silu_mul_block16<SILU>(z, smem + s * SLOT + r * ROWP, off[i], K * 2, stab, p.debug);
                       } else {
-                        gather16(smem + s * SLOT + r * ROWP, off[i], z);
+                        gather16<F16>(smem + s * SLOT + r * ROWP, off[i], z);
                         if (NORM) norm16w(z, greg[i], rscale[s * R + r]);
                       }
                       // stage 1 (Eq.1 with the NVFP4 two-level scale, Q7 op order)
@@ -563,12 +571,12 @@ __global__ void __launch_bounds__(1024) arc_quant_kernel(QuantArgs p) {
             const bool live = has && r < nr;
             float z[16];
             if (live && it0 == (warp - npw) * 32) {
-              gather16(smem + s * SLOT, moff, z);
+              gather16<F16>(smem + s * SLOT, moff, z);
             } else if (live) {
               const int* pp = p.perm + 16 * jb;
 #pragma unroll
               for (int q = 0; q < 16; ++q)
-                z[q] = bf16_bits_to_f32(*reinterpret_cast<const uint16_t*>(smem + s * SLOT + r * ROWP + 2 * __ldg(pp + q)));
+                z[q] = in16_to_f32<F16>(*reinterpret_cast<const uint16_t*>(smem + s * SLOT + r * ROWP + 2 * __ldg(pp + q)));
             } else {
 #pragma unroll
               for (int q = 0; q < 16; ++q) z[q] = 0.0f;
@@ -663,7 +671,7 @@ __global__ void __launch_bounds__(1024) arc_quant_kernel(QuantArgs p) {
               if (SILU) {
                 silu_mul_block16<SILU>(z, smem + s * SLOT, off, K * 2, stab, p.debug);
               } else {
-                gather16(smem + s * SLOT, off, z);
+                gather16<F16>(smem + s * SLOT, off, z);
                 if (NORM) norm16(z, gam + 32 * jb, rscale[s * R + r]);
               }
               const uint32_t sf1 = e4m3_ceil_nb(__fmul_rn(absmax16(z), c6g));
@@ -695,8 +703,12 @@ __global__ void __launch_bounds__(1024) arc_quant_kernel(QuantArgs p) {
 // Column abs-max over rows (calibration).  |bf16| bit patterns order like
 // their values, so the max is taken on integers (exact) and merged with an
 // integer atomicMax on the float bits (non-negative floats order as ints).
+// f16: the 15-bit magnitudes are IEEE fp16 (they order as integers too) -> converted to float bits at the end
+ARC_DEV uint32_t mag16_to_f32_bits(uint32_t m, int f16) {
+  return f16 ? __float_as_uint(__half2float(__ushort_as_half((unsigned short)m))) : m << 16;
+}
 __global__ void arc_calib_absmax_kernel(const uint16_t* x, int64_t rows, int K, int64_t ld, int rows_per_cta,
-                                        float* chan_max) {
+                                        float* chan_max, int f16) {
   const int c8 = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
   if (c8 >= K) return;
   const int64_t r0 = (int64_t)blockIdx.y * rows_per_cta;
@@ -712,11 +724,12 @@ __global__ void arc_calib_absmax_kernel(const uint16_t* x, int64_t rows, int K, 
     }
   }
 #pragma unroll
-  for (int j = 0; j < 8; ++j) atomicMax(reinterpret_cast<unsigned int*>(chan_max + c8 + j), mx[j] << 16);
+  for (int j = 0; j < 8; ++j) atomicMax(reinterpret_cast<unsigned int*>(chan_max + c8 + j), mag16_to_f32_bits(mx[j], f16));
 }
 
 // max |x| over a whole matrix into *amax_bits (float bits, caller zeroes it).
-__global__ void arc_absmax_all_kernel(const uint16_t* x, int64_t rows, int K, int64_t ld, unsigned int* amax_bits) {
+__global__ void arc_absmax_all_kernel(const uint16_t* x, int64_t rows, int K, int64_t ld, unsigned int* amax_bits,
+                                      int f16) {
   uint32_t mx = 0;
   const int64_t n8 = rows * (K / 8);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
@@ -728,7 +741,7 @@ __global__ void arc_absmax_all_kernel(const uint16_t* x, int64_t rows, int K, in
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  if ((threadIdx.x & 31) == 0) atomicMax(amax_bits, mx << 16);
+  if ((threadIdx.x & 31) == 0) atomicMax(amax_bits, mag16_to_f32_bits(mx, f16));
 }
 
 // gs = 2688 / amax (reading Q3), in place over the amax bits; amax = 0 -> 1.
@@ -877,7 +890,7 @@ __global__ void arc_mxfp8_quant_kernel(const uint16_t* __restrict__ x, int64_t r
 // Per-(kernel, threads, smem) launch configuration, computed once per process:
 // the attribute calls and the occupancy query cost more host time than the
 // kernel itself at decode sizes.
-template <int IPT, int R, int ROWB, int ST, bool NORM, int SILU = 0, bool MX = false>
+template <int IPT, int R, int ROWB, int ST, bool NORM, int SILU = 0, bool MX = false, bool F16 = false>
 static cudaError_t launch_quant_cfg(QuantArgs a, int threads, cudaStream_t stream) {
   a.rows_per_tile = R;
   a.stages = ST;
@@ -892,13 +905,13 @@ static cudaError_t launch_quant_cfg(QuantArgs a, int threads, cudaStream_t strea
   for (int i = 0; i < ncache && i < 8; ++i)
     if (cache[i].dev == dev && cache[i].threads == threads && cache[i].smem == smem) occ = cache[i].occ;
   if (occ == 0) {
-    cudaError_t e = cudaFuncSetAttribute(arc_quant_kernel<IPT, R, ROWB, ST, NORM, SILU, MX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(arc_quant_kernel<IPT, R, ROWB, ST, NORM, SILU, MX, F16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          227 * 1024);
     if (e != cudaSuccess) return e;
     // the full shared-memory carveout so several CTAs' rings fit per SM
-    e = cudaFuncSetAttribute(arc_quant_kernel<IPT, R, ROWB, ST, NORM, SILU, MX>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    e = cudaFuncSetAttribute(arc_quant_kernel<IPT, R, ROWB, ST, NORM, SILU, MX, F16>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e != cudaSuccess) return e;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, arc_quant_kernel<IPT, R, ROWB, ST, NORM, SILU, MX>, threads, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, arc_quant_kernel<IPT, R, ROWB, ST, NORM, SILU, MX, F16>, threads, smem);
     if (e != cudaSuccess) return e;
     if (occ < 1) occ = 1;
     cache[ncache % 8] = Cfg{dev, threads, smem, occ};
@@ -917,7 +930,7 @@ static cudaError_t launch_quant_cfg(QuantArgs a, int threads, cudaStream_t strea
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, arc_quant_kernel<IPT, R, ROWB, ST, NORM, SILU, MX>, a);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, arc_quant_kernel<IPT, R, ROWB, ST, NORM, SILU, MX, F16>, a);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
@@ -978,10 +991,17 @@ __global__ void __launch_bounds__(256) arc_quant_small_kernel(QuantArgs p) {
     float z[16];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      z[4 * q + 0] = bf16_bits_to_f32(__ldg(xr + c[q].x));
-      z[4 * q + 1] = bf16_bits_to_f32(__ldg(xr + c[q].y));
-      z[4 * q + 2] = bf16_bits_to_f32(__ldg(xr + c[q].z));
-      z[4 * q + 3] = bf16_bits_to_f32(__ldg(xr + c[q].w));
+      if (p.f16) {
+        z[4 * q + 0] = in16_to_f32<true>(__ldg(xr + c[q].x));
+        z[4 * q + 1] = in16_to_f32<true>(__ldg(xr + c[q].y));
+        z[4 * q + 2] = in16_to_f32<true>(__ldg(xr + c[q].z));
+        z[4 * q + 3] = in16_to_f32<true>(__ldg(xr + c[q].w));
+      } else {
+        z[4 * q + 0] = bf16_bits_to_f32(__ldg(xr + c[q].x));
+        z[4 * q + 1] = bf16_bits_to_f32(__ldg(xr + c[q].y));
+        z[4 * q + 2] = bf16_bits_to_f32(__ldg(xr + c[q].z));
+        z[4 * q + 3] = bf16_bits_to_f32(__ldg(xr + c[q].w));
+      }
     }
     const uint32_t sf1 = e4m3_ceil_nb(__fmul_rn(absmax16(z), __fdiv_rn(gs, 6.0f)));
     const float d1 = e4m3_value(sf1);
@@ -1003,9 +1023,12 @@ __global__ void __launch_bounds__(256) arc_quant_small_kernel(QuantArgs p) {
 
 cudaError_t launch_quant(const void* x, int64_t rows, int K, int64_t ld, const int32_t* perm, int S, const float* gs,
                          int layout, int weight_mode, uint8_t* codes, uint8_t* sf, cudaStream_t stream,
-                         const void* gamma, float eps, int64_t up_off, int mx, int consts_ready) {
+                         const void* gamma, float eps, int64_t up_off, int mx, int consts_ready, int f16) {
   QuantArgs a;
   a.consts_ready = consts_ready;
+  a.f16 = f16;
+  // fp16 rows (ARC_FP16): the plain quantize / weight kernels; the bf16 model producers do not take them
+  if (f16 && (gamma != nullptr || up_off != -1 || mx)) return cudaErrorInvalidValue;
   a.up_off = up_off;
   a.trace = trace_slot();
   a.gamma = static_cast<const uint16_t*>(gamma);
@@ -1084,6 +1107,11 @@ cudaError_t launch_quant(const void* x, int64_t rows, int K, int64_t ld, const i
         if (rowb <= 16384) return launch_quant_cfg<1, 2, 16384, 3, false, 0, true>(a, th, stream);
         return launch_quant_cfg<1, 2, 32768, 3, false, 0, true>(a, th, stream);
       }
+      if (f16) {
+        if (rowb <= 8192) return launch_quant_cfg<1, 4, 8192, 3, false, 0, false, true>(a, th, stream);
+        if (rowb <= 16384) return launch_quant_cfg<1, 2, 16384, 3, false, 0, false, true>(a, th, stream);
+        return launch_quant_cfg<1, 2, 32768, 3, false, 0, false, true>(a, th, stream);
+      }
       if (rowb <= 8192) return launch_quant_cfg<1, 4, 8192, 3, false>(a, th, stream);
       if (rowb <= 16384) return launch_quant_cfg<1, 2, 16384, 3, false>(a, th, stream);
       return launch_quant_cfg<1, 2, 32768, 3, false>(a, th, stream);
@@ -1097,6 +1125,7 @@ cudaError_t launch_quant(const void* x, int64_t rows, int K, int64_t ld, const i
     if (threads > 1024) return cudaErrorInvalidValue;
     if (a.norm) return launch_quant_cfg<2, 1, 65536, 2, true>(a, threads, stream);
     if (mx) return launch_quant_cfg<2, 1, 65536, 3, false, 0, true>(a, threads, stream);
+    if (f16) return launch_quant_cfg<2, 1, 65536, 3, false, 0, false, true>(a, threads, stream);
     return launch_quant_cfg<2, 1, 65536, 3, false>(a, threads, stream);
   }
   return cudaErrorInvalidValue;  // K + S > 32768 is rejected in api.cu
@@ -1185,23 +1214,24 @@ cudaError_t launch_silu_mul(const void* gu, int64_t rows, int K, int64_t ld, int
   return cudaGetLastError();
 }
 
-cudaError_t launch_calib_absmax(const void* x, int64_t rows, int K, int64_t ld, float* chan_max, cudaStream_t s) {
+cudaError_t launch_calib_absmax(const void* x, int64_t rows, int K, int64_t ld, float* chan_max, cudaStream_t s,
+                                int f16) {
   const int threads = 128;
   const int rows_per_cta = 64;
   dim3 grid((unsigned)((K / 8 + threads - 1) / threads), (unsigned)((rows + rows_per_cta - 1) / rows_per_cta));
   arc_calib_absmax_kernel<<<grid, threads, 0, s>>>(static_cast<const uint16_t*>(x), rows, K, ld, rows_per_cta,
-                                                   chan_max);
+                                                   chan_max, f16);
   return cudaGetLastError();
 }
 
 cudaError_t launch_tensor_scale(const void* x, int64_t rows, int K, int64_t ld, float* gs_out, cudaStream_t s,
-                                int mx) {
+                                int mx, int f16) {
   cudaError_t e = cudaMemsetAsync(gs_out, 0, sizeof(float), s);
   if (e != cudaSuccess) return e;
   const int64_t n8 = rows * (K / 8);
   const int64_t grid = imax64(1, imin64((n8 + 255) / 256, (int64_t)num_sms() * 8));
   arc_absmax_all_kernel<<<(unsigned)grid, 256, 0, s>>>(static_cast<const uint16_t*>(x), rows, K, ld,
-                                                      reinterpret_cast<unsigned int*>(gs_out));
+                                                      reinterpret_cast<unsigned int*>(gs_out), f16);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   if (mx) arc_finalize_mx_scale_kernel<<<1, 1, 0, s>>>(gs_out);
