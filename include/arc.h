@@ -145,7 +145,8 @@ ARC_API arc_status_t arc_calib_absmax_ex(const void* x, arc_dtype_t x_dtype, int
 ARC_API arc_status_t arc_select_outliers(const float* chan_max_host, int64_t K, int32_t s_override,
                                          int32_t* perm_host, int32_t* S, int32_t* S_raw, float* M, float* tau,
                                          float* gs);
-/* Host, synchronous, deterministic.  perm_out assigns every 16-channel block the
+/* Host, synchronous, deterministic (independent of the number of host threads it
+ * uses: each group of 32 blocks is searched with its own seed).  perm_out assigns every 16-channel block the
  * same SET of channels as perm_host (so the outlier set, every block maximum and
  * scale, the codes as a multiset and the GEMM result are unchanged; reading Q22:
  * the channel order inside a block is free) and orders the channels inside each

@@ -7,10 +7,12 @@
 #include "arc_internal.h"
 
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <thread>
 #include <vector>
 
 namespace arc {
@@ -273,18 +275,22 @@ arc_status_t arc_gather_order_ex(const int32_t* perm_host, int64_t K, int elem_b
     seen[(size_t)c] = 1;
   }
   std::vector<int32_t> out(perm_host, perm_host + K);
-  const int64_t nblk = K / 16;
-  uint64_t rng = 0x9E3779B97F4A7C15ull;
-  for (int64_t c0 = 0; c0 < nblk; c0 += 32) {
+  const int64_t nblk = K / 16, nchunk = (nblk + 31) / 32;
+  // Chunks are independent: each has its own seed (the result does not depend on the thread count) and
+  // stops early once every step costs one word per bank (the minimum).
+  auto search = [&](int64_t ch) {
+    const int64_t c0 = ch * 32;
     const int n = (int)std::min<int64_t>(32, nblk - c0);
     int32_t* B = out.data() + c0 * 16;  // B[i*16 + q]
     const int32_t* col[32];
-    int cost[16];
+    int cost[16], total = 0;
     for (int q = 0; q < 16; ++q) {
       for (int i = 0; i < n; ++i) col[i] = &B[i * 16 + q];
       cost[q] = gather_step_cost(col, n, shift);
+      total += cost[q];
     }
-    for (int it = 0; it < 4000; ++it) {
+    uint64_t rng = 0x9E3779B97F4A7C15ull ^ (0xD1B54A32D192ED03ull * (uint64_t)(ch + 1));
+    for (int it = 0; it < 4000 && total > 16; ++it) {
       rng ^= rng << 13; rng ^= rng >> 7; rng ^= rng << 17;
       const int i = (int)(rng % (uint64_t)n), a = (int)((rng >> 16) & 15), b = (int)((rng >> 24) & 15);
       if (a == b) continue;
@@ -294,13 +300,23 @@ arc_status_t arc_gather_order_ex(const int32_t* perm_host, int64_t K, int elem_b
       for (int k = 0; k < n; ++k) col[k] = &B[k * 16 + b];
       const int cb = gather_step_cost(col, n, shift);
       if (ca + cb <= cost[a] + cost[b]) {
+        total += ca + cb - cost[a] - cost[b];
         cost[a] = ca;
         cost[b] = cb;
       } else {
         std::swap(B[i * 16 + a], B[i * 16 + b]);
       }
     }
-  }
+  };
+  const int nth = (int)std::min<int64_t>(nchunk, std::max(1u, std::min(32u, std::thread::hardware_concurrency())));
+  std::atomic<int64_t> next{0};
+  auto worker = [&] {
+    for (int64_t ch; (ch = next.fetch_add(1)) < nchunk;) search(ch);
+  };
+  std::vector<std::thread> pool;
+  for (int t = 1; t < nth; ++t) pool.emplace_back(worker);
+  worker();
+  for (auto& t : pool) t.join();
   std::memcpy(perm_out_host, out.data(), sizeof(int32_t) * (size_t)K);
   return ARC_OK;
 }
