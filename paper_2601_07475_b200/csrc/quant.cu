@@ -64,6 +64,8 @@ struct QuantArgs {
   unsigned long long* trace;  // timing experiments only (ARC_TRACE): [cta][8] globaltimer stamps
   int32_t consts_ready;       // perm may be read before griddepcontrol.wait (arc_linear)
   int32_t f16;                // the 16-bit rows are IEEE fp16 (ARC_FP16), else bf16
+  int32_t stage_rows;         // arc_quant_small_kernel: copy the CTA's x rows to shared memory with 16-byte
+                              // coalesced loads, then gather from there (else 16 2-byte gathers from L2)
 };
 
 ARC_DEV void qtrace(const QuantArgs& a, int i) {
@@ -977,6 +979,21 @@ __global__ void __launch_bounds__(256) arc_quant_small_kernel(QuantArgs p) {
   pdl_wait();
   pdl_launch_dependents();  // (after the wait: see arc_quant_kernel)
   if (threadIdx.x == 0) qtrace(p, 1);
+  const unsigned short* xs = nullptr;  // this thread's row, staged (stage_rows)
+  if (p.stage_rows) {
+    extern __shared__ __align__(16) uint8_t qsmall_rows[];
+    const int64_t it0 = (int64_t)blockIdx.x * blockDim.x;
+    const int m0 = (int)(it0 / NB);
+    const int m1 = (int)min(p.rows - 1, (it0 + (int64_t)blockDim.x - 1) / NB);
+    const int n16 = p.K >> 3;  // 16-byte pieces per row
+    uint4* dst = reinterpret_cast<uint4*>(qsmall_rows);
+    for (int i = threadIdx.x; i < (m1 - m0 + 1) * n16; i += blockDim.x) {
+      const int r = i / n16, j = i - r * n16;
+      dst[i] = __ldg(reinterpret_cast<const uint4*>(p.x + (int64_t)(m0 + r) * p.ld) + j);
+    }
+    __syncthreads();
+    xs = reinterpret_cast<const unsigned short*>(qsmall_rows) + (int64_t)(m - m0) * p.K;
+  }
   if (!live) return;
   if (!p.consts_ready && l >= 0) {
     const int4* pp = reinterpret_cast<const int4*>(p.perm + 16 * l);
@@ -989,6 +1006,15 @@ __global__ void __launch_bounds__(256) arc_quant_small_kernel(QuantArgs p) {
     const float gs = __ldg(p.gs);
     const unsigned short* xr = reinterpret_cast<const unsigned short*>(p.x) + (int64_t)m * p.ld;
     float z[16];
+    if (xs) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        z[4 * q + 0] = p.f16 ? in16_to_f32<true>(xs[c[q].x]) : bf16_bits_to_f32(xs[c[q].x]);
+        z[4 * q + 1] = p.f16 ? in16_to_f32<true>(xs[c[q].y]) : bf16_bits_to_f32(xs[c[q].y]);
+        z[4 * q + 2] = p.f16 ? in16_to_f32<true>(xs[c[q].z]) : bf16_bits_to_f32(xs[c[q].z]);
+        z[4 * q + 3] = p.f16 ? in16_to_f32<true>(xs[c[q].w]) : bf16_bits_to_f32(xs[c[q].w]);
+      }
+    } else {
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       if (p.f16) {
@@ -1002,6 +1028,7 @@ __global__ void __launch_bounds__(256) arc_quant_small_kernel(QuantArgs p) {
         z[4 * q + 2] = bf16_bits_to_f32(__ldg(xr + c[q].z));
         z[4 * q + 3] = bf16_bits_to_f32(__ldg(xr + c[q].w));
       }
+    }
     }
     const uint32_t sf1 = e4m3_ceil_nb(__fmul_rn(absmax16(z), __fdiv_rn(gs, 6.0f)));
     const float d1 = e4m3_value(sf1);
@@ -1025,6 +1052,7 @@ cudaError_t launch_quant(const void* x, int64_t rows, int K, int64_t ld, const i
                          int layout, int weight_mode, uint8_t* codes, uint8_t* sf, cudaStream_t stream,
                          const void* gamma, float eps, int64_t up_off, int mx, int consts_ready, int f16) {
   QuantArgs a;
+  a.stage_rows = 0;
   a.consts_ready = consts_ready;
   a.f16 = f16;
   // fp16 rows (ARC_FP16): the plain quantize / weight kernels; the bf16 model producers do not take them
@@ -1063,6 +1091,23 @@ cudaError_t launch_quant(const void* x, int64_t rows, int K, int64_t ld, const i
     memset(&cfg, 0, sizeof(cfg));
     cfg.gridDim = dim3((unsigned)((rows * NB + tpb - 1) / tpb));
     cfg.blockDim = dim3(tpb);
+    // staged rows: a window of tpb consecutive (row, block) items spans at most (tpb - 1) / NB + 2 rows
+    // Auto: stage when the gathers are many (>= 32 rows) and the staged rows are at most twice the bytes
+    // the CTA's items use (measured, LLaMA-3-8B decode step: M = 32 / 64 faster by 1-2 us, M <= 16 and
+    // K = 14336 rows slower -- profiles/r2_decode_cluster.txt).  ARC_QSMALL_STAGE=0 / 1 forces it.
+    static const int env_stage = getenv("ARC_QSMALL_STAGE") ? atoi(getenv("ARC_QSMALL_STAGE")) : -1;
+    const int span = (int)std::min<int64_t>(rows, (tpb - 1) / NB + 2);
+    const size_t stage_bytes = (size_t)span * (size_t)K * 2;
+    const bool auto_stage = rows >= 32 && stage_bytes <= (size_t)2 * tpb * 32;
+    a.stage_rows = (env_stage < 0 ? auto_stage : env_stage != 0) && stage_bytes <= 200 * 1024 ? 1 : 0;
+    if (a.stage_rows) {
+      cfg.dynamicSmemBytes = stage_bytes;
+      static PerDeviceOnce small_attr;
+      const cudaError_t ae = small_attr.run([] {
+        return cudaFuncSetAttribute(arc_quant_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      });
+      if (ae != cudaSuccess) return ae;
+    }
     cfg.stream = stream;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;

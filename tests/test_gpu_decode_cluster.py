@@ -1,6 +1,7 @@
 """GPU parity of the round-2 decode-size kernels (M <= 64; Eq.1-2):
 
-* arc_quant_small_kernel (direct-gather quantize, taken at M <= 64): codes and scale bytes bit-exact
+* arc_quant_small_kernel (direct-gather quantize, taken at M <= 64; x gathered from L2, or from the CTA's
+  rows staged in shared memory -- both variants forced in subprocesses): codes and scale bytes bit-exact
   against the oracle's quantize_activation for every M in 1..64 at shapes with residual blocks, K
   padding, S = 0 and both block layouts; and bit-identical to the rows of an M > 64 call of the same
   activation (the staging-ring kernel) -- quantization is row-independent;
@@ -91,3 +92,18 @@ def test_decode_gemm_vs_oracle(A, M, N, K, S, out_dtype):
     tol = bound + (np.abs(yref) * 2.0 ** -8 if out_dtype == torch.bfloat16 else 0.0)
     err = np.abs(got - yref)
     assert (err <= tol).all(), f"{(err > tol).sum()} outputs out of tolerance; worst {np.max(err / tol)}"
+
+
+@pytest.mark.parametrize("stage", ["0", "1"])
+def test_small_quantize_forced_variants(stage):
+    """Both gather variants of arc_quant_small_kernel at every M of the bit-exact test (auto stages the rows
+    in shared memory only at M >= 32 with compact rows): ARC_QSMALL_STAGE=0 gathers from L2 everywhere, =1
+    stages everywhere (K = 4096 and K = 1040 rows included), in a fresh process (read once per process)."""
+    import os
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    r = subprocess.run([sys.executable, "-m", "pytest", os.path.join(here, "test_gpu_decode_cluster.py"), "-q", "-x",
+                        "-k", "small_quantize_bit_exact"],
+                       env={**os.environ, "ARC_QSMALL_STAGE": stage}, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
