@@ -119,9 +119,12 @@ __device__ __forceinline__ void dwait_cluster(uint64_t* bar, uint32_t parity, in
       : "memory");
 }
 __device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
-__device__ __forceinline__ float ld_dsmem_f32(uint32_t cluster_addr) {
-  float v;
-  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(cluster_addr) : "memory");
+__device__ __forceinline__ float4 ld_dsmem_v4(uint32_t cluster_addr) {
+  float4 v;
+  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(cluster_addr)
+               : "memory");
   return v;
 }
 __device__ __forceinline__ uint32_t mapa_u32(uint32_t smem_addr, uint32_t rank) {
@@ -130,7 +133,9 @@ __device__ __forceinline__ uint32_t mapa_u32(uint32_t smem_addr, uint32_t rank) 
   return r;
 }
 
-__global__ void __launch_bounds__(D_THREADS, 1)
+// min 4 CTAs per SM: the one-wave planner (plan_decode) co-schedules up to 4 per SM by shared memory,
+// so the registers must allow 4 as well (<= 85 per thread)
+__global__ void __launch_bounds__(D_THREADS, 4)
     arc_decode_gemm_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
                            DArgs args) {
   extern __shared__ uint8_t smem_raw[];
@@ -373,32 +378,51 @@ __global__ void __launch_bounds__(D_THREADS, 1)
     // scales and stores Y
     asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
     if (warp >= 2 && r < args.M) {
-      const int n = (warp & 3) * 32 + lane;
-      const int gn = tile * DBW + n;
+      // warp w of the epilogue reduces this CTA's tokens i = w, w + 4, ... (token m = r + ks i); each lane
+      // owns 4 consecutive weight rows: one 16-byte ld.shared::cluster per (token, source CTA)
+      const int w = warp - 2;
+      const int n4 = lane * 4;
+      const int gn = tile * DBW + n4;
       if (threadIdx.x == 64) ck[2] = clock64() - clk2;
-      // up to 4 of this CTA's tokens per round, all 4 x ks remote loads issued before the first add
-      for (int m0 = r; m0 < args.M; m0 += 4 * ks) {
-        float p[4][8];
+      uint32_t base[8];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int m = m0 + u * ks;
-          const uint32_t off = smem_u32(smem) + (uint32_t)(m * DBW + n) * 4u;
+      for (int src = 0; src < 8; ++src) base[src] = src < ks ? mapa_u32(smem_u32(smem), (uint32_t)src) : 0u;
+      for (int m = r + ks * w; m < args.M; m += 4 * ks) {  // one token per round: its ks loads issued first
+        const uint32_t off = (uint32_t)(m * DBW + n4) * 4u;
+        float4 p[8];
 #pragma unroll
-          for (int src = 0; src < 8; ++src)
-            p[u][src] = (src < ks && m < args.M) ? ld_dsmem_f32(mapa_u32(off, (uint32_t)src)) : 0.0f;
+        for (int src = 0; src < 8; ++src)
+          p[src] = src < ks ? ld_dsmem_v4(base[src] + off) : make_float4(0.f, 0.f, 0.f, 0.f);
+        float4 acc = p[0];
+#pragma unroll
+        for (int src = 1; src < 8; ++src) {
+          if (src < ks) {  // rank order: the fixed summation order of every call
+            acc.x = __fadd_rn(acc.x, p[src].x);
+            acc.y = __fadd_rn(acc.y, p[src].y);
+            acc.z = __fadd_rn(acc.z, p[src].z);
+            acc.w = __fadd_rn(acc.w, p[src].w);
+          }
         }
+        const float o[4] = {__fmul_rn(acc.x, alpha_pull), __fmul_rn(acc.y, alpha_pull),
+                            __fmul_rn(acc.z, alpha_pull), __fmul_rn(acc.w, alpha_pull)};
+        if (gn + 3 < args.N) {
+          if (args.y_fp32) {
+            *reinterpret_cast<float4*>(static_cast<float*>(args.y) + (int64_t)m * args.ldy + gn) =
+                make_float4(o[0], o[1], o[2], o[3]);
+          } else {
+            __nv_bfloat162 lo = __floats2bfloat162_rn(o[0], o[1]), hi = __floats2bfloat162_rn(o[2], o[3]);
+            uint2 v;
+            v.x = *reinterpret_cast<uint32_t*>(&lo);
+            v.y = *reinterpret_cast<uint32_t*>(&hi);
+            *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(args.y) + (int64_t)m * args.ldy + gn) = v;
+          }
+        } else {
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int m = m0 + u * ks;
-          if (m >= args.M) break;
-          float acc = p[u][0];
-#pragma unroll
-          for (int src = 1; src < 8; ++src)
-            if (src < ks) acc = __fadd_rn(acc, p[u][src]);
-          const float out = __fmul_rn(acc, alpha_pull);
-          if (gn < args.N) {
-            if (args.y_fp32) static_cast<float*>(args.y)[(int64_t)m * args.ldy + gn] = out;
-            else static_cast<__nv_bfloat16*>(args.y)[(int64_t)m * args.ldy + gn] = __float2bfloat16_rn(out);
+          for (int k = 0; k < 4; ++k) {
+            if (gn + k < args.N) {
+              if (args.y_fp32) static_cast<float*>(args.y)[(int64_t)m * args.ldy + gn + k] = o[k];
+              else static_cast<__nv_bfloat16*>(args.y)[(int64_t)m * args.ldy + gn + k] = __float2bfloat16_rn(o[k]);
+            }
           }
         }
       }
