@@ -504,11 +504,13 @@ DecodePlan plan_decode(int64_t M, int64_t N, int64_t Kp) {
   // Among the one-wave configurations take the largest grid (most SMs and bytes in flight), then the
   // most ring stages; if none fits in one wave, one CTA per tile.
   // enough tiles to give every SM one: no split (no reduction tail)
-  // clusters of at most 6 (measured, profiles/r2_decode_cluster.txt: the reduction tail waits for the slowest
-  // CTA of the cluster, and 8-CTA clusters lost more there than their extra streaming SMs gained)
-  static const int env_ksmax = getenv("ARC_DECODE_KSMAX") ? atoi(getenv("ARC_DECODE_KSMAX")) : 6;
+  // clusters of at most 6 CTAs at M <= 16, 4 above (measured, profiles/r2_decode_cluster.txt steps 8 and 12:
+  // the reduction tail waits for the slowest CTA of the cluster and grows with the tokens each owner sums;
+  // 8-CTA clusters lost more there than their extra streaming SMs gained)
+  static const int env_ksmax = getenv("ARC_DECODE_KSMAX") ? atoi(getenv("ARC_DECODE_KSMAX")) : 0;
+  const int64_t ksmax = env_ksmax > 0 ? env_ksmax : (M <= 16 ? 6 : 4);
   const int64_t ks_hi =
-      pl.n_tiles >= num_sms() ? 1 : std::max<int64_t>(1, std::min<int64_t>({(int64_t)env_ksmax, 8, pl.nkb / 2}));
+      pl.n_tiles >= num_sms() ? 1 : std::max<int64_t>(1, std::min<int64_t>({ksmax, 8, pl.nkb / 2}));
   int64_t best_grid = -1;
   for (int64_t ks = 1; ks <= ks_hi; ++ks) {
     if (env_ks > 0 && ks != std::min<int64_t>(env_ks, ks_hi)) continue;
