@@ -952,7 +952,7 @@ static cudaError_t launch_silu_cfg(QuantArgs a, int th, int ipt, int64_t rb, cud
 // block's 16 calibrated channels straight from x (L2) -- no staging ring, no mbarriers, one memory
 // round trip between griddepcontrol.wait and the stores.  The STAGE arithmetic of arc_quant_kernel
 // (Q7 op order: primary stage, residual stage of P:138 for residual blocks), bit-identical.
-__global__ void __launch_bounds__(256) arc_quant_small_kernel(QuantArgs p) {
+__global__ void __launch_bounds__(1024) arc_quant_small_kernel(QuantArgs p) {
   if (threadIdx.x == 0) qtrace(p, 0);
   const int NB = p.Kp >> 4, nb = p.K >> 4, ns = p.S >> 4;
   const int it = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1085,21 +1085,31 @@ cudaError_t launch_quant(const void* x, int64_t rows, int K, int64_t ld, const i
   // decode-size activations: the direct-gather kernel (ARC_QUANT_SMALL=0 keeps the ring kernel)
   static const int env_small = getenv("ARC_QUANT_SMALL") ? atoi(getenv("ARC_QUANT_SMALL")) : 1;
   if (env_small && rows <= 64 && !weight_mode && !a.norm && up_off == -1 && !mx) {
-    static const int env_tpb = getenv("ARC_QSMALL_TPB") ? atoi(getenv("ARC_QSMALL_TPB")) : 256;
-    const int tpb = (env_tpb == 64 || env_tpb == 128 || env_tpb == 256) ? env_tpb : 256;
+    static const int env_tpb = getenv("ARC_QSMALL_TPB") ? atoi(getenv("ARC_QSMALL_TPB")) : 0;
+    int tpb = (env_tpb == 64 || env_tpb == 128 || env_tpb == 256 || env_tpb == 1024) ? env_tpb : 256;
+    // staged rows: a window of tpb consecutive (row, block) items spans at most (tpb - 1) / NB + 2 rows
+    // Auto: stage when the gathers are many (>= 32 rows) and the staged rows are at most twice the bytes
+    // the CTA's items use (measured, LLaMA-3-8B decode step: M = 32 / 64 faster by 1-2 us, M <= 16 and
+    // K = 14336 rows at 256 threads slower -- profiles/r2_decode_cluster.txt); long rows (K = 14336) are
+    // staged by 1024-thread CTAs, which cover a whole row (<= 3x the bytes their items use; each 2-byte
+    // gather from L2 moves a 32-byte sector).  ARC_QSMALL_STAGE=0 / 1 forces staging on / off,
+    // ARC_QSMALL_WIDE=0 keeps 256-thread CTAs for long rows.
+    static const int env_stage = getenv("ARC_QSMALL_STAGE") ? atoi(getenv("ARC_QSMALL_STAGE")) : -1;
+    static const int env_wide = getenv("ARC_QSMALL_WIDE") ? atoi(getenv("ARC_QSMALL_WIDE")) : 1;
+    auto span_bytes = [&](int t) {
+      return (size_t)std::min<int64_t>(rows, (t - 1) / NB + 2) * (size_t)K * 2;
+    };
+    bool auto_stage = rows >= 32 && span_bytes(tpb) <= (size_t)2 * tpb * 32;
+    if (rows >= 32 && !auto_stage && env_tpb == 0 && env_wide && span_bytes(1024) <= (size_t)3 * 1024 * 32) {
+      tpb = 1024;
+      auto_stage = true;
+    }
+    const size_t stage_bytes = span_bytes(tpb);
+    a.stage_rows = (env_stage < 0 ? auto_stage : env_stage != 0) && stage_bytes <= 200 * 1024 ? 1 : 0;
     cudaLaunchConfig_t cfg;
     memset(&cfg, 0, sizeof(cfg));
     cfg.gridDim = dim3((unsigned)((rows * NB + tpb - 1) / tpb));
     cfg.blockDim = dim3(tpb);
-    // staged rows: a window of tpb consecutive (row, block) items spans at most (tpb - 1) / NB + 2 rows
-    // Auto: stage when the gathers are many (>= 32 rows) and the staged rows are at most twice the bytes
-    // the CTA's items use (measured, LLaMA-3-8B decode step: M = 32 / 64 faster by 1-2 us, M <= 16 and
-    // K = 14336 rows slower -- profiles/r2_decode_cluster.txt).  ARC_QSMALL_STAGE=0 / 1 forces it.
-    static const int env_stage = getenv("ARC_QSMALL_STAGE") ? atoi(getenv("ARC_QSMALL_STAGE")) : -1;
-    const int span = (int)std::min<int64_t>(rows, (tpb - 1) / NB + 2);
-    const size_t stage_bytes = (size_t)span * (size_t)K * 2;
-    const bool auto_stage = rows >= 32 && stage_bytes <= (size_t)2 * tpb * 32;
-    a.stage_rows = (env_stage < 0 ? auto_stage : env_stage != 0) && stage_bytes <= 200 * 1024 ? 1 : 0;
     if (a.stage_rows) {
       cfg.dynamicSmemBytes = stage_bytes;
       static PerDeviceOnce small_attr;

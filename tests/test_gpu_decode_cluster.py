@@ -37,7 +37,8 @@ def _sf_rows_equal(got, want, rows, Kp):
     return True, None
 
 
-@pytest.mark.parametrize("K,S,layout", [(4096, 128, 0), (1024, 64, 1), (272, 16, 0), (512, 0, 0), (1040, 48, 1)])
+@pytest.mark.parametrize("K,S,layout", [(4096, 128, 0), (1024, 64, 1), (272, 16, 0), (512, 0, 0), (1040, 48, 1),
+                                             (14336, 128, 0)])  # long rows: 1024-thread staged CTAs at M >= 32
 def test_small_quantize_bit_exact_every_m(A, K, S, layout):
     st = synth.Structure(K, max(S, 16), seed=K + S)
     prof = A.calibrate([synth.activation(256, K, st, seed=11, device="cuda")], s_override=S, layout=layout)
