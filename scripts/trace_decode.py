@@ -3,7 +3,7 @@ records per-CTA globaltimer stamps; one CUDA-graph replay of the step (weights H
 bench) is traced and each launch is summarised relative to the step's first stamp (us):
 first entry / median entry, griddepcontrol.wait passed (min/median/max), acc ready (GEMM), last exit.
 
-    ARC_TRACE=1 python scripts/trace_decode.py [M]
+    ARC_TRACE=1 [MODEL=70b] python scripts/trace_decode.py [M]
 """
 import ctypes
 import os
@@ -22,9 +22,10 @@ lib.arc_debug_trace.restype = ctypes.c_int
 lib.arc_debug_trace.argtypes = [ctypes.c_void_p]
 M = int(sys.argv[1]) if len(sys.argv) > 1 else 16
 mode = os.environ.get("MODE", "unfused")
+SITES = synth.LLAMA3_70B_SITES if os.environ.get("MODEL", "8b") == "70b" else synth.LLAMA3_8B_SITES
 
 sites = []
-for name, K, N in synth.LLAMA3_8B_SITES:
+for name, K, N in SITES:
     st = synth.Structure(K, 128, seed=0)
     prof = A.calibrate([synth.activation(1024, K, st, seed=1000, device="cuda")], s_override=128)
     qw = A.quantize_weight(synth.weight(N, K, seed=1, device="cuda"), prof)
